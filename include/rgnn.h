@@ -1,0 +1,198 @@
+/*
+ * rgnn.h -- C ABI of librgnn.so: one RGCN / RGAT layer over a heterogeneous
+ * graph on NVIDIA B200 (sm_100a).  This is the boundary the Python binding
+ * (paper_2301_06284_b200/_binding.py) and every GPU test call through.
+ *
+ * Paper: arXiv 2301.06284 (PAPER.md = its LaTeX source; "P:n" = line n).
+ *   RGCN layer ............ Sec. 2.1 equation
+ *   RGAT attention ........ Sec. 2.1, fig:rgnn_layer caption P:313,
+ *                           Listing 1 P:461-478 (zi, zj, inner_prod with
+ *                           concat, leakyrelu, edge_softmax)
+ *   typed linear / segment MM  Sec. 2.2; P:845 ("presorted")
+ *   preprocessing list .... Sec. 3.6 P:756 ("converting COO to CSR")
+ *   backward .............. Sec. 3.5 P:731-742 (only the required grads)
+ * Readings where the paper is silent are DESIGN.md Sec. 3 (O1..O22).
+ *
+ * Conventions (all entry points):
+ *  - Pointers are DEVICE pointers unless marked [host].  `stream` is a
+ *    cudaStream_t passed as void*; every call is asynchronous on it unless
+ *    marked SYNC.  Asynchronous device faults surface at the caller's next
+ *    synchronisation.
+ *  - The library never allocates device memory.  Every device buffer (graph
+ *    storage, scratch, workspace, saved activations, outputs) is owned by the
+ *    caller (PyTorch tensors in the binding); the library carves them.
+ *    Buffers must be 256-byte aligned.  The graph storage must outlive the
+ *    handle; a workspace must not be shared by two concurrent calls.
+ *  - Errors are status codes; nothing throws or aborts across the ABI.
+ *    rgnn_last_error() (thread-local) describes the last failure.
+ *  - Layouts are row major.  Ids are int32 (E < 2^31; RGNN_E_UNSUPPORTED
+ *    otherwise).  Feature widths d_in, d_out must be in {32, 64, 128}.
+ *  - Determinism: the forward has no atomics and is bit-reproducible; the
+ *    backward reduces in a fixed order and is bit-reproducible for a fixed
+ *    graph and dst range.  Row-split decisions depend only on the row, so
+ *    the owned rows of a dst-range shard are bit-identical to 1-GPU rows.
+ */
+#ifndef RGNN_H_
+#define RGNN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RGNN_OK = 0,
+  RGNN_E_INVALID_ARG = 1,  /* NULL required pointer, bad size or range      */
+  RGNN_E_RANGE = 2,        /* an edge id out of range (see rgnn_last_error) */
+  RGNN_E_UNSUPPORTED = 3,  /* width / size / feature not supported          */
+  RGNN_E_WORKSPACE = 4,    /* a caller buffer is smaller than required      */
+  RGNN_E_CUDA = 5,         /* a CUDA runtime call or launch failed          */
+  RGNN_E_NCCL = 6          /* an NCCL call failed                           */
+} rgnn_status;
+
+/* Operand precision of X / Z / dZ.  Accumulation is always fp32; Y, dW, dA
+ * are fp32.  RGNN_BF16: X arrives as bf16, W is rounded to bf16 (RNE) inside
+ * the call, the typed GEMMs run on tcgen05 tensor cores (bf16 x bf16 -> fp32
+ * in TMEM) and Z / dZ are stored bf16 (RNE).  RGNN_F32: fp32 everywhere,
+ * SIMT FFMA GEMMs (reading O16).                                            */
+typedef enum { RGNN_F32 = 0, RGNN_BF16 = 1 } rgnn_prec;
+
+/* RGCN normalisation 1/c_{v,r} ("a problem-specific normalization
+ * factor"; reading O7): relation in-degree |N_v^r| (default), none (c = 1),
+ * or a caller-supplied per-edge factor edge_norm[e].                        */
+typedef enum { RGNN_NORM_REL_INDEG = 0, RGNN_NORM_NONE = 1, RGNN_NORM_EDGE = 2 } rgnn_norm;
+
+typedef enum { RGNN_RGCN = 0, RGNN_RGAT = 1 } rgnn_model;
+
+typedef struct rgnn_graph rgnn_graph;
+typedef struct rgnn_comm rgnn_comm;
+
+/* Graph description (heterograph; tab:ir_constructs P:498). */
+typedef struct {
+  int64_t num_nodes;         /* V (global)                                   */
+  int64_t num_edges;         /* E = length of src / dst / etype              */
+  int32_t num_etypes;        /* R (relations)                                */
+  int32_t num_ntypes;        /* T; checked only if ntype != NULL             */
+  const int32_t* src;        /* [E] COO source ids (or CSR column ids)       */
+  const int32_t* dst;        /* [E] COO destination ids; ignored for CSR     */
+  const int32_t* etype;      /* [E] relation id of each edge                 */
+  const int32_t* row_ptr;    /* [V+1] CSR-by-dst input, or NULL for COO      */
+  const int32_t* ntype;      /* [V] node types, or NULL (validated only)     */
+  const float* edge_norm;    /* [E] required iff norm == RGNN_NORM_EDGE      */
+  int32_t norm;              /* rgnn_norm                                    */
+  int32_t row_split_cap;     /* max in-edges per work item; 0 = 256          */
+  int64_t dst_begin;         /* owned destination range [dst_begin, dst_end) */
+  int64_t dst_end;           /* (0, V) on one GPU                            */
+} rgnn_graph_desc;
+
+/* What the preprocessing built (device pointers into the caller's graph
+ * storage), for inspection and the bit-exact tests.  Positions p index the
+ * owned edges sorted by (etype, dst), ties by ascending edge id (reading
+ * O14); slots q index CSR-by-dst.                                          */
+typedef struct {
+  int64_t V, V_own, dst_begin, E_own, num_runs, num_tiles, num_items, num_split_rows;
+  int32_t R;
+  const int32_t* perm;     /* [E_own] original edge id of position p        */
+  const int32_t* src_s;    /* [E_own] src of position p                     */
+  const int32_t* dst_s;    /* [E_own] local dst (v - dst_begin) of p        */
+  const int32_t* seg;      /* [R+1]   relation segments in position space   */
+  const int32_t* row_ptr;  /* [V_own+1] CSR-by-dst over local rows          */
+  const int32_t* pos;      /* [E_own] positions of each row, ascending      */
+  const int32_t* et_slot;  /* [E_own] relation of slot q                    */
+  const float* inv_c;      /* [E_own] RGCN factor of position p (1/c_{v,r}) */
+  const int32_t* run_ptr;  /* [num_runs+1] (etype,dst) runs, position space */
+  const int32_t* rseg;     /* [R+1]   runs of relation r                    */
+  const int32_t* seg_host; /* [host, R+1] copy of seg                       */
+} rgnn_graph_view;
+
+/* Sizes of the caller-owned graph storage (kept for the handle's life) and
+ * scratch (needed only during rgnn_graph_create).  [host] desc.           */
+rgnn_status rgnn_graph_bytes(const rgnn_graph_desc* desc, size_t* dev_bytes, size_t* scratch_bytes);
+
+/* Preprocessing (Sec. 3.6; DESIGN.md Sec. 6 "a0"): validate
+ * ids; keep edges whose dst is owned; stable sort by (etype, dst); relation
+ * segments; CSR-by-dst; (etype,dst) runs and 1/c; GEMM tile table; degree-
+ * aware work list (rows longer than row_split_cap are split into chunks).
+ * SYNC: host synchronisations read the validation flag, the owned-edge
+ * count and the final counts (tile / chunk tables are built on the host).
+ * RGNN_E_RANGE names the SMALLEST offending edge id (atomicMin).         */
+rgnn_status rgnn_graph_create(const rgnn_graph_desc* desc, void* dev, size_t dev_bytes, void* scratch,
+                              size_t scratch_bytes, void* stream, rgnn_graph** out);
+rgnn_status rgnn_graph_export(const rgnn_graph* g, rgnn_graph_view* view /* [host] */);
+void rgnn_graph_destroy(rgnn_graph* g); /* frees the host struct only */
+
+/* Workspace and saved-activation sizes for one layer call.  `saved` links a
+ * forward to its backward (RGAT: Z, s_src, lse; RGCN: nothing).          */
+rgnn_status rgnn_workspace_bytes(const rgnn_graph* g, rgnn_model model, int d_in, int d_out, rgnn_prec prec,
+                                 int training, size_t* ws_bytes, size_t* saved_bytes);
+
+/* RGCN forward: Y_v = sum_{e: dst=v} (1/c_{v,r}) X_src W_r
+ * (+ X_v W0 if W0 != NULL) for owned v, pre-activation (reading O9).
+ *   X  [V, d_in]  fp32 or bf16 (per prec), all V rows (replicated)
+ *   W  [R, d_in, d_out] fp32, z = x W_r (reading O11); W0 [d_in, d_out] or NULL
+ *   Y  [V_own, d_out] fp32 (owned rows, local order)
+ * If comm != NULL and Y_full != NULL, owned rows of every rank are gathered
+ * into Y_full [V, d_out] (NCCL grouped broadcasts); Y may alias
+ * Y_full + dst_begin * d_out.                                              */
+rgnn_status rgcn_forward(const rgnn_graph* g, int d_in, int d_out, rgnn_prec prec, const void* X, const float* W,
+                         const float* W0, float* Y, void* saved, void* ws, size_t ws_bytes, rgnn_comm* comm,
+                         float* Y_full, void* stream);
+
+/* RGAT forward (Listing 1; readings O1-O6):
+ *   pre_e = A[r,0].(X_src W_r) + A[r,1].(X_dst W_r),  s_e = LeakyReLU_slope(pre_e)
+ *   alpha_e = softmax over ALL incoming edges of dst,  Y_v = sum alpha_e X_src W_r
+ *   A [R, 2, d_out] fp32.  Zero in-degree rows give Y_v = 0.  saved must be
+ *   passed unchanged to rgnn_backward.                                     */
+rgnn_status rgat_forward(const rgnn_graph* g, int d_in, int d_out, rgnn_prec prec, const void* X, const float* W,
+                         const float* A, float slope, float* Y, void* saved, void* ws, size_t ws_bytes,
+                         rgnn_comm* comm, float* Y_full, void* stream);
+
+/* Backward of L = <Y, dY> over the owned rows (Sec. 3.5; reading O17):
+ *   dW [R, d_in, d_out] fp32 (required), dA [R, 2, d_out] (RGAT, required),
+ *   dW0 [d_in, d_out] (RGCN, iff W0 was used, else NULL).  dX must be NULL
+ *   (RGNN_E_UNSUPPORTED otherwise; NEXT-2).  Y is the forward output for the
+ *   owned rows and dY [V_own, d_out] fp32.  With comm != NULL, dW / dA / dW0
+ *   are all-reduced (sum) in place across ranks.  Outputs are overwritten. */
+rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int d_in, int d_out, rgnn_prec prec,
+                          const void* X, const float* W, const float* A, float slope, const float* Y,
+                          const float* dY, const void* saved, float* dW, float* dA, float* dW0, float* dX,
+                          void* ws, size_t ws_bytes, rgnn_comm* comm, void* stream);
+
+/* Multi-GPU (one process per GPU; dst-range partition).
+ * rgnn_comm_unique_id writes a 128-byte NCCL id to `id` [host]; rank 0
+ * creates it and the caller broadcasts it (torch.distributed).  `bounds`
+ * (identical on every rank) gives rank k the rows [bounds[k], bounds[k+1]);
+ * each rank's graph must be created with exactly its range.  SYNC.        */
+rgnn_status rgnn_comm_unique_id(void* id /* [host] 128 B */);
+rgnn_status rgnn_comm_create(const void* id /* [host] 128 B */, int nranks, int rank,
+                             const int64_t* bounds /* [host] nranks+1 dst-range cut */, rgnn_comm** out);
+void rgnn_comm_destroy(rgnn_comm* c);
+
+/* Balanced dst-range cut from the global in-degree prefix (host helper):
+ * bounds[k] = the v whose indeg_prefix[v] is closest to k*E/P (ties -> the
+ * smaller v), nondecreasing, bounds[0] = 0, bounds[P] = V.  Deterministic.
+ * indeg_prefix [host, V+1], bounds [host, P+1].                            */
+rgnn_status rgnn_partition_dst(int64_t V, const int64_t* indeg_prefix, int nparts, int64_t* bounds);
+
+/* Phase profiler (tracing).  When enabled, every layer call records CUDA
+ * events on the caller's stream around each kernel phase ("gemm_fwd",
+ * "aggregate", "merge", "bwd_traverse", "gemm_dw", "dw_reduce", "fold_u",
+ * "comm").  rgnn_profile_read (SYNC: waits for the events) returns up to
+ * `max` phases -- name (32 chars each, NUL padded), total ms and number of
+ * launches since the last read -- and resets the accumulators.             */
+void rgnn_profile_enable(int on);
+int rgnn_profile_read(char* names /* [host] max*32 */, double* ms /* [host] */, int64_t* count /* [host] */,
+                      int max);
+
+/* Kernel-launch counter (every kernel the library launches increments it). */
+uint64_t rgnn_launch_count(void);
+
+const char* rgnn_last_error(void);
+const char* rgnn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RGNN_H_ */

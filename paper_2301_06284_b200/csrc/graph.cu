@@ -1,0 +1,429 @@
+// graph.cu -- graph preprocessing (DESIGN.md Sec. 6 step a0).
+//
+// PAPER.md Sec. 3.6 P:756 emits a preprocessing list ("transposition,
+// converting COO to CSR, etc.") run before training/inference, and P:845
+// presorts for segment MM.  Here, on the device, for the owned dst range:
+//   validate ids (smallest bad edge via atomicMin) -> keep owned edges in
+//   input order -> stable radix sort by key = etype*V_own + (dst-v0) ->
+//   perm / src_s / dst_s, relation segments seg[R+1], CSR-by-dst row_ptr and
+//   pos (second stable sort of positions by dst), et_slot, (etype,dst) runs
+//   with 1/c_{v,r}, the destination-walk work list (rows longer than `cap`
+//   split into chunks), then -- after the single host sync -- the 128-row
+//   GEMM tile table and the dW split-K chunk table (host built, uploaded).
+// Tie-break contract = DESIGN.md reading O14 (bit-exact vs the oracle).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace rgnn {
+
+struct Counters {
+  int32_t bad_edge, bad_node, E_own, J, num_items, num_parts, num_split_rows, pad;
+};
+
+__global__ void k_init_counters(Counters* c, int32_t big) {
+  c->bad_edge = big; c->bad_node = big; c->E_own = 0; c->J = 0;
+  c->num_items = 0; c->num_parts = 0; c->num_split_rows = 0; c->pad = 0;
+}
+
+// CSR-by-dst input: dst of every edge from row_ptr (one warp per row).
+__global__ void k_expand_csr(const int32_t* __restrict__ row_ptr, int64_t V, int32_t* __restrict__ dst) {
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  for (int64_t v = w; v < V; v += ((int64_t)gridDim.x * blockDim.x) >> 5)
+    for (int64_t e = row_ptr[v] + lane; e < row_ptr[v + 1]; e += 32) dst[e] = (int32_t)v;
+}
+
+__global__ void k_validate(int64_t E, int64_t V, int32_t R, const int32_t* __restrict__ src,
+                           const int32_t* __restrict__ dst, const int32_t* __restrict__ et, Counters* c) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+    int32_t s = src[e], d = dst[e], r = et[e];
+    if (s < 0 || s >= V || d < 0 || d >= V || r < 0 || r >= R) atomicMin(&c->bad_edge, (int32_t)e);
+  }
+}
+
+__global__ void k_validate_ntype(int64_t V, int32_t T, const int32_t* __restrict__ nt, Counters* c) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x)
+    if (nt[v] < 0 || nt[v] >= T) atomicMin(&c->bad_node, (int32_t)v);
+}
+
+__global__ void k_own_flags(int64_t E, const int32_t* __restrict__ dst, int64_t v0, int64_t v1,
+                            int32_t* __restrict__ flag) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
+    flag[e] = (dst[e] >= v0 && dst[e] < v1) ? 1 : 0;
+}
+
+// Compact owned edges in input order: key = etype*V_own + (dst - v0), val = edge id.
+__global__ void k_own_scatter(int64_t E, const int32_t* __restrict__ dst, const int32_t* __restrict__ et,
+                              int64_t v0, int64_t v1, int64_t V_own, const int32_t* __restrict__ slot,
+                              uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+    int32_t d = dst[e];
+    if (d >= v0 && d < v1) {
+      int32_t o = slot[e];
+      keys[o] = (uint32_t)((int64_t)et[e] * V_own + (d - v0));
+      vals[o] = (uint32_t)e;
+    }
+  }
+}
+
+// After the (etype,dst) sort: perm, src_s, dst_s, run heads and histograms.
+__global__ void k_after_sort(int64_t n, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                             const int32_t* __restrict__ src, int64_t V_own, int32_t* __restrict__ perm,
+                             int32_t* __restrict__ src_s, int32_t* __restrict__ dst_s, int32_t* __restrict__ et_s,
+                             int32_t* __restrict__ head, int32_t* __restrict__ seg_cnt,
+                             int32_t* __restrict__ row_cnt) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t k = keys[p];
+    int32_t e = (int32_t)vals[p];
+    int32_t r = (int32_t)(k / (uint32_t)V_own);
+    int32_t i = (int32_t)(k - (uint32_t)r * (uint32_t)V_own);
+    perm[p] = e;
+    src_s[p] = src[e];
+    dst_s[p] = i;
+    et_s[p] = r;
+    head[p] = (p == 0 || keys[p - 1] != k) ? 1 : 0;
+    atomicAdd(&seg_cnt[r], 1);  // integer counts: order independent, deterministic
+    atomicAdd(&row_cnt[i], 1);
+  }
+}
+
+__global__ void k_copy_u32_to_i32(int64_t n, const uint32_t* __restrict__ a, int32_t* __restrict__ b) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+    b[p] = (int32_t)a[p];
+}
+
+__global__ void k_iota_keys(int64_t n, const int32_t* __restrict__ dst_s, uint32_t* __restrict__ k,
+                            uint32_t* __restrict__ v) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    k[p] = (uint32_t)dst_s[p];
+    v[p] = (uint32_t)p;
+  }
+}
+
+__global__ void k_slots(int64_t n, const uint32_t* __restrict__ sorted_pos, const int32_t* __restrict__ et_s,
+                        int32_t* __restrict__ pos, int32_t* __restrict__ et_slot) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    int32_t p = (int32_t)sorted_pos[q];
+    pos[q] = p;
+    et_slot[q] = et_s[p];
+  }
+}
+
+// Runs of equal (etype, dst): run_ptr[j] = first position of run j.
+__global__ void k_runs(int64_t n, const int32_t* __restrict__ head, const int32_t* __restrict__ run_ex,
+                       const int32_t* __restrict__ et_s, int32_t* __restrict__ run_ptr,
+                       int32_t* __restrict__ rseg_cnt) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    if (head[p]) {
+      run_ptr[run_ex[p]] = (int32_t)p;
+      atomicAdd(&rseg_cnt[et_s[p]], 1);
+    }
+  }
+}
+
+__global__ void k_run_end(const Counters* c, int32_t* run_ptr) { run_ptr[c->J] = c->E_own; }
+
+// 1/c per position (reading O7): relation in-degree = run length; none; or edge_norm[perm[p]].
+__global__ void k_inv_c(int64_t n, int norm, const int32_t* __restrict__ head, const int32_t* __restrict__ run_ex,
+                        const int32_t* __restrict__ run_ptr, const int32_t* __restrict__ perm,
+                        const float* __restrict__ edge_norm, float* __restrict__ inv_c) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    float f;
+    if (norm == RGNN_NORM_NONE) {
+      f = 1.0f;
+    } else if (norm == RGNN_NORM_EDGE) {
+      f = edge_norm[perm[p]];
+    } else {
+      int32_t j = run_ex[p] + head[p] - 1;
+      f = 1.0f / (float)(run_ptr[j + 1] - run_ptr[j]);
+    }
+    inv_c[p] = f;
+  }
+}
+
+// Work list: rows with more than cap in-edges are split into ceil(deg/cap) chunks.
+__global__ void k_item_counts(int64_t V_own, const int32_t* __restrict__ row_ptr, int cap, int32_t* __restrict__ n_items,
+                              int32_t* __restrict__ n_parts, int32_t* __restrict__ n_split) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < V_own; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t deg = row_ptr[i + 1] - row_ptr[i];
+    int32_t c = deg > cap ? (deg + cap - 1) / cap : 1;
+    n_items[i] = c;
+    n_parts[i] = c > 1 ? c : 0;
+    n_split[i] = c > 1 ? 1 : 0;
+  }
+}
+
+__global__ void k_fill_items(int64_t V_own, const int32_t* __restrict__ row_ptr, int cap,
+                             const int32_t* __restrict__ item_ex, const int32_t* __restrict__ part_ex,
+                             const int32_t* __restrict__ split_ex, Item* __restrict__ items,
+                             SplitRow* __restrict__ split_rows) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < V_own; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t lo = row_ptr[i], hi = row_ptr[i + 1], deg = hi - lo;
+    int32_t c = deg > cap ? (deg + cap - 1) / cap : 1;
+    int32_t b = item_ex[i];
+    for (int32_t k = 0; k < c; ++k) {
+      Item it;
+      it.row = (int32_t)i;
+      it.q0 = lo + k * cap;
+      it.q1 = min(lo + (k + 1) * cap, hi);
+      it.part = c > 1 ? part_ex[i] + k : -1;
+      if (c == 1) { it.q0 = lo; it.q1 = hi; }
+      items[b + k] = it;
+    }
+    if (c > 1) {
+      SplitRow s;
+      s.row = (int32_t)i; s.part0 = part_ex[i]; s.nparts = c; s.pad = 0;
+      split_rows[split_ex[i]] = s;
+    }
+  }
+}
+
+static int bits_for(uint64_t maxval) {
+  int b = 0;
+  while (b < 64 && (maxval >> b) != 0) ++b;
+  return b;
+}
+
+struct GraphLayout {
+  // device storage
+  int32_t *perm, *src_s, *dst_s, *seg, *row_ptr, *pos, *et_slot, *run_ptr, *rseg;
+  float* inv_c;
+  Item* items;
+  SplitRow* split_rows;
+  Tile *tiles, *chunks;
+  int32_t* chunk_seg;
+  size_t dev_bytes;
+  // scratch
+  Counters* ctr;
+  int32_t *dst_tmp, *flags, *head, *run_ex, *et_s, *n_items, *n_parts, *n_split, *rseg_cnt;
+  uint32_t *k0, *v0, *k1, *v1;
+  void* prim;
+  size_t prim_bytes, scratch_bytes;
+};
+
+static int64_t max_chunks(int64_t E, int32_t R) { return 1024 + R; }
+
+static GraphLayout layout(const rgnn_graph_desc* d, void* dev, void* scr) {
+  GraphLayout L{};
+  const int64_t E = d->num_edges, V_own = d->dst_end - d->dst_begin;
+  const int32_t R = d->num_etypes;
+  const int cap = d->row_split_cap > 0 ? d->row_split_cap : kDefaultSplitCap;
+  const int64_t Ec = E > 0 ? E : 1;
+  Carver c(dev);
+  L.perm = c.take<int32_t>(Ec);
+  L.src_s = c.take<int32_t>(Ec);
+  L.dst_s = c.take<int32_t>(Ec);
+  L.pos = c.take<int32_t>(Ec);
+  L.et_slot = c.take<int32_t>(Ec);
+  L.inv_c = c.take<float>(Ec);
+  L.run_ptr = c.take<int32_t>(Ec + 1);
+  L.seg = c.take<int32_t>(R + 1);
+  L.rseg = c.take<int32_t>(R + 1);
+  L.row_ptr = c.take<int32_t>(V_own + 1);
+  L.items = c.take<Item>(V_own + Ec / cap + 1);
+  L.split_rows = c.take<SplitRow>(Ec / cap + 1);
+  L.tiles = c.take<Tile>(Ec / kTileRows + R + 1);
+  L.chunks = c.take<Tile>(max_chunks(E, R));
+  L.chunk_seg = c.take<int32_t>(R + 1);
+  L.dev_bytes = c.off;
+  Carver s(scr);
+  L.ctr = s.take<Counters>(1);
+  L.dst_tmp = s.take<int32_t>(d->row_ptr ? Ec : 1);
+  L.flags = s.take<int32_t>(Ec + 1);
+  L.head = s.take<int32_t>(Ec);
+  L.run_ex = s.take<int32_t>(Ec);
+  L.et_s = s.take<int32_t>(Ec);
+  L.n_items = s.take<int32_t>(V_own + 1);
+  L.n_parts = s.take<int32_t>(V_own + 1);
+  L.n_split = s.take<int32_t>(V_own + 1);
+  L.rseg_cnt = s.take<int32_t>(R + 1);
+  L.k0 = s.take<uint32_t>(Ec);
+  L.v0 = s.take<uint32_t>(Ec);
+  L.k1 = s.take<uint32_t>(Ec);
+  L.v1 = s.take<uint32_t>(Ec);
+  L.prim_bytes = std::max(radix_scratch_bytes(Ec), scan_scratch_bytes(std::max<int64_t>(Ec + 1, V_own + 1)));
+  L.prim = s.take<char>(L.prim_bytes);
+  L.scratch_bytes = s.off;
+  return L;
+}
+
+static rgnn_status check_desc(const rgnn_graph_desc* d) {
+  if (!d) return set_error(RGNN_E_INVALID_ARG, "desc is NULL");
+  if (d->num_nodes < 0 || d->num_edges < 0 || d->num_etypes < 1)
+    return set_error(RGNN_E_INVALID_ARG, "bad sizes V=%lld E=%lld R=%d", (long long)d->num_nodes,
+                     (long long)d->num_edges, d->num_etypes);
+  if (d->num_edges >= (int64_t)INT32_MAX || d->num_nodes >= (int64_t)INT32_MAX)
+    return set_error(RGNN_E_UNSUPPORTED, "E and V must be < 2^31 (reading O22)");
+  if (d->dst_begin < 0 || d->dst_end < d->dst_begin || d->dst_end > d->num_nodes)
+    return set_error(RGNN_E_INVALID_ARG, "bad dst range [%lld, %lld)", (long long)d->dst_begin,
+                     (long long)d->dst_end);
+  int64_t V_own = d->dst_end - d->dst_begin;
+  if ((uint64_t)d->num_etypes * (uint64_t)(V_own > 0 ? V_own : 1) > 0xffffffffull)
+    return set_error(RGNN_E_UNSUPPORTED, "R * V_own must fit 32 bits (sort key)");
+  if (d->num_edges > 0 && (!d->src || !d->etype || (!d->dst && !d->row_ptr)))
+    return set_error(RGNN_E_INVALID_ARG, "src/dst/etype must not be NULL");
+  if (d->norm < 0 || d->norm > 2) return set_error(RGNN_E_INVALID_ARG, "bad norm %d", d->norm);
+  if (d->norm == RGNN_NORM_EDGE && d->num_edges > 0 && !d->edge_norm)
+    return set_error(RGNN_E_INVALID_ARG, "edge_norm required for RGNN_NORM_EDGE");
+  if (d->ntype && d->num_ntypes < 1) return set_error(RGNN_E_INVALID_ARG, "num_ntypes must be >= 1");
+  if (d->row_split_cap < 0) return set_error(RGNN_E_INVALID_ARG, "row_split_cap < 0");
+  return RGNN_OK;
+}
+
+static unsigned grid_for(int64_t n, int threads = 256) {
+  int64_t b = (n + threads - 1) / threads;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32));
+}
+
+}  // namespace rgnn
+
+using namespace rgnn;
+
+extern "C" {
+
+rgnn_status rgnn_graph_bytes(const rgnn_graph_desc* d, size_t* dev_bytes, size_t* scratch_bytes) {
+  RGNN_TRY(check_desc(d));
+  GraphLayout L = layout(d, nullptr, nullptr);
+  if (dev_bytes) *dev_bytes = L.dev_bytes;
+  if (scratch_bytes) *scratch_bytes = L.scratch_bytes;
+  return RGNN_OK;
+}
+
+rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_bytes, void* scratch,
+                              size_t scratch_bytes, void* stream, rgnn_graph** out) {
+  RGNN_TRY(check_desc(d));
+  if (!out || !dev || !scratch) return set_error(RGNN_E_INVALID_ARG, "NULL buffer or out pointer");
+  if (((uintptr_t)dev | (uintptr_t)scratch) % kAlign) return set_error(RGNN_E_INVALID_ARG, "buffers must be 256B aligned");
+  GraphLayout need = layout(d, nullptr, nullptr);
+  if (dev_bytes < need.dev_bytes || scratch_bytes < need.scratch_bytes)
+    return set_error(RGNN_E_WORKSPACE, "graph buffers too small: need dev %zu scratch %zu", need.dev_bytes,
+                     need.scratch_bytes);
+  GraphLayout L = layout(d, dev, scratch);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t E = d->num_edges, V = d->num_nodes, v0 = d->dst_begin, v1 = d->dst_end, V_own = v1 - v0;
+  const int32_t R = d->num_etypes;
+  const int cap = d->row_split_cap > 0 ? d->row_split_cap : kDefaultSplitCap;
+  const int T = 256;
+
+  RGNN_LAUNCH(k_init_counters, 1, 1, 0, s, L.ctr, INT32_MAX);
+  const int32_t* dst = d->dst;
+  if (d->row_ptr) {
+    RGNN_LAUNCH(k_expand_csr, grid_for(V * 32), T, 0, s, d->row_ptr, V, L.dst_tmp);
+    dst = L.dst_tmp;
+  }
+  if (E > 0) RGNN_LAUNCH(k_validate, grid_for(E), T, 0, s, E, V, R, d->src, dst, d->etype, L.ctr);
+  if (d->ntype && V > 0) RGNN_LAUNCH(k_validate_ntype, grid_for(V), T, 0, s, V, d->num_ntypes, d->ntype, L.ctr);
+  // Owned edges, compacted in input order.
+  Counters h{};
+  RGNN_CUDA_TRY(cudaMemcpyAsync(&h, L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+  RGNN_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h.bad_edge != INT32_MAX)
+    return set_error(RGNN_E_RANGE, "edge %d has an id out of range (V=%lld, R=%d)", h.bad_edge, (long long)V, R);
+  if (h.bad_node != INT32_MAX)
+    return set_error(RGNN_E_RANGE, "node %d has a node type out of range (T=%d)", h.bad_node, d->num_ntypes);
+
+  int32_t* E_own_d = &L.ctr->E_own;
+  if (E > 0) {
+    RGNN_LAUNCH(k_own_flags, grid_for(E), T, 0, s, E, dst, v0, v1, L.flags);
+    RGNN_TRY(scan_exclusive(L.flags, L.flags, E, E_own_d, L.prim, L.prim_bytes, s));
+    RGNN_LAUNCH(k_own_scatter, grid_for(E), T, 0, s, E, dst, d->etype, v0, v1, V_own, L.flags, L.k0, L.v0);
+  }
+  RGNN_CUDA_TRY(cudaMemcpyAsync(&h, L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+  RGNN_CUDA_TRY(cudaStreamSynchronize(s));
+  const int64_t n = h.E_own;
+
+  // Stable sort of owned edges by (etype, dst).
+  bool alt = false;
+  int kbits = bits_for((uint64_t)R * (uint64_t)(V_own > 0 ? V_own : 1) - 1);
+  RGNN_TRY(radix_sort_pairs(L.k0, L.v0, L.k1, L.v1, n, kbits, L.prim, L.prim_bytes, s, &alt));
+  uint32_t* keys = alt ? L.k1 : L.k0;
+  uint32_t* vals = alt ? L.v1 : L.v0;
+  RGNN_CUDA_TRY(cudaMemsetAsync(L.rseg_cnt, 0, sizeof(int32_t) * (R + 1), s));
+  RGNN_CUDA_TRY(cudaMemsetAsync(L.seg, 0, sizeof(int32_t) * (R + 1), s));
+  RGNN_CUDA_TRY(cudaMemsetAsync(L.row_ptr, 0, sizeof(int32_t) * (V_own + 1), s));
+  if (n > 0)
+    RGNN_LAUNCH(k_after_sort, grid_for(n), T, 0, s, n, keys, vals, d->src, V_own, L.perm, L.src_s, L.dst_s, L.et_s,
+                L.head, L.seg, L.row_ptr);
+  RGNN_TRY(scan_exclusive(L.seg, L.seg, R + 1, nullptr, L.prim, L.prim_bytes, s));
+  RGNN_TRY(scan_exclusive(L.row_ptr, L.row_ptr, V_own + 1, nullptr, L.prim, L.prim_bytes, s));
+  // CSR-by-dst: stable sort of positions by local dst -> ascending p within a row.
+  if (n > 0) {
+    RGNN_LAUNCH(k_iota_keys, grid_for(n), T, 0, s, n, L.dst_s, L.k0, L.v0);
+    RGNN_TRY(radix_sort_pairs(L.k0, L.v0, L.k1, L.v1, n, bits_for((uint64_t)(V_own > 0 ? V_own - 1 : 0)), L.prim,
+                              L.prim_bytes, s, &alt));
+    RGNN_LAUNCH(k_slots, grid_for(n), T, 0, s, n, alt ? L.v1 : L.v0, L.et_s, L.pos, L.et_slot);
+    // (etype, dst) runs
+    RGNN_TRY(scan_exclusive(L.head, L.run_ex, n, &L.ctr->J, L.prim, L.prim_bytes, s));
+    RGNN_LAUNCH(k_runs, grid_for(n), T, 0, s, n, L.head, L.run_ex, L.et_s, L.run_ptr, L.rseg_cnt);
+  }
+  RGNN_LAUNCH(k_run_end, 1, 1, 0, s, L.ctr, L.run_ptr);
+  RGNN_TRY(scan_exclusive(L.rseg_cnt, L.rseg, R + 1, nullptr, L.prim, L.prim_bytes, s));
+  if (n > 0)
+    RGNN_LAUNCH(k_inv_c, grid_for(n), T, 0, s, n, d->norm, L.head, L.run_ex, L.run_ptr, L.perm, d->edge_norm,
+                L.inv_c);
+  // Destination-walk work list.
+  if (V_own > 0) {
+    RGNN_LAUNCH(k_item_counts, grid_for(V_own), T, 0, s, V_own, L.row_ptr, cap, L.n_items, L.n_parts, L.n_split);
+    RGNN_TRY(scan_exclusive(L.n_items, L.n_items, V_own, &L.ctr->num_items, L.prim, L.prim_bytes, s));
+    RGNN_TRY(scan_exclusive(L.n_parts, L.n_parts, V_own, &L.ctr->num_parts, L.prim, L.prim_bytes, s));
+    RGNN_TRY(scan_exclusive(L.n_split, L.n_split, V_own, &L.ctr->num_split_rows, L.prim, L.prim_bytes, s));
+    RGNN_LAUNCH(k_fill_items, grid_for(V_own), T, 0, s, V_own, L.row_ptr, cap, L.n_items, L.n_parts, L.n_split,
+                L.items, L.split_rows);
+  }
+  // The single readback: counts + relation segments.
+  std::vector<int32_t> seg_h(R + 1);
+  RGNN_CUDA_TRY(cudaMemcpyAsync(&h, L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+  RGNN_CUDA_TRY(cudaMemcpyAsync(seg_h.data(), L.seg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
+  RGNN_CUDA_TRY(cudaStreamSynchronize(s));
+
+  // Host: 128-row GEMM tiles and dW split-K chunks, never straddling relations.
+  std::vector<Tile> tiles, chunks;
+  std::vector<int32_t> chunk_seg(R + 1, 0);
+  int64_t chunk_rows = std::max<int64_t>(kTileRows, ((n / 512) + kTileRows - 1) / kTileRows * kTileRows);
+  for (int32_t r = 0; r < R; ++r) {
+    for (int64_t a = seg_h[r]; a < seg_h[r + 1]; a += kTileRows)
+      tiles.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + kTileRows, seg_h[r + 1]), 0});
+    chunk_seg[r] = (int32_t)chunks.size();
+    for (int64_t a = seg_h[r]; a < seg_h[r + 1]; a += chunk_rows)
+      chunks.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + chunk_rows, seg_h[r + 1]), 0});
+  }
+  chunk_seg[R] = (int32_t)chunks.size();
+  if ((int64_t)chunks.size() > max_chunks(E, R)) return set_error(RGNN_E_CUDA, "internal: chunk table overflow");
+  if (!tiles.empty())
+    RGNN_CUDA_TRY(cudaMemcpyAsync(L.tiles, tiles.data(), sizeof(Tile) * tiles.size(), cudaMemcpyHostToDevice, s));
+  if (!chunks.empty())
+    RGNN_CUDA_TRY(cudaMemcpyAsync(L.chunks, chunks.data(), sizeof(Tile) * chunks.size(), cudaMemcpyHostToDevice, s));
+  RGNN_CUDA_TRY(cudaMemcpyAsync(L.chunk_seg, chunk_seg.data(), sizeof(int32_t) * (R + 1), cudaMemcpyHostToDevice, s));
+  RGNN_CUDA_TRY(cudaStreamSynchronize(s));  // host vectors go out of scope
+
+  rgnn_graph* g = new rgnn_graph();
+  g->V = V; g->V_own = V_own; g->v0 = v0; g->E_in = E; g->E_own = n; g->J = h.J;
+  g->R = R; g->norm = d->norm; g->cap = cap;
+  g->num_tiles = (int64_t)tiles.size(); g->num_items = h.num_items; g->num_parts = h.num_parts;
+  g->num_split_rows = h.num_split_rows; g->num_chunks = (int64_t)chunks.size();
+  g->perm = L.perm; g->src_s = L.src_s; g->dst_s = L.dst_s; g->seg = L.seg; g->row_ptr = L.row_ptr;
+  g->pos = L.pos; g->et_slot = L.et_slot; g->run_ptr = L.run_ptr; g->rseg = L.rseg; g->inv_c = L.inv_c;
+  g->items = L.items; g->split_rows = L.split_rows; g->tiles = L.tiles; g->chunks = L.chunks;
+  g->chunk_seg = L.chunk_seg;
+  g->seg_host = seg_h;
+  g->chunk_seg_host = chunk_seg;
+  RGNN_CUDA_TRY(cudaGetDevice(&g->device));
+  RGNN_CUDA_TRY(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device));
+  *out = g;
+  return RGNN_OK;
+}
+
+rgnn_status rgnn_graph_export(const rgnn_graph* g, rgnn_graph_view* v) {
+  if (!g || !v) return set_error(RGNN_E_INVALID_ARG, "NULL graph or view");
+  v->V = g->V; v->V_own = g->V_own; v->dst_begin = g->v0; v->E_own = g->E_own; v->num_runs = g->J;
+  v->num_tiles = g->num_tiles; v->num_items = g->num_items; v->num_split_rows = g->num_split_rows; v->R = g->R;
+  v->perm = g->perm; v->src_s = g->src_s; v->dst_s = g->dst_s; v->seg = g->seg; v->row_ptr = g->row_ptr;
+  v->pos = g->pos; v->et_slot = g->et_slot; v->inv_c = g->inv_c; v->run_ptr = g->run_ptr; v->rseg = g->rseg;
+  v->seg_host = g->seg_host.data();
+  return RGNN_OK;
+}
+
+void rgnn_graph_destroy(rgnn_graph* g) { delete g; }
+
+}  // extern "C"

@@ -1,0 +1,111 @@
+// kernels.cuh -- declarations of the per-layer launchers (one .cu each).
+#pragma once
+#include "common.cuh"
+
+namespace rgnn {
+
+// Arguments of the typed grouped GEMM, forward (DESIGN.md Sec. 6 "a2"):
+//   Z[p, :] = X[gather(p), :] . W_{r(p)}  for every row p of every tile,
+//   then the epilogue: Z *= row_scale[p] (RGCN 1/c, the paper's per-row
+//   scalar on GEMM tiles) and s_src[p] = Z_fp32[p] . A[r,0] (RGAT).
+struct GemmFwdArgs {
+  const Tile* tiles;        // [num_tiles] (r, row0, row1) or null: one segment [0, rows) with weight 0
+  int64_t num_tiles;
+  int64_t rows;             // used when tiles == null
+  const void* X;            // [V, K] T
+  const int32_t* gather;    // [rows] X row of output row p, or null: row p -> X[gofs + p]
+  int64_t gofs;
+  const float* W;           // [R, K, N] fp32 master
+  void* Z;                  // [rows, N] T
+  const float* row_scale;   // [rows] or null
+  const float* A;           // [R, 2, N] or null
+  float* s_src;             // [rows] (with A)
+  void* wt_bf16;            // workspace for the tcgen05 path: [R, N, K] bf16 (transposed W)
+};
+
+// dW split-K GEMM over chunks (DESIGN.md Sec. 6 "a5"):
+//   part[c] = sum_{p in chunk c} X[gather(p)]^T B[p]   (K x N)
+//   RGAT extras: bvec = sum dpre_p X[src_p], cvec = sum dpre_p X[dst_p]  (K each)
+// B rows: dZ[p] (T), or (bgather) G[bgather[p]] * bscale[p] (fp32).
+struct GemmDwArgs {
+  const Tile* chunks;       // [num_chunks] or null: chunk c = rows [c*chunk_rows, ...) of [0, rows)
+  int64_t num_chunks, rows, chunk_rows;
+  const void* X;
+  const int32_t* gather;
+  int64_t gofs;
+  const void* Bz;           // dZ [rows, N] T, or null
+  const float* Bg;          // G [*, N] fp32 when Bz is null
+  const int32_t* bgather;   // B row index (null = identity)
+  const float* bscale;      // per-row scale (null = 1)
+  const float* dpre;        // RGAT: [rows] or null
+  const int32_t* dst_local; // RGAT: local dst of row p
+  int64_t v0;
+  float* part;              // [num_chunks, K*N + 2K]
+};
+
+rgnn_status launch_gemm_fwd(int prec, int K, int N, const GemmFwdArgs& a, cudaStream_t s);
+rgnn_status launch_gemm_dw(int prec, int K, int N, const GemmDwArgs& a, cudaStream_t s);
+rgnn_status launch_dw_reduce(int prec, int K, int N, int R, int64_t num_chunks, const int32_t* chunk_seg,
+                             const float* part, const float* A, const float* W, float* dW, float* dA, cudaStream_t s);
+rgnn_status launch_fold_u(int prec, int R, int K, int N, const float* W, const float* A, float* U, cudaStream_t s);
+
+struct AggArgs {
+  const Item* items;
+  int64_t num_items;
+  const int32_t* pos;
+  const int32_t* et_slot;
+  const void* Z;
+  const float* s_src;
+  const void* X;
+  int64_t v0;
+  const float* U;
+  float slope;
+  const void* Z0;        // RGCN self-loop rows [V_own, N] T or null
+  float* Y;
+  float* lse;
+  float* part;           // [num_parts, N+4]
+  const SplitRow* split_rows;
+  int64_t num_split_rows;
+};
+rgnn_status launch_aggregate(int prec, int K, int N, bool rgat, const AggArgs& a, cudaStream_t s);
+
+struct BwdArgs {
+  const Item* items;
+  int64_t num_items;
+  const int32_t* pos;
+  const int32_t* et_slot;
+  const void* Z;
+  const float* s_src;
+  const void* X;
+  int64_t v0;
+  const float* U;
+  const float* A;
+  float slope;
+  const float* Y;
+  const float* dY;
+  const float* lse;
+  void* dZ;
+  float* dpre;
+};
+rgnn_status launch_bwd_traverse(int prec, int K, int N, const BwdArgs& a, cudaStream_t s);
+
+// tcgen05 path (gemm_tc.cu): returns RGNN_E_UNSUPPORTED if the shape is not covered.
+rgnn_status launch_gemm_fwd_tc(int K, int N, const GemmFwdArgs& a, cudaStream_t s);
+
+}  // namespace rgnn
+
+#define RGNN_DISPATCH_KN(K, N, ...)                                                        \
+  [&]() -> rgnn_status {                                                                   \
+    switch ((K) * 1000 + (N)) {                                                            \
+      case 32032: { constexpr int kK = 32, kN = 32; return __VA_ARGS__(); }                \
+      case 32064: { constexpr int kK = 32, kN = 64; return __VA_ARGS__(); }                \
+      case 32128: { constexpr int kK = 32, kN = 128; return __VA_ARGS__(); }               \
+      case 64032: { constexpr int kK = 64, kN = 32; return __VA_ARGS__(); }                \
+      case 64064: { constexpr int kK = 64, kN = 64; return __VA_ARGS__(); }                \
+      case 64128: { constexpr int kK = 64, kN = 128; return __VA_ARGS__(); }               \
+      case 128032: { constexpr int kK = 128, kN = 32; return __VA_ARGS__(); }              \
+      case 128064: { constexpr int kK = 128, kN = 64; return __VA_ARGS__(); }              \
+      case 128128: { constexpr int kK = 128, kN = 128; return __VA_ARGS__(); }             \
+      default: return ::rgnn::set_error(RGNN_E_UNSUPPORTED, "d_in=%d d_out=%d not in {32,64,128}", (K), (N)); \
+    }                                                                                      \
+  }()

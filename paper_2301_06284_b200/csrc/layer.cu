@@ -1,0 +1,216 @@
+// layer.cu -- the C-ABI layer entry points: argument checks, workspace
+// carving and the launch sequence of one RGCN / RGAT layer:
+//   RGAT fwd : fold U -> typed GEMM (Z, s_src) -> fused walk (Y, lse) -> merge
+//   RGCN fwd : typed GEMM (Z * 1/c) [-> self-loop GEMM Z0] -> walk -> merge
+//   RGAT bwd : fold U -> backward walk (dZ, dpre) -> dW split-K GEMM -> reduce (dW, dA)
+//   RGCN bwd : dW split-K GEMM gathering G rows by dst with 1/c -> reduce [-> dW0]
+//   then, with a communicator, the NCCL gather of Y / all-reduce of dW, dA, dW0.
+#include "kernels.cuh"
+
+namespace rgnn {
+rgnn_status comm_check_range(const rgnn_comm* c, int64_t v0, int64_t v1);
+rgnn_status comm_gather_rows(rgnn_comm* c, const float* Y_own, int64_t N, float* Y_full, cudaStream_t s);
+rgnn_status comm_allreduce_sum(rgnn_comm* c, float* const* bufs, const size_t* counts, int n, cudaStream_t s);
+
+struct WsLayout {
+  float* U;        // [R, K] fp32 (fold of W_r A[r,1])
+  float* part;     // [num_parts, N+4] split-row partial states
+  void* Z;         // RGCN: [E_own, N] T (RGAT keeps Z in `saved`)
+  void* Z0;        // RGCN self-loop rows [V_own, N] T
+  void* dZ;        // RGAT: [E_own, N] T
+  float* dpre;     // RGAT: [E_own]
+  float* dwpart;   // [num_chunks, K*N + 2K]
+  float* dw0part;  // [n0, K*N + 2K]
+  void* wt;        // tcgen05: bf16 W^T [R, N, K]
+  size_t bytes;
+};
+struct SavedLayout {
+  void* Z;         // RGAT: [E_own, N] T
+  float* s_src;    // RGAT: [E_own]
+  float* lse;      // RGAT: [V_own]
+  size_t bytes;
+};
+
+static size_t elt(int prec) { return prec == RGNN_BF16 ? 2 : 4; }
+static int64_t dw0_chunk_rows(const rgnn_graph* g) {
+  return std::max<int64_t>(kTileRows, (g->V_own / 256 + kTileRows - 1) / kTileRows * kTileRows);
+}
+static int64_t dw0_chunks(const rgnn_graph* g) {
+  int64_t cr = dw0_chunk_rows(g);
+  return (g->V_own + cr - 1) / cr;
+}
+
+static WsLayout ws_layout(const rgnn_graph* g, int model, int K, int N, int prec, void* base) {
+  WsLayout w{};
+  Carver c(base);
+  const size_t e = elt(prec);
+  const int64_t E = std::max<int64_t>(g->E_own, 1);
+  w.U = c.take<float>((size_t)g->R * K);
+  w.part = c.take<float>((size_t)std::max<int64_t>(g->num_parts, 1) * (N + 4));
+  w.wt = c.take<char>(prec == RGNN_BF16 ? (size_t)g->R * K * N * 2 : 1);
+  if (model == RGNN_RGCN) {
+    w.Z = c.take<char>((size_t)E * N * e);
+    w.Z0 = c.take<char>((size_t)std::max<int64_t>(g->V_own, 1) * N * e);
+  } else {
+    w.dZ = c.take<char>((size_t)E * N * e);
+    w.dpre = c.take<float>((size_t)E);
+  }
+  w.dwpart = c.take<float>((size_t)std::max<int64_t>(g->num_chunks, 1) * (K * N + 2 * K));
+  w.dw0part = c.take<float>(model == RGNN_RGCN ? (size_t)std::max<int64_t>(dw0_chunks(g), 1) * (K * N + 2 * K) : 1);
+  w.bytes = c.off;
+  return w;
+}
+
+static SavedLayout saved_layout(const rgnn_graph* g, int model, int N, int prec, void* base) {
+  SavedLayout s{};
+  Carver c(base);
+  if (model == RGNN_RGAT) {
+    s.Z = c.take<char>((size_t)std::max<int64_t>(g->E_own, 1) * N * elt(prec));
+    s.s_src = c.take<float>((size_t)std::max<int64_t>(g->E_own, 1));
+    s.lse = c.take<float>((size_t)std::max<int64_t>(g->V_own, 1));
+  }
+  s.bytes = c.off;
+  return s;
+}
+
+static bool width_ok(int d) { return d == 32 || d == 64 || d == 128; }
+
+static rgnn_status check_common(const rgnn_graph* g, int K, int N, int prec, const void* ws, size_t ws_bytes,
+                                const WsLayout& need) {
+  if (!g) return set_error(RGNN_E_INVALID_ARG, "graph is NULL");
+  if (!width_ok(K) || !width_ok(N)) return set_error(RGNN_E_UNSUPPORTED, "d_in=%d d_out=%d not in {32,64,128}", K, N);
+  if (prec != RGNN_F32 && prec != RGNN_BF16) return set_error(RGNN_E_INVALID_ARG, "bad precision %d", prec);
+  if (!ws) return set_error(RGNN_E_INVALID_ARG, "workspace is NULL");
+  if ((uintptr_t)ws % kAlign) return set_error(RGNN_E_INVALID_ARG, "workspace must be 256B aligned");
+  if (ws_bytes < need.bytes) return set_error(RGNN_E_WORKSPACE, "workspace %zu < required %zu", ws_bytes, need.bytes);
+  return RGNN_OK;
+}
+
+static rgnn_status typed_gemm(int prec, int K, int N, const GemmFwdArgs& a, cudaStream_t s) {
+  if (prec == RGNN_BF16) {
+    rgnn_status st = launch_gemm_fwd_tc(K, N, a, s);
+    if (st != RGNN_E_UNSUPPORTED) return st;
+  }
+  return launch_gemm_fwd(prec, K, N, a, s);
+}
+
+static rgnn_status forward(const rgnn_graph* g, int model, int K, int N, int prec, const void* X, const float* W,
+                           const float* W0, const float* A, float slope, float* Y, void* saved, void* ws,
+                           size_t ws_bytes, rgnn_comm* comm, float* Y_full, void* stream) {
+  const WsLayout need = ws_layout(g, model, K, N, prec, nullptr);
+  RGNN_TRY(check_common(g, K, N, prec, ws, ws_bytes, need));
+  if (!X || !W || !Y || (model == RGNN_RGAT && (!A || !saved)))
+    return set_error(RGNN_E_INVALID_ARG, "X, W, Y (and A, saved for RGAT) must not be NULL");
+  if (comm) RGNN_TRY(comm_check_range(comm, g->v0, g->v0 + g->V_own));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  WsLayout w = ws_layout(g, model, K, N, prec, ws);
+  SavedLayout sv = saved_layout(g, model, N, prec, saved);
+
+  GemmFwdArgs ga{};
+  ga.tiles = g->tiles; ga.num_tiles = g->num_tiles; ga.X = X; ga.gather = g->src_s; ga.W = W; ga.wt_bf16 = w.wt;
+  AggArgs aa{};
+  aa.items = g->items; aa.num_items = g->num_items; aa.pos = g->pos; aa.et_slot = g->et_slot; aa.X = X;
+  aa.v0 = g->v0; aa.slope = slope; aa.Y = Y; aa.part = w.part; aa.split_rows = g->split_rows;
+  aa.num_split_rows = g->num_split_rows;
+  if (model == RGNN_RGAT) {
+    { Phase ph("fold_u", s); RGNN_TRY(launch_fold_u(prec, g->R, K, N, W, A, w.U, s)); }
+    ga.Z = sv.Z; ga.A = A; ga.s_src = sv.s_src;
+    if (g->num_tiles) { Phase ph("gemm_fwd", s); RGNN_TRY(typed_gemm(prec, K, N, ga, s)); }
+    aa.Z = sv.Z; aa.s_src = sv.s_src; aa.U = w.U; aa.lse = sv.lse;
+    { Phase ph("aggregate", s); RGNN_TRY(launch_aggregate(prec, K, N, true, aa, s)); }
+  } else {
+    ga.Z = w.Z; ga.row_scale = g->inv_c;
+    if (g->num_tiles) { Phase ph("gemm_fwd", s); RGNN_TRY(typed_gemm(prec, K, N, ga, s)); }
+    if (W0 && g->V_own > 0) {
+      GemmFwdArgs g0{};
+      g0.rows = g->V_own; g0.X = X; g0.gofs = g->v0; g0.W = W0; g0.Z = w.Z0; g0.wt_bf16 = w.wt;
+      { Phase ph("gemm_self", s); RGNN_TRY(typed_gemm(prec, K, N, g0, s)); }
+      aa.Z0 = w.Z0;
+    }
+    aa.Z = w.Z;
+    { Phase ph("aggregate", s); RGNN_TRY(launch_aggregate(prec, K, N, false, aa, s)); }
+  }
+  if (comm && Y_full) { Phase ph("comm", s); RGNN_TRY(comm_gather_rows(comm, Y, N, Y_full, s)); }
+  return RGNN_OK;
+}
+
+}  // namespace rgnn
+
+using namespace rgnn;
+
+extern "C" {
+
+rgnn_status rgnn_workspace_bytes(const rgnn_graph* g, rgnn_model model, int d_in, int d_out, rgnn_prec prec,
+                                 int training, size_t* ws_bytes, size_t* saved_bytes) {
+  (void)training;
+  if (!g) return set_error(RGNN_E_INVALID_ARG, "graph is NULL");
+  if (!width_ok(d_in) || !width_ok(d_out)) return set_error(RGNN_E_UNSUPPORTED, "widths not in {32,64,128}");
+  if (ws_bytes) *ws_bytes = ws_layout(g, model, d_in, d_out, prec, nullptr).bytes;
+  if (saved_bytes) *saved_bytes = saved_layout(g, model, d_out, prec, nullptr).bytes;
+  return RGNN_OK;
+}
+
+rgnn_status rgcn_forward(const rgnn_graph* g, int d_in, int d_out, rgnn_prec prec, const void* X, const float* W,
+                         const float* W0, float* Y, void* saved, void* ws, size_t ws_bytes, rgnn_comm* comm,
+                         float* Y_full, void* stream) {
+  return forward(g, RGNN_RGCN, d_in, d_out, prec, X, W, W0, nullptr, 0.f, Y, saved, ws, ws_bytes, comm, Y_full,
+                 stream);
+}
+
+rgnn_status rgat_forward(const rgnn_graph* g, int d_in, int d_out, rgnn_prec prec, const void* X, const float* W,
+                         const float* A, float slope, float* Y, void* saved, void* ws, size_t ws_bytes,
+                         rgnn_comm* comm, float* Y_full, void* stream) {
+  return forward(g, RGNN_RGAT, d_in, d_out, prec, X, W, nullptr, A, slope, Y, saved, ws, ws_bytes, comm, Y_full,
+                 stream);
+}
+
+rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, rgnn_prec prec, const void* X,
+                          const float* W, const float* A, float slope, const float* Y, const float* dY,
+                          const void* saved, float* dW, float* dA, float* dW0, float* dX, void* ws, size_t ws_bytes,
+                          rgnn_comm* comm, void* stream) {
+  const WsLayout need = ws_layout(g, model, K, N, prec, nullptr);
+  RGNN_TRY(check_common(g, K, N, prec, ws, ws_bytes, need));
+  if (dX) return set_error(RGNN_E_UNSUPPORTED, "dX is not computed in v1 (NEXT-2)");
+  if (!X || !dY || !dW) return set_error(RGNN_E_INVALID_ARG, "X, dY, dW must not be NULL");
+  if (model == RGNN_RGAT && (!W || !A || !Y || !saved || !dA))
+    return set_error(RGNN_E_INVALID_ARG, "RGAT backward needs W, A, Y, saved and dA");
+  if (comm) RGNN_TRY(comm_check_range(comm, g->v0, g->v0 + g->V_own));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  WsLayout w = ws_layout(g, model, K, N, prec, ws);
+  SavedLayout sv = saved_layout(g, model, N, prec, const_cast<void*>(saved));
+
+  GemmDwArgs da{};
+  da.chunks = g->chunks; da.num_chunks = g->num_chunks; da.X = X; da.gather = g->src_s; da.part = w.dwpart;
+  if (model == RGNN_RGAT) {
+    { Phase ph("fold_u", s); RGNN_TRY(launch_fold_u(prec, g->R, K, N, W, A, w.U, s)); }
+    BwdArgs ba{};
+    ba.items = g->items; ba.num_items = g->num_items; ba.pos = g->pos; ba.et_slot = g->et_slot; ba.Z = sv.Z;
+    ba.s_src = sv.s_src; ba.X = X; ba.v0 = g->v0; ba.U = w.U; ba.A = A; ba.slope = slope; ba.Y = Y; ba.dY = dY;
+    ba.lse = sv.lse; ba.dZ = w.dZ; ba.dpre = w.dpre;
+    { Phase ph("bwd_traverse", s); RGNN_TRY(launch_bwd_traverse(prec, K, N, ba, s)); }
+    da.Bz = w.dZ; da.dpre = w.dpre; da.dst_local = g->dst_s; da.v0 = g->v0;
+    { Phase ph("gemm_dw", s); RGNN_TRY(launch_gemm_dw(prec, K, N, da, s)); }
+    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, A, W, dW, dA, s)); }
+  } else {
+    da.Bg = dY; da.bgather = g->dst_s; da.bscale = g->inv_c;
+    { Phase ph("gemm_dw", s); RGNN_TRY(launch_gemm_dw(prec, K, N, da, s)); }
+    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, nullptr, nullptr, dW, nullptr, s)); }
+    if (dW0) {
+      GemmDwArgs d0{};
+      d0.num_chunks = dw0_chunks(g); d0.rows = g->V_own; d0.chunk_rows = dw0_chunk_rows(g); d0.X = X;
+      d0.gofs = g->v0; d0.Bg = dY; d0.part = w.dw0part;
+      Phase ph("gemm_dw0", s);
+      RGNN_TRY(launch_gemm_dw(prec, K, N, d0, s));
+      RGNN_TRY(launch_dw_reduce(prec, K, N, 1, d0.num_chunks, nullptr, w.dw0part, nullptr, nullptr, dW0, nullptr, s));
+    }
+  }
+  if (comm) {
+    float* bufs[3] = {dW, model == RGNN_RGAT ? dA : nullptr, model == RGNN_RGCN ? dW0 : nullptr};
+    size_t counts[3] = {(size_t)g->R * K * N, (size_t)g->R * 2 * N, (size_t)K * N};
+    Phase ph("comm", s);
+    RGNN_TRY(comm_allreduce_sum(comm, bufs, counts, 3, s));
+  }
+  return RGNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,352 @@
+// traverse.cu -- destination walks over CSR-by-dst (DESIGN.md Sec. 6 "a3", "a4").
+//
+// Forward (fused score + edge softmax + aggregate, no atomics):
+//   The paper's edge loop is rewritten as a dst-node loop over incoming edges
+//   (graph-semantic loop transform, Sec. 3.3.3, Sec. 3.4.2),
+//   per-dst loads are hoisted out of the edge loop, and exp / sum /
+//   divide of Listing 1's edge_softmax are fused with the
+//   attention score and the alpha-weighted aggregation into one
+//   pass with an online (running max) softmax -- exact in real arithmetic
+//   (reading O5).  RGAT score: pre_e = s_src[p] + x_dst . U[r]  where
+//   s_src[p] = A[r,0].Z[p] came from the GEMM epilogue and U[r] = W_r A[r,1]
+//   (linear-operator fusion, Sec. 3.4.1).
+// One warp per work item (a row or a <= cap-edge chunk of a long row).  A Z
+// row is read by L = N*sizeof(T)/16 lanes with 16-byte loads; the warp's
+// G = 32/L lane groups take interleaved edges, each keeps its own online
+// state, and the states are merged in a fixed shuffle tree: deterministic.
+// Split rows write unnormalised partial states; k_merge combines them in slot
+// order.
+//
+// Backward (RGAT): per edge recompute s_e and alpha_e = exp(s_e - lse_v),
+//   dalpha_e = G_v . Z[p],  S_v = G_v . Y_v,
+//   dpre_e = alpha_e (dalpha_e - S_v) leaky'(pre_e),
+//   dZ[p] = alpha_e G_v + dpre_e A[r,0]   (stored in (etype,dst) order), dpre[p].
+#include <math_constants.h>
+
+#include "kernels.cuh"
+
+namespace rgnn {
+
+__device__ __forceinline__ float leaky(float x, float slope) { return x > 0.f ? x : slope * x; }
+
+template <typename T, int K, int N>
+struct WalkShape {
+  static constexpr int EPL = 16 / sizeof(T);  // features per lane (one 16-byte load)
+  static constexpr int L = N / EPL;           // lanes per Z row
+  static constexpr int G = 32 / L;            // edge groups per warp
+  static constexpr int UNR = G >= 4 ? 2 : 4;  // edges per group per step
+  static constexpr int B = G * UNR;           // edges per warp step (<= 32)
+  static constexpr int KPL = K / L;           // x_dst features per lane
+  static_assert(L >= 1 && L <= 32 && B <= 32, "shape");
+  static_assert(K % L == 0, "K must be a multiple of the lane group");
+};
+
+template <int KPL, typename T>
+__device__ __forceinline__ void load_slice(const T* p, float* out) {
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) out[i] = to_f(p[i]);
+}
+
+template <typename T, int K, int N, bool RGAT>
+__global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
+  using S = WalkShape<T, K, N>;
+  constexpr int EPL = S::EPL, L = S::L, G = S::G, UNR = S::UNR, B = S::B, KPL = S::KPL;
+  const T* Z = static_cast<const T*>(a.Z);
+  const T* X = static_cast<const T*>(a.X);
+  const int lane = threadIdx.x & 31, g = lane / L, l = lane % L;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = warp0; w < a.num_items; w += nwarps) {
+    const Item it = a.items[w];
+    float acc[EPL];
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
+    float m = -CUDART_INF_F, lsum = 0.f;
+    float xv[KPL];
+    if constexpr (RGAT) load_slice<KPL>(X + (a.v0 + it.row) * (int64_t)K + l * KPL, xv);
+    for (int base = it.q0; base < it.q1; base += B) {
+      const int q = base + lane;
+      const bool ok = lane < B && q < it.q1;
+      const int myp = ok ? a.pos[q] : 0;
+      const int myr = ok ? a.et_slot[q] : 0;
+      float mys = 0.f;
+      if constexpr (RGAT) mys = ok ? a.s_src[myp] : 0.f;
+      uint4 zr[UNR];
+      float sc[UNR];
+      bool val[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int j = u * G + g;
+        const int p = __shfl_sync(0xffffffffu, myp, j);
+        const int r = __shfl_sync(0xffffffffu, myr, j);
+        const float ss = __shfl_sync(0xffffffffu, mys, j);
+        val[u] = base + j < it.q1;
+        zr[u] = val[u] ? ldg16(Z + (size_t)p * N + l * EPL) : make_uint4(0, 0, 0, 0);
+        if constexpr (RGAT) {
+          const float* Ur = a.U + (size_t)r * K + l * KPL;
+          float d = 0.f;
+#pragma unroll
+          for (int i = 0; i < KPL; ++i) d = fmaf(xv[i], __ldg(Ur + i), d);
+          sc[u] = l == 0 ? d + ss : d;  // lane partial; s_src added once, then reduced
+        }
+      }
+      if constexpr (RGAT) {
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+#pragma unroll
+          for (int o = L / 2; o > 0; o >>= 1) sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
+          sc[u] = val[u] ? leaky(sc[u], a.slope) : -CUDART_INF_F;
+        }
+        float mnew = m;
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) mnew = fmaxf(mnew, sc[u]);
+        if (mnew != -CUDART_INF_F) {
+          const float corr = __expf(m - mnew);  // m = -inf -> 0
+          lsum *= corr;
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) acc[i] *= corr;
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) {
+            const float e = val[u] ? __expf(sc[u] - mnew) : 0.f;
+            lsum += e;
+            float zf[EPL];
+            Vec16<T>{zr[u]}.to_float(zf);
+#pragma unroll
+            for (int i = 0; i < EPL; ++i) acc[i] = fmaf(e, zf[i], acc[i]);
+          }
+          m = mnew;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          float zf[EPL];
+          Vec16<T>{zr[u]}.to_float(zf);
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) acc[i] += zf[i];
+        }
+      }
+    }
+    // merge the G group states (fixed xor tree)
+#pragma unroll
+    for (int o = L; o < 32; o <<= 1) {
+      if constexpr (RGAT) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        const float l2 = __shfl_xor_sync(0xffffffffu, lsum, o);
+        const float mn = fmaxf(m, m2);
+        const float c1 = mn == -CUDART_INF_F ? 0.f : __expf(m - mn);
+        const float c2 = mn == -CUDART_INF_F ? 0.f : __expf(m2 - mn);
+        lsum = lsum * c1 + l2 * c2;
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) {
+          const float a2 = __shfl_xor_sync(0xffffffffu, acc[i], o);
+          acc[i] = acc[i] * c1 + a2 * c2;
+        }
+        m = mn;
+      } else {
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+      }
+    }
+    if (g == 0) {
+      if (it.part < 0) {
+        float* y = a.Y + (size_t)it.row * N + l * EPL;
+        if constexpr (RGAT) {
+          const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) acc[i] *= inv;
+          if (l == 0) a.lse[it.row] = lsum > 0.f ? m + __logf(lsum) : -CUDART_INF_F;
+        } else if (a.Z0) {
+          float z0[EPL];
+          Vec16<T>{ldg16(static_cast<const T*>(a.Z0) + (size_t)it.row * N + l * EPL)}.to_float(z0);
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) acc[i] += z0[i];
+        }
+#pragma unroll
+        for (int i = 0; i < EPL; i += 4) stg16(y + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]),
+                                                                 __float_as_uint(acc[i + 2]), __float_as_uint(acc[i + 3])));
+      } else {
+        float* pp = a.part + (size_t)it.part * (N + 4);
+#pragma unroll
+        for (int i = 0; i < EPL; i += 4) stg16(pp + l * EPL + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]),
+                                                                           __float_as_uint(acc[i + 2]), __float_as_uint(acc[i + 3])));
+        if (l == 0) { pp[N] = m; pp[N + 1] = lsum; }
+      }
+    }
+  }
+}
+
+// Combine the partial states of each split row in slot order (one warp per row).
+template <typename T, int N, bool RGAT>
+__global__ void __launch_bounds__(256) k_merge(AggArgs a) {
+  constexpr int PER = (N + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = warp0; w < a.num_split_rows; w += nwarps) {
+    const SplitRow sr = a.split_rows[w];
+    float acc[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) acc[i] = 0.f;
+    float m = -CUDART_INF_F, lsum = 0.f;
+    if constexpr (RGAT)
+      for (int k = 0; k < sr.nparts; ++k) m = fmaxf(m, a.part[(size_t)(sr.part0 + k) * (N + 4) + N]);
+    for (int k = 0; k < sr.nparts; ++k) {
+      const float* pp = a.part + (size_t)(sr.part0 + k) * (N + 4);
+      float c = 1.f;
+      if constexpr (RGAT) {
+        const float mk = pp[N];
+        c = mk == -CUDART_INF_F ? 0.f : __expf(mk - m);
+        lsum = fmaf(pp[N + 1], c, lsum);
+      }
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int n = lane + 32 * i;
+        if (n < N) acc[i] = fmaf(pp[n], c, acc[i]);
+      }
+    }
+    float* y = a.Y + (size_t)sr.row * N;
+    if constexpr (RGAT) {
+      const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+      if (lane == 0) a.lse[sr.row] = lsum > 0.f ? m + __logf(lsum) : -CUDART_INF_F;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) acc[i] *= inv;
+    } else if (a.Z0) {
+      const T* z0 = static_cast<const T*>(a.Z0) + (size_t)sr.row * N;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int n = lane + 32 * i;
+        if (n < N) acc[i] += to_f(z0[n]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int n = lane + 32 * i;
+      if (n < N) y[n] = acc[i];
+    }
+  }
+}
+
+template <typename T, int K, int N>
+__global__ void __launch_bounds__(256) k_bwd_rgat(BwdArgs a) {
+  using S = WalkShape<T, K, N>;
+  constexpr int EPL = S::EPL, L = S::L, G = S::G, UNR = S::UNR, B = S::B, KPL = S::KPL;
+  const T* Z = static_cast<const T*>(a.Z);
+  const T* X = static_cast<const T*>(a.X);
+  T* dZ = static_cast<T*>(a.dZ);
+  const int lane = threadIdx.x & 31, g = lane / L, l = lane % L;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = warp0; w < a.num_items; w += nwarps) {
+    const Item it = a.items[w];
+    if (it.q1 <= it.q0) continue;
+    float gv[EPL], yv[EPL], xv[KPL];
+    {
+      const float* gp = a.dY + (size_t)it.row * N + l * EPL;
+      const float* yp = a.Y + (size_t)it.row * N + l * EPL;
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) { gv[i] = gp[i]; yv[i] = yp[i]; }
+    }
+    load_slice<KPL>(X + (a.v0 + it.row) * (int64_t)K + l * KPL, xv);
+    float Sv = 0.f;
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) Sv = fmaf(gv[i], yv[i], Sv);
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1) Sv += __shfl_xor_sync(0xffffffffu, Sv, o);
+    const float lse = a.lse[it.row];
+    for (int base = it.q0; base < it.q1; base += B) {
+      const int q = base + lane;
+      const bool ok = lane < B && q < it.q1;
+      const int myp = ok ? a.pos[q] : 0;
+      const int myr = ok ? a.et_slot[q] : 0;
+      const float mys = ok ? a.s_src[myp] : 0.f;
+      uint4 zr[UNR];
+      float sc[UNR], da[UNR];
+      int pp[UNR], rr[UNR];
+      bool val[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int j = u * G + g;
+        pp[u] = __shfl_sync(0xffffffffu, myp, j);
+        rr[u] = __shfl_sync(0xffffffffu, myr, j);
+        const float ss = __shfl_sync(0xffffffffu, mys, j);
+        val[u] = base + j < it.q1;
+        zr[u] = val[u] ? ldg16(Z + (size_t)pp[u] * N + l * EPL) : make_uint4(0, 0, 0, 0);
+        const float* Ur = a.U + (size_t)rr[u] * K + l * KPL;
+        float d = 0.f;
+#pragma unroll
+        for (int i = 0; i < KPL; ++i) d = fmaf(xv[i], __ldg(Ur + i), d);
+        sc[u] = l == 0 ? d + ss : d;
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        float zf[EPL];
+        Vec16<T>{zr[u]}.to_float(zf);
+        float d = 0.f;
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) d = fmaf(gv[i], zf[i], d);
+        da[u] = d;
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+#pragma unroll
+        for (int o = L / 2; o > 0; o >>= 1) {
+          sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
+          da[u] += __shfl_xor_sync(0xffffffffu, da[u], o);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        if (!val[u]) continue;
+        const float pre = sc[u];
+        const float alpha = __expf(leaky(pre, a.slope) - lse);
+        const float dpre = alpha * (da[u] - Sv) * (pre > 0.f ? 1.f : a.slope);
+        const float* A0 = a.A + (size_t)rr[u] * 2 * N + l * EPL;
+        float o[EPL];
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) o[i] = fmaf(alpha, gv[i], dpre * __ldg(A0 + i));
+        Vec16<T> v;
+        v.from_float(o);
+        stg16(dZ + (size_t)pp[u] * N + l * EPL, v.raw);
+        if (l == 0) a.dpre[pp[u]] = dpre;
+      }
+    }
+  }
+}
+
+static unsigned warps_grid(int64_t items) {
+  int64_t blocks = (items + 7) / 8;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 16));
+}
+
+template <typename T, int K, int N>
+static rgnn_status aggregate(bool rgat, const AggArgs& a, cudaStream_t s) {
+  if (a.num_items > 0) {
+    if (rgat) RGNN_LAUNCH((k_aggregate<T, K, N, true>), warps_grid(a.num_items), 256, 0, s, a);
+    else RGNN_LAUNCH((k_aggregate<T, K, N, false>), warps_grid(a.num_items), 256, 0, s, a);
+  }
+  if (a.num_split_rows > 0) {
+    if (rgat) RGNN_LAUNCH((k_merge<T, N, true>), warps_grid(a.num_split_rows), 256, 0, s, a);
+    else RGNN_LAUNCH((k_merge<T, N, false>), warps_grid(a.num_split_rows), 256, 0, s, a);
+  }
+  return RGNN_OK;
+}
+
+rgnn_status launch_aggregate(int prec, int K, int N, bool rgat, const AggArgs& a, cudaStream_t s) {
+  return RGNN_DISPATCH_KN(K, N, [&] {
+    return prec == RGNN_BF16 ? aggregate<__nv_bfloat16, kK, kN>(rgat, a, s) : aggregate<float, kK, kN>(rgat, a, s);
+  });
+}
+
+template <typename T, int K, int N>
+static rgnn_status bwd(const BwdArgs& a, cudaStream_t s) {
+  if (a.num_items > 0) RGNN_LAUNCH((k_bwd_rgat<T, K, N>), warps_grid(a.num_items), 256, 0, s, a);
+  return RGNN_OK;
+}
+
+rgnn_status launch_bwd_traverse(int prec, int K, int N, const BwdArgs& a, cudaStream_t s) {
+  return RGNN_DISPATCH_KN(K, N, [&] {
+    return prec == RGNN_BF16 ? bwd<__nv_bfloat16, kK, kN>(a, s) : bwd<float, kK, kN>(a, s);
+  });
+}
+
+}  // namespace rgnn

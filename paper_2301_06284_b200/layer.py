@@ -1,0 +1,206 @@
+"""Torch-facing wrappers of the C ABI (marshalling only).
+
+PyTorch supplies device memory, streams and process groups; every step of
+the layer runs inside librgnn.so (include/rgnn.h).  Names follow the C entry
+points: ``rgnn_graph_create`` -> :class:`Graph`, ``rgcn_forward``,
+``rgat_forward``, ``rgnn_backward``, ``rgnn_comm_create`` -> :class:`Comm`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _binding as B
+
+PREC = {"f32": B.RGNN_F32, "fp32": B.RGNN_F32, "bf16": B.RGNN_BF16}
+MODEL = {"rgcn": B.RGNN_RGCN, "rgat": B.RGNN_RGAT}
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _dev_i32(a, device) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=torch.int32).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(device)
+
+
+def _prec(p) -> int:
+    return PREC[p] if isinstance(p, str) else int(p)
+
+
+def _model(m) -> int:
+    return MODEL[m] if isinstance(m, str) else int(m)
+
+
+class Graph:
+    """rgnn_graph_create on caller-owned (torch) device storage."""
+
+    def __init__(self, num_nodes: int, src, dst, etype, num_etypes: int, *, row_ptr=None, ntype=None,
+                 num_ntypes: int = 0, norm: int = B.RGNN_NORM_REL_INDEG, edge_norm=None, row_split_cap: int = 0,
+                 dst_begin: int = 0, dst_end: Optional[int] = None, device="cuda", stream=None):
+        self.device = torch.device(device)
+        self.V, self.R = int(num_nodes), int(num_etypes)
+        self.src = _dev_i32(src, self.device)
+        self.etype = _dev_i32(etype, self.device)
+        self.dst = _dev_i32(dst, self.device) if dst is not None else None
+        self.row_ptr_in = _dev_i32(row_ptr, self.device) if row_ptr is not None else None
+        self.ntype = _dev_i32(ntype, self.device) if ntype is not None else None
+        self.edge_norm = (torch.as_tensor(edge_norm, dtype=torch.float32).to(self.device).contiguous()
+                          if edge_norm is not None else None)
+        self.dst_begin = int(dst_begin)
+        self.dst_end = self.V if dst_end is None else int(dst_end)
+        E = int(self.src.shape[0])
+        d = B.rgnn_graph_desc(num_nodes=self.V, num_edges=E, num_etypes=self.R, num_ntypes=int(num_ntypes),
+                              src=_ptr(self.src), dst=_ptr(self.dst), etype=_ptr(self.etype),
+                              row_ptr=_ptr(self.row_ptr_in), ntype=_ptr(self.ntype), edge_norm=_ptr(self.edge_norm),
+                              norm=int(norm), row_split_cap=int(row_split_cap), dst_begin=self.dst_begin,
+                              dst_end=self.dst_end)
+        self._desc = d
+        dev_b, scr_b = C.c_size_t(), C.c_size_t()
+        B.call("rgnn_graph_bytes", C.byref(d), C.byref(dev_b), C.byref(scr_b))
+        self.storage = torch.empty(max(dev_b.value, 256), dtype=torch.uint8, device=self.device)
+        scratch = torch.empty(max(scr_b.value, 256), dtype=torch.uint8, device=self.device)
+        h = C.c_void_p()
+        self._handle = None
+        B.call("rgnn_graph_create", C.byref(d), _ptr(self.storage), dev_b.value, _ptr(scratch), scr_b.value,
+               _stream(stream), C.byref(h))  # SYNC
+        self._handle = h
+        del scratch
+        v = B.rgnn_graph_view()
+        B.call("rgnn_graph_export", h, C.byref(v))
+        self.view = v
+        self.V_own, self.E_own = int(v.V_own), int(v.E_own)
+
+    @property
+    def handle(self):
+        return self._handle
+
+    def __del__(self):
+        if getattr(self, "_handle", None) is not None:
+            B.lib.rgnn_graph_destroy(self._handle)
+            self._handle = None
+
+    def _arr(self, ptr, n, dtype) -> torch.Tensor:
+        off = int(ptr) - self.storage.data_ptr()
+        nbytes = n * torch.tensor([], dtype=dtype).element_size()
+        return self.storage[off:off + nbytes].view(dtype)
+
+    def arrays(self) -> dict:
+        """Preprocessing outputs as torch views into the graph storage (tests)."""
+        v = self.view
+        E, Vo, R = int(v.E_own), int(v.V_own), int(v.R)
+        i32, f32 = torch.int32, torch.float32
+        return {"perm": self._arr(v.perm, E, i32), "src_s": self._arr(v.src_s, E, i32),
+                "dst_s": self._arr(v.dst_s, E, i32), "seg": self._arr(v.seg, R + 1, i32),
+                "row_ptr": self._arr(v.row_ptr, Vo + 1, i32), "pos": self._arr(v.pos, E, i32),
+                "et_slot": self._arr(v.et_slot, E, i32), "inv_c": self._arr(v.inv_c, E, f32),
+                "run_ptr": self._arr(v.run_ptr, int(v.num_runs) + 1, i32), "rseg": self._arr(v.rseg, R + 1, i32)}
+
+
+class Comm:
+    """rgnn_comm_create: NCCL communicator over the dst-range partition `bounds`."""
+
+    def __init__(self, bounds, rank: int, world: int, group=None):
+        import torch.distributed as dist
+        idbuf = (C.c_char * 128)()
+        if rank == 0:
+            B.call("rgnn_comm_unique_id", C.cast(idbuf, C.c_void_p))
+        obj = [bytes(idbuf)]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        idbuf = (C.c_char * 128).from_buffer_copy(obj[0])
+        b = (C.c_int64 * (world + 1))(*[int(x) for x in bounds])
+        h = C.c_void_p()
+        B.call("rgnn_comm_create", C.cast(idbuf, C.c_void_p), world, rank, b, C.byref(h))
+        self._handle = h
+        self.bounds = [int(x) for x in bounds]
+
+    @property
+    def handle(self):
+        return self._handle
+
+    def __del__(self):
+        if getattr(self, "_handle", None) is not None:
+            B.lib.rgnn_comm_destroy(self._handle)
+            self._handle = None
+
+
+def partition_dst(indeg_prefix, nparts: int):
+    """rgnn_partition_dst: balanced dst ranges from the in-degree prefix (host)."""
+    p = np.ascontiguousarray(indeg_prefix, dtype=np.int64)
+    V = p.shape[0] - 1
+    out = np.zeros(nparts + 1, np.int64)
+    B.call("rgnn_partition_dst", V, p.ctypes.data_as(C.POINTER(C.c_int64)), nparts,
+           out.ctypes.data_as(C.POINTER(C.c_int64)))
+    return out
+
+
+class Workspace:
+    """Workspace + saved buffers sized by rgnn_workspace_bytes (reused across calls)."""
+
+    def __init__(self, g: Graph, model, d_in: int, d_out: int, prec, training: bool = True):
+        ws, sv = C.c_size_t(), C.c_size_t()
+        B.call("rgnn_workspace_bytes", g.handle, _model(model), d_in, d_out, _prec(prec), int(training),
+               C.byref(ws), C.byref(sv))
+        self.ws = torch.empty(max(ws.value, 256), dtype=torch.uint8, device=g.device)
+        self.saved = torch.empty(max(sv.value, 256), dtype=torch.uint8, device=g.device)
+        self.key = (_model(model), d_in, d_out, _prec(prec))
+
+
+def _check_x(X: torch.Tensor, prec: int):
+    want = torch.bfloat16 if prec == B.RGNN_BF16 else torch.float32
+    if X.dtype != want or not X.is_contiguous() or not X.is_cuda:
+        raise ValueError(f"X must be a contiguous CUDA {want} tensor")
+
+
+def rgcn_forward(g: Graph, X: torch.Tensor, W: torch.Tensor, W0: Optional[torch.Tensor] = None, *, prec="f32",
+                 ws: Optional[Workspace] = None, Y: Optional[torch.Tensor] = None, comm: Optional[Comm] = None,
+                 Y_full: Optional[torch.Tensor] = None, stream=None):
+    p = _prec(prec)
+    _check_x(X, p)
+    R, K, N = W.shape
+    ws = ws or Workspace(g, "rgcn", K, N, p)
+    Y = Y if Y is not None else torch.empty(g.V_own, N, dtype=torch.float32, device=g.device)
+    B.call("rgcn_forward", g.handle, K, N, p, _ptr(X), _ptr(W), _ptr(W0), _ptr(Y), _ptr(ws.saved), _ptr(ws.ws),
+           ws.ws.numel(), comm.handle if comm else None, _ptr(Y_full), _stream(stream))
+    return Y, ws
+
+
+def rgat_forward(g: Graph, X: torch.Tensor, W: torch.Tensor, A: torch.Tensor, slope: float = 0.2, *, prec="bf16",
+                 ws: Optional[Workspace] = None, Y: Optional[torch.Tensor] = None, comm: Optional[Comm] = None,
+                 Y_full: Optional[torch.Tensor] = None, stream=None):
+    p = _prec(prec)
+    _check_x(X, p)
+    R, K, N = W.shape
+    ws = ws or Workspace(g, "rgat", K, N, p)
+    Y = Y if Y is not None else torch.empty(g.V_own, N, dtype=torch.float32, device=g.device)
+    B.call("rgat_forward", g.handle, K, N, p, _ptr(X), _ptr(W), _ptr(A), float(slope), _ptr(Y), _ptr(ws.saved),
+           _ptr(ws.ws), ws.ws.numel(), comm.handle if comm else None, _ptr(Y_full), _stream(stream))
+    return Y, ws
+
+
+def rgnn_backward(g: Graph, model, X: torch.Tensor, W: torch.Tensor, dY: torch.Tensor, ws: Workspace, *,
+                  A: Optional[torch.Tensor] = None, slope: float = 0.2, Y: Optional[torch.Tensor] = None,
+                  with_w0: bool = False, prec="bf16", comm: Optional[Comm] = None, dW=None, dA=None, dW0=None,
+                  stream=None):
+    p, m = _prec(prec), _model(model)
+    R, K, N = W.shape
+    dW = dW if dW is not None else torch.empty(R, K, N, dtype=torch.float32, device=g.device)
+    if m == B.RGNN_RGAT and dA is None:
+        dA = torch.empty(R, 2, N, dtype=torch.float32, device=g.device)
+    if with_w0 and dW0 is None:
+        dW0 = torch.empty(K, N, dtype=torch.float32, device=g.device)
+    B.call("rgnn_backward", g.handle, m, K, N, p, _ptr(X), _ptr(W), _ptr(A), float(slope), _ptr(Y), _ptr(dY),
+           _ptr(ws.saved), _ptr(dW), _ptr(dA), _ptr(dW0) if with_w0 else None, None, _ptr(ws.ws), ws.ws.numel(),
+           comm.handle if comm else None, _stream(stream))
+    return dW, dA, dW0

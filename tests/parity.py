@@ -1,0 +1,104 @@
+"""Shared helpers of the parity tests: run the CUDA path (through the C ABI)
+and the fp64 oracle on the same seeded inputs and compare.
+
+Tolerances (reading O19, from north_star's "1e-4 rel / 1e-5 abs"
+for fp32 and "2e-2 rel" for bf16):
+  |got - ref| <= atol + rtol |ref| elementwise, and ||got-ref||_F <= rtol ||ref||_F
+  fp32: rtol 1e-4, atol 1e-5 * max(1, rms(ref))
+  bf16: rtol 2e-2, atol 2e-2 * rms(ref)
+"""
+from __future__ import annotations
+
+import numpy as np
+
+TOL = {"f32": (1e-4, 1e-5, True), "bf16": (2e-2, 2e-2, False)}
+
+
+def assert_close(got, ref, prec: str, what: str = ""):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    assert got.shape == ref.shape, (what, got.shape, ref.shape)
+    if ref.size == 0:
+        return
+    rtol, ascale, floor1 = TOL[prec]
+    rms = float(np.sqrt(np.mean(ref * ref)))
+    atol = ascale * (max(1.0, rms) if floor1 else rms)
+    err = np.abs(got - ref)
+    bad = err > atol + rtol * np.abs(ref)
+    if bad.any():
+        i = np.unravel_index(np.argmax(err - (atol + rtol * np.abs(ref))), ref.shape)
+        raise AssertionError(f"{what}: {int(bad.sum())}/{ref.size} elements out of tolerance "
+                             f"(prec {prec}, rtol {rtol}, atol {atol:.3g}); worst at {i}: got {got[i]!r} ref {ref[i]!r}; "
+                             f"max abs err {err.max():.3g}")
+    fro = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300)
+    assert fro <= rtol, f"{what}: relative Frobenius error {fro:.3g} > {rtol}"
+
+
+def run_gpu(m, g, t, model: str, prec: str, *, slope=0.2, with_w0=False, norm=0, edge_norm=None,
+            split_cap=0, dst_range=None, backward=True):
+    """Build the graph and run fwd (+bwd) on the GPU. Returns dict of numpy arrays."""
+    import torch
+    dev = "cuda"
+    v0, v1 = dst_range or (0, g.V)
+    G = m.Graph(g.V, g.src, g.dst, g.etype, g.R, norm=norm, edge_norm=edge_norm, row_split_cap=split_cap,
+                dst_begin=v0, dst_end=v1)
+    Xt = torch.from_numpy(t.X).to(dev)
+    X = Xt.to(torch.bfloat16) if prec == "bf16" else Xt
+    W = torch.from_numpy(t.W).to(dev)
+    A = torch.from_numpy(t.A).to(dev)
+    W0 = torch.from_numpy(t.W0).to(dev) if with_w0 else None
+    dY = torch.from_numpy(np.ascontiguousarray(t.dY[v0:v1])).to(dev)
+    out = {"graph": G}
+    if model == "rgat":
+        Y, ws = m.rgat_forward(G, X, W, A, slope, prec=prec)
+    else:
+        Y, ws = m.rgcn_forward(G, X, W, W0, prec=prec)
+    out["Y"] = Y
+    if backward:
+        dW, dA, dW0 = m.rgnn_backward(G, model, X, W, dY, ws, A=A if model == "rgat" else None, slope=slope, Y=Y,
+                                      with_w0=with_w0, prec=prec)
+        out.update(dW=dW, dA=dA, dW0=dW0)
+    torch.cuda.synchronize()
+    res = {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in out.items() if v is not None}
+    res["ws"] = ws
+    return res
+
+
+def bf16_round(a) -> np.ndarray:
+    """fp32 -> nearest bf16 (round to nearest even), returned as fp32 values (test input prep)."""
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32)
+
+
+def bf16_inputs(t):
+    """The bf16 path's inputs (reading O16): X arrives bf16 and W is rounded to bf16 (RNE); A, dY stay fp32.
+    The oracle evaluates the exact layer of these values in fp64, so the LeakyReLU branch (a float decision)
+    is taken on the same input values by both sides."""
+    import dataclasses
+    return dataclasses.replace(t, X=bf16_round(t.X), W=bf16_round(t.W), W0=bf16_round(t.W0))
+
+
+def run_oracle(oracle, g, t, model: str, *, slope=0.2, with_w0=False, norm=0, edge_norm=None, dst_range=None,
+               backward=True, rels=None, prec="f32"):
+    if prec == "bf16":
+        t = bf16_inputs(t)
+    v0, v1 = dst_range or (0, g.V)
+    rows = np.arange(v0, v1)
+    K, N = t.W.shape[1], t.W.shape[2]
+    G = np.zeros((g.V, N)); G[v0:v1] = t.dY[v0:v1]
+    out = {}
+    if model == "rgat":
+        Y, lse, _ = oracle.rgat_forward(g.V, g.R, g.src, g.dst, g.etype, t.X, t.W, t.A, slope=slope, rows=rows)
+        out["Y"], out["lse"] = Y, lse
+        if backward:
+            out["dW"], out["dA"] = oracle.rgat_backward(g.V, g.R, g.src, g.dst, g.etype, t.X, t.W, t.A, G,
+                                                        slope=slope, v0=v0, v1=v1, rels=rels)
+    else:
+        out["Y"] = oracle.rgcn_forward(g.V, g.R, g.src, g.dst, g.etype, t.X, t.W, t.W0 if with_w0 else None,
+                                       norm=norm, edge_norm=edge_norm, rows=rows)
+        if backward:
+            out["dW"], out["dW0"] = oracle.rgcn_backward(g.V, g.R, g.src, g.dst, g.etype, t.X, G, K, N, norm=norm,
+                                                         edge_norm=edge_norm, with_w0=with_w0, v0=v0, v1=v1,
+                                                         rels=rels)
+    return out
