@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""bench.py -- one RGAT / RGCN layer forward + backward step on B200.
+
+Default workload: BASELINE.json configs[3], the ogbn-mag-shaped heterograph
+(1.94M nodes, 21.1M edges, 4 relations), RGAT, d_in = d_out = 128, bf16
+operands (tcgen05 typed GEMM path), dst-partitioned over the ranks.  A step
+is one full pass of the hot path: RGAT forward (typed GEMM, fused score /
+edge softmax / aggregate) + backward (backward walk, segmented dW GEMM, dW /
+dA), plus -- for N > 1 -- the NCCL gather of Y and all-reduce of dW / dA.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config mag|am|wikikg2|bgs|mutag|aifb]
+                  [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  Inputs are synthetic (synth/, seeded) and
+larger than L2 for the default config (X 497 MB, Z 5.4 GB), so no flush is
+needed between steps.  `--impl reference` times the fp64 CPU oracle on a
+bounded sample of the same workload (rank 0 only; other ranks exit 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "RGAT/RGCN layer fwd+bwd edges/sec"
+UNIT = "edges/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="mag")
+    ap.add_argument("--model", default=None)
+    ap.add_argument("--prec", default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--slope", type=float, default=0.2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time of the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def workload(args):
+    cfg = synth.get_config(args.config)
+    model = args.model or cfg.model
+    prec = args.prec or cfg.prec
+    return cfg, model, prec
+
+
+def config_json(cfg, model, prec, g, world):
+    return {"workload": f"{cfg.name}-shaped heterograph, {model.upper()} layer fwd+bwd, d={cfg.K}",
+            "model": model, "prec": prec, "V": int(g.V), "E": int(g.E), "R": int(g.R), "d_in": cfg.K,
+            "d_out": cfg.N, "seeds": "graph 0, X 1, W 2, A 3, dY 4 (synth/)",
+            "l2": "no flush: per-step inputs larger than L2 (X %.0f MB, Z %.0f MB)" % (
+                g.V * cfg.K * (2 if prec == "bf16" else 4) / 1e6, g.E * cfg.N * (2 if prec == "bf16" else 4) / 1e6),
+            "parallelism": f"dst-range partition x{world} (NCCL Y gather + dW all-reduce)" if world > 1
+            else "1 GPU"}
+
+
+# --------------------------------------------------------------------- algorithmic bytes
+def algorithmic_bytes(phase, model, prec, K, N, E, V_own, J, num_items):
+    """Bytes the method must move per launch of each phase (no L2 reuse assumed)."""
+    b = 2 if prec == "bf16" else 4
+    if phase == "gemm_fwd":  # gather X rows, write Z, read src index (+ s_src write for RGAT, + 1/c read for RGCN)
+        return E * (K * b + N * b + 4 + 4)
+    if phase == "aggregate":  # read pos, et, Z row (+ s_src) per edge; X_dst, Y, lse, item per row
+        per_e = N * b + 8 + (4 if model == "rgat" else 0)
+        per_v = (K * b + N * 4 + 4 + 16) if model == "rgat" else (N * 4 + 16)
+        return E * per_e + num_items * per_v
+    if phase == "bwd_traverse":  # read pos, et, s_src, Z; write dZ, dpre; per row X, Y, dY, lse, item
+        return E * (2 * N * b + 16) + num_items * (K * b + 2 * N * 4 + 4 + 16)
+    if phase == "gemm_dw":  # gather X rows, read dZ (RGAT) or gather G rows (RGCN), indices; dst term per run
+        if model == "rgat":
+            return E * (K * b + N * b + 4 + 4 + 4) + J * K * b
+        return E * (K * b + N * 4 + 4 + 4 + 4)
+    return 0
+
+
+def sample_clocks_start(path):
+    try:
+        return subprocess.Popen(
+            ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+             "--format=csv,noheader,nounits", "-lms", "200"], stdout=open(path, "w"), stderr=subprocess.DEVNULL)
+    except Exception:
+        return None
+
+
+def sample_clocks_stop(proc, path, gpu_index):
+    if proc is None:
+        return None
+    proc.terminate()
+    try:
+        proc.wait(timeout=5)
+    except Exception:
+        proc.kill()
+    sm, mx, reasons = [], 0.0, set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    try:
+        for line in open(path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9 or not f[0].isdigit() or int(f[0]) != gpu_index:
+                continue
+            try:
+                sm.append(float(f[1])); mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+    except FileNotFoundError:
+        return None
+    if not sm:
+        return None
+    load = [x for x in sm if x > 0.5 * mx] or sm
+    return {"sm_mhz": float(np.median(load)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+# --------------------------------------------------------------------- oracle (cpu baseline / reference arm)
+def oracle_sample(g, t, model, K, N, target_s, slope, prec):
+    """Contiguous dst range [a, b) of the same graph sized for ~target_s of oracle fwd+bwd."""
+    import oracle
+    tt = t
+    if prec == "bf16":
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from parity import bf16_inputs
+        tt = bf16_inputs(t)
+    X, W, A = (np.ascontiguousarray(a, dtype=np.float64) for a in (tt.X, tt.W, tt.A))
+    W0 = np.ascontiguousarray(tt.W0, dtype=np.float64)
+    indeg = np.r_[0, np.cumsum(np.bincount(g.dst, minlength=g.V))]
+    a = g.V // 3
+    G = np.zeros((g.V, N))
+
+    def run(ne):
+        b = int(min(g.V, np.searchsorted(indeg, indeg[a] + ne)))
+        b = max(b, a + 1)
+        G[a:b] = t.dY[a:b]
+        t0 = time.perf_counter()
+        if model == "rgat":
+            oracle.rgat_forward(g.V, g.R, g.src, g.dst, g.etype, X, W, A, slope=slope, rows=np.arange(a, b))
+            oracle.rgat_backward(g.V, g.R, g.src, g.dst, g.etype, X, W, A, G, slope=slope, v0=a, v1=b)
+        else:
+            oracle.rgcn_forward(g.V, g.R, g.src, g.dst, g.etype, X, W, None, rows=np.arange(a, b))
+            oracle.rgcn_backward(g.V, g.R, g.src, g.dst, g.etype, X, G, K, N, v0=a, v1=b)
+        dt = time.perf_counter() - t0
+        G[a:b] = 0
+        return int(indeg[b] - indeg[a]), dt, (a, b)
+
+    ne, dt, _ = run(2000)
+    per_edge = max(dt, 1e-3) / max(ne, 1)
+    want = int(max(2000, min(g.E, target_s / per_edge)))
+    return run, want, oracle.num_threads()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg, model, prec = workload(args)
+    g = synth.make_graph(cfg)
+    t = synth.make_tensors(g.V, g.R, cfg.K, cfg.N)
+    per_step = max(1.0, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
+    run, want, cores = oracle_sample(g, t, model, cfg.K, cfg.N, per_step, args.slope, prec)
+    for _ in range(args.warmup):
+        run(want)
+    tot_e, tot_s, rng = 0, 0.0, None
+    for _ in range(args.steps):
+        ne, dt, rng = run(want)
+        tot_e += ne
+        tot_s += dt
+    v = tot_e / tot_s
+    sample = (f"dst rows [{rng[0]},{rng[1]}) of the {cfg.name}-shaped graph ({tot_e // max(args.steps, 1)} in-edges, "
+              f"{model} fwd+bwd in fp64), per step")
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": config_json(cfg, model, prec, g, 1),
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# --------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2301_06284_b200 as m
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg, model, prec = workload(args)
+    K, N = cfg.K, cfg.N
+    t_gen = time.perf_counter()
+    g = synth.make_graph(cfg)
+    t = synth.make_tensors(g.V, g.R, K, N)
+    t_gen = time.perf_counter() - t_gen
+    indeg = np.r_[0, np.cumsum(np.bincount(g.dst, minlength=g.V))]
+    bounds = m.partition_dst(indeg, world)
+    v0, v1 = int(bounds[rank]), int(bounds[rank + 1])
+
+    # preprocessing (timed separately, not part of the step)
+    src = torch.from_numpy(g.src).to(dev); dst = torch.from_numpy(g.dst).to(dev)
+    et = torch.from_numpy(g.etype).to(dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    G = m.Graph(g.V, src, dst, et, g.R, dst_begin=v0, dst_end=v1, device=dev)
+    torch.cuda.synchronize()
+    prep_ms = 1e3 * (time.perf_counter() - t0)
+    del src, dst, et
+
+    xdt = torch.bfloat16 if prec == "bf16" else torch.float32
+    X = torch.from_numpy(t.X).to(dev).to(xdt)
+    W = torch.from_numpy(t.W).to(dev)
+    A = torch.from_numpy(t.A).to(dev)
+    dY = torch.from_numpy(np.ascontiguousarray(t.dY[v0:v1])).to(dev)
+    ws = m.Workspace(G, model, K, N, prec)
+    Y_full = torch.empty(g.V, N, dtype=torch.float32, device=dev) if world > 1 else None
+    Y = Y_full[v0:v1] if world > 1 else torch.empty(v1 - v0, N, dtype=torch.float32, device=dev)
+    dW = torch.empty(g.R, K, N, dtype=torch.float32, device=dev)
+    dA = torch.empty(g.R, 2, N, dtype=torch.float32, device=dev) if model == "rgat" else None
+    comm = m.Comm(bounds, rank, world) if world > 1 else None
+    stream = torch.cuda.current_stream(dev)
+
+    def step(Xs=X, Ws=W, As=A, dYs=dY):
+        if model == "rgat":
+            m.rgat_forward(G, Xs, Ws, As, args.slope, prec=prec, ws=ws, Y=Y, comm=comm, Y_full=Y_full)
+        else:
+            m.rgcn_forward(G, Xs, Ws, prec=prec, ws=ws, Y=Y, comm=comm, Y_full=Y_full)
+        m.rgnn_backward(G, model, Xs, Ws, dYs, ws, A=As if model == "rgat" else None, slope=args.slope, Y=Y,
+                        prec=prec, comm=comm, dW=dW, dA=dA)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3) if args.warmup >= 3 else args.warmup):
+        step()
+    barrier()
+    clk_path = os.path.join("/tmp", f"rgnn_clocks_{os.getpid()}.csv")
+    clk = sample_clocks_start(clk_path) if local == 0 or world == 1 else None
+    time.sleep(0.3 if clk else 0)
+    m._binding.profile_enable(True)
+    m._binding.profile_read()
+    l0 = m.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    launches = m.launch_count() - l0
+    phases = m._binding.profile_read()
+    m._binding.profile_enable(False)
+    clocks = sample_clocks_stop(clk, clk_path, local)
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        tm = torch.tensor([ms], device=dev)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        ms = float(tm.item())
+    value = g.E / (ms * 1e-3)
+
+    # ---- end to end through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hX = t.X.astype(np.float32)
+        hX = torch.from_numpy(hX).to(xdt).pin_memory()
+        hW = torch.from_numpy(t.W).pin_memory(); hA = torch.from_numpy(t.A).pin_memory()
+        hdY = torch.from_numpy(np.ascontiguousarray(t.dY[v0:v1])).pin_memory()
+        oY = torch.empty(v1 - v0, N, dtype=torch.float32).pin_memory()
+        odW = torch.empty(g.R, K, N, dtype=torch.float32).pin_memory()
+        odA = torch.empty(g.R, 2, N, dtype=torch.float32).pin_memory() if dA is not None else None
+        dX_, dW_, dA_, ddY = torch.empty_like(X), torch.empty_like(W), torch.empty_like(A), torch.empty_like(dY)
+        h2d = hX.numel() * hX.element_size() + hW.numel() * 4 + hA.numel() * 4 + hdY.numel() * 4
+        d2h = oY.numel() * 4 + odW.numel() * 4 + (odA.numel() * 4 if odA is not None else 0)
+        n_e2e = max(1, min(args.steps, 5))
+
+        def e2e_step():
+            dX_.copy_(hX, non_blocking=True); dW_.copy_(hW, non_blocking=True)
+            dA_.copy_(hA, non_blocking=True); ddY.copy_(hdY, non_blocking=True)
+            step(dX_, dW_, dA_, ddY)
+            oY.copy_(Y, non_blocking=True); odW.copy_(dW, non_blocking=True)
+            if odA is not None:
+                odA.copy_(dA, non_blocking=True)
+            torch.cuda.current_stream().synchronize()  # the host reads the result every step
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            e2e_step()
+        barrier()
+        ems = 1e3 * (time.perf_counter() - t0) / n_e2e
+        if world > 1:
+            tm = torch.tensor([ems], device=dev)
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+            ems = float(tm.item())
+        e2e = {"value": g.E / (ems * 1e-3), "unit": UNIT, "ms_per_step": ems, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": n_e2e}
+
+    # ---- roofline of the dominant kernel phase (live CUDA-event durations from the timed region)
+    hbm, tflops, peak_src = peaks()
+    v = G.view
+    step_phase = {k: (tot / args.steps, n // max(args.steps, 1)) for k, (tot, n) in phases.items()}
+    cand = {k: x for k, x in step_phase.items() if k in ("gemm_fwd", "aggregate", "bwd_traverse", "gemm_dw")}
+    roof = None
+    if cand:
+        dom = max(cand, key=lambda k: cand[k][0])
+        per_launch_ms = phases[dom][0] / max(phases[dom][1], 1)
+        byts = algorithmic_bytes(dom, model, prec, K, N, int(v.E_own), int(v.V_own), int(v.num_runs),
+                                 int(v.num_items))
+        ach = byts / (per_launch_ms * 1e-3) / 1e9
+        traffic = None
+        try:
+            tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+            traffic = tj.get(f"{cfg.name}:{model}:{prec}:{dom}")
+        except Exception:
+            pass
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": traffic, "algorithmic_bytes_per_launch": int(byts), "launch_ms": per_launch_ms,
+                "peak_source": peak_src}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        run, want, cores = oracle_sample(g, t, model, K, N, args.cpu_seconds, args.slope, prec)
+        ne, dt, rng = run(want)
+        cpu = {"value": ne / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"dst rows [{rng[0]},{rng[1]}) ({ne} in-edges) of the same graph, {model} fwd+bwd fp64, "
+                         f"{dt:.1f} s"}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": prec, "data": "synthetic (seeded generator, random-init weights)",
+               "config": config_json(cfg, model, prec, g, world), "clocks": clocks, "e2e": e2e,
+               "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu,
+               "phases_ms_per_step": {k: round(x[0], 4) for k, x in sorted(step_phase.items())},
+               "preprocess_ms": prep_ms, "generate_s": round(t_gen, 1)}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
