@@ -1,7 +1,321 @@
-// gemm_tc.cu -- tcgen05 typed grouped GEMM (placeholder until the tensor-core
-// kernel lands; the SIMT kernel in gemm_simt.cu serves every shape meanwhile).
+// gemm_tc.cu -- typed grouped GEMM on the 5th-generation tensor cores (bf16 path).
+//
+//   Z[p, :] = X[src_s[p], :] . W_{r(p)}      for every 128-row tile (r, row0, row1)
+//
+// Segment MM (Sec. 2.2): tiles never straddle relations, one
+// bf16 copy of W_r per relation (never replicated per edge), X rows
+// gathered on load (the GEMM template's gather list) with TMA
+// tile::gather4, accumulators in TMEM, epilogue fused: RGAT source score
+// s_src[p] = A[r,0] . Z_fp32[p] and RGCN per-row 1/c ("per-row
+// scalar ... applied to A tiles"), bf16 Z written through an XOR-swizzled smem
+// stage with coalesced 16-byte stores (rows beyond row1 are never written).
+//
+// Persistent, warp specialised, one CTA per SM:
+//   warp 0   TMA producer: W_r into a 2-slot ring (reloaded only when r changes),
+//            X rows by gather4 into an S-stage ring (each lane issues one gather4)
+//   warp 1   TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=d_out,
+//            K-steps of 16), commits to the smem-empty / accumulator-full barriers
+//   warps 2-5 epilogue: tcgen05.ld (32 lanes x 16 columns) -> fp32 math -> bf16
+// TMEM holds two accumulators (tile i+1's MMAs overlap tile i's epilogue).
+#include <cudaTypedefs.h>
+
 #include "kernels.cuh"
+#include "tc_common.cuh"
 
 namespace rgnn {
-rgnn_status launch_gemm_fwd_tc(int, int, const GemmFwdArgs&, cudaStream_t) { return RGNN_E_UNSUPPORTED; }
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+rgnn_status make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch_bytes,
+                              uint32_t box_cols, uint32_t box_rows, int swizzle_bytes) {
+  auto fn = encode_fn();
+  if (!fn) return set_error(RGNN_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch_bytes};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                          : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(RGNN_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return RGNN_OK;
+}
+
+// W [R, K, N] fp32 -> Wt [R, N, K] bf16 (RNE): the K-major B operand.
+__global__ void k_w_to_bf16_t(int R, int K, int N, const float* __restrict__ W, __nv_bfloat16* __restrict__ Wt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)R * K * N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int r = (int)(i / ((int64_t)K * N));
+    int rem = (int)(i - (int64_t)r * K * N);
+    int n = rem / K, k = rem - n * K;
+    Wt[i] = __float2bfloat16_rn(W[((size_t)r * K + k) * N + n]);
+  }
+}
+
+template <int K, int N>
+struct FwdCfg {
+  static constexpr int M = 128;
+  static constexpr int RB = (K * 2 < 128) ? K * 2 : 128;    // bytes per row of one swizzle block
+  static constexpr int KBLK = (K * 2) / RB;                 // column blocks
+  static constexpr int SWZ = RB;                            // 64 or 128 byte swizzle
+  static constexpr uint32_t LAYOUT = RB == 128 ? 2u : 4u;   // UMMA layout type
+  static constexpr int A_BYTES = M * K * 2;
+  static constexpr int B_BYTES = N * K * 2;
+  static constexpr int STAGES = (96 * 1024) / A_BYTES > 8 ? 8 : (96 * 1024) / A_BYTES;
+  static constexpr int STG_BYTES = M * N * 2;
+  static constexpr int NCOLS = (2 * N) <= 32 ? 32 : (2 * N) <= 64 ? 64 : (2 * N) <= 128 ? 128 : 256;
+  static constexpr int SMEM = 1024 + STAGES * A_BYTES + 2 * B_BYTES + STG_BYTES + 256;
+  static constexpr int THREADS = 192;
+  static constexpr uint32_t IDESC = tc::idesc_bf16(128, N, 0, 0);
+};
+
+struct TcFwdParams {
+  const Tile* tiles;
+  int64_t num_tiles, rows, gofs;
+  const int32_t* gather;
+  __nv_bfloat16* Z;
+  const float* row_scale;
+  const float* A;
+  float* s_src;
+};
+
+template <int K, int N>
+__global__ void __launch_bounds__(192, 1)
+    k_gemm_fwd_tc(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap, TcFwdParams pr) {
+  using C = FwdCfg<K, N>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + C::STAGES * C::A_BYTES;
+  uint8_t* sStg = sB + 2 * C::B_BYTES;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sStg + C::STG_BYTES);
+  uint64_t* a_full = bar;
+  uint64_t* a_empty = a_full + C::STAGES;
+  uint64_t* b_full = a_empty + C::STAGES;
+  uint64_t* b_empty = b_full + 2;
+  uint64_t* acc_full = b_empty + 2;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = pr.tiles ? pr.num_tiles : (pr.rows + C::M - 1) / C::M;
+  const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * per, t1 = min(ntiles, t0 + per);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::STAGES; ++i) { tc::mbar_init(&a_full[i], 1); tc::mbar_init(&a_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&b_full[i], 1); tc::mbar_init(&b_empty[i], 1);
+      tc::mbar_init(&acc_full[i], 1); tc::mbar_init(&acc_empty[i], 4);
+    }
+    tc::mbar_fence_init();
+    tc::tma_prefetch_desc(&xmap);
+    tc::tma_prefetch_desc(&wmap);
+  }
+  if (warp == 1) tc::tmem_alloc<C::NCOLS>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto tile_of = [&](int64_t t, int& r, int& row0, int& row1) {
+    if (pr.tiles) { Tile tl = pr.tiles[t]; r = tl.r; row0 = tl.row0; row1 = tl.row1; }
+    else { r = 0; row0 = (int)(t * C::M); row1 = (int)min(pr.rows, (int64_t)row0 + C::M); }
+  };
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    int cur_r = -1, bslot = 1;
+    uint32_t buse[2] = {0, 0};
+    int64_t it = 0;
+    for (int64_t t = t0; t < t1; ++t, ++it) {
+      int r, row0, row1;
+      tile_of(t, r, row0, row1);
+      if (r != cur_r) {
+        bslot ^= 1;
+        if (buse[bslot] > 0) tc::mbar_wait(&b_empty[bslot], (buse[bslot] - 1) & 1);
+        ++buse[bslot];
+        if (lane == 0) {
+          tc::mbar_expect_tx(&b_full[bslot], C::B_BYTES);
+#pragma unroll
+          for (int kb = 0; kb < C::KBLK; ++kb)
+            tc::tma_load_2d(sB + bslot * C::B_BYTES + kb * N * C::RB, &wmap, &b_full[bslot], kb * (C::RB / 2), r * N);
+        }
+        cur_r = r;
+      }
+      const int stage = (int)(it % C::STAGES);
+      const uint32_t use = (uint32_t)(it / C::STAGES);
+      if (use > 0) tc::mbar_wait(&a_empty[stage], (use - 1) & 1);
+      // lane l gathers rows 4l .. 4l+3 of the tile (rows past row1 re-read a valid row, never stored)
+      int idx[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int p = min(row0 + 4 * lane + j, row1 - 1);
+        idx[j] = pr.gather ? __ldg(pr.gather + p) : (int)(pr.gofs + p);
+      }
+      if (lane == 0) tc::mbar_expect_tx(&a_full[stage], C::A_BYTES);
+      __syncwarp();
+      uint8_t* dstA = sA + stage * C::A_BYTES;
+#pragma unroll
+      for (int kb = 0; kb < C::KBLK; ++kb)
+        tc::tma_gather4(dstA + kb * C::M * C::RB + lane * 4 * C::RB, &xmap, &a_full[stage], kb * (C::RB / 2), idx[0],
+                        idx[1], idx[2], idx[3]);
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    int cur_r = -1, bslot = 1;
+    uint32_t buse[2] = {0, 0};
+    int64_t it = 0;
+    for (int64_t t = t0; t < t1; ++t, ++it) {
+      int r, row0, row1;
+      tile_of(t, r, row0, row1);
+      if (r != cur_r) {
+        if (cur_r >= 0 && lane == 0) tc::umma_commit(&b_empty[bslot]);  // old slot free once its MMAs finish
+        bslot ^= 1;
+        tc::mbar_wait(&b_full[bslot], buse[bslot] & 1);
+        ++buse[bslot];
+        cur_r = r;
+      }
+      const int stage = (int)(it % C::STAGES);
+      const uint32_t use = (uint32_t)(it / C::STAGES);
+      const int acc = (int)(it & 1);
+      const uint32_t ause = (uint32_t)(it >> 1);
+      tc::mbar_wait(&a_full[stage], use & 1);
+      if (ause > 0) tc::mbar_wait(&acc_empty[acc], (ause - 1) & 1);
+      tc::tc_fence_after();
+      if (lane == 0) {
+        const uint32_t a0 = tc::smem_u32(sA + stage * C::A_BYTES);
+        const uint32_t b0 = tc::smem_u32(sB + bslot * C::B_BYTES);
+        const uint32_t d = tmem + acc * N;
+#pragma unroll
+        for (int ks = 0; ks < K / 16; ++ks) {
+          const int kb = (ks * 32) / C::RB, off = (ks * 32) % C::RB;
+          const uint64_t ad = tc::umma_desc(a0 + kb * C::M * C::RB + off, 16, 8 * C::RB, C::LAYOUT);
+          const uint64_t bd = tc::umma_desc(b0 + kb * N * C::RB + off, 16, 8 * C::RB, C::LAYOUT);
+          tc::umma_bf16(d, ad, bd, C::IDESC, ks > 0 ? 1u : 0u);
+        }
+        tc::umma_commit(&a_empty[stage]);
+        tc::umma_commit(&acc_full[acc]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue (warps 2..5)
+    const int q = warp & 3;                 // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;          // tile row owned by this thread
+    const int et = threadIdx.x - 64;        // 0..127
+    constexpr int NCH = N / 8;              // 16-byte chunks per Z row
+    constexpr int SWM = (NCH < 8 ? NCH : 8) - 1;
+    int64_t it = 0;
+    for (int64_t t = t0; t < t1; ++t, ++it) {
+      int r, row0, row1;
+      tile_of(t, r, row0, row1);
+      const int acc = (int)(it & 1);
+      tc::mbar_wait(&acc_full[acc], (uint32_t)(it >> 1) & 1);
+      tc::tc_fence_after();
+      const int p = row0 + row;
+      const bool valid = p < row1;
+      const float scale = (pr.row_scale && valid) ? __ldg(pr.row_scale + p) : 1.f;
+      const float* A0 = pr.A ? pr.A + (size_t)r * 2 * N : nullptr;
+      float sdot = 0.f;
+      tc::named_bar(1, 128);  // previous tile's copy-out finished reading the stage
+      uint8_t* srow = sStg + row * (N * 2);
+#pragma unroll
+      for (int c0 = 0; c0 < N; c0 += 16) {
+        uint32_t v[16];
+        tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * N + c0, v);
+        tc::tmem_ld_wait();
+        float f[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
+        if (A0) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) sdot = fmaf(f[j], __ldg(A0 + c0 + j), sdot);
+        }
+        uint4 w0, w1;
+        w0.x = tc::pack_bf16(f[0] * scale, f[1] * scale); w0.y = tc::pack_bf16(f[2] * scale, f[3] * scale);
+        w0.z = tc::pack_bf16(f[4] * scale, f[5] * scale); w0.w = tc::pack_bf16(f[6] * scale, f[7] * scale);
+        w1.x = tc::pack_bf16(f[8] * scale, f[9] * scale); w1.y = tc::pack_bf16(f[10] * scale, f[11] * scale);
+        w1.z = tc::pack_bf16(f[12] * scale, f[13] * scale); w1.w = tc::pack_bf16(f[14] * scale, f[15] * scale);
+        const int ch = c0 / 8;
+        *reinterpret_cast<uint4*>(srow + (((ch) ^ (row & SWM)) * 16)) = w0;
+        *reinterpret_cast<uint4*>(srow + (((ch + 1) ^ (row & SWM)) * 16)) = w1;
+      }
+      // accumulator drained: hand it back to the MMA warp
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&acc_empty[acc]);
+      if (pr.s_src && valid) pr.s_src[p] = sdot;
+      tc::named_bar(1, 128);
+      // coalesced copy-out of the valid rows
+      const int nvalid = row1 - row0;
+      for (int i = et; i < C::M * NCH; i += 128) {
+        const int rr = i / NCH, ch = i - rr * NCH;
+        if (rr < nvalid) {
+          uint4 val = *reinterpret_cast<const uint4*>(sStg + rr * (N * 2) + ((ch ^ (rr & SWM)) * 16));
+          *reinterpret_cast<uint4*>(pr.Z + (size_t)(row0 + rr) * N + ch * 8) = val;
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<C::NCOLS>(tmem);
+  }
+}
+
+template <int K, int N>
+static rgnn_status gemm_fwd_tc(const GemmFwdArgs& a, cudaStream_t s) {
+  using C = FwdCfg<K, N>;
+  const int64_t ntiles = a.tiles ? a.num_tiles : (a.rows + C::M - 1) / C::M;
+  if (ntiles == 0) return RGNN_OK;
+  auto* wt = static_cast<__nv_bfloat16*>(a.wt_bf16);
+  const int64_t nw = (int64_t)a.num_w * K * N;
+  RGNN_LAUNCH(k_w_to_bf16_t, (unsigned)std::max<int64_t>(1, std::min<int64_t>((nw + 255) / 256, 4096)), 256, 0, s,
+              a.num_w, K, N, a.W, wt);
+  CUtensorMap xmap, wmap;
+  RGNN_TRY(make_tmap_2d_bf16(&xmap, a.X, K, (uint64_t)a.x_rows, K * 2, C::RB / 2, 1, C::SWZ));
+  RGNN_TRY(make_tmap_2d_bf16(&wmap, wt, K, (uint64_t)a.num_w * N, K * 2, C::RB / 2, N, C::SWZ));
+  auto kern = k_gemm_fwd_tc<K, N>;
+  RGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  int dev, sms;
+  RGNN_CUDA_TRY(cudaGetDevice(&dev));
+  RGNN_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  TcFwdParams pr{a.tiles, a.num_tiles, a.rows, a.gofs, a.gather, static_cast<__nv_bfloat16*>(a.Z), a.row_scale, a.A,
+                 a.s_src};
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, sms);
+  RGNN_LAUNCH(kern, grid, C::THREADS, C::SMEM, s, xmap, wmap, pr);
+  return RGNN_OK;
+}
+
+bool tc_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RGNN_DISABLE_TCGEN05");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+rgnn_status launch_gemm_fwd_tc(int K, int N, const GemmFwdArgs& a, cudaStream_t s) {
+  if (tc_disabled()) return RGNN_E_UNSUPPORTED;
+  return RGNN_DISPATCH_KN(K, N, [&] { return gemm_fwd_tc<kK, kN>(a, s); });
+}
+
 }  // namespace rgnn

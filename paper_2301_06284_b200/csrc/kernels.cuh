@@ -20,7 +20,9 @@ struct GemmFwdArgs {
   const float* row_scale;   // [rows] or null
   const float* A;           // [R, 2, N] or null
   float* s_src;             // [rows] (with A)
-  void* wt_bf16;            // workspace for the tcgen05 path: [R, N, K] bf16 (transposed W)
+  void* wt_bf16;            // workspace for the tcgen05 path: [num_w, N, K] bf16 (transposed W)
+  int num_w;                // number of weight matrices in W (R, or 1 for the self-loop W0)
+  int64_t x_rows;           // rows of X (V)
 };
 
 // dW split-K GEMM over chunks (DESIGN.md Sec. 6 "a5"):

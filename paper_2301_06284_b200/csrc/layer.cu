@@ -108,6 +108,7 @@ static rgnn_status forward(const rgnn_graph* g, int model, int K, int N, int pre
 
   GemmFwdArgs ga{};
   ga.tiles = g->tiles; ga.num_tiles = g->num_tiles; ga.X = X; ga.gather = g->src_s; ga.W = W; ga.wt_bf16 = w.wt;
+  ga.num_w = g->R; ga.x_rows = g->V;
   AggArgs aa{};
   aa.items = g->items; aa.num_items = g->num_items; aa.pos = g->pos; aa.et_slot = g->et_slot; aa.X = X;
   aa.v0 = g->v0; aa.slope = slope; aa.Y = Y; aa.part = w.part; aa.split_rows = g->split_rows;
@@ -124,6 +125,7 @@ static rgnn_status forward(const rgnn_graph* g, int model, int K, int N, int pre
     if (W0 && g->V_own > 0) {
       GemmFwdArgs g0{};
       g0.rows = g->V_own; g0.X = X; g0.gofs = g->v0; g0.W = W0; g0.Z = w.Z0; g0.wt_bf16 = w.wt;
+      g0.num_w = 1; g0.x_rows = g->V;
       { Phase ph("gemm_self", s); RGNN_TRY(typed_gemm(prec, K, N, g0, s)); }
       aa.Z0 = w.Z0;
     }
