@@ -97,14 +97,14 @@ __global__ void __launch_bounds__(256) k_gemm_fwd_simt(GemmFwdArgs a) {
 
 // -------------------------------------------------------------- dW split-K
 // part[c] (K x N) = sum over rows p of chunk c of X[g(p)]^T B[p]; 32-row
-// sub-tiles staged in smem; a thread owns a K/16 x N/16 block.  Threads
-// [0,K) also accumulate bvec = sum dpre X_src, threads [K,2K) cvec = sum dpre X_dst.
+// sub-tiles staged in smem; a thread owns a K/16 x N/16 block.  For RGAT,
+// threads [0,K) also accumulate bvec = sum dpre X_src (the dst term lives in
+// dst_term.cu).  part row stride = K*N + K.
 template <typename T, int K, int N, bool RGAT>
 __global__ void __launch_bounds__(256) k_gemm_dw_simt(GemmDwArgs a) {
   constexpr int KB = K / 16, NB = N / 16, SR = (K + N >= 192) ? 16 : 32;
   __shared__ float Xs[SR][K + 1];
   __shared__ float Bs[SR][N + 1];
-  __shared__ float Xd[RGAT ? SR : 1][K + 1];
   __shared__ float Dp[SR];
   const T* X = static_cast<const T*>(a.X);
   const T* Bz = static_cast<const T*>(a.Bz);
@@ -123,14 +123,12 @@ __global__ void __launch_bounds__(256) k_gemm_dw_simt(GemmDwArgs a) {
       __syncthreads();
       for (int i = tid; i < SR * K; i += 256) {
         int rr = i / K, k = i - rr * K, p = s0 + rr;
-        float x = 0.f, xd = 0.f;
+        float x = 0.f;
         if (p < row1) {
           int64_t xr = a.gather ? (int64_t)a.gather[p] : a.gofs + p;
           x = to_f(X[xr * K + k]);
-          if constexpr (RGAT) xd = to_f(X[(a.v0 + a.dst_local[p]) * K + k]);
         }
         Xs[rr][k] = x;
-        if constexpr (RGAT) Xd[rr][k] = xd;
       }
       for (int i = tid; i < SR * N; i += 256) {
         int rr = i / N, n = i - rr * N, p = s0 + rr;
@@ -160,53 +158,57 @@ __global__ void __launch_bounds__(256) k_gemm_dw_simt(GemmDwArgs a) {
           for (int j = 0; j < NB; ++j) acc[i][j] = fmaf(xa[i], bb[j], acc[i][j]);
       }
       if constexpr (RGAT) {
-        if (tid < K) {
+        if (tid < K)
           for (int rr = 0; rr < SR; ++rr) vacc = fmaf(Dp[rr], Xs[rr][tid], vacc);
-        } else if (tid < 2 * K) {
-          for (int rr = 0; rr < SR; ++rr) vacc = fmaf(Dp[rr], Xd[rr][tid - K], vacc);
-        }
       }
     }
-    float* out = a.part + (size_t)c * (K * N + 2 * K);
+    float* out = a.part + (size_t)c * (K * N + K);
 #pragma unroll
     for (int i = 0; i < KB; ++i)
 #pragma unroll
       for (int j = 0; j < NB; ++j) out[(ky * KB + i) * N + cx * NB + j] = acc[i][j];
-    if (tid < 2 * K) out[K * N + tid] = RGAT ? vacc : 0.f;
+    if (tid < K) out[K * N + tid] = RGAT ? vacc : 0.f;
   }
 }
 
-// dW[r] = sum_c part[c] (+ (sum_c cvec_c) (x) A[r,1] for RGAT), chunks of r in order.
+// dW[r] = sum_c part[c] (+ (sum_c cpart[c]) (x) A[r,1] for RGAT), chunks of r in order.
 __global__ void k_dw_reduce(int K, int N, int R, int64_t num_chunks, const int32_t* __restrict__ chunk_seg,
-                            const float* __restrict__ part, const float* __restrict__ A, float* __restrict__ dW) {
+                            const float* __restrict__ part, const int32_t* __restrict__ cseg,
+                            const float* __restrict__ cpart, const float* __restrict__ A, float* __restrict__ dW) {
   const int64_t total = (int64_t)R * K * N;
-  const int stride = K * N + 2 * K;
+  const int stride = K * N + K;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     int r = (int)(i / (K * N));
     int kn = (int)(i - (int64_t)r * K * N);
     int k = kn / N, n = kn - k * N;
     int c0 = chunk_seg ? chunk_seg[r] : 0, c1 = chunk_seg ? chunk_seg[r + 1] : (int)num_chunks;
-    float s = 0.f, cv = 0.f;
-    for (int c = c0; c < c1; ++c) {
-      s += part[(size_t)c * stride + kn];
-      if (A) cv += part[(size_t)c * stride + K * N + K + k];
+    float s = 0.f;
+    for (int c = c0; c < c1; ++c) s += part[(size_t)c * stride + kn];
+    if (A) {
+      float cv = 0.f;
+      for (int c = cseg[r]; c < cseg[r + 1]; ++c) cv += cpart[(size_t)c * K + k];
+      s = fmaf(cv, A[(size_t)r * 2 * N + N + n], s);
     }
-    if (A) s = fmaf(cv, A[(size_t)r * 2 * N + N + n], s);
     dW[i] = s;
   }
 }
 
-// dA[r,0,n] = (sum_c bvec_c) . W_r[:,n];  dA[r,1,n] = (sum_c cvec_c) . W_r[:,n]
+// dA[r,0,n] = (sum_c bvec_c) . W_r[:,n];  dA[r,1,n] = (sum_rc cpart_rc) . W_r[:,n]
 __global__ void k_da(int K, int N, int R, const int32_t* __restrict__ chunk_seg, const float* __restrict__ part,
+                     const int32_t* __restrict__ cseg, const float* __restrict__ cpart,
                      const float* __restrict__ W, float* __restrict__ dA, int round_bf16) {
-  const int stride = K * N + 2 * K;
+  const int stride = K * N + K;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)R * 2 * N;
        i += (int64_t)gridDim.x * blockDim.x) {
     int r = (int)(i / (2 * N)), h = (int)((i / N) % 2), n = (int)(i % N);
     float s = 0.f;
     for (int k = 0; k < K; ++k) {
       float v = 0.f;
-      for (int c = chunk_seg[r]; c < chunk_seg[r + 1]; ++c) v += part[(size_t)c * stride + K * N + h * K + k];
+      if (h == 0) {
+        for (int c = chunk_seg[r]; c < chunk_seg[r + 1]; ++c) v += part[(size_t)c * stride + K * N + k];
+      } else {
+        for (int c = cseg[r]; c < cseg[r + 1]; ++c) v += cpart[(size_t)c * K + k];
+      }
       float w = W[((size_t)r * K + k) * N + n];
       if (round_bf16) w = __bfloat162float(__float2bfloat16_rn(w));
       s = fmaf(v, w, s);
@@ -271,13 +273,14 @@ rgnn_status launch_gemm_dw(int prec, int K, int N, const GemmDwArgs& a, cudaStre
 }
 
 rgnn_status launch_dw_reduce(int prec, int K, int N, int R, int64_t num_chunks, const int32_t* chunk_seg,
-                             const float* part, const float* A, const float* W, float* dW, float* dA, cudaStream_t s) {
+                             const float* part, const int32_t* cseg, const float* cpart, const float* A,
+                             const float* W, float* dW, float* dA, cudaStream_t s) {
   int64_t total = (int64_t)R * K * N;
   unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16));
-  RGNN_LAUNCH(k_dw_reduce, grid, 256, 0, s, K, N, R, num_chunks, chunk_seg, part, A, dW);
+  RGNN_LAUNCH(k_dw_reduce, grid, 256, 0, s, K, N, R, num_chunks, chunk_seg, part, cseg, cpart, A, dW);
   if (dA) {
     unsigned g2 = (unsigned)std::max<int64_t>(1, ((int64_t)R * 2 * N + 127) / 128);
-    RGNN_LAUNCH(k_da, g2, 128, 0, s, K, N, R, chunk_seg, part, W, dA, prec == RGNN_BF16 ? 1 : 0);
+    RGNN_LAUNCH(k_da, g2, 128, 0, s, K, N, R, chunk_seg, part, cseg, cpart, W, dA, prec == RGNN_BF16 ? 1 : 0);
   }
   return RGNN_OK;
 }

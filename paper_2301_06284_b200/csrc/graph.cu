@@ -71,8 +71,7 @@ __global__ void k_own_scatter(int64_t E, const int32_t* __restrict__ dst, const 
 __global__ void k_after_sort(int64_t n, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
                              const int32_t* __restrict__ src, int64_t V_own, int32_t* __restrict__ perm,
                              int32_t* __restrict__ src_s, int32_t* __restrict__ dst_s, int32_t* __restrict__ et_s,
-                             int32_t* __restrict__ head, int32_t* __restrict__ seg_cnt,
-                             int32_t* __restrict__ row_cnt) {
+                             int32_t* __restrict__ head) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
     uint32_t k = keys[p];
     int32_t e = (int32_t)vals[p];
@@ -83,8 +82,17 @@ __global__ void k_after_sort(int64_t n, const uint32_t* __restrict__ keys, const
     dst_s[p] = i;
     et_s[p] = r;
     head[p] = (p == 0 || keys[p - 1] != k) ? 1 : 0;
-    atomicAdd(&seg_cnt[r], 1);  // integer counts: order independent, deterministic
-    atomicAdd(&row_cnt[i], 1);
+  }
+}
+
+// Bin boundaries of a sorted key array: out[b] = first index q with key[q] >= b,
+// for b in [0, nbins]  (segment offsets / CSR row pointers without atomics).
+template <typename KeyT>
+__global__ void k_bounds(int64_t n, const KeyT* __restrict__ key, int64_t nbins, int32_t* __restrict__ out) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q <= n; q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t kp = q > 0 ? (int64_t)key[q - 1] : -1;
+    int64_t kc = q < n ? (int64_t)key[q] : nbins;
+    for (int64_t b = kp + 1; b <= kc; ++b) out[b] = (int32_t)q;
   }
 }
 
@@ -112,14 +120,17 @@ __global__ void k_slots(int64_t n, const uint32_t* __restrict__ sorted_pos, cons
 
 // Runs of equal (etype, dst): run_ptr[j] = first position of run j.
 __global__ void k_runs(int64_t n, const int32_t* __restrict__ head, const int32_t* __restrict__ run_ex,
-                       const int32_t* __restrict__ et_s, int32_t* __restrict__ run_ptr,
-                       int32_t* __restrict__ rseg_cnt) {
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-    if (head[p]) {
-      run_ptr[run_ex[p]] = (int32_t)p;
-      atomicAdd(&rseg_cnt[et_s[p]], 1);
-    }
-  }
+                       int32_t* __restrict__ run_ptr) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+    if (head[p]) run_ptr[run_ex[p]] = (int32_t)p;
+}
+
+// Runs are in position order and relation r starts at seg[r] with a new run, so
+// rseg[r] = number of runs before position seg[r].
+__global__ void k_rseg(int32_t R, int64_t n, const int32_t* __restrict__ seg, const int32_t* __restrict__ run_ex,
+                       const Counters* c, int32_t* __restrict__ rseg) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r <= R; r += gridDim.x * blockDim.x)
+    rseg[r] = seg[r] < n ? run_ex[seg[r]] : c->J;
 }
 
 __global__ void k_run_end(const Counters* c, int32_t* run_ptr) { run_ptr[c->J] = c->E_own; }
@@ -202,7 +213,7 @@ struct GraphLayout {
   size_t prim_bytes, scratch_bytes;
 };
 
-static int64_t max_chunks(int64_t E, int32_t R) { return 1024 + R; }
+static int64_t max_chunks(int64_t E, int32_t R) { (void)E; return 8 * 1024 + 2 * (int64_t)R; }
 
 static GraphLayout layout(const rgnn_graph_desc* d, void* dev, void* scr) {
   GraphLayout L{};
@@ -339,26 +350,24 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   RGNN_TRY(radix_sort_pairs(L.k0, L.v0, L.k1, L.v1, n, kbits, L.prim, L.prim_bytes, s, &alt));
   uint32_t* keys = alt ? L.k1 : L.k0;
   uint32_t* vals = alt ? L.v1 : L.v0;
-  RGNN_CUDA_TRY(cudaMemsetAsync(L.rseg_cnt, 0, sizeof(int32_t) * (R + 1), s));
-  RGNN_CUDA_TRY(cudaMemsetAsync(L.seg, 0, sizeof(int32_t) * (R + 1), s));
-  RGNN_CUDA_TRY(cudaMemsetAsync(L.row_ptr, 0, sizeof(int32_t) * (V_own + 1), s));
   if (n > 0)
     RGNN_LAUNCH(k_after_sort, grid_for(n), T, 0, s, n, keys, vals, d->src, V_own, L.perm, L.src_s, L.dst_s, L.et_s,
-                L.head, L.seg, L.row_ptr);
-  RGNN_TRY(scan_exclusive(L.seg, L.seg, R + 1, nullptr, L.prim, L.prim_bytes, s));
-  RGNN_TRY(scan_exclusive(L.row_ptr, L.row_ptr, V_own + 1, nullptr, L.prim, L.prim_bytes, s));
+                L.head);
+  RGNN_LAUNCH(k_bounds<int32_t>, grid_for(n + 1), T, 0, s, n, L.et_s, (int64_t)R, L.seg);
   // CSR-by-dst: stable sort of positions by local dst -> ascending p within a row.
   if (n > 0) {
     RGNN_LAUNCH(k_iota_keys, grid_for(n), T, 0, s, n, L.dst_s, L.k0, L.v0);
     RGNN_TRY(radix_sort_pairs(L.k0, L.v0, L.k1, L.v1, n, bits_for((uint64_t)(V_own > 0 ? V_own - 1 : 0)), L.prim,
                               L.prim_bytes, s, &alt));
     RGNN_LAUNCH(k_slots, grid_for(n), T, 0, s, n, alt ? L.v1 : L.v0, L.et_s, L.pos, L.et_slot);
+    RGNN_LAUNCH(k_bounds<uint32_t>, grid_for(n + 1), T, 0, s, n, alt ? L.k1 : L.k0, V_own, L.row_ptr);
     // (etype, dst) runs
     RGNN_TRY(scan_exclusive(L.head, L.run_ex, n, &L.ctr->J, L.prim, L.prim_bytes, s));
-    RGNN_LAUNCH(k_runs, grid_for(n), T, 0, s, n, L.head, L.run_ex, L.et_s, L.run_ptr, L.rseg_cnt);
+    RGNN_LAUNCH(k_runs, grid_for(n), T, 0, s, n, L.head, L.run_ex, L.run_ptr);
   }
+  if (n == 0) RGNN_LAUNCH(k_bounds<int32_t>, grid_for(V_own + 1), T, 0, s, (int64_t)0, L.et_s, V_own, L.row_ptr);
   RGNN_LAUNCH(k_run_end, 1, 1, 0, s, L.ctr, L.run_ptr);
-  RGNN_TRY(scan_exclusive(L.rseg_cnt, L.rseg, R + 1, nullptr, L.prim, L.prim_bytes, s));
+  RGNN_LAUNCH(k_rseg, (unsigned)((R + 256) / 256), 256, 0, s, R, n, L.seg, L.run_ex, L.ctr, L.rseg);
   if (n > 0)
     RGNN_LAUNCH(k_inv_c, grid_for(n), T, 0, s, n, d->norm, L.head, L.run_ex, L.run_ptr, L.perm, d->edge_norm,
                 L.inv_c);
@@ -376,11 +385,15 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   RGNN_CUDA_TRY(cudaMemcpyAsync(&h, L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
   RGNN_CUDA_TRY(cudaMemcpyAsync(seg_h.data(), L.seg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
   RGNN_CUDA_TRY(cudaStreamSynchronize(s));
+  int dev_id = 0, sms = 148;
+  RGNN_CUDA_TRY(cudaGetDevice(&dev_id));
+  RGNN_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev_id));
 
   // Host: 128-row GEMM tiles and dW split-K chunks, never straddling relations.
+  // dW chunks: about two per SM (split-K), multiples of the 128-row tile.
   std::vector<Tile> tiles, chunks;
   std::vector<int32_t> chunk_seg(R + 1, 0);
-  int64_t chunk_rows = std::max<int64_t>(kTileRows, ((n / 512) + kTileRows - 1) / kTileRows * kTileRows);
+  int64_t chunk_rows = std::max<int64_t>(kTileRows, ((n / (2 * sms) + 1) + kTileRows - 1) / kTileRows * kTileRows);
   for (int32_t r = 0; r < R; ++r) {
     for (int64_t a = seg_h[r]; a < seg_h[r + 1]; a += kTileRows)
       tiles.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + kTileRows, seg_h[r + 1]), 0});
@@ -389,7 +402,8 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
       chunks.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + chunk_rows, seg_h[r + 1]), 0});
   }
   chunk_seg[R] = (int32_t)chunks.size();
-  if ((int64_t)chunks.size() > max_chunks(E, R)) return set_error(RGNN_E_CUDA, "internal: chunk table overflow");
+  if ((int64_t)chunks.size() > max_chunks(E, R))
+    return set_error(RGNN_E_CUDA, "internal: chunk table overflow");
   if (!tiles.empty())
     RGNN_CUDA_TRY(cudaMemcpyAsync(L.tiles, tiles.data(), sizeof(Tile) * tiles.size(), cudaMemcpyHostToDevice, s));
   if (!chunks.empty())

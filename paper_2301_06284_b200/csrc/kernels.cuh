@@ -27,7 +27,7 @@ struct GemmFwdArgs {
 
 // dW split-K GEMM over chunks (DESIGN.md Sec. 6 "a5"):
 //   part[c] = sum_{p in chunk c} X[gather(p)]^T B[p]   (K x N)
-//   RGAT extras: bvec = sum dpre_p X[src_p], cvec = sum dpre_p X[dst_p]  (K each)
+//   RGAT extra: bvec = sum dpre_p X[src_p] (K); part row stride K*N + K
 // B rows: dZ[p] (T), or (bgather) G[bgather[p]] * bscale[p] (fp32).
 struct GemmDwArgs {
   const Tile* chunks;       // [num_chunks] or null: chunk c = rows [c*chunk_rows, ...) of [0, rows)
@@ -42,13 +42,17 @@ struct GemmDwArgs {
   const float* dpre;        // RGAT: [rows] or null
   const int32_t* dst_local; // RGAT: local dst of row p
   int64_t v0;
-  float* part;              // [num_chunks, K*N + 2K]
+  float* part;              // [num_chunks, K*N + K]
+  int64_t x_rows;           // rows of X (tensor map bound, tcgen05 path)
 };
 
 rgnn_status launch_gemm_fwd(int prec, int K, int N, const GemmFwdArgs& a, cudaStream_t s);
 rgnn_status launch_gemm_dw(int prec, int K, int N, const GemmDwArgs& a, cudaStream_t s);
 rgnn_status launch_dw_reduce(int prec, int K, int N, int R, int64_t num_chunks, const int32_t* chunk_seg,
-                             const float* part, const float* A, const float* W, float* dW, float* dA, cudaStream_t s);
+                             const float* part, const int32_t* cseg, const float* cpart, const float* A,
+                             const float* W, float* dW, float* dA, cudaStream_t s);
+rgnn_status launch_dst_term(int prec, int K, const rgnn_graph* g, const float* dpre, const void* X, float* cpart,
+                            cudaStream_t s);
 rgnn_status launch_fold_u(int prec, int R, int K, int N, const float* W, const float* A, float* U, cudaStream_t s);
 
 struct AggArgs {
@@ -93,6 +97,9 @@ rgnn_status launch_bwd_traverse(int prec, int K, int N, const BwdArgs& a, cudaSt
 
 // tcgen05 path (gemm_tc.cu): returns RGNN_E_UNSUPPORTED if the shape is not covered.
 rgnn_status launch_gemm_fwd_tc(int K, int N, const GemmFwdArgs& a, cudaStream_t s);
+rgnn_status launch_gemm_dw_tc(int K, int N, const GemmDwArgs& a, cudaStream_t s);
+rgnn_status launch_expand_dz(int64_t E, int N, const int32_t* dst_s, const float* inv_c, const float* G, void* dZ,
+                             cudaStream_t s);
 
 }  // namespace rgnn
 

@@ -19,8 +19,9 @@ struct WsLayout {
   void* Z0;        // RGCN self-loop rows [V_own, N] T
   void* dZ;        // RGAT: [E_own, N] T
   float* dpre;     // RGAT: [E_own]
-  float* dwpart;   // [num_chunks, K*N + 2K]
-  float* dw0part;  // [n0, K*N + 2K]
+  float* dwpart;   // [num_chunks, K*N + K]
+  float* dw0part;  // [n0, K*N + K]
+  float* cpart;    // RGAT dst term: [num_chunks, K]
   void* wt;        // tcgen05: bf16 W^T [R, N, K]
   size_t bytes;
 };
@@ -33,7 +34,7 @@ struct SavedLayout {
 
 static size_t elt(int prec) { return prec == RGNN_BF16 ? 2 : 4; }
 static int64_t dw0_chunk_rows(const rgnn_graph* g) {
-  return std::max<int64_t>(kTileRows, (g->V_own / 256 + kTileRows - 1) / kTileRows * kTileRows);
+  return std::max<int64_t>(kTileRows, (g->V_own / (2 * g->num_sms) + kTileRows) / kTileRows * kTileRows);
 }
 static int64_t dw0_chunks(const rgnn_graph* g) {
   int64_t cr = dw0_chunk_rows(g);
@@ -55,8 +56,9 @@ static WsLayout ws_layout(const rgnn_graph* g, int model, int K, int N, int prec
     w.dZ = c.take<char>((size_t)E * N * e);
     w.dpre = c.take<float>((size_t)E);
   }
-  w.dwpart = c.take<float>((size_t)std::max<int64_t>(g->num_chunks, 1) * (K * N + 2 * K));
-  w.dw0part = c.take<float>(model == RGNN_RGCN ? (size_t)std::max<int64_t>(dw0_chunks(g), 1) * (K * N + 2 * K) : 1);
+  w.dwpart = c.take<float>((size_t)std::max<int64_t>(g->num_chunks, 1) * (K * N + K));
+  w.dw0part = c.take<float>(model == RGNN_RGCN ? (size_t)std::max<int64_t>(dw0_chunks(g), 1) * (K * N + K) : 1);
+  w.cpart = c.take<float>((size_t)std::max<int64_t>(g->num_chunks, 1) * K);
   w.bytes = c.off;
   return w;
 }
@@ -182,7 +184,16 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
   SavedLayout sv = saved_layout(g, model, N, prec, const_cast<void*>(saved));
 
   GemmDwArgs da{};
-  da.chunks = g->chunks; da.num_chunks = g->num_chunks; da.X = X; da.gather = g->src_s; da.part = w.dwpart;
+  da.chunks = g->chunks; da.num_chunks = g->num_chunks; da.rows = g->E_own; da.X = X; da.gather = g->src_s;
+  da.part = w.dwpart; da.x_rows = g->V;
+  const bool tc_ok = prec == RGNN_BF16 && K >= 64;  // tcgen05 dW needs UMMA M = d_in in {64, 128}
+  auto dw_gemm = [&](const GemmDwArgs& args) -> rgnn_status {
+    if (tc_ok && args.Bz) {
+      rgnn_status st = launch_gemm_dw_tc(K, N, args, s);
+      if (st != RGNN_E_UNSUPPORTED) return st;
+    }
+    return launch_gemm_dw(prec, K, N, args, s);
+  };
   if (model == RGNN_RGAT) {
     { Phase ph("fold_u", s); RGNN_TRY(launch_fold_u(prec, g->R, K, N, W, A, w.U, s)); }
     BwdArgs ba{};
@@ -190,20 +201,32 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     ba.s_src = sv.s_src; ba.X = X; ba.v0 = g->v0; ba.U = w.U; ba.A = A; ba.slope = slope; ba.Y = Y; ba.dY = dY;
     ba.lse = sv.lse; ba.dZ = w.dZ; ba.dpre = w.dpre;
     { Phase ph("bwd_traverse", s); RGNN_TRY(launch_bwd_traverse(prec, K, N, ba, s)); }
+    { Phase ph("dst_term", s); RGNN_TRY(launch_dst_term(prec, K, g, w.dpre, X, w.cpart, s)); }
     da.Bz = w.dZ; da.dpre = w.dpre; da.dst_local = g->dst_s; da.v0 = g->v0;
-    { Phase ph("gemm_dw", s); RGNN_TRY(launch_gemm_dw(prec, K, N, da, s)); }
-    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, A, W, dW, dA, s)); }
+    { Phase ph("gemm_dw", s); RGNN_TRY(dw_gemm(da)); }
+    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, g->chunk_seg, w.cpart, A, W, dW, dA, s)); }
   } else {
-    da.Bg = dY; da.bgather = g->dst_s; da.bscale = g->inv_c;
-    { Phase ph("gemm_dw", s); RGNN_TRY(launch_gemm_dw(prec, K, N, da, s)); }
-    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, nullptr, nullptr, dW, nullptr, s)); }
+    if (tc_ok) {  // dZ[p] = bf16(1/c * G[dst]) materialised in position order, then the tensor-core dW
+      { Phase ph("expand_dz", s); RGNN_TRY(launch_expand_dz(g->E_own, N, g->dst_s, g->inv_c, dY, w.Z, s)); }
+      da.Bz = w.Z;
+    } else {
+      da.Bg = dY; da.bgather = g->dst_s; da.bscale = g->inv_c;
+    }
+    { Phase ph("gemm_dw", s); RGNN_TRY(dw_gemm(da)); }
+    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, nullptr, nullptr, nullptr, nullptr, dW, nullptr, s)); }
     if (dW0) {
+      Phase ph("gemm_dw0", s);
       GemmDwArgs d0{};
       d0.num_chunks = dw0_chunks(g); d0.rows = g->V_own; d0.chunk_rows = dw0_chunk_rows(g); d0.X = X;
-      d0.gofs = g->v0; d0.Bg = dY; d0.part = w.dw0part;
-      Phase ph("gemm_dw0", s);
-      RGNN_TRY(launch_gemm_dw(prec, K, N, d0, s));
-      RGNN_TRY(launch_dw_reduce(prec, K, N, 1, d0.num_chunks, nullptr, w.dw0part, nullptr, nullptr, dW0, nullptr, s));
+      d0.gofs = g->v0; d0.part = w.dw0part; d0.x_rows = g->V;
+      if (tc_ok) {
+        RGNN_TRY(launch_expand_dz(g->V_own, N, nullptr, nullptr, dY, w.Z0, s));
+        d0.Bz = w.Z0;
+      } else {
+        d0.Bg = dY;
+      }
+      RGNN_TRY(dw_gemm(d0));
+      RGNN_TRY(launch_dw_reduce(prec, K, N, 1, d0.num_chunks, nullptr, w.dw0part, nullptr, nullptr, nullptr, nullptr, dW0, nullptr, s));
     }
   }
   if (comm) {
