@@ -168,9 +168,12 @@ def oracle_sample(g, t, model, K, N, target_s, slope, prec):
         G[a:b] = 0
         return int(indeg[b] - indeg[a]), dt, (a, b)
 
-    ne, dt, _ = run(2000)
-    per_edge = max(dt, 1e-3) / max(ne, 1)
-    want = int(max(2000, min(g.E, target_s / per_edge)))
+    # two-point fit t(n) = a + b n (a = the O(E) in-list build and fixed costs)
+    n1, t1, _ = run(2000)
+    n2, t2, _ = run(40000)
+    slope_t = max((t2 - t1) / max(n2 - n1, 1), 1e-9)
+    fixed_t = max(t1 - slope_t * n1, 0.0)
+    want = int(max(2000, min(g.E, (target_s - fixed_t) / slope_t)))
     return run, want, oracle.num_threads()
 
 

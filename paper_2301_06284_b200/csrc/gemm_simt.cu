@@ -193,25 +193,35 @@ __global__ void k_dw_reduce(int K, int N, int R, int64_t num_chunks, const int32
   }
 }
 
-// dA[r,0,n] = (sum_c bvec_c) . W_r[:,n];  dA[r,1,n] = (sum_rc cpart_rc) . W_r[:,n]
-__global__ void k_da(int K, int N, int R, const int32_t* __restrict__ chunk_seg, const float* __restrict__ part,
-                     const int32_t* __restrict__ cseg, const float* __restrict__ cpart,
-                     const float* __restrict__ W, float* __restrict__ dA, int round_bf16) {
+// Per-relation sums of the dA vectors: vsum[r][0][k] = sum_c bvec_c[k], vsum[r][1][k] = sum_c cpart_c[k].
+__global__ void k_da_vsum(int K, int N, int R, const int32_t* __restrict__ chunk_seg, const float* __restrict__ part,
+                          const int32_t* __restrict__ cseg, const float* __restrict__ cpart, float* __restrict__ vsum) {
   const int stride = K * N + K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)R * 2 * K;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / (2 * K)), h = (int)((i / K) % 2), k = (int)(i % K);
+    float v = 0.f;
+    if (h == 0) {
+      for (int c = chunk_seg[r]; c < chunk_seg[r + 1]; ++c) v += part[(size_t)c * stride + K * N + k];
+    } else {
+      for (int c = cseg[r]; c < cseg[r + 1]; ++c) v += cpart[(size_t)c * K + k];
+    }
+    vsum[i] = v;
+  }
+}
+
+// dA[r,h,n] = vsum[r][h] . W_r[:,n]  (h = 0: sum dpre x_src, h = 1: sum dpre x_dst)
+__global__ void k_da(int K, int N, int R, const float* __restrict__ vsum, const float* __restrict__ W,
+                     float* __restrict__ dA, int round_bf16) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)R * 2 * N;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int r = (int)(i / (2 * N)), h = (int)((i / N) % 2), n = (int)(i % N);
+    const int r = (int)(i / (2 * N)), h = (int)((i / N) % 2), n = (int)(i % N);
+    const float* v = vsum + ((size_t)r * 2 + h) * K;
     float s = 0.f;
     for (int k = 0; k < K; ++k) {
-      float v = 0.f;
-      if (h == 0) {
-        for (int c = chunk_seg[r]; c < chunk_seg[r + 1]; ++c) v += part[(size_t)c * stride + K * N + k];
-      } else {
-        for (int c = cseg[r]; c < cseg[r + 1]; ++c) v += cpart[(size_t)c * K + k];
-      }
       float w = W[((size_t)r * K + k) * N + n];
       if (round_bf16) w = __bfloat162float(__float2bfloat16_rn(w));
-      s = fmaf(v, w, s);
+      s = fmaf(v[k], w, s);
     }
     dA[i] = s;
   }
@@ -274,13 +284,16 @@ rgnn_status launch_gemm_dw(int prec, int K, int N, const GemmDwArgs& a, cudaStre
 
 rgnn_status launch_dw_reduce(int prec, int K, int N, int R, int64_t num_chunks, const int32_t* chunk_seg,
                              const float* part, const int32_t* cseg, const float* cpart, const float* A,
-                             const float* W, float* dW, float* dA, cudaStream_t s) {
+                             const float* W, float* dW, float* dA, float* dA_scratch, cudaStream_t s) {
   int64_t total = (int64_t)R * K * N;
   unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16));
   RGNN_LAUNCH(k_dw_reduce, grid, 256, 0, s, K, N, R, num_chunks, chunk_seg, part, cseg, cpart, A, dW);
   if (dA) {
+    float* vsum = dA_scratch;
+    unsigned g1 = (unsigned)std::max<int64_t>(1, ((int64_t)R * 2 * K + 127) / 128);
+    RGNN_LAUNCH(k_da_vsum, g1, 128, 0, s, K, N, R, chunk_seg, part, cseg, cpart, vsum);
     unsigned g2 = (unsigned)std::max<int64_t>(1, ((int64_t)R * 2 * N + 127) / 128);
-    RGNN_LAUNCH(k_da, g2, 128, 0, s, K, N, R, chunk_seg, part, cseg, cpart, W, dA, prec == RGNN_BF16 ? 1 : 0);
+    RGNN_LAUNCH(k_da, g2, 128, 0, s, K, N, R, vsum, W, dA, prec == RGNN_BF16 ? 1 : 0);
   }
   return RGNN_OK;
 }

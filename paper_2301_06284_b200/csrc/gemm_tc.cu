@@ -77,8 +77,11 @@ struct FwdCfg {
   static constexpr int B_BYTES = N * K * 2;
   static constexpr int STAGES = (96 * 1024) / A_BYTES > 8 ? 8 : (96 * 1024) / A_BYTES;
   static constexpr int STG_BYTES = M * N * 2;
+  static constexpr int ORB = (N * 2 < 128) ? N * 2 : 128;   // Z staging: bytes per row of one swizzle block
+  static constexpr int ONB = (N * 2) / ORB;                 // Z column blocks (TMA store boxes)
+  static constexpr int OCPB = ORB / 16;                     // 16-byte chunks per block row
   static constexpr int NCOLS = (2 * N) <= 32 ? 32 : (2 * N) <= 64 ? 64 : (2 * N) <= 128 ? 128 : 256;
-  static constexpr int SMEM = 1024 + STAGES * A_BYTES + 2 * B_BYTES + STG_BYTES + 256;
+  static constexpr int SMEM = 1024 + STAGES * A_BYTES + 2 * B_BYTES + STG_BYTES + N * 4 + 256;
   static constexpr int THREADS = 192;
   static constexpr uint32_t IDESC = tc::idesc_bf16(128, N, 0, 0);
 };
@@ -88,6 +91,7 @@ struct TcFwdParams {
   int64_t num_tiles, rows, gofs;
   const int32_t* gather;
   __nv_bfloat16* Z;
+  int64_t z_rows;
   const float* row_scale;
   const float* A;
   float* s_src;
@@ -95,14 +99,16 @@ struct TcFwdParams {
 
 template <int K, int N>
 __global__ void __launch_bounds__(192, 1)
-    k_gemm_fwd_tc(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap, TcFwdParams pr) {
+    k_gemm_fwd_tc(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
+                  const __grid_constant__ CUtensorMap zmap, TcFwdParams pr) {
   using C = FwdCfg<K, N>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = sA + C::STAGES * C::A_BYTES;
   uint8_t* sStg = sB + 2 * C::B_BYTES;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sStg + C::STG_BYTES);
+  float* sA0 = reinterpret_cast<float*>(sStg + C::STG_BYTES);  // A[r,0] of the current relation
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sA0 + N);
   uint64_t* a_full = bar;
   uint64_t* a_empty = a_full + C::STAGES;
   uint64_t* b_full = a_empty + C::STAGES;
@@ -125,6 +131,7 @@ __global__ void __launch_bounds__(192, 1)
     tc::mbar_fence_init();
     tc::tma_prefetch_desc(&xmap);
     tc::tma_prefetch_desc(&wmap);
+    tc::tma_prefetch_desc(&zmap);
   }
   if (warp == 1) tc::tmem_alloc<C::NCOLS>(tmem_slot);
   tc::tc_fence_before();
@@ -142,9 +149,23 @@ __global__ void __launch_bounds__(192, 1)
     int cur_r = -1, bslot = 1;
     uint32_t buse[2] = {0, 0};
     int64_t it = 0;
+    // gather indices of the next tile are loaded one tile ahead (hides their latency)
+    int idx[4] = {0, 0, 0, 0};
+    auto load_idx = [&](int64_t t, int* out) {
+      int r, row0, row1;
+      tile_of(t, r, row0, row1);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int p = min(row0 + 4 * lane + j, row1 - 1);  // rows past row1 re-read a valid row, never stored
+        out[j] = pr.gather ? __ldg(pr.gather + p) : (int)(pr.gofs + p);
+      }
+    };
+    if (t0 < t1) load_idx(t0, idx);
     for (int64_t t = t0; t < t1; ++t, ++it) {
       int r, row0, row1;
       tile_of(t, r, row0, row1);
+      int nidx[4] = {0, 0, 0, 0};
+      if (t + 1 < t1) load_idx(t + 1, nidx);
       if (r != cur_r) {
         bslot ^= 1;
         if (buse[bslot] > 0) tc::mbar_wait(&b_empty[bslot], (buse[bslot] - 1) & 1);
@@ -160,13 +181,6 @@ __global__ void __launch_bounds__(192, 1)
       const int stage = (int)(it % C::STAGES);
       const uint32_t use = (uint32_t)(it / C::STAGES);
       if (use > 0) tc::mbar_wait(&a_empty[stage], (use - 1) & 1);
-      // lane l gathers rows 4l .. 4l+3 of the tile (rows past row1 re-read a valid row, never stored)
-      int idx[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        int p = min(row0 + 4 * lane + j, row1 - 1);
-        idx[j] = pr.gather ? __ldg(pr.gather + p) : (int)(pr.gofs + p);
-      }
       if (lane == 0) tc::mbar_expect_tx(&a_full[stage], C::A_BYTES);
       __syncwarp();
       uint8_t* dstA = sA + stage * C::A_BYTES;
@@ -174,6 +188,8 @@ __global__ void __launch_bounds__(192, 1)
       for (int kb = 0; kb < C::KBLK; ++kb)
         tc::tma_gather4(dstA + kb * C::M * C::RB + lane * 4 * C::RB, &xmap, &a_full[stage], kb * (C::RB / 2), idx[0],
                         idx[1], idx[2], idx[3]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) idx[j] = nidx[j];
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
@@ -218,22 +234,29 @@ __global__ void __launch_bounds__(192, 1)
     const int q = warp & 3;                 // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;          // tile row owned by this thread
     const int et = threadIdx.x - 64;        // 0..127
-    constexpr int NCH = N / 8;              // 16-byte chunks per Z row
-    constexpr int SWM = (NCH < 8 ? NCH : 8) - 1;
+    // Z staging = ONB column blocks of [128 rows x ORB bytes], swizzled like the TMA store map
+    auto stg_off = [&](int rr, int ch) -> int {
+      const int nb = ch / C::OCPB, c = ch % C::OCPB;
+      const int phys = C::ORB == 128 ? (c ^ (rr & 7)) : C::ORB == 64 ? (c ^ ((rr >> 1) & 3)) : (c ^ ((rr >> 2) & 1));
+      return nb * C::M * C::ORB + rr * C::ORB + phys * 16;
+    };
+    int cur_r = -1;
     int64_t it = 0;
     for (int64_t t = t0; t < t1; ++t, ++it) {
       int r, row0, row1;
       tile_of(t, r, row0, row1);
       const int acc = (int)(it & 1);
-      tc::mbar_wait(&acc_full[acc], (uint32_t)(it >> 1) & 1);
-      tc::tc_fence_after();
       const int p = row0 + row;
       const bool valid = p < row1;
       const float scale = (pr.row_scale && valid) ? __ldg(pr.row_scale + p) : 1.f;
-      const float* A0 = pr.A ? pr.A + (size_t)r * 2 * N : nullptr;
+      tc::mbar_wait(&acc_full[acc], (uint32_t)(it >> 1) & 1);
+      tc::tc_fence_after();
+      if (et == 0) tc::bulk_wait_read0();  // the previous tile's TMA store has read the stage
+      if (pr.A && r != cur_r)
+        for (int n = et; n < N; n += 128) sA0[n] = __ldg(pr.A + (size_t)r * 2 * N + n);
+      cur_r = r;
+      tc::named_bar(1, 128);
       float sdot = 0.f;
-      tc::named_bar(1, 128);  // previous tile's copy-out finished reading the stage
-      uint8_t* srow = sStg + row * (N * 2);
 #pragma unroll
       for (int c0 = 0; c0 < N; c0 += 16) {
         uint32_t v[16];
@@ -242,35 +265,42 @@ __global__ void __launch_bounds__(192, 1)
         float f[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
-        if (A0) {
+        if (pr.A) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) sdot = fmaf(f[j], __ldg(A0 + c0 + j), sdot);
+          for (int j = 0; j < 16; ++j) sdot = fmaf(f[j], sA0[c0 + j], sdot);
         }
         uint4 w0, w1;
         w0.x = tc::pack_bf16(f[0] * scale, f[1] * scale); w0.y = tc::pack_bf16(f[2] * scale, f[3] * scale);
         w0.z = tc::pack_bf16(f[4] * scale, f[5] * scale); w0.w = tc::pack_bf16(f[6] * scale, f[7] * scale);
         w1.x = tc::pack_bf16(f[8] * scale, f[9] * scale); w1.y = tc::pack_bf16(f[10] * scale, f[11] * scale);
         w1.z = tc::pack_bf16(f[12] * scale, f[13] * scale); w1.w = tc::pack_bf16(f[14] * scale, f[15] * scale);
-        const int ch = c0 / 8;
-        *reinterpret_cast<uint4*>(srow + (((ch) ^ (row & SWM)) * 16)) = w0;
-        *reinterpret_cast<uint4*>(srow + (((ch + 1) ^ (row & SWM)) * 16)) = w1;
+        *reinterpret_cast<uint4*>(sStg + stg_off(row, c0 / 8)) = w0;
+        *reinterpret_cast<uint4*>(sStg + stg_off(row, c0 / 8 + 1)) = w1;
       }
       // accumulator drained: hand it back to the MMA warp
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&acc_empty[acc]);
       if (pr.s_src && valid) pr.s_src[p] = sdot;
+      tc::fence_proxy_async_smem();
       tc::named_bar(1, 128);
-      // coalesced copy-out of the valid rows
       const int nvalid = row1 - row0;
-      for (int i = et; i < C::M * NCH; i += 128) {
-        const int rr = i / NCH, ch = i - rr * NCH;
-        if (rr < nvalid) {
-          uint4 val = *reinterpret_cast<const uint4*>(sStg + rr * (N * 2) + ((ch ^ (rr & SWM)) * 16));
+      if (nvalid == C::M) {  // full tile: asynchronous TMA store of the swizzled stage
+        if (et == 0) {
+#pragma unroll
+          for (int nb = 0; nb < C::ONB; ++nb) tc::tma_store_2d(&zmap, sStg + nb * C::M * C::ORB, nb * (C::ORB / 2), row0);
+          tc::bulk_commit();
+        }
+      } else {  // segment tail: coalesced copy of the valid rows only
+        constexpr int NCH = N / 8;
+        for (int i = et; i < nvalid * NCH; i += 128) {
+          const int rr = i / NCH, ch = i - rr * NCH;
+          const uint4 val = *reinterpret_cast<const uint4*>(sStg + stg_off(rr, ch));
           *reinterpret_cast<uint4*>(pr.Z + (size_t)(row0 + rr) * N + ch * 8) = val;
         }
       }
     }
+    if (et == 0) tc::bulk_wait0();
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -297,10 +327,13 @@ static rgnn_status gemm_fwd_tc(const GemmFwdArgs& a, cudaStream_t s) {
   int dev, sms;
   RGNN_CUDA_TRY(cudaGetDevice(&dev));
   RGNN_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  TcFwdParams pr{a.tiles, a.num_tiles, a.rows, a.gofs, a.gather, static_cast<__nv_bfloat16*>(a.Z), a.row_scale, a.A,
-                 a.s_src};
+  const int64_t zrows = a.tiles ? a.z_rows : a.rows;
+  CUtensorMap zmap;
+  RGNN_TRY(make_tmap_2d_bf16(&zmap, a.Z, N, (uint64_t)std::max<int64_t>(zrows, 1), N * 2, C::ORB / 2, C::M, C::ORB));
+  TcFwdParams pr{a.tiles, a.num_tiles, a.rows, a.gofs, a.gather, static_cast<__nv_bfloat16*>(a.Z), zrows, a.row_scale,
+                 a.A, a.s_src};
   const unsigned grid = (unsigned)std::min<int64_t>(ntiles, sms);
-  RGNN_LAUNCH(kern, grid, C::THREADS, C::SMEM, s, xmap, wmap, pr);
+  RGNN_LAUNCH(kern, grid, C::THREADS, C::SMEM, s, xmap, wmap, zmap, pr);
   return RGNN_OK;
 }
 

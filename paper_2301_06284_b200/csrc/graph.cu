@@ -86,13 +86,17 @@ __global__ void k_after_sort(int64_t n, const uint32_t* __restrict__ keys, const
 }
 
 // Bin boundaries of a sorted key array: out[b] = first index q with key[q] >= b,
-// for b in [0, nbins]  (segment offsets / CSR row pointers without atomics).
+// for b in [0, nbins]: one binary search per bin (balanced even when long runs
+// of empty bins exist, e.g. node types that receive no edges).
 template <typename KeyT>
 __global__ void k_bounds(int64_t n, const KeyT* __restrict__ key, int64_t nbins, int32_t* __restrict__ out) {
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q <= n; q += (int64_t)gridDim.x * blockDim.x) {
-    int64_t kp = q > 0 ? (int64_t)key[q - 1] : -1;
-    int64_t kc = q < n ? (int64_t)key[q] : nbins;
-    for (int64_t b = kp + 1; b <= kc; ++b) out[b] = (int32_t)q;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= nbins; b += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)key[mid] < b) lo = mid + 1; else hi = mid;
+    }
+    out[b] = (int32_t)lo;
   }
 }
 
@@ -353,14 +357,14 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   if (n > 0)
     RGNN_LAUNCH(k_after_sort, grid_for(n), T, 0, s, n, keys, vals, d->src, V_own, L.perm, L.src_s, L.dst_s, L.et_s,
                 L.head);
-  RGNN_LAUNCH(k_bounds<int32_t>, grid_for(n + 1), T, 0, s, n, L.et_s, (int64_t)R, L.seg);
+  RGNN_LAUNCH(k_bounds<int32_t>, grid_for(R + 1), T, 0, s, n, L.et_s, (int64_t)R, L.seg);
   // CSR-by-dst: stable sort of positions by local dst -> ascending p within a row.
   if (n > 0) {
     RGNN_LAUNCH(k_iota_keys, grid_for(n), T, 0, s, n, L.dst_s, L.k0, L.v0);
     RGNN_TRY(radix_sort_pairs(L.k0, L.v0, L.k1, L.v1, n, bits_for((uint64_t)(V_own > 0 ? V_own - 1 : 0)), L.prim,
                               L.prim_bytes, s, &alt));
     RGNN_LAUNCH(k_slots, grid_for(n), T, 0, s, n, alt ? L.v1 : L.v0, L.et_s, L.pos, L.et_slot);
-    RGNN_LAUNCH(k_bounds<uint32_t>, grid_for(n + 1), T, 0, s, n, alt ? L.k1 : L.k0, V_own, L.row_ptr);
+    RGNN_LAUNCH(k_bounds<uint32_t>, grid_for(V_own + 1), T, 0, s, n, alt ? L.k1 : L.k0, V_own, L.row_ptr);
     // (etype, dst) runs
     RGNN_TRY(scan_exclusive(L.head, L.run_ex, n, &L.ctr->J, L.prim, L.prim_bytes, s));
     RGNN_LAUNCH(k_runs, grid_for(n), T, 0, s, n, L.head, L.run_ex, L.run_ptr);

@@ -23,6 +23,7 @@ struct GemmFwdArgs {
   void* wt_bf16;            // workspace for the tcgen05 path: [num_w, N, K] bf16 (transposed W)
   int num_w;                // number of weight matrices in W (R, or 1 for the self-loop W0)
   int64_t x_rows;           // rows of X (V)
+  int64_t z_rows;           // rows of Z (E_own) when tiles != null
 };
 
 // dW split-K GEMM over chunks (DESIGN.md Sec. 6 "a5"):
@@ -50,7 +51,7 @@ rgnn_status launch_gemm_fwd(int prec, int K, int N, const GemmFwdArgs& a, cudaSt
 rgnn_status launch_gemm_dw(int prec, int K, int N, const GemmDwArgs& a, cudaStream_t s);
 rgnn_status launch_dw_reduce(int prec, int K, int N, int R, int64_t num_chunks, const int32_t* chunk_seg,
                              const float* part, const int32_t* cseg, const float* cpart, const float* A,
-                             const float* W, float* dW, float* dA, cudaStream_t s);
+                             const float* W, float* dW, float* dA, float* dA_scratch /* [R*2*K] */, cudaStream_t s);
 rgnn_status launch_dst_term(int prec, int K, const rgnn_graph* g, const float* dpre, const void* X, float* cpart,
                             cudaStream_t s);
 rgnn_status launch_fold_u(int prec, int R, int K, int N, const float* W, const float* A, float* U, cudaStream_t s);

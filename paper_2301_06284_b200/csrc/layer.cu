@@ -22,6 +22,7 @@ struct WsLayout {
   float* dwpart;   // [num_chunks, K*N + K]
   float* dw0part;  // [n0, K*N + K]
   float* cpart;    // RGAT dst term: [num_chunks, K]
+  float* vsum;     // RGAT dA vectors: [R, 2, K]
   void* wt;        // tcgen05: bf16 W^T [R, N, K]
   size_t bytes;
 };
@@ -59,6 +60,7 @@ static WsLayout ws_layout(const rgnn_graph* g, int model, int K, int N, int prec
   w.dwpart = c.take<float>((size_t)std::max<int64_t>(g->num_chunks, 1) * (K * N + K));
   w.dw0part = c.take<float>(model == RGNN_RGCN ? (size_t)std::max<int64_t>(dw0_chunks(g), 1) * (K * N + K) : 1);
   w.cpart = c.take<float>((size_t)std::max<int64_t>(g->num_chunks, 1) * K);
+  w.vsum = c.take<float>((size_t)g->R * 2 * K);
   w.bytes = c.off;
   return w;
 }
@@ -110,7 +112,7 @@ static rgnn_status forward(const rgnn_graph* g, int model, int K, int N, int pre
 
   GemmFwdArgs ga{};
   ga.tiles = g->tiles; ga.num_tiles = g->num_tiles; ga.X = X; ga.gather = g->src_s; ga.W = W; ga.wt_bf16 = w.wt;
-  ga.num_w = g->R; ga.x_rows = g->V;
+  ga.num_w = g->R; ga.x_rows = g->V; ga.z_rows = g->E_own;
   AggArgs aa{};
   aa.items = g->items; aa.num_items = g->num_items; aa.pos = g->pos; aa.et_slot = g->et_slot; aa.X = X;
   aa.v0 = g->v0; aa.slope = slope; aa.Y = Y; aa.part = w.part; aa.split_rows = g->split_rows;
@@ -204,7 +206,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     { Phase ph("dst_term", s); RGNN_TRY(launch_dst_term(prec, K, g, w.dpre, X, w.cpart, s)); }
     da.Bz = w.dZ; da.dpre = w.dpre; da.dst_local = g->dst_s; da.v0 = g->v0;
     { Phase ph("gemm_dw", s); RGNN_TRY(dw_gemm(da)); }
-    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, g->chunk_seg, w.cpart, A, W, dW, dA, s)); }
+    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, g->chunk_seg, w.cpart, A, W, dW, dA, w.vsum, s)); }
   } else {
     if (tc_ok) {  // dZ[p] = bf16(1/c * G[dst]) materialised in position order, then the tensor-core dW
       { Phase ph("expand_dz", s); RGNN_TRY(launch_expand_dz(g->E_own, N, g->dst_s, g->inv_c, dY, w.Z, s)); }
@@ -213,7 +215,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
       da.Bg = dY; da.bgather = g->dst_s; da.bscale = g->inv_c;
     }
     { Phase ph("gemm_dw", s); RGNN_TRY(dw_gemm(da)); }
-    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, nullptr, nullptr, nullptr, nullptr, dW, nullptr, s)); }
+    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, nullptr, nullptr, nullptr, nullptr, dW, nullptr, nullptr, s)); }
     if (dW0) {
       Phase ph("gemm_dw0", s);
       GemmDwArgs d0{};
@@ -226,7 +228,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
         d0.Bg = dY;
       }
       RGNN_TRY(dw_gemm(d0));
-      RGNN_TRY(launch_dw_reduce(prec, K, N, 1, d0.num_chunks, nullptr, w.dw0part, nullptr, nullptr, nullptr, nullptr, dW0, nullptr, s));
+      RGNN_TRY(launch_dw_reduce(prec, K, N, 1, d0.num_chunks, nullptr, w.dw0part, nullptr, nullptr, nullptr, nullptr, dW0, nullptr, nullptr, s));
     }
   }
   if (comm) {

@@ -175,54 +175,109 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
   }
 }
 
-// Combine the partial states of each split row in slot order (one warp per row).
+// Combine the partial states of each split row: one block per split row, warp w
+// merges parts w, w+16, ... (4 per step), then warp 0 merges the 16 warp states
+// in warp order.  Fixed assignment and order: deterministic.
 template <typename T, int N, bool RGAT>
-__global__ void __launch_bounds__(256) k_merge(AggArgs a) {
-  constexpr int PER = (N + 31) / 32;
-  const int lane = threadIdx.x & 31;
-  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t w = warp0; w < a.num_split_rows; w += nwarps) {
-    const SplitRow sr = a.split_rows[w];
-    float acc[PER];
+__global__ void __launch_bounds__(512) k_merge(AggArgs a) {
+  constexpr int PER = (N + 31) / 32, NW = 16, U = 4;
+  __shared__ float s_st[NW][N + 2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const SplitRow sr = a.split_rows[blockIdx.x];
+  float acc[PER];
 #pragma unroll
-    for (int i = 0; i < PER; ++i) acc[i] = 0.f;
-    float m = -CUDART_INF_F, lsum = 0.f;
-    if constexpr (RGAT)
-      for (int k = 0; k < sr.nparts; ++k) m = fmaxf(m, a.part[(size_t)(sr.part0 + k) * (N + 4) + N]);
-    for (int k = 0; k < sr.nparts; ++k) {
-      const float* pp = a.part + (size_t)(sr.part0 + k) * (N + 4);
-      float c = 1.f;
-      if constexpr (RGAT) {
-        const float mk = pp[N];
-        c = mk == -CUDART_INF_F ? 0.f : __expf(mk - m);
-        lsum = fmaf(pp[N + 1], c, lsum);
-      }
+  for (int i = 0; i < PER; ++i) acc[i] = 0.f;
+  float m = -CUDART_INF_F, lsum = 0.f;
+  for (int k0 = warp; k0 < sr.nparts; k0 += NW * U) {
+    float mk[U], lk[U], ak[U][PER];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u * NW;
+      const bool ok = k < sr.nparts;
+      const float* pp = a.part + (size_t)(sr.part0 + (ok ? k : 0)) * (N + 4);
+      mk[u] = ok && RGAT ? pp[N] : -CUDART_INF_F;
+      lk[u] = ok && RGAT ? pp[N + 1] : 0.f;
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
         const int n = lane + 32 * i;
-        if (n < N) acc[i] = fmaf(pp[n], c, acc[i]);
+        ak[u][i] = (ok && n < N) ? pp[n] : 0.f;
       }
     }
-    float* y = a.Y + (size_t)sr.row * N;
     if constexpr (RGAT) {
-      const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
-      if (lane == 0) a.lse[sr.row] = lsum > 0.f ? m + __logf(lsum) : -CUDART_INF_F;
+      float mn = m;
 #pragma unroll
-      for (int i = 0; i < PER; ++i) acc[i] *= inv;
-    } else if (a.Z0) {
-      const T* z0 = static_cast<const T*>(a.Z0) + (size_t)sr.row * N;
+      for (int u = 0; u < U; ++u) mn = fmaxf(mn, mk[u]);
+      if (mn != -CUDART_INF_F) {
+        const float c = __expf(m - mn);
+        lsum *= c;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) acc[i] *= c;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const float cu = mk[u] == -CUDART_INF_F ? 0.f : __expf(mk[u] - mn);
+          lsum = fmaf(lk[u], cu, lsum);
+#pragma unroll
+          for (int i = 0; i < PER; ++i) acc[i] = fmaf(ak[u][i], cu, acc[i]);
+        }
+        m = mn;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int i = 0; i < PER; ++i) acc[i] += ak[u][i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int n = lane + 32 * i;
+    if (n < N) s_st[warp][n] = acc[i];
+  }
+  if (lane == 0) { s_st[warp][N] = m; s_st[warp][N + 1] = lsum; }
+  __syncthreads();
+  if (warp != 0) return;
+  m = -CUDART_INF_F; lsum = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) acc[i] = 0.f;
+  for (int w = 0; w < NW; ++w) {
+    if constexpr (RGAT) {
+      const float mw = s_st[w][N], lw = s_st[w][N + 1];
+      const float mn = fmaxf(m, mw);
+      if (mn == -CUDART_INF_F) continue;
+      const float c1 = __expf(m - mn), c2 = mw == -CUDART_INF_F ? 0.f : __expf(mw - mn);
+      lsum = lsum * c1 + lw * c2;
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
         const int n = lane + 32 * i;
-        if (n < N) acc[i] += to_f(z0[n]);
+        if (n < N) acc[i] = acc[i] * c1 + s_st[w][n] * c2;
+      }
+      m = mn;
+    } else {
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int n = lane + 32 * i;
+        if (n < N) acc[i] += s_st[w][n];
       }
     }
+  }
+  float* y = a.Y + (size_t)sr.row * N;
+  if constexpr (RGAT) {
+    const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+    if (lane == 0) a.lse[sr.row] = lsum > 0.f ? m + __logf(lsum) : -CUDART_INF_F;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) acc[i] *= inv;
+  } else if (a.Z0) {
+    const T* z0 = static_cast<const T*>(a.Z0) + (size_t)sr.row * N;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int n = lane + 32 * i;
-      if (n < N) y[n] = acc[i];
+      if (n < N) acc[i] += to_f(z0[n]);
     }
+  }
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int n = lane + 32 * i;
+    if (n < N) y[n] = acc[i];
   }
 }
 
@@ -325,8 +380,8 @@ static rgnn_status aggregate(bool rgat, const AggArgs& a, cudaStream_t s) {
     else RGNN_LAUNCH((k_aggregate<T, K, N, false>), warps_grid(a.num_items), 256, 0, s, a);
   }
   if (a.num_split_rows > 0) {
-    if (rgat) RGNN_LAUNCH((k_merge<T, N, true>), warps_grid(a.num_split_rows), 256, 0, s, a);
-    else RGNN_LAUNCH((k_merge<T, N, false>), warps_grid(a.num_split_rows), 256, 0, s, a);
+    if (rgat) RGNN_LAUNCH((k_merge<T, N, true>), (unsigned)a.num_split_rows, 512, 0, s, a);
+    else RGNN_LAUNCH((k_merge<T, N, false>), (unsigned)a.num_split_rows, 512, 0, s, a);
   }
   return RGNN_OK;
 }
