@@ -1,0 +1,346 @@
+// bwd_fused_tc.cu -- fused RGAT backward on the tensor cores (bf16 path).
+//
+// One CTA per split-K chunk of positions (relation r fixed, positions in
+// (etype, dst) order).  Per 128-position stage:
+//   * warp 0 (TMA): X[src_s[p]] rows -> smem by tile::gather4 (MMA operand A,
+//     MN-major SW128), gather indices loaded one stage ahead;
+//   * warps 2..9 (CUDA cores) recompute the attention of each edge and write
+//     its gradient row straight into the MMA's B operand in shared memory:
+//        pre = s_src[p] + x_v . U[r]            (U[r] = W_r A[r,1])
+//        alpha = exp(leaky(pre) - lse_v),  dalpha = G_v . Z[p],  S_v = G_v . Y_v
+//        dpre = alpha (dalpha - S_v) leaky'(pre)
+//        dZ[p] = alpha G_v + dpre A[r,0]   -> bf16, MN-major SW128 smem line p
+//     plus dpre into a 16-column side operand (column 0) and the destination
+//     term c_r += dpre x_v in registers (SURVEY §8 backward formulas);
+//   * warp 1: tcgen05.mma  D[d_in x d_out] += X_src^T dZ  and  Db += X_src^T dpre.
+// dZ never touches HBM (the unfused path writes and re-reads E x d_out bf16),
+// and the per-destination quantities (G_v, Y_v, x_v, lse_v) are reloaded only
+// when v changes (positions of one relation are sorted by destination).
+// Epilogue: TMEM -> part[c] (d_in x d_out + bvec); c_r partial -> cpart[c];
+// reduced in chunk order by k_dw_reduce / k_da (deterministic).
+#include <math_constants.h>
+
+#include "kernels.cuh"
+#include "tc_common.cuh"
+
+namespace rgnn {
+
+template <int K, int N>
+struct BfCfg {
+  static constexpr int MT = 128;                             // positions per stage
+  static constexpr int A_BYTES = MT * K * 2;
+  static constexpr int B_BYTES = MT * N * 2;
+  static constexpr int B2_BYTES = MT * 16 * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES + B2_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE > 6 ? 6 : (200 * 1024) / STAGE;
+  static constexpr int CW = 8;                               // compute warps
+  static constexpr int THREADS = 64 + CW * 32;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + CW * K * 4 + 256;
+  static constexpr int NCOLS = (N + 16) <= 32 ? 32 : (N + 16) <= 64 ? 64 : (N + 16) <= 128 ? 128 : 256;
+  static constexpr uint32_t IDESC = tc::idesc_bf16(K, N, 1, 1);
+  static constexpr uint32_t IDESC_B = tc::idesc_bf16(K, 16, 1, 1);
+  // compute mapping: L lanes per position (16 bytes of Z each), G positions per warp step
+  static constexpr int EPL = 8;
+  static constexpr int L = N / EPL;
+  static constexpr int G = 32 / L;
+  static constexpr int PPW = MT / CW;                        // positions per warp per stage (16)
+  static constexpr int PG = PPW / G;                         // positions per lane group
+  static constexpr int KPL = K / L;                          // x_v features per lane
+};
+
+struct BwdFusedParams {
+  const Tile* chunks;
+  const int32_t* src_s;
+  const int32_t* dst_s;
+  const float* s_src;
+  const __nv_bfloat16* Z;
+  const __nv_bfloat16* X;
+  const float* lse;
+  const float* Y;
+  const float* dY;
+  const float* U;
+  const float* A;
+  float slope;
+  int64_t v0;
+  float* part;
+  float* cpart;
+};
+
+__device__ __forceinline__ float leaky_f(float x, float s) { return x > 0.f ? x : s * x; }
+
+template <int K, int N>
+__global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
+    k_bwd_fused_tc(const __grid_constant__ CUtensorMap xmap, BwdFusedParams pr) {
+  using C = BfCfg<K, N>;
+  constexpr int L = C::L, PG = C::PG, KPL = C::KPL, EPL = C::EPL;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* s_c = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE);  // [CW][K] dst-term partials
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_c + C::CW * K);
+  uint64_t* a_full = bar;
+  uint64_t* b_full = a_full + C::STAGES;
+  uint64_t* empty = b_full + C::STAGES;
+  uint64_t* acc_full = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  auto sA = [&](int s) { return smem + s * C::STAGE; };
+  auto sB = [&](int s) { return smem + s * C::STAGE + C::A_BYTES; };
+  auto sB2 = [&](int s) { return smem + s * C::STAGE + C::A_BYTES + C::B_BYTES; };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Tile ch = pr.chunks[blockIdx.x];
+  const int r = ch.r, row0 = ch.row0, row1 = ch.row1;
+  const int nsub = (row1 - row0 + C::MT - 1) / C::MT;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::STAGES; ++i) {
+      tc::mbar_init(&a_full[i], 1);
+      tc::mbar_init(&b_full[i], C::CW);
+      tc::mbar_init(&empty[i], 1);
+    }
+    tc::mbar_init(acc_full, 1);
+    tc::mbar_fence_init();
+    tc::tma_prefetch_desc(&xmap);
+  }
+  for (int i = threadIdx.x; i < C::STAGES * C::B2_BYTES / 16; i += blockDim.x) {  // dpre operand: cols 1..15 = 0
+    const int s = i / (C::B2_BYTES / 16), o = i % (C::B2_BYTES / 16);
+    reinterpret_cast<uint4*>(sB2(s))[o] = make_uint4(0, 0, 0, 0);
+  }
+  tc::fence_proxy_async_smem();
+  if (warp == 1) tc::tmem_alloc<C::NCOLS>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (X_src rows)
+    auto load_idx = [&](int it, int* out) {
+      const int p0 = row0 + it * C::MT;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) out[j] = __ldg(pr.src_s + min(p0 + 4 * lane + j, row1 - 1));
+    };
+    int idx[4] = {0, 0, 0, 0};
+    if (nsub > 0) load_idx(0, idx);
+    for (int it = 0; it < nsub; ++it) {
+      const int st = it % C::STAGES;
+      const uint32_t use = (uint32_t)(it / C::STAGES);
+      int nidx[4] = {0, 0, 0, 0};
+      if (it + 1 < nsub) load_idx(it + 1, nidx);
+      if (use > 0) tc::mbar_wait(&empty[st], (use - 1) & 1);
+      if (lane == 0) tc::mbar_expect_tx(&a_full[st], C::A_BYTES);
+      __syncwarp();
+#pragma unroll
+      for (int kb = 0; kb < K / 64; ++kb)
+        tc::tma_gather4(sA(st) + kb * C::MT * 128 + lane * 4 * 128, &xmap, &a_full[st], kb * 64, idx[0], idx[1],
+                        idx[2], idx[3]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) idx[j] = nidx[j];
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    for (int it = 0; it < nsub; ++it) {
+      const int st = it % C::STAGES;
+      const uint32_t ph = (uint32_t)(it / C::STAGES) & 1;
+      tc::mbar_wait(&a_full[st], ph);
+      tc::mbar_wait(&b_full[st], ph);
+      tc::tc_fence_after();
+      if (lane == 0) {
+        const uint32_t a0 = tc::smem_u32(sA(st)), b0 = tc::smem_u32(sB(st)), c0 = tc::smem_u32(sB2(st));
+#pragma unroll
+        for (int ks = 0; ks < C::MT / 16; ++ks) {
+          const uint32_t acc = (it > 0 || ks > 0) ? 1u : 0u;
+          const uint64_t ad = tc::umma_desc(a0 + ks * 16 * 128, C::MT * 128, 1024, 2u);
+          const uint64_t bd = tc::umma_desc(b0 + ks * 16 * 128, C::MT * 128, 1024, 2u);
+          tc::umma_bf16(tmem, ad, bd, C::IDESC, acc);
+          const uint64_t cd = tc::umma_desc(c0 + ks * 512, 256, 128, 0u);
+          tc::umma_bf16(tmem + N, ad, cd, C::IDESC_B, acc);
+        }
+        tc::umma_commit(&empty[st]);
+        if (it == nsub - 1) tc::umma_commit(acc_full);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ compute warps: dZ -> smem B operand
+    const int cw = warp - 2;                 // 0..7
+    const int g = lane / L, l = lane % L;    // lane group (one position at a time), lane within group
+    const float* Ur = pr.U + (size_t)r * K + l * KPL;
+    const float* A0 = pr.A + (size_t)r * 2 * N + l * EPL;
+    float u[KPL], a0[EPL];
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) u[i] = __ldg(Ur + i);
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) a0[i] = __ldg(A0 + i);
+    float cacc[KPL];
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) cacc[i] = 0.f;
+    int cur_v = -1;
+    float gv[EPL], xv[KPL], Sv = 0.f, dsc = 0.f, lse = 0.f;
+    const uint32_t gmask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (g * L));
+    for (int it = 0; it < nsub; ++it) {
+      const int st = it % C::STAGES;
+      const uint32_t use = (uint32_t)(it / C::STAGES);
+      const int pbase = row0 + it * C::MT + cw * C::PPW;  // this warp's 16 positions
+      // cooperative loads of dst and s_src for the warp's positions
+      const int pl = pbase + (lane & 15);
+      const bool okl = lane < C::PPW && pl < row1;
+      const int myv = okl ? __ldg(pr.dst_s + pl) : -1;
+      const float mys = okl ? __ldg(pr.s_src + pl) : 0.f;
+      // Z rows of this group's positions, issued before the wait
+      uint4 zr[PG];
+#pragma unroll
+      for (int i = 0; i < PG; ++i) {
+        const int p = pbase + g * PG + i;
+        zr[i] = p < row1 ? ldg_nc16(pr.Z + (size_t)p * N + l * EPL) : make_uint4(0, 0, 0, 0);
+      }
+      if (use > 0) tc::mbar_wait(&empty[st], (use - 1) & 1);
+      uint8_t* b = sB(st);
+      uint8_t* b2 = sB2(st);
+#pragma unroll
+      for (int i = 0; i < PG; ++i) {
+        const int lp = cw * C::PPW + g * PG + i;  // row of the stage (0..127)
+        const int src_lane = g * PG + i;
+        const int v = __shfl_sync(0xffffffffu, myv, src_lane);
+        const float ss = __shfl_sync(0xffffffffu, mys, src_lane);
+        float dz[EPL];
+        float dpre = 0.f;
+        if (v >= 0) {
+          if (v != cur_v) {  // per-destination values (group-uniform branch)
+            const float* gp = pr.dY + (size_t)v * N + l * EPL;
+            const float* yp = pr.Y + (size_t)v * N + l * EPL;
+            const __nv_bfloat16* xp = pr.X + (pr.v0 + v) * (int64_t)K + l * KPL;
+            float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+            for (int j = 0; j < EPL; j += 4) {
+              const float4 gg = __ldg(reinterpret_cast<const float4*>(gp + j));
+              const float4 yy = __ldg(reinterpret_cast<const float4*>(yp + j));
+              gv[j] = gg.x; gv[j + 1] = gg.y; gv[j + 2] = gg.z; gv[j + 3] = gg.w;
+              s1 = fmaf(gg.x, yy.x, s1); s1 = fmaf(gg.y, yy.y, s1); s1 = fmaf(gg.z, yy.z, s1); s1 = fmaf(gg.w, yy.w, s1);
+            }
+#pragma unroll
+            for (int j = 0; j < KPL; ++j) {
+              xv[j] = __bfloat162float(xp[j]);
+              s2 = fmaf(xv[j], u[j], s2);
+            }
+#pragma unroll
+            for (int o = L / 2; o > 0; o >>= 1) {
+              s1 += __shfl_xor_sync(gmask, s1, o);
+              s2 += __shfl_xor_sync(gmask, s2, o);
+            }
+            Sv = s1;
+            dsc = s2;
+            lse = __ldg(pr.lse + v);
+            cur_v = v;
+          }
+          float zf[EPL];
+          Vec16<__nv_bfloat16>{zr[i]}.to_float(zf);
+          float da = 0.f;
+#pragma unroll
+          for (int j = 0; j < EPL; ++j) da = fmaf(gv[j], zf[j], da);
+#pragma unroll
+          for (int o = L / 2; o > 0; o >>= 1) da += __shfl_xor_sync(gmask, da, o);
+          const float pre = ss + dsc;
+          const float alpha = __expf(leaky_f(pre, pr.slope) - lse);
+          dpre = alpha * (da - Sv) * (pre > 0.f ? 1.f : pr.slope);
+#pragma unroll
+          for (int j = 0; j < EPL; ++j) dz[j] = fmaf(alpha, gv[j], dpre * a0[j]);
+#pragma unroll
+          for (int j = 0; j < KPL; ++j) cacc[j] = fmaf(dpre, xv[j], cacc[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < EPL; ++j) dz[j] = 0.f;
+        }
+        // MN-major SW128 line `lp`: features l*8..l*8+7 = 16-byte chunk (l % 8) of block l / 8
+        uint4 o;
+        o.x = tc::pack_bf16(dz[0], dz[1]); o.y = tc::pack_bf16(dz[2], dz[3]);
+        o.z = tc::pack_bf16(dz[4], dz[5]); o.w = tc::pack_bf16(dz[6], dz[7]);
+        *reinterpret_cast<uint4*>(b + (l >> 3) * (C::MT * 128) + lp * 128 + (((l & 7) ^ (lp & 7)) << 4)) = o;
+        if (l == 0) *reinterpret_cast<__nv_bfloat16*>(b2 + (lp >> 3) * 256 + (lp & 7) * 16) = __float2bfloat16_rn(dpre);
+      }
+      tc::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&b_full[st]);
+    }
+    // destination-term partial: sum over lane groups, then over warps (fixed order)
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) {
+      float v = cacc[j];
+#pragma unroll
+      for (int o = L; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      cacc[j] = v;
+    }
+    if (g == 0) {
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) s_c[cw * K + l * KPL + j] = cacc[j];
+    }
+    // epilogue: TMEM accumulators -> part[c]; two warps per lane quarter split the columns
+    tc::mbar_wait(acc_full, 0);
+    tc::tc_fence_after();
+    const int q = warp & 3, half = cw >> 2;  // warps 2..5 -> half 0, 6..9 -> half 1
+    const int row = K == 128 ? q * 32 + lane : q * 16 + lane;
+    const bool rvalid = K == 128 || lane < 16;
+    float* out = pr.part + (size_t)blockIdx.x * (K * N + K);
+    constexpr int HALF = N / 2;
+#pragma unroll
+    for (int c0 = half * HALF; c0 < (half + 1) * HALF; c0 += 16) {
+      uint32_t v[16];
+      tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
+      tc::tmem_ld_wait();
+      if (rvalid) {
+        float4* o = reinterpret_cast<float4*>(out + (size_t)row * N + c0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          o[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]), __uint_as_float(v[4 * j + 2]),
+                             __uint_as_float(v[4 * j + 3]));
+      }
+    }
+    if (half == 0) {
+      uint32_t v[16];
+      tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + N, v);
+      tc::tmem_ld_wait();
+      if (rvalid) out[K * N + row] = __uint_as_float(v[0]);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < C::CW; ++w) s += s_c[w * K + k];
+    pr.cpart[(size_t)blockIdx.x * K + k] = s;
+  }
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<C::NCOLS>(tmem);
+  }
+}
+
+template <int K, int N>
+static rgnn_status bwd_fused(const rgnn_graph* g, const BwdFusedParams& p0, const void* X, cudaStream_t s) {
+  using C = BfCfg<K, N>;
+  if (g->num_chunks == 0) return RGNN_OK;
+  CUtensorMap xmap;
+  RGNN_TRY(make_tmap_2d_bf16(&xmap, X, K, (uint64_t)g->V, K * 2, 64, 1, 128));
+  auto kern = k_bwd_fused_tc<K, N>;
+  RGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  RGNN_LAUNCH(kern, (unsigned)g->num_chunks, C::THREADS, C::SMEM, s, xmap, p0);
+  return RGNN_OK;
+}
+
+bool tc_disabled();
+
+rgnn_status launch_bwd_fused_tc(int K, int N, const rgnn_graph* g, const void* X, const void* Z, const float* s_src,
+                                const float* lse, const float* Y, const float* dY, const float* U, const float* A,
+                                float slope, float* part, float* cpart, cudaStream_t s) {
+  if (tc_disabled()) return RGNN_E_UNSUPPORTED;
+  if (getenv("RGNN_DISABLE_FUSED_BWD")) return RGNN_E_UNSUPPORTED;
+  BwdFusedParams p{g->chunks, g->src_s, g->dst_s, s_src, static_cast<const __nv_bfloat16*>(Z),
+                   static_cast<const __nv_bfloat16*>(X), lse, Y, dY, U, A, slope, g->v0, part, cpart};
+  if (K == 64 && N == 64) return bwd_fused<64, 64>(g, p, X, s);
+  if (K == 64 && N == 128) return bwd_fused<64, 128>(g, p, X, s);
+  if (K == 128 && N == 64) return bwd_fused<128, 64>(g, p, X, s);
+  if (K == 128 && N == 128) return bwd_fused<128, 128>(g, p, X, s);
+  return RGNN_E_UNSUPPORTED;
+}
+
+}  // namespace rgnn

@@ -198,6 +198,17 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
   };
   if (model == RGNN_RGAT) {
     { Phase ph("fold_u", s); RGNN_TRY(launch_fold_u(prec, g->R, K, N, W, A, w.U, s)); }
+    rgnn_status fst = RGNN_E_UNSUPPORTED;
+    if (tc_ok) {  // fused position-order backward: dZ built in smem, dW MMA + dst term in one kernel
+      Phase ph("bwd_fused", s);
+      fst = launch_bwd_fused_tc(K, N, g, X, sv.Z, sv.s_src, sv.lse, Y, dY, w.U, A, slope, w.dwpart, w.cpart, s);
+      if (fst != RGNN_OK && fst != RGNN_E_UNSUPPORTED) return fst;
+    }
+    if (fst == RGNN_OK) {
+      Phase ph("dw_reduce", s);
+      RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, g->chunk_seg, w.cpart, A, W,
+                                dW, dA, w.vsum, s));
+    } else {
     BwdArgs ba{};
     ba.items = g->items; ba.num_items = g->num_items; ba.pos = g->pos; ba.et_slot = g->et_slot; ba.Z = sv.Z;
     ba.s_src = sv.s_src; ba.X = X; ba.v0 = g->v0; ba.U = w.U; ba.A = A; ba.slope = slope; ba.Y = Y; ba.dY = dY;
@@ -207,6 +218,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     da.Bz = w.dZ; da.dpre = w.dpre; da.dst_local = g->dst_s; da.v0 = g->v0;
     { Phase ph("gemm_dw", s); RGNN_TRY(dw_gemm(da)); }
     { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, g->chunk_seg, w.cpart, A, W, dW, dA, w.vsum, s)); }
+    }
   } else {
     if (tc_ok) {  // dZ[p] = bf16(1/c * G[dst]) materialised in position order, then the tensor-core dW
       { Phase ph("expand_dz", s); RGNN_TRY(launch_expand_dz(g->E_own, N, g->dst_s, g->inv_c, dY, w.Z, s)); }
