@@ -106,7 +106,10 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
     reinterpret_cast<uint4*>(sB2(s))[o] = make_uint4(0, 0, 0, 0);
   }
   tc::fence_proxy_async_smem();
-  if (warp == 1) tc::tmem_alloc<C::NCOLS>(tmem_slot);
+  if (warp == 1) {
+    __syncwarp();
+    tc::tmem_alloc<C::NCOLS>(tmem_slot);
+  }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();

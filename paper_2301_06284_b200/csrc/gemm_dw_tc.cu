@@ -82,7 +82,10 @@ __global__ void __launch_bounds__(192, 1)
     }
     tc::fence_proxy_async_smem();
   }
-  if (warp == 1) tc::tmem_alloc<C::NCOLS>(tmem_slot);
+  if (warp == 1) {
+    __syncwarp();
+    tc::tmem_alloc<C::NCOLS>(tmem_slot);
+  }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();

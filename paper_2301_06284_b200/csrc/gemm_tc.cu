@@ -11,11 +11,13 @@
 // stage with coalesced 16-byte stores (rows beyond row1 are never written).
 //
 // Persistent, warp specialised, one CTA per SM:
-//   warp 0   TMA producer: W_r into a 2-slot ring (reloaded only when r changes),
-//            X rows by gather4 into an S-stage ring (each lane issues one gather4)
-//   warp 1   TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=d_out,
-//            K-steps of 16), commits to the smem-empty / accumulator-full barriers
-//   warps 2-5 epilogue: tcgen05.ld (32 lanes x 16 columns) -> fp32 math -> bf16
+//   warp 0    TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=d_out,
+//             K-steps of 16), commits to the smem-empty / accumulator-full barriers
+//   warps 1-4 producers: X rows gathered with 16-byte cp.async straight into the
+//             128B-swizzled K-major layout (r4 profile: TMA tile::gather4 issued
+//             ~1 op / 100 cycles / SM and starved the MMA), W_r by TMA into a
+//             2-slot ring reloaded only when the relation changes
+//   warps 5-8 epilogue: tcgen05.ld (32 lanes x 16 columns) -> fp32 math -> bf16
 // TMEM holds two accumulators (tile i+1's MMAs overlap tile i's epilogue).
 #include <cudaTypedefs.h>
 
@@ -76,13 +78,13 @@ struct FwdCfg {
   static constexpr int A_BYTES = M * K * 2;
   static constexpr int B_BYTES = N * K * 2;
   static constexpr int STAGES = (96 * 1024) / A_BYTES > 8 ? 8 : (96 * 1024) / A_BYTES;
+  static constexpr int DEPTH = STAGES - 1;                  // cp.async groups kept in flight per producer thread
   static constexpr int STG_BYTES = M * N * 2;
-  static constexpr int ORB = (N * 2 < 128) ? N * 2 : 128;   // Z staging: bytes per row of one swizzle block
-  static constexpr int ONB = (N * 2) / ORB;                 // Z column blocks (TMA store boxes)
-  static constexpr int OCPB = ORB / 16;                     // 16-byte chunks per block row
   static constexpr int NCOLS = (2 * N) <= 32 ? 32 : (2 * N) <= 64 ? 64 : (2 * N) <= 128 ? 128 : 256;
   static constexpr int SMEM = 1024 + STAGES * A_BYTES + 2 * B_BYTES + STG_BYTES + N * 4 + 256;
-  static constexpr int THREADS = 192;
+  static constexpr int THREADS = 288;                       // 1 MMA warp, 4 producer warps, 4 epilogue warps
+  static constexpr int CPR = K * 2 / 16;                    // 16-byte chunks per X row
+  static constexpr int RPI = 32 / CPR;                      // X rows per warp-wide cp.async
   static constexpr uint32_t IDESC = tc::idesc_bf16(128, N, 0, 0);
 };
 
@@ -90,17 +92,16 @@ struct TcFwdParams {
   const Tile* tiles;
   int64_t num_tiles, rows, gofs;
   const int32_t* gather;
+  const __nv_bfloat16* X;
   __nv_bfloat16* Z;
-  int64_t z_rows;
   const float* row_scale;
   const float* A;
   float* s_src;
 };
 
 template <int K, int N>
-__global__ void __launch_bounds__(192, 1)
-    k_gemm_fwd_tc(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
-                  const __grid_constant__ CUtensorMap zmap, TcFwdParams pr) {
+__global__ void __launch_bounds__(288, 1)
+    k_gemm_fwd_tc(const __grid_constant__ CUtensorMap wmap, TcFwdParams pr) {
   using C = FwdCfg<K, N>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -123,17 +124,18 @@ __global__ void __launch_bounds__(192, 1)
   const int64_t t0 = (int64_t)blockIdx.x * per, t1 = min(ntiles, t0 + per);
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < C::STAGES; ++i) { tc::mbar_init(&a_full[i], 1); tc::mbar_init(&a_empty[i], 1); }
+    for (int i = 0; i < C::STAGES; ++i) { tc::mbar_init(&a_full[i], 128); tc::mbar_init(&a_empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&b_full[i], 1); tc::mbar_init(&b_empty[i], 1);
       tc::mbar_init(&acc_full[i], 1); tc::mbar_init(&acc_empty[i], 4);
     }
     tc::mbar_fence_init();
-    tc::tma_prefetch_desc(&xmap);
     tc::tma_prefetch_desc(&wmap);
-    tc::tma_prefetch_desc(&zmap);
   }
-  if (warp == 1) tc::tmem_alloc<C::NCOLS>(tmem_slot);
+  if (warp == 0) {
+    __syncwarp();  // .sync.aligned: the warp must be converged (thread 0 initialised the barriers)
+    tc::tmem_alloc<C::NCOLS>(tmem_slot);
+  }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -145,53 +147,6 @@ __global__ void __launch_bounds__(192, 1)
   };
 
   if (warp == 0) {
-    // ---------------------------------------------------------------- TMA producer
-    int cur_r = -1, bslot = 1;
-    uint32_t buse[2] = {0, 0};
-    int64_t it = 0;
-    // gather indices of the next tile are loaded one tile ahead (hides their latency)
-    int idx[4] = {0, 0, 0, 0};
-    auto load_idx = [&](int64_t t, int* out) {
-      int r, row0, row1;
-      tile_of(t, r, row0, row1);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        int p = min(row0 + 4 * lane + j, row1 - 1);  // rows past row1 re-read a valid row, never stored
-        out[j] = pr.gather ? __ldg(pr.gather + p) : (int)(pr.gofs + p);
-      }
-    };
-    if (t0 < t1) load_idx(t0, idx);
-    for (int64_t t = t0; t < t1; ++t, ++it) {
-      int r, row0, row1;
-      tile_of(t, r, row0, row1);
-      int nidx[4] = {0, 0, 0, 0};
-      if (t + 1 < t1) load_idx(t + 1, nidx);
-      if (r != cur_r) {
-        bslot ^= 1;
-        if (buse[bslot] > 0) tc::mbar_wait(&b_empty[bslot], (buse[bslot] - 1) & 1);
-        ++buse[bslot];
-        if (lane == 0) {
-          tc::mbar_expect_tx(&b_full[bslot], C::B_BYTES);
-#pragma unroll
-          for (int kb = 0; kb < C::KBLK; ++kb)
-            tc::tma_load_2d(sB + bslot * C::B_BYTES + kb * N * C::RB, &wmap, &b_full[bslot], kb * (C::RB / 2), r * N);
-        }
-        cur_r = r;
-      }
-      const int stage = (int)(it % C::STAGES);
-      const uint32_t use = (uint32_t)(it / C::STAGES);
-      if (use > 0) tc::mbar_wait(&a_empty[stage], (use - 1) & 1);
-      if (lane == 0) tc::mbar_expect_tx(&a_full[stage], C::A_BYTES);
-      __syncwarp();
-      uint8_t* dstA = sA + stage * C::A_BYTES;
-#pragma unroll
-      for (int kb = 0; kb < C::KBLK; ++kb)
-        tc::tma_gather4(dstA + kb * C::M * C::RB + lane * 4 * C::RB, &xmap, &a_full[stage], kb * (C::RB / 2), idx[0],
-                        idx[1], idx[2], idx[3]);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) idx[j] = nidx[j];
-    }
-  } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     int cur_r = -1, bslot = 1;
     uint32_t buse[2] = {0, 0};
@@ -229,17 +184,80 @@ __global__ void __launch_bounds__(192, 1)
       }
       __syncwarp();
     }
+  } else if (warp <= 4) {
+    // ---------------------------------------------------------------- producers (warps 1..4)
+    // X rows gathered with 16-byte cp.async straight into the swizzled K-major layout;
+    // each thread keeps DEPTH tiles in flight, then publishes a tile with a proxy
+    // fence + mbarrier arrive (128 producer threads per tile).  W_r: TMA, warp 1.
+    const int pw = warp - 1;
+    int cur_r = -1, bslot = 1;
+    uint32_t buse[2] = {0, 0};
+    auto load_idx = [&](int64_t t) -> int {
+      int r, row0, row1;
+      tile_of(t, r, row0, row1);
+      const int p = min(row0 + pw * 32 + lane, row1 - 1);  // rows past row1 re-read a valid row, never stored
+      return pr.gather ? __ldg(pr.gather + p) : (int)(pr.gofs + p);
+    };
+    int myidx = t0 < t1 ? load_idx(t0) : 0;
+    int64_t it = 0, pub = 0;  // tiles [0, pub) published by this thread
+    auto flush = [&]() {      // publish every pending tile (before any blocking wait: the MMA may need them)
+      tc::cp_async_wait<0>();
+      tc::fence_proxy_async_smem();
+      for (; pub < it; ++pub) tc::mbar_arrive(&a_full[pub % C::STAGES]);
+    };
+    for (int64_t t = t0; t < t1; ++t, ++it) {
+      int r, row0, row1;
+      tile_of(t, r, row0, row1);
+      const int nidx = t + 1 < t1 ? load_idx(t + 1) : 0;
+      if (pw == 0 && r != cur_r) {
+        bslot ^= 1;
+        if (buse[bslot] > 0) {
+          flush();
+          tc::mbar_wait(&b_empty[bslot], (buse[bslot] - 1) & 1);
+        }
+        ++buse[bslot];
+        if (lane == 0) {
+          tc::mbar_expect_tx(&b_full[bslot], C::B_BYTES);
+#pragma unroll
+          for (int kb = 0; kb < C::KBLK; ++kb)
+            tc::tma_load_2d(sB + bslot * C::B_BYTES + kb * N * C::RB, &wmap, &b_full[bslot], kb * (C::RB / 2), r * N);
+        }
+        cur_r = r;
+      }
+      const int stage = (int)(it % C::STAGES);
+      const uint32_t use = (uint32_t)(it / C::STAGES);
+      if (use > 0) {
+        if (pub < it - C::STAGES + 1) flush();  // the stage's previous tile must be published before waiting on it
+        tc::mbar_wait(&a_empty[stage], (use - 1) & 1);
+      }
+      uint8_t* dstA = sA + stage * C::A_BYTES;
+#pragma unroll
+      for (int i = 0; i < 32 / C::RPI; ++i) {
+        const int rr = i * C::RPI + lane / C::CPR;  // row within this warp's 32
+        const int c = lane % C::CPR;                // 16-byte chunk of the row
+        const int row = pw * 32 + rr;
+        const int xr = __shfl_sync(0xffffffffu, myidx, rr);
+        const int cb = c % (C::RB / 16), blk = c / (C::RB / 16);
+        const int phys = C::RB == 128 ? (cb ^ (row & 7)) : (cb ^ ((row >> 1) & 3));
+        tc::cp_async16(dstA + blk * C::M * C::RB + row * C::RB + phys * 16, pr.X + (size_t)xr * K + c * 8);
+      }
+      tc::cp_async_commit();
+      if (it - pub >= C::DEPTH) {  // more than DEPTH tiles pending: the oldest has landed
+        tc::cp_async_wait<C::DEPTH>();
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(&a_full[pub % C::STAGES]);
+        ++pub;
+      }
+      myidx = nidx;
+    }
+    flush();
   } else {
-    // ---------------------------------------------------------------- epilogue (warps 2..5)
+    // ---------------------------------------------------------------- epilogue (warps 5..8)
     const int q = warp & 3;                 // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;          // tile row owned by this thread
-    const int et = threadIdx.x - 64;        // 0..127
-    // Z staging = ONB column blocks of [128 rows x ORB bytes], swizzled like the TMA store map
-    auto stg_off = [&](int rr, int ch) -> int {
-      const int nb = ch / C::OCPB, c = ch % C::OCPB;
-      const int phys = C::ORB == 128 ? (c ^ (rr & 7)) : C::ORB == 64 ? (c ^ ((rr >> 1) & 3)) : (c ^ ((rr >> 2) & 1));
-      return nb * C::M * C::ORB + rr * C::ORB + phys * 16;
-    };
+    const int et = threadIdx.x - 160;       // 0..127
+    constexpr int NCH = N / 8;              // 16-byte chunks per Z row
+    constexpr int SWM = (NCH < 8 ? NCH : 8) - 1;
     int cur_r = -1;
     int64_t it = 0;
     for (int64_t t = t0; t < t1; ++t, ++it) {
@@ -251,11 +269,11 @@ __global__ void __launch_bounds__(192, 1)
       const float scale = (pr.row_scale && valid) ? __ldg(pr.row_scale + p) : 1.f;
       tc::mbar_wait(&acc_full[acc], (uint32_t)(it >> 1) & 1);
       tc::tc_fence_after();
-      if (et == 0) tc::bulk_wait_read0();  // the previous tile's TMA store has read the stage
       if (pr.A && r != cur_r)
         for (int n = et; n < N; n += 128) sA0[n] = __ldg(pr.A + (size_t)r * 2 * N + n);
       cur_r = r;
-      tc::named_bar(1, 128);
+      tc::named_bar(1, 128);  // previous tile's copy-out done; A[r,0] visible
+      uint8_t* srow = sStg + row * (N * 2);
       float sdot = 0.f;
 #pragma unroll
       for (int c0 = 0; c0 < N; c0 += 16) {
@@ -274,37 +292,28 @@ __global__ void __launch_bounds__(192, 1)
         w0.z = tc::pack_bf16(f[4] * scale, f[5] * scale); w0.w = tc::pack_bf16(f[6] * scale, f[7] * scale);
         w1.x = tc::pack_bf16(f[8] * scale, f[9] * scale); w1.y = tc::pack_bf16(f[10] * scale, f[11] * scale);
         w1.z = tc::pack_bf16(f[12] * scale, f[13] * scale); w1.w = tc::pack_bf16(f[14] * scale, f[15] * scale);
-        *reinterpret_cast<uint4*>(sStg + stg_off(row, c0 / 8)) = w0;
-        *reinterpret_cast<uint4*>(sStg + stg_off(row, c0 / 8 + 1)) = w1;
+        const int ch = c0 / 8;
+        *reinterpret_cast<uint4*>(srow + (((ch) ^ (row & SWM)) * 16)) = w0;
+        *reinterpret_cast<uint4*>(srow + (((ch + 1) ^ (row & SWM)) * 16)) = w1;
       }
       // accumulator drained: hand it back to the MMA warp
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&acc_empty[acc]);
       if (pr.s_src && valid) pr.s_src[p] = sdot;
-      tc::fence_proxy_async_smem();
       tc::named_bar(1, 128);
+      // coalesced copy-out of the valid rows (never past row1: the next segment's rows)
       const int nvalid = row1 - row0;
-      if (nvalid == C::M) {  // full tile: asynchronous TMA store of the swizzled stage
-        if (et == 0) {
-#pragma unroll
-          for (int nb = 0; nb < C::ONB; ++nb) tc::tma_store_2d(&zmap, sStg + nb * C::M * C::ORB, nb * (C::ORB / 2), row0);
-          tc::bulk_commit();
-        }
-      } else {  // segment tail: coalesced copy of the valid rows only
-        constexpr int NCH = N / 8;
-        for (int i = et; i < nvalid * NCH; i += 128) {
-          const int rr = i / NCH, ch = i - rr * NCH;
-          const uint4 val = *reinterpret_cast<const uint4*>(sStg + stg_off(rr, ch));
-          *reinterpret_cast<uint4*>(pr.Z + (size_t)(row0 + rr) * N + ch * 8) = val;
-        }
+      for (int i = et; i < nvalid * NCH; i += 128) {
+        const int rr = i / NCH, ch = i - rr * NCH;
+        const uint4 val = *reinterpret_cast<const uint4*>(sStg + rr * (N * 2) + ((ch ^ (rr & SWM)) * 16));
+        *reinterpret_cast<uint4*>(pr.Z + (size_t)(row0 + rr) * N + ch * 8) = val;
       }
     }
-    if (et == 0) tc::bulk_wait0();
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == 0) {
     tc::tc_fence_after();
     tc::tmem_dealloc<C::NCOLS>(tmem);
   }
@@ -319,21 +328,17 @@ static rgnn_status gemm_fwd_tc(const GemmFwdArgs& a, cudaStream_t s) {
   const int64_t nw = (int64_t)a.num_w * K * N;
   RGNN_LAUNCH(k_w_to_bf16_t, (unsigned)std::max<int64_t>(1, std::min<int64_t>((nw + 255) / 256, 4096)), 256, 0, s,
               a.num_w, K, N, a.W, wt);
-  CUtensorMap xmap, wmap;
-  RGNN_TRY(make_tmap_2d_bf16(&xmap, a.X, K, (uint64_t)a.x_rows, K * 2, C::RB / 2, 1, C::SWZ));
+  CUtensorMap wmap;
   RGNN_TRY(make_tmap_2d_bf16(&wmap, wt, K, (uint64_t)a.num_w * N, K * 2, C::RB / 2, N, C::SWZ));
   auto kern = k_gemm_fwd_tc<K, N>;
   RGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   int dev, sms;
   RGNN_CUDA_TRY(cudaGetDevice(&dev));
   RGNN_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int64_t zrows = a.tiles ? a.z_rows : a.rows;
-  CUtensorMap zmap;
-  RGNN_TRY(make_tmap_2d_bf16(&zmap, a.Z, N, (uint64_t)std::max<int64_t>(zrows, 1), N * 2, C::ORB / 2, C::M, C::ORB));
-  TcFwdParams pr{a.tiles, a.num_tiles, a.rows, a.gofs, a.gather, static_cast<__nv_bfloat16*>(a.Z), zrows, a.row_scale,
-                 a.A, a.s_src};
+  TcFwdParams pr{a.tiles, a.num_tiles, a.rows, a.gofs, a.gather, static_cast<const __nv_bfloat16*>(a.X),
+                 static_cast<__nv_bfloat16*>(a.Z), a.row_scale, a.A, a.s_src};
   const unsigned grid = (unsigned)std::min<int64_t>(ntiles, sms);
-  RGNN_LAUNCH(kern, grid, C::THREADS, C::SMEM, s, xmap, wmap, zmap, pr);
+  RGNN_LAUNCH(kern, grid, C::THREADS, C::SMEM, s, wmap, pr);
   return RGNN_OK;
 }
 

@@ -56,21 +56,33 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
   const int lane = threadIdx.x & 31, g = lane / L, l = lane % L;
   const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  Item nit = warp0 < a.num_items ? a.items[warp0] : Item{0, 0, 0, -1};
   for (int64_t w = warp0; w < a.num_items; w += nwarps) {
-    const Item it = a.items[w];
+    const Item it = nit;
+    if (w + nwarps < a.num_items) nit = a.items[w + nwarps];  // next item's descriptor in flight
     float acc[EPL];
 #pragma unroll
     for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
     float m = -CUDART_INF_F, lsum = 0.f;
     float xv[KPL];
-    if constexpr (RGAT) load_slice<KPL>(X + (a.v0 + it.row) * (int64_t)K + l * KPL, xv);
+    if constexpr (RGAT) {
+      if (it.q1 > it.q0) load_slice<KPL>(X + (a.v0 + it.row) * (int64_t)K + l * KPL, xv);
+    }
+    // slot indices are loaded one step ahead of their use
+    int nq = it.q0 + lane;
+    bool nok = lane < B && nq < it.q1;
+    int np = nok ? a.pos[nq] : 0;
+    int nr = nok ? a.et_slot[nq] : 0;
     for (int base = it.q0; base < it.q1; base += B) {
-      const int q = base + lane;
-      const bool ok = lane < B && q < it.q1;
-      const int myp = ok ? a.pos[q] : 0;
-      const int myr = ok ? a.et_slot[q] : 0;
+      const bool ok = nok;
+      const int myp = np;
+      const int myr = nr;
       float mys = 0.f;
       if constexpr (RGAT) mys = ok ? a.s_src[myp] : 0.f;
+      nq = base + B + lane;
+      nok = lane < B && nq < it.q1;
+      np = nok ? a.pos[nq] : 0;
+      nr = nok ? a.et_slot[nq] : 0;
       uint4 zr[UNR];
       float sc[UNR];
       bool val[UNR];
