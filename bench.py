@@ -81,6 +81,8 @@ def algorithmic_bytes(phase, model, prec, K, N, E, V_own, J, num_items):
         return E * per_e + num_items * per_v
     if phase == "bwd_traverse":  # read pos, et, s_src, Z; write dZ, dpre; per row X, Y, dY, lse, item
         return E * (2 * N * b + 16) + num_items * (K * b + 2 * N * 4 + 4 + 16)
+    if phase == "bwd_fused":  # read Z, s_src, dst, src per edge, gather X_src; per (etype,dst) run G_v, Y_v, X_v, lse
+        return E * (N * b + K * b + 12) + J * (8 * N + K * b + 4)
     if phase == "gemm_dw":  # gather X rows, read dZ (RGAT) or gather G rows (RGCN), indices; dst term per run
         if model == "rgat":
             return E * (K * b + N * b + 4 + 4 + 4) + J * K * b
@@ -338,7 +340,8 @@ def run_ours(args):
     hbm, tflops, peak_src = peaks()
     v = G.view
     step_phase = {k: (tot / args.steps, n // max(args.steps, 1)) for k, (tot, n) in phases.items()}
-    cand = {k: x for k, x in step_phase.items() if k in ("gemm_fwd", "aggregate", "bwd_traverse", "gemm_dw")}
+    cand = {k: x for k, x in step_phase.items()
+            if k in ("gemm_fwd", "aggregate", "bwd_traverse", "gemm_dw", "bwd_fused")}
     roof = None
     if cand:
         dom = max(cand, key=lambda k: cand[k][0])

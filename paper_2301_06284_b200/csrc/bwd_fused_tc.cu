@@ -2,9 +2,9 @@
 //
 // One CTA per split-K chunk of positions (relation r fixed, positions in
 // (etype, dst) order).  Per 128-position stage:
-//   * warp 0 (TMA): X[src_s[p]] rows -> smem by tile::gather4 (MMA operand A,
-//     MN-major SW128), gather indices loaded one stage ahead;
-//   * warps 2..9 (CUDA cores) recompute the attention of each edge and write
+//   * warps 1..2: X[src_s[p]] rows -> smem with 16-byte cp.async (MMA operand A,
+//     MN-major SW128; TMA tile::gather4 is issue-rate bound, ~1 op / 100 cycles);
+//   * warps 3..10 (CUDA cores) recompute the attention of each edge and write
 //     its gradient row straight into the MMA's B operand in shared memory:
 //        pre = s_src[p] + x_v . U[r]            (U[r] = W_r A[r,1])
 //        alpha = exp(leaky(pre) - lse_v),  dalpha = G_v . Z[p],  S_v = G_v . Y_v
@@ -12,7 +12,7 @@
 //        dZ[p] = alpha G_v + dpre A[r,0]   -> bf16, MN-major SW128 smem line p
 //     plus dpre into a 16-column side operand (column 0) and the destination
 //     term c_r += dpre x_v in registers (SURVEY §8 backward formulas);
-//   * warp 1: tcgen05.mma  D[d_in x d_out] += X_src^T dZ  and  Db += X_src^T dpre.
+//   * warp 0: TMEM allocator, tcgen05.mma  D[d_in x d_out] += X_src^T dZ  and  Db += X_src^T dpre.
 // dZ never touches HBM (the unfused path writes and re-reads E x d_out bf16),
 // and the per-destination quantities (G_v, Y_v, x_v, lse_v) are reloaded only
 // when v changes (positions of one relation are sorted by destination).
@@ -34,7 +34,11 @@ struct BfCfg {
   static constexpr int STAGE = A_BYTES + B_BYTES + B2_BYTES;
   static constexpr int STAGES = (200 * 1024) / STAGE > 6 ? 6 : (200 * 1024) / STAGE;
   static constexpr int CW = 8;                               // compute warps
-  static constexpr int THREADS = 64 + CW * 32;
+  static constexpr int PW = 2;                               // cp.async producer warps
+  static constexpr int THREADS = 32 + PW * 32 + CW * 32;     // MMA warp, producers, compute warps
+  static constexpr int DEPTH = STAGES - 1;                   // cp.async groups in flight per producer thread
+  static constexpr int CPR = K * 2 / 16;                     // 16-byte chunks per X row
+  static constexpr int RPI = 32 / CPR;                       // X rows per warp-wide cp.async
   static constexpr int SMEM = 1024 + STAGES * STAGE + CW * K * 4 + 256;
   static constexpr int NCOLS = (N + 16) <= 32 ? 32 : (N + 16) <= 64 ? 64 : (N + 16) <= 128 ? 128 : 256;
   static constexpr uint32_t IDESC = tc::idesc_bf16(K, N, 1, 1);
@@ -70,7 +74,7 @@ __device__ __forceinline__ float leaky_f(float x, float s) { return x > 0.f ? x 
 
 template <int K, int N>
 __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
-    k_bwd_fused_tc(const __grid_constant__ CUtensorMap xmap, BwdFusedParams pr) {
+    k_bwd_fused_tc(BwdFusedParams pr) {
   using C = BfCfg<K, N>;
   constexpr int L = C::L, PG = C::PG, KPL = C::KPL, EPL = C::EPL;
   extern __shared__ uint8_t smem_raw[];
@@ -93,20 +97,19 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::STAGES; ++i) {
-      tc::mbar_init(&a_full[i], 1);
+      tc::mbar_init(&a_full[i], C::PW * 32);
       tc::mbar_init(&b_full[i], C::CW);
       tc::mbar_init(&empty[i], 1);
     }
     tc::mbar_init(acc_full, 1);
     tc::mbar_fence_init();
-    tc::tma_prefetch_desc(&xmap);
   }
   for (int i = threadIdx.x; i < C::STAGES * C::B2_BYTES / 16; i += blockDim.x) {  // dpre operand: cols 1..15 = 0
     const int s = i / (C::B2_BYTES / 16), o = i % (C::B2_BYTES / 16);
     reinterpret_cast<uint4*>(sB2(s))[o] = make_uint4(0, 0, 0, 0);
   }
   tc::fence_proxy_async_smem();
-  if (warp == 1) {
+  if (warp == 0) {
     __syncwarp();
     tc::tmem_alloc<C::NCOLS>(tmem_slot);
   }
@@ -115,31 +118,48 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer (X_src rows)
+  if (warp >= 1 && warp <= C::PW) {
+    // ------------------------------------------------------------ producers: X_src rows by cp.async
+    const int pw = warp - 1;                      // rows pw*64 .. pw*64+63 of each stage
     auto load_idx = [&](int it, int* out) {
-      const int p0 = row0 + it * C::MT;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) out[j] = __ldg(pr.src_s + min(p0 + 4 * lane + j, row1 - 1));
+      const int p0 = row0 + it * C::MT + pw * 64;
+      out[0] = __ldg(pr.src_s + min(p0 + lane, row1 - 1));
+      out[1] = __ldg(pr.src_s + min(p0 + 32 + lane, row1 - 1));
     };
-    int idx[4] = {0, 0, 0, 0};
+    int idx[2] = {0, 0};
     if (nsub > 0) load_idx(0, idx);
+    int pub = 0;
     for (int it = 0; it < nsub; ++it) {
       const int st = it % C::STAGES;
       const uint32_t use = (uint32_t)(it / C::STAGES);
-      int nidx[4] = {0, 0, 0, 0};
+      int nidx[2] = {0, 0};
       if (it + 1 < nsub) load_idx(it + 1, nidx);
       if (use > 0) tc::mbar_wait(&empty[st], (use - 1) & 1);
-      if (lane == 0) tc::mbar_expect_tx(&a_full[st], C::A_BYTES);
-      __syncwarp();
-#pragma unroll
-      for (int kb = 0; kb < K / 64; ++kb)
-        tc::tma_gather4(sA(st) + kb * C::MT * 128 + lane * 4 * 128, &xmap, &a_full[st], kb * 64, idx[0], idx[1],
-                        idx[2], idx[3]);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) idx[j] = nidx[j];
+      uint8_t* a = sA(st);
+#pragma unroll 4
+      for (int i = 0; i < 64 / C::RPI; ++i) {
+        const int rr = i * C::RPI + lane / C::CPR;  // row within this warp's 64
+        const int c = lane % C::CPR;
+        const int row = pw * 64 + rr;
+        const int xr = __shfl_sync(0xffffffffu, rr < 32 ? idx[0] : idx[1], rr & 31);
+        // MN-major SW128: feature block c/8 at (MT*128), line `row`, chunk (c%8) ^ (row%8)
+        tc::cp_async16(a + (c >> 3) * (C::MT * 128) + row * 128 + (((c & 7) ^ (row & 7)) << 4),
+                       pr.X + (size_t)xr * K + c * 8);
+      }
+      tc::cp_async_commit();
+      if (it - pub >= C::DEPTH) {
+        tc::cp_async_wait<C::DEPTH>();
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(&a_full[pub % C::STAGES]);
+        ++pub;
+      }
+      idx[0] = nidx[0];
+      idx[1] = nidx[1];
     }
-  } else if (warp == 1) {
+    tc::cp_async_wait<0>();
+    tc::fence_proxy_async_smem();
+    for (; pub < nsub; ++pub) tc::mbar_arrive(&a_full[pub % C::STAGES]);
+  } else if (warp == 0) {
     // ------------------------------------------------------------ MMA issuer
     for (int it = 0; it < nsub; ++it) {
       const int st = it % C::STAGES;
@@ -165,7 +185,7 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
     }
   } else {
     // ------------------------------------------------------------ compute warps: dZ -> smem B operand
-    const int cw = warp - 2;                 // 0..7
+    const int cw = warp - 1 - C::PW;         // 0..7
     const int g = lane / L, l = lane % L;    // lane group (one position at a time), lane within group
     const float* Ur = pr.U + (size_t)r * K + l * KPL;
     const float* A0 = pr.A + (size_t)r * 2 * N + l * EPL;
@@ -221,10 +241,14 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
               s1 = fmaf(gg.x, yy.x, s1); s1 = fmaf(gg.y, yy.y, s1); s1 = fmaf(gg.z, yy.z, s1); s1 = fmaf(gg.w, yy.w, s1);
             }
 #pragma unroll
-            for (int j = 0; j < KPL; ++j) {
-              xv[j] = __bfloat162float(xp[j]);
-              s2 = fmaf(xv[j], u[j], s2);
+            for (int j = 0; j < KPL; j += 8) {
+              float xf[8];
+              Vec16<__nv_bfloat16>{ldg16(xp + j)}.to_float(xf);
+#pragma unroll
+              for (int t = 0; t < 8; ++t) xv[j + t] = xf[t];
             }
+#pragma unroll
+            for (int j = 0; j < KPL; ++j) s2 = fmaf(xv[j], u[j], s2);
 #pragma unroll
             for (int o = L / 2; o > 0; o >>= 1) {
               s1 += __shfl_xor_sync(gmask, s1, o);
@@ -279,7 +303,7 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
     // epilogue: TMEM accumulators -> part[c]; two warps per lane quarter split the columns
     tc::mbar_wait(acc_full, 0);
     tc::tc_fence_after();
-    const int q = warp & 3, half = cw >> 2;  // warps 2..5 -> half 0, 6..9 -> half 1
+    const int q = warp & 3, half = cw >> 2;  // warps 3..6 -> half 0, 7..10 -> half 1 (each quarter twice)
     const int row = K == 128 ? q * 32 + lane : q * 16 + lane;
     const bool rvalid = K == 128 || lane < 16;
     float* out = pr.part + (size_t)blockIdx.x * (K * N + K);
@@ -312,7 +336,7 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
     for (int w = 0; w < C::CW; ++w) s += s_c[w * K + k];
     pr.cpart[(size_t)blockIdx.x * K + k] = s;
   }
-  if (warp == 1) {
+  if (warp == 0) {
     tc::tc_fence_after();
     tc::tmem_dealloc<C::NCOLS>(tmem);
   }
@@ -322,11 +346,10 @@ template <int K, int N>
 static rgnn_status bwd_fused(const rgnn_graph* g, const BwdFusedParams& p0, const void* X, cudaStream_t s) {
   using C = BfCfg<K, N>;
   if (g->num_chunks == 0) return RGNN_OK;
-  CUtensorMap xmap;
-  RGNN_TRY(make_tmap_2d_bf16(&xmap, X, K, (uint64_t)g->V, K * 2, 64, 1, 128));
+  (void)X;
   auto kern = k_bwd_fused_tc<K, N>;
   RGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-  RGNN_LAUNCH(kern, (unsigned)g->num_chunks, C::THREADS, C::SMEM, s, xmap, p0);
+  RGNN_LAUNCH(kern, (unsigned)g->num_chunks, C::THREADS, C::SMEM, s, p0);
   return RGNN_OK;
 }
 
