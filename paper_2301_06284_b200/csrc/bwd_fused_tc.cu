@@ -33,7 +33,7 @@ struct BfCfg {
   static constexpr int B2_BYTES = MT * 16 * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES + B2_BYTES;
   static constexpr int STAGES = (200 * 1024) / STAGE > 6 ? 6 : (200 * 1024) / STAGE;
-  static constexpr int CW = 8;                               // compute warps
+  static constexpr int CW = 16;                              // compute warps
   static constexpr int PW = 2;                               // cp.async producer warps
   static constexpr int THREADS = 32 + PW * 32 + CW * 32;     // MMA warp, producers, compute warps
   static constexpr int DEPTH = STAGES - 1;                   // cp.async groups in flight per producer thread
@@ -47,7 +47,7 @@ struct BfCfg {
   static constexpr int EPL = 8;
   static constexpr int L = N / EPL;
   static constexpr int G = 32 / L;
-  static constexpr int PPW = MT / CW;                        // positions per warp per stage (16)
+  static constexpr int PPW = MT / CW;                        // positions per warp per stage (8)
   static constexpr int PG = PPW / G;                         // positions per lane group
   static constexpr int KPL = K / L;                          // x_v features per lane
 };
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
       const uint32_t use = (uint32_t)(it / C::STAGES);
       const int pbase = row0 + it * C::MT + cw * C::PPW;  // this warp's 16 positions
       // cooperative loads of dst and s_src for the warp's positions
-      const int pl = pbase + (lane & 15);
+      const int pl = pbase + (lane % C::PPW);
       const bool okl = lane < C::PPW && pl < row1;
       const int myv = okl ? __ldg(pr.dst_s + pl) : -1;
       const float mys = okl ? __ldg(pr.s_src + pl) : 0.f;
@@ -303,11 +303,11 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
     // epilogue: TMEM accumulators -> part[c]; two warps per lane quarter split the columns
     tc::mbar_wait(acc_full, 0);
     tc::tc_fence_after();
-    const int q = warp & 3, half = cw >> 2;  // warps 3..6 -> half 0, 7..10 -> half 1 (each quarter twice)
+    const int q = warp & 3, half = cw >> 2;  // 16 compute warps: each TMEM lane quarter read by 4 warps
     const int row = K == 128 ? q * 32 + lane : q * 16 + lane;
     const bool rvalid = K == 128 || lane < 16;
     float* out = pr.part + (size_t)blockIdx.x * (K * N + K);
-    constexpr int HALF = N / 2;
+    constexpr int HALF = N / (C::CW / 4);
 #pragma unroll
     for (int c0 = half * HALF; c0 < (half + 1) * HALF; c0 += 16) {
       uint32_t v[16];

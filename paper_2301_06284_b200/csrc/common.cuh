@@ -87,6 +87,8 @@ struct rgnn_graph {
   float* inv_c;
   rgnn::Item* items;
   rgnn::SplitRow* split_rows;
+  int32_t* empty_rows;  // rows without in-edges (no work item)
+  int64_t num_empty;
   rgnn::Tile* tiles;   // 128-row GEMM tiles (never straddle relations)
   rgnn::Tile* chunks;  // dW split-K chunks (never straddle relations)
   int32_t* chunk_seg;  // [R+1] chunks of relation r

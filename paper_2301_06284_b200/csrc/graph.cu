@@ -18,12 +18,12 @@
 namespace rgnn {
 
 struct Counters {
-  int32_t bad_edge, bad_node, E_own, J, num_items, num_parts, num_split_rows, pad;
+  int32_t bad_edge, bad_node, E_own, J, num_items, num_parts, num_split_rows, num_empty;
 };
 
 __global__ void k_init_counters(Counters* c, int32_t big) {
   c->bad_edge = big; c->bad_node = big; c->E_own = 0; c->J = 0;
-  c->num_items = 0; c->num_parts = 0; c->num_split_rows = 0; c->pad = 0;
+  c->num_items = 0; c->num_parts = 0; c->num_split_rows = 0; c->num_empty = 0;
 }
 
 // CSR-by-dst input: dst of every edge from row_ptr (one warp per row).
@@ -157,16 +157,25 @@ __global__ void k_inv_c(int64_t n, int norm, const int32_t* __restrict__ head, c
   }
 }
 
-// Work list: rows with more than cap in-edges are split into ceil(deg/cap) chunks.
+// Work list: rows with more than cap in-edges are split into ceil(deg/cap) chunks;
+// rows without in-edges get no item and go to the empty-row list (Y = 0 / self term).
 __global__ void k_item_counts(int64_t V_own, const int32_t* __restrict__ row_ptr, int cap, int32_t* __restrict__ n_items,
-                              int32_t* __restrict__ n_parts, int32_t* __restrict__ n_split) {
+                              int32_t* __restrict__ n_parts, int32_t* __restrict__ n_split,
+                              int32_t* __restrict__ n_empty) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < V_own; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t deg = row_ptr[i + 1] - row_ptr[i];
-    int32_t c = deg > cap ? (deg + cap - 1) / cap : 1;
+    int32_t c = deg > cap ? (deg + cap - 1) / cap : (deg > 0 ? 1 : 0);
     n_items[i] = c;
     n_parts[i] = c > 1 ? c : 0;
     n_split[i] = c > 1 ? 1 : 0;
+    n_empty[i] = deg == 0 ? 1 : 0;
   }
+}
+
+__global__ void k_fill_empty(int64_t V_own, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ empty_ex,
+                             int32_t* __restrict__ empty_rows) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < V_own; i += (int64_t)gridDim.x * blockDim.x)
+    if (row_ptr[i + 1] == row_ptr[i]) empty_rows[empty_ex[i]] = (int32_t)i;
 }
 
 __global__ void k_fill_items(int64_t V_own, const int32_t* __restrict__ row_ptr, int cap,
@@ -175,7 +184,7 @@ __global__ void k_fill_items(int64_t V_own, const int32_t* __restrict__ row_ptr,
                              SplitRow* __restrict__ split_rows) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < V_own; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t lo = row_ptr[i], hi = row_ptr[i + 1], deg = hi - lo;
-    int32_t c = deg > cap ? (deg + cap - 1) / cap : 1;
+    int32_t c = deg > cap ? (deg + cap - 1) / cap : (deg > 0 ? 1 : 0);
     int32_t b = item_ex[i];
     for (int32_t k = 0; k < c; ++k) {
       Item it;
@@ -206,12 +215,13 @@ struct GraphLayout {
   float* inv_c;
   Item* items;
   SplitRow* split_rows;
+  int32_t* empty_rows;
   Tile *tiles, *chunks;
   int32_t* chunk_seg;
   size_t dev_bytes;
   // scratch
   Counters* ctr;
-  int32_t *dst_tmp, *flags, *head, *run_ex, *et_s, *n_items, *n_parts, *n_split, *rseg_cnt;
+  int32_t *dst_tmp, *flags, *head, *run_ex, *et_s, *n_items, *n_parts, *n_split, *n_empty, *rseg_cnt;
   uint32_t *k0, *v0, *k1, *v1;
   void* prim;
   size_t prim_bytes, scratch_bytes;
@@ -238,6 +248,7 @@ static GraphLayout layout(const rgnn_graph_desc* d, void* dev, void* scr) {
   L.row_ptr = c.take<int32_t>(V_own + 1);
   L.items = c.take<Item>(V_own + Ec / cap + 1);
   L.split_rows = c.take<SplitRow>(Ec / cap + 1);
+  L.empty_rows = c.take<int32_t>(V_own + 1);
   L.tiles = c.take<Tile>(Ec / kTileRows + R + 1);
   L.chunks = c.take<Tile>(max_chunks(E, R));
   L.chunk_seg = c.take<int32_t>(R + 1);
@@ -252,6 +263,7 @@ static GraphLayout layout(const rgnn_graph_desc* d, void* dev, void* scr) {
   L.n_items = s.take<int32_t>(V_own + 1);
   L.n_parts = s.take<int32_t>(V_own + 1);
   L.n_split = s.take<int32_t>(V_own + 1);
+  L.n_empty = s.take<int32_t>(V_own + 1);
   L.rseg_cnt = s.take<int32_t>(R + 1);
   L.k0 = s.take<uint32_t>(Ec);
   L.v0 = s.take<uint32_t>(Ec);
@@ -377,7 +389,10 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
                 L.inv_c);
   // Destination-walk work list.
   if (V_own > 0) {
-    RGNN_LAUNCH(k_item_counts, grid_for(V_own), T, 0, s, V_own, L.row_ptr, cap, L.n_items, L.n_parts, L.n_split);
+    RGNN_LAUNCH(k_item_counts, grid_for(V_own), T, 0, s, V_own, L.row_ptr, cap, L.n_items, L.n_parts, L.n_split,
+                L.n_empty);
+    RGNN_TRY(scan_exclusive(L.n_empty, L.n_empty, V_own, &L.ctr->num_empty, L.prim, L.prim_bytes, s));
+    RGNN_LAUNCH(k_fill_empty, grid_for(V_own), T, 0, s, V_own, L.row_ptr, L.n_empty, L.empty_rows);
     RGNN_TRY(scan_exclusive(L.n_items, L.n_items, V_own, &L.ctr->num_items, L.prim, L.prim_bytes, s));
     RGNN_TRY(scan_exclusive(L.n_parts, L.n_parts, V_own, &L.ctr->num_parts, L.prim, L.prim_bytes, s));
     RGNN_TRY(scan_exclusive(L.n_split, L.n_split, V_own, &L.ctr->num_split_rows, L.prim, L.prim_bytes, s));
@@ -423,6 +438,7 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   g->perm = L.perm; g->src_s = L.src_s; g->dst_s = L.dst_s; g->seg = L.seg; g->row_ptr = L.row_ptr;
   g->pos = L.pos; g->et_slot = L.et_slot; g->run_ptr = L.run_ptr; g->rseg = L.rseg; g->inv_c = L.inv_c;
   g->items = L.items; g->split_rows = L.split_rows; g->tiles = L.tiles; g->chunks = L.chunks;
+  g->empty_rows = L.empty_rows; g->num_empty = h.num_empty;
   g->chunk_seg = L.chunk_seg;
   g->seg_host = seg_h;
   g->chunk_seg_host = chunk_seg;

@@ -73,6 +73,8 @@ struct AggArgs {
   float* part;           // [num_parts, N+4]
   const SplitRow* split_rows;
   int64_t num_split_rows;
+  const int32_t* empty_rows;
+  int64_t num_empty;
 };
 rgnn_status launch_aggregate(int prec, int K, int N, bool rgat, const AggArgs& a, cudaStream_t s);
 

@@ -116,7 +116,7 @@ static rgnn_status forward(const rgnn_graph* g, int model, int K, int N, int pre
   AggArgs aa{};
   aa.items = g->items; aa.num_items = g->num_items; aa.pos = g->pos; aa.et_slot = g->et_slot; aa.X = X;
   aa.v0 = g->v0; aa.slope = slope; aa.Y = Y; aa.part = w.part; aa.split_rows = g->split_rows;
-  aa.num_split_rows = g->num_split_rows;
+  aa.num_split_rows = g->num_split_rows; aa.empty_rows = g->empty_rows; aa.num_empty = g->num_empty;
   if (model == RGNN_RGAT) {
     { Phase ph("fold_u", s); RGNN_TRY(launch_fold_u(prec, g->R, K, N, W, A, w.U, s)); }
     ga.Z = sv.Z; ga.A = A; ga.s_src = sv.s_src;

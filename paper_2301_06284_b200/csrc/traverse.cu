@@ -41,10 +41,34 @@ struct WalkShape {
   static_assert(K % L == 0, "K must be a multiple of the lane group");
 };
 
+// KPL consecutive features -> fp32 registers, 16-byte loads when the slice allows it.
 template <int KPL, typename T>
 __device__ __forceinline__ void load_slice(const T* p, float* out) {
+  constexpr int V = 16 / sizeof(T);
+  if constexpr (KPL % V == 0) {
 #pragma unroll
-  for (int i = 0; i < KPL; ++i) out[i] = to_f(p[i]);
+    for (int i = 0; i < KPL; i += V) Vec16<T>{ldg16(p + i)}.to_float(out + i);
+  } else {
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) out[i] = to_f(p[i]);
+  }
+}
+
+// x . U[r] over this lane's KPL features (U fp32, float4 loads when possible).
+template <int KPL>
+__device__ __forceinline__ float dot_u(const float* xv, const float* Ur) {
+  float d = 0.f;
+  if constexpr (KPL % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < KPL; i += 4) {
+      const float4 u = __ldg(reinterpret_cast<const float4*>(Ur + i));
+      d = fmaf(xv[i], u.x, d); d = fmaf(xv[i + 1], u.y, d); d = fmaf(xv[i + 2], u.z, d); d = fmaf(xv[i + 3], u.w, d);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) d = fmaf(xv[i], __ldg(Ur + i), d);
+  }
+  return d;
 }
 
 template <typename T, int K, int N, bool RGAT>
@@ -95,10 +119,7 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
         val[u] = base + j < it.q1;
         zr[u] = val[u] ? ldg16(Z + (size_t)p * N + l * EPL) : make_uint4(0, 0, 0, 0);
         if constexpr (RGAT) {
-          const float* Ur = a.U + (size_t)r * K + l * KPL;
-          float d = 0.f;
-#pragma unroll
-          for (int i = 0; i < KPL; ++i) d = fmaf(xv[i], __ldg(Ur + i), d);
+          const float d = dot_u<KPL>(xv, a.U + (size_t)r * K + l * KPL);
           sc[u] = l == 0 ? d + ss : d;  // lane partial; s_src added once, then reduced
         }
       }
@@ -338,10 +359,7 @@ __global__ void __launch_bounds__(256) k_bwd_rgat(BwdArgs a) {
         const float ss = __shfl_sync(0xffffffffu, mys, j);
         val[u] = base + j < it.q1;
         zr[u] = val[u] ? ldg16(Z + (size_t)pp[u] * N + l * EPL) : make_uint4(0, 0, 0, 0);
-        const float* Ur = a.U + (size_t)rr[u] * K + l * KPL;
-        float d = 0.f;
-#pragma unroll
-        for (int i = 0; i < KPL; ++i) d = fmaf(xv[i], __ldg(Ur + i), d);
+        const float d = dot_u<KPL>(xv, a.U + (size_t)rr[u] * K + l * KPL);
         sc[u] = l == 0 ? d + ss : d;
       }
 #pragma unroll
@@ -380,6 +398,25 @@ __global__ void __launch_bounds__(256) k_bwd_rgat(BwdArgs a) {
   }
 }
 
+// Rows without in-edges: Y_v = 0 (RGCN: the self-loop row X_v W0 if present), lse_v = -inf.
+template <typename T, int N>
+__global__ void __launch_bounds__(256) k_empty_rows(AggArgs a) {
+  constexpr int NCH = N / 4;  // float4 chunks per Y row
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.num_empty * NCH;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i / NCH;
+    const int c = (int)(i - k * NCH);
+    const int row = a.empty_rows[k];
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (a.Z0) {
+      const T* z = static_cast<const T*>(a.Z0) + (size_t)row * N + c * 4;
+      v = make_float4(to_f(z[0]), to_f(z[1]), to_f(z[2]), to_f(z[3]));
+    }
+    reinterpret_cast<float4*>(a.Y + (size_t)row * N)[c] = v;
+    if (a.lse && c == 0) a.lse[row] = -CUDART_INF_F;
+  }
+}
+
 static unsigned warps_grid(int64_t items) {
   int64_t blocks = (items + 7) / 8;
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 16));
@@ -387,6 +424,10 @@ static unsigned warps_grid(int64_t items) {
 
 template <typename T, int K, int N>
 static rgnn_status aggregate(bool rgat, const AggArgs& a, cudaStream_t s) {
+  if (a.num_empty > 0) {
+    const int64_t n = a.num_empty * (N / 4);
+    RGNN_LAUNCH((k_empty_rows<T, N>), (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, s, a);
+  }
   if (a.num_items > 0) {
     if (rgat) RGNN_LAUNCH((k_aggregate<T, K, N, true>), warps_grid(a.num_items), 256, 0, s, a);
     else RGNN_LAUNCH((k_aggregate<T, K, N, false>), warps_grid(a.num_items), 256, 0, s, a);
