@@ -59,12 +59,27 @@ def workload(args):
     return cfg, model, prec
 
 
+L2_BYTES = 126 * 1024 * 1024
+
+
+def working_set_bytes(cfg, prec, g):
+    b = 2 if prec == "bf16" else 4
+    return g.V * cfg.K * b + 2 * g.E * cfg.N * b + 2 * g.V * cfg.N * 4 + 16 * g.E
+
+
+def needs_flush(cfg, prec, g):
+    return working_set_bytes(cfg, prec, g) < 4 * L2_BYTES
+
+
 def config_json(cfg, model, prec, g, world):
+    ws = working_set_bytes(cfg, prec, g)
+    l2 = ("L2 flushed between timed steps (write of a 512 MB buffer outside the per-step events); working set %.0f MB"
+          % (ws / 1e6)) if needs_flush(cfg, prec, g) else (
+        "no flush: per-step inputs larger than L2 (X %.0f MB, Z %.0f MB)" % (
+            g.V * cfg.K * (2 if prec == "bf16" else 4) / 1e6, g.E * cfg.N * (2 if prec == "bf16" else 4) / 1e6))
     return {"workload": f"{cfg.name}-shaped heterograph, {model.upper()} layer fwd+bwd, d={cfg.K}",
             "model": model, "prec": prec, "V": int(g.V), "E": int(g.E), "R": int(g.R), "d_in": cfg.K,
-            "d_out": cfg.N, "seeds": "graph 0, X 1, W 2, A 3, dY 4 (synth/)",
-            "l2": "no flush: per-step inputs larger than L2 (X %.0f MB, Z %.0f MB)" % (
-                g.V * cfg.K * (2 if prec == "bf16" else 4) / 1e6, g.E * cfg.N * (2 if prec == "bf16" else 4) / 1e6),
+            "d_out": cfg.N, "seeds": "graph 0, X 1, W 2, A 3, dY 4 (synth/)", "l2": l2,
             "parallelism": f"dst-range partition x{world} (NCCL Y gather + dW all-reduce)" if world > 1
             else "1 GPU"}
 
@@ -279,19 +294,34 @@ def run_ours(args):
     time.sleep(0.3 if clk else 0)
     m._binding.profile_enable(True)
     m._binding.profile_read()
+    flush = needs_flush(cfg, prec, g)
+    fbuf = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev) if flush else None
     l0 = m.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    barrier()
+    if not flush:  # inputs larger than L2: one event pair around the K steps
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+        ms = e0.elapsed_time(e1) / args.steps
+    else:  # small working set: flush L2 between steps, time each step with its own events
+        evs = []
+        barrier()
+        for _ in range(args.steps):
+            fbuf.fill_(1)
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            step()
+            b_.record(stream)
+            evs.append((a_, b_))
+        barrier()
+        ms = sum(a_.elapsed_time(b_) for a_, b_ in evs) / args.steps
     launches = m.launch_count() - l0
     phases = m._binding.profile_read()
     m._binding.profile_enable(False)
     clocks = sample_clocks_stop(clk, clk_path, local)
-    ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
         tm = torch.tensor([ms], device=dev)
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)

@@ -200,22 +200,35 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
     int cur_v = -1;
     float gv[EPL], xv[KPL], Sv = 0.f, dsc = 0.f, lse = 0.f;
     const uint32_t gmask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (g * L));
-    for (int it = 0; it < nsub; ++it) {
-      const int st = it % C::STAGES;
-      const uint32_t use = (uint32_t)(it / C::STAGES);
-      const int pbase = row0 + it * C::MT + cw * C::PPW;  // this warp's 16 positions
-      // cooperative loads of dst and s_src for the warp's positions
-      const int pl = pbase + (lane % C::PPW);
+    // dst and s_src of the warp's positions (lanes < PPW), loaded one stage ahead; Z rows of the
+    // group's positions one stage ahead as well (their latency overlaps the current stage)
+    auto load_pos = [&](int it, int& v, float& sv) {
+      const int pl = row0 + it * C::MT + cw * C::PPW + (lane % C::PPW);
       const bool okl = lane < C::PPW && pl < row1;
-      const int myv = okl ? __ldg(pr.dst_s + pl) : -1;
-      const float mys = okl ? __ldg(pr.s_src + pl) : 0.f;
-      // Z rows of this group's positions, issued before the wait
-      uint4 zr[PG];
+      v = okl ? __ldg(pr.dst_s + pl) : -1;
+      sv = okl ? __ldg(pr.s_src + pl) : 0.f;
+    };
+    auto load_z = [&](int it, uint4* z) {
+      const int pbase = row0 + it * C::MT + cw * C::PPW;
 #pragma unroll
       for (int i = 0; i < PG; ++i) {
         const int p = pbase + g * PG + i;
-        zr[i] = p < row1 ? ldg_nc16(pr.Z + (size_t)p * N + l * EPL) : make_uint4(0, 0, 0, 0);
+        z[i] = p < row1 ? ldg_nc16(pr.Z + (size_t)p * N + l * EPL) : make_uint4(0, 0, 0, 0);
       }
+    };
+    int nv = -1;
+    float ns = 0.f;
+    uint4 nz[PG];
+    if (nsub > 0) { load_pos(0, nv, ns); load_z(0, nz); }
+    for (int it = 0; it < nsub; ++it) {
+      const int st = it % C::STAGES;
+      const uint32_t use = (uint32_t)(it / C::STAGES);
+      const int myv = nv;
+      const float mys = ns;
+      uint4 zr[PG];
+#pragma unroll
+      for (int i = 0; i < PG; ++i) zr[i] = nz[i];
+      if (it + 1 < nsub) { load_pos(it + 1, nv, ns); load_z(it + 1, nz); }
       if (use > 0) tc::mbar_wait(&empty[st], (use - 1) & 1);
       uint8_t* b = sB(st);
       uint8_t* b2 = sB2(st);

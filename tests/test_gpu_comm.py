@@ -1,0 +1,52 @@
+"""The library's NCCL path on one GPU (nranks = 1): rgnn_comm_create, the grouped
+broadcast gather of Y into Y_full and the in-place all-reduce of dW / dA must
+reproduce the communicator-free call bit for bit.  Multi-rank composition is
+covered on CPU by tests/test_multirank_cpu.py (gloo)."""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("model", ["rgat", "rgcn"])
+def test_single_rank_nccl_matches_no_comm(rgnn, model):
+    import torch
+    g = synth.make_graph(synth.get_config("bgs").scaled(10))
+    t = synth.make_tensors(g.V, g.R, 64, 64)
+    G = rgnn.Graph(g.V, g.src, g.dst, g.etype, g.R)
+    X = torch.from_numpy(t.X).cuda().to(torch.bfloat16)
+    W, A = torch.from_numpy(t.W).cuda(), torch.from_numpy(t.A).cuda()
+    dY = torch.from_numpy(t.dY).cuda()
+    comm = rgnn.Comm([0, g.V], 0, 1)
+
+    def run(c):
+        Y_full = torch.full((g.V, 64), float("nan"), device="cuda") if c else None
+        if model == "rgat":
+            Y, ws = rgnn.rgat_forward(G, X, W, A, prec="bf16", comm=c, Y_full=Y_full)
+        else:
+            Y, ws = rgnn.rgcn_forward(G, X, W, prec="bf16", comm=c, Y_full=Y_full)
+        dW, dA, _ = rgnn.rgnn_backward(G, model, X, W, dY, ws, A=A if model == "rgat" else None, Y=Y, prec="bf16",
+                                       comm=c)
+        torch.cuda.synchronize()
+        return Y, Y_full, dW, dA
+
+    Y0, _, dW0, dA0 = run(None)
+    Y1, Yf, dW1, dA1 = run(comm)
+    assert torch.equal(Y0, Y1) and torch.equal(Yf, Y1)
+    assert torch.equal(dW0, dW1)
+    if model == "rgat":
+        assert torch.equal(dA0, dA1)
+
+
+def test_comm_rejects_mismatched_range(rgnn):
+    import torch
+    g = synth.random_graph(100, 500, 3, seed=2)
+    G = rgnn.Graph(g.V, g.src, g.dst, g.etype, g.R, dst_begin=0, dst_end=50)
+    comm = rgnn.Comm([0, g.V], 0, 1)
+    X = torch.zeros(g.V, 32, device="cuda")
+    W = torch.zeros(g.R, 32, 32, device="cuda")
+    with pytest.raises(rgnn.RgnnError) as ei:
+        rgnn.rgcn_forward(G, X, W, prec="f32", comm=comm)
+    assert ei.value.status == 1
