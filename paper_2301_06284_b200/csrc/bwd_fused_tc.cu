@@ -64,6 +64,7 @@ struct BwdFusedParams {
   const float* dY;
   const float* U;
   const float* A;
+  const float* inv_c;  // RGCN: 1/c_{v,r} per position
   float slope;
   int64_t v0;
   float* part;
@@ -72,7 +73,8 @@ struct BwdFusedParams {
 
 __device__ __forceinline__ float leaky_f(float x, float s) { return x > 0.f ? x : s * x; }
 
-template <int K, int N>
+// GAT = true: RGAT (dZ = alpha G_v + dpre A[r,0], bvec, dst term); false: RGCN (dZ = G_v / c_{v,r}).
+template <int K, int N, bool GAT>
 __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
     k_bwd_fused_tc(BwdFusedParams pr) {
   using C = BfCfg<K, N>;
@@ -175,8 +177,10 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
           const uint64_t ad = tc::umma_desc(a0 + ks * 16 * 128, C::MT * 128, 1024, 2u);
           const uint64_t bd = tc::umma_desc(b0 + ks * 16 * 128, C::MT * 128, 1024, 2u);
           tc::umma_bf16(tmem, ad, bd, C::IDESC, acc);
-          const uint64_t cd = tc::umma_desc(c0 + ks * 512, 256, 128, 0u);
-          tc::umma_bf16(tmem + N, ad, cd, C::IDESC_B, acc);
+          if (GAT) {
+            const uint64_t cd = tc::umma_desc(c0 + ks * 512, 256, 128, 0u);
+            tc::umma_bf16(tmem + N, ad, cd, C::IDESC_B, acc);
+          }
         }
         tc::umma_commit(&empty[st]);
         if (it == nsub - 1) tc::umma_commit(acc_full);
@@ -187,13 +191,15 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
     // ------------------------------------------------------------ compute warps: dZ -> smem B operand
     const int cw = warp - 1 - C::PW;         // 0..7
     const int g = lane / L, l = lane % L;    // lane group (one position at a time), lane within group
-    const float* Ur = pr.U + (size_t)r * K + l * KPL;
-    const float* A0 = pr.A + (size_t)r * 2 * N + l * EPL;
     float u[KPL], a0[EPL];
+    if constexpr (GAT) {
+      const float* Ur = pr.U + (size_t)r * K + l * KPL;
+      const float* A0 = pr.A + (size_t)r * 2 * N + l * EPL;
 #pragma unroll
-    for (int i = 0; i < KPL; ++i) u[i] = __ldg(Ur + i);
+      for (int i = 0; i < KPL; ++i) u[i] = __ldg(Ur + i);
 #pragma unroll
-    for (int i = 0; i < EPL; ++i) a0[i] = __ldg(A0 + i);
+      for (int i = 0; i < EPL; ++i) a0[i] = __ldg(A0 + i);
+    }
     float cacc[KPL];
 #pragma unroll
     for (int i = 0; i < KPL; ++i) cacc[i] = 0.f;
@@ -206,9 +212,10 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
       const int pl = row0 + it * C::MT + cw * C::PPW + (lane % C::PPW);
       const bool okl = lane < C::PPW && pl < row1;
       v = okl ? __ldg(pr.dst_s + pl) : -1;
-      sv = okl ? __ldg(pr.s_src + pl) : 0.f;
+      sv = okl ? __ldg((GAT ? pr.s_src : pr.inv_c) + pl) : 0.f;
     };
     auto load_z = [&](int it, uint4* z) {
+      if constexpr (!GAT) return;
       const int pbase = row0 + it * C::MT + cw * C::PPW;
 #pragma unroll
       for (int i = 0; i < PG; ++i) {
@@ -240,7 +247,19 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
         const float ss = __shfl_sync(0xffffffffu, mys, src_lane);
         float dz[EPL];
         float dpre = 0.f;
-        if (v >= 0) {
+        if (v >= 0 && !GAT) {  // RGCN: dZ[p] = G_v / c_{v,r}
+          if (v != cur_v) {
+            const float* gp = pr.dY + (size_t)v * N + l * EPL;
+#pragma unroll
+            for (int j = 0; j < EPL; j += 4) {
+              const float4 gg = __ldg(reinterpret_cast<const float4*>(gp + j));
+              gv[j] = gg.x; gv[j + 1] = gg.y; gv[j + 2] = gg.z; gv[j + 3] = gg.w;
+            }
+            cur_v = v;
+          }
+#pragma unroll
+          for (int j = 0; j < EPL; ++j) dz[j] = gv[j] * ss;
+        } else if (v >= 0) {
           if (v != cur_v) {  // per-destination values (group-uniform branch)
             const float* gp = pr.dY + (size_t)v * N + l * EPL;
             const float* yp = pr.Y + (size_t)v * N + l * EPL;
@@ -295,7 +314,8 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
         o.x = tc::pack_bf16(dz[0], dz[1]); o.y = tc::pack_bf16(dz[2], dz[3]);
         o.z = tc::pack_bf16(dz[4], dz[5]); o.w = tc::pack_bf16(dz[6], dz[7]);
         *reinterpret_cast<uint4*>(b + (l >> 3) * (C::MT * 128) + lp * 128 + (((l & 7) ^ (lp & 7)) << 4)) = o;
-        if (l == 0) *reinterpret_cast<__nv_bfloat16*>(b2 + (lp >> 3) * 256 + (lp & 7) * 16) = __float2bfloat16_rn(dpre);
+        if (GAT && l == 0)
+          *reinterpret_cast<__nv_bfloat16*>(b2 + (lp >> 3) * 256 + (lp & 7) * 16) = __float2bfloat16_rn(dpre);
       }
       tc::fence_proxy_async_smem();
       __syncwarp();
@@ -338,7 +358,7 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
       uint32_t v[16];
       tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + N, v);
       tc::tmem_ld_wait();
-      if (rvalid) out[K * N + row] = __uint_as_float(v[0]);
+      if (rvalid) out[K * N + row] = GAT ? __uint_as_float(v[0]) : 0.f;
     }
   }
   tc::tc_fence_before();
@@ -360,7 +380,7 @@ static rgnn_status bwd_fused(const rgnn_graph* g, const BwdFusedParams& p0, cons
   using C = BfCfg<K, N>;
   if (g->num_chunks == 0) return RGNN_OK;
   (void)X;
-  auto kern = k_bwd_fused_tc<K, N>;
+  auto kern = p0.s_src ? k_bwd_fused_tc<K, N, true> : k_bwd_fused_tc<K, N, false>;
   RGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   RGNN_LAUNCH(kern, (unsigned)g->num_chunks, C::THREADS, C::SMEM, s, p0);
   return RGNN_OK;
@@ -368,13 +388,14 @@ static rgnn_status bwd_fused(const rgnn_graph* g, const BwdFusedParams& p0, cons
 
 bool tc_disabled();
 
+// RGAT when s_src != null, RGCN (dZ = G_v / c_{v,r}) otherwise.
 rgnn_status launch_bwd_fused_tc(int K, int N, const rgnn_graph* g, const void* X, const void* Z, const float* s_src,
                                 const float* lse, const float* Y, const float* dY, const float* U, const float* A,
                                 float slope, float* part, float* cpart, cudaStream_t s) {
   if (tc_disabled()) return RGNN_E_UNSUPPORTED;
   if (getenv("RGNN_DISABLE_FUSED_BWD")) return RGNN_E_UNSUPPORTED;
   BwdFusedParams p{g->chunks, g->src_s, g->dst_s, s_src, static_cast<const __nv_bfloat16*>(Z),
-                   static_cast<const __nv_bfloat16*>(X), lse, Y, dY, U, A, slope, g->v0, part, cpart};
+                   static_cast<const __nv_bfloat16*>(X), lse, Y, dY, U, A, g->inv_c, slope, g->v0, part, cpart};
   if (K == 64 && N == 64) return bwd_fused<64, 64>(g, p, X, s);
   if (K == 64 && N == 128) return bwd_fused<64, 128>(g, p, X, s);
   if (K == 128 && N == 64) return bwd_fused<128, 64>(g, p, X, s);

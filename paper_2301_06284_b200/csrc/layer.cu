@@ -220,13 +220,22 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, g->chunk_seg, w.cpart, A, W, dW, dA, w.vsum, s)); }
     }
   } else {
-    if (tc_ok) {  // dZ[p] = bf16(1/c * G[dst]) materialised in position order, then the tensor-core dW
-      { Phase ph("expand_dz", s); RGNN_TRY(launch_expand_dz(g->E_own, N, g->dst_s, g->inv_c, dY, w.Z, s)); }
-      da.Bz = w.Z;
-    } else {
-      da.Bg = dY; da.bgather = g->dst_s; da.bscale = g->inv_c;
+    rgnn_status fst = RGNN_E_UNSUPPORTED;
+    if (tc_ok) {  // fused: dZ rows = G_v / c built in smem, tensor-core dW in the same kernel
+      Phase ph("bwd_fused", s);
+      fst = launch_bwd_fused_tc(K, N, g, X, nullptr, nullptr, nullptr, nullptr, dY, nullptr, nullptr, 0.f, w.dwpart,
+                                w.cpart, s);
+      if (fst != RGNN_OK && fst != RGNN_E_UNSUPPORTED) return fst;
     }
-    { Phase ph("gemm_dw", s); RGNN_TRY(dw_gemm(da)); }
+    if (fst != RGNN_OK) {
+      if (tc_ok) {  // dZ[p] = bf16(1/c * G[dst]) materialised in position order, then the tensor-core dW
+        { Phase ph("expand_dz", s); RGNN_TRY(launch_expand_dz(g->E_own, N, g->dst_s, g->inv_c, dY, w.Z, s)); }
+        da.Bz = w.Z;
+      } else {
+        da.Bg = dY; da.bgather = g->dst_s; da.bscale = g->inv_c;
+      }
+      { Phase ph("gemm_dw", s); RGNN_TRY(dw_gemm(da)); }
+    }
     { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, nullptr, nullptr, nullptr, nullptr, dW, nullptr, nullptr, s)); }
     if (dW0) {
       Phase ph("gemm_dw0", s);

@@ -73,40 +73,38 @@ __device__ __forceinline__ float dot_u(const float* xv, const float* Ur) {
 
 template <typename T, int K, int N, bool RGAT>
 __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
-  // One work item per lane group (L lanes = one 16-byte slice each of a Z row):
-  // a warp walks G rows at once, each group UNR edges per step, online softmax
-  // per group, no cross-group merge.  Group shuffles use the group's lane mask.
   using S = WalkShape<T, K, N>;
-  constexpr int EPL = S::EPL, L = S::L, G = S::G, KPL = S::KPL;
-  constexpr int UNR = 4;
-  static_assert(UNR <= L || L == 4, "index lanes");
+  constexpr int EPL = S::EPL, L = S::L, G = S::G, UNR = S::UNR, B = S::B, KPL = S::KPL;
   const T* Z = static_cast<const T*>(a.Z);
   const T* X = static_cast<const T*>(a.X);
   const int lane = threadIdx.x & 31, g = lane / L, l = lane % L;
-  const uint32_t gmask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (g * L));
   const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t w = warp0 * G + g; w < a.num_items; w += nwarps * G) {
-    const Item it = a.items[w];
+  Item nit = warp0 < a.num_items ? a.items[warp0] : Item{0, 0, 0, -1};
+  for (int64_t w = warp0; w < a.num_items; w += nwarps) {
+    const Item it = nit;
+    if (w + nwarps < a.num_items) nit = a.items[w + nwarps];  // next item's descriptor in flight
     float acc[EPL];
 #pragma unroll
     for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
     float m = -CUDART_INF_F, lsum = 0.f;
     float xv[KPL];
-    if constexpr (RGAT) load_slice<KPL>(X + (a.v0 + it.row) * (int64_t)K + l * KPL, xv);
-    // lane l < UNR of the group holds slot base + l; indices loaded one step ahead
-    int nq = it.q0 + l;
-    bool nok = l < UNR && nq < it.q1;
+    if constexpr (RGAT) {
+      if (it.q1 > it.q0) load_slice<KPL>(X + (a.v0 + it.row) * (int64_t)K + l * KPL, xv);
+    }
+    // slot indices are loaded one step ahead of their use
+    int nq = it.q0 + lane;
+    bool nok = lane < B && nq < it.q1;
     int np = nok ? a.pos[nq] : 0;
     int nr = nok ? a.et_slot[nq] : 0;
-    for (int base = it.q0; base < it.q1; base += UNR) {
+    for (int base = it.q0; base < it.q1; base += B) {
       const bool ok = nok;
       const int myp = np;
       const int myr = nr;
       float mys = 0.f;
       if constexpr (RGAT) mys = ok ? a.s_src[myp] : 0.f;
-      nq = base + UNR + l;
-      nok = l < UNR && nq < it.q1;
+      nq = base + B + lane;
+      nok = lane < B && nq < it.q1;
       np = nok ? a.pos[nq] : 0;
       nr = nok ? a.et_slot[nq] : 0;
       uint4 zr[UNR];
@@ -114,10 +112,11 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
       bool val[UNR];
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
-        const int p = __shfl_sync(gmask, myp, u, L);
-        const int r = __shfl_sync(gmask, myr, u, L);
-        const float ss = __shfl_sync(gmask, mys, u, L);
-        val[u] = base + u < it.q1;
+        const int j = u * G + g;
+        const int p = __shfl_sync(0xffffffffu, myp, j);
+        const int r = __shfl_sync(0xffffffffu, myr, j);
+        const float ss = __shfl_sync(0xffffffffu, mys, j);
+        val[u] = base + j < it.q1;
         zr[u] = val[u] ? ldg16(Z + (size_t)p * N + l * EPL) : make_uint4(0, 0, 0, 0);
         if constexpr (RGAT) {
           const float d = dot_u<KPL>(xv, a.U + (size_t)r * K + l * KPL);
@@ -126,29 +125,30 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
       }
       if constexpr (RGAT) {
 #pragma unroll
-        for (int o = L / 2; o > 0; o >>= 1)
+        for (int u = 0; u < UNR; ++u) {
 #pragma unroll
-          for (int u = 0; u < UNR; ++u) sc[u] += __shfl_xor_sync(gmask, sc[u], o);
+          for (int o = L / 2; o > 0; o >>= 1) sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
+          sc[u] = val[u] ? leaky(sc[u], a.slope) : -CUDART_INF_F;
+        }
         float mnew = m;
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-          sc[u] = val[u] ? leaky(sc[u], a.slope) : -CUDART_INF_F;
-          mnew = fmaxf(mnew, sc[u]);
+        for (int u = 0; u < UNR; ++u) mnew = fmaxf(mnew, sc[u]);
+        if (mnew != -CUDART_INF_F) {
+          const float corr = __expf(m - mnew);  // m = -inf -> 0
+          lsum *= corr;
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) acc[i] *= corr;
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) {
+            const float e = val[u] ? __expf(sc[u] - mnew) : 0.f;
+            lsum += e;
+            float zf[EPL];
+            Vec16<T>{zr[u]}.to_float(zf);
+#pragma unroll
+            for (int i = 0; i < EPL; ++i) acc[i] = fmaf(e, zf[i], acc[i]);
+          }
+          m = mnew;
         }
-        const float corr = __expf(m - mnew);  // m = -inf -> 0 (mnew is finite: edge u = 0 is valid)
-        lsum *= corr;
-#pragma unroll
-        for (int i = 0; i < EPL; ++i) acc[i] *= corr;
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-          const float e = val[u] ? __expf(sc[u] - mnew) : 0.f;
-          lsum += e;
-          float zf[EPL];
-          Vec16<T>{zr[u]}.to_float(zf);
-#pragma unroll
-          for (int i = 0; i < EPL; ++i) acc[i] = fmaf(e, zf[i], acc[i]);
-        }
-        m = mnew;
       } else {
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
@@ -159,28 +159,51 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
         }
       }
     }
-    if (it.part < 0) {
-      float* y = a.Y + (size_t)it.row * N + l * EPL;
+    // merge the G group states (fixed xor tree)
+#pragma unroll
+    for (int o = L; o < 32; o <<= 1) {
       if constexpr (RGAT) {
-        const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        const float l2 = __shfl_xor_sync(0xffffffffu, lsum, o);
+        const float mn = fmaxf(m, m2);
+        const float c1 = mn == -CUDART_INF_F ? 0.f : __expf(m - mn);
+        const float c2 = mn == -CUDART_INF_F ? 0.f : __expf(m2 - mn);
+        lsum = lsum * c1 + l2 * c2;
 #pragma unroll
-        for (int i = 0; i < EPL; ++i) acc[i] *= inv;
-        if (l == 0) a.lse[it.row] = lsum > 0.f ? m + __logf(lsum) : -CUDART_INF_F;
-      } else if (a.Z0) {
-        float z0[EPL];
-        Vec16<T>{ldg16(static_cast<const T*>(a.Z0) + (size_t)it.row * N + l * EPL)}.to_float(z0);
+        for (int i = 0; i < EPL; ++i) {
+          const float a2 = __shfl_xor_sync(0xffffffffu, acc[i], o);
+          acc[i] = acc[i] * c1 + a2 * c2;
+        }
+        m = mn;
+      } else {
 #pragma unroll
-        for (int i = 0; i < EPL; ++i) acc[i] += z0[i];
+        for (int i = 0; i < EPL; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
       }
+    }
+    if (g == 0) {
+      if (it.part < 0) {
+        float* y = a.Y + (size_t)it.row * N + l * EPL;
+        if constexpr (RGAT) {
+          const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
 #pragma unroll
-      for (int i = 0; i < EPL; i += 4) stg16(y + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]),
-                                                               __float_as_uint(acc[i + 2]), __float_as_uint(acc[i + 3])));
-    } else {
-      float* pp = a.part + (size_t)it.part * (N + 4);
+          for (int i = 0; i < EPL; ++i) acc[i] *= inv;
+          if (l == 0) a.lse[it.row] = lsum > 0.f ? m + __logf(lsum) : -CUDART_INF_F;
+        } else if (a.Z0) {
+          float z0[EPL];
+          Vec16<T>{ldg16(static_cast<const T*>(a.Z0) + (size_t)it.row * N + l * EPL)}.to_float(z0);
 #pragma unroll
-      for (int i = 0; i < EPL; i += 4) stg16(pp + l * EPL + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]),
-                                                                         __float_as_uint(acc[i + 2]), __float_as_uint(acc[i + 3])));
-      if (l == 0) { pp[N] = m; pp[N + 1] = lsum; }
+          for (int i = 0; i < EPL; ++i) acc[i] += z0[i];
+        }
+#pragma unroll
+        for (int i = 0; i < EPL; i += 4) stg16(y + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]),
+                                                                 __float_as_uint(acc[i + 2]), __float_as_uint(acc[i + 3])));
+      } else {
+        float* pp = a.part + (size_t)it.part * (N + 4);
+#pragma unroll
+        for (int i = 0; i < EPL; i += 4) stg16(pp + l * EPL + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]),
+                                                                           __float_as_uint(acc[i + 2]), __float_as_uint(acc[i + 3])));
+        if (l == 0) { pp[N] = m; pp[N + 1] = lsum; }
+      }
     }
   }
 }
@@ -401,15 +424,13 @@ static unsigned warps_grid(int64_t items) {
 
 template <typename T, int K, int N>
 static rgnn_status aggregate(bool rgat, const AggArgs& a, cudaStream_t s) {
-  constexpr int G = WalkShape<T, K, N>::G;
   if (a.num_empty > 0) {
     const int64_t n = a.num_empty * (N / 4);
     RGNN_LAUNCH((k_empty_rows<T, N>), (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, s, a);
   }
   if (a.num_items > 0) {
-    const unsigned grid = warps_grid((a.num_items + G - 1) / G);
-    if (rgat) RGNN_LAUNCH((k_aggregate<T, K, N, true>), grid, 256, 0, s, a);
-    else RGNN_LAUNCH((k_aggregate<T, K, N, false>), grid, 256, 0, s, a);
+    if (rgat) RGNN_LAUNCH((k_aggregate<T, K, N, true>), warps_grid(a.num_items), 256, 0, s, a);
+    else RGNN_LAUNCH((k_aggregate<T, K, N, false>), warps_grid(a.num_items), 256, 0, s, a);
   }
   if (a.num_split_rows > 0) {
     if (rgat) RGNN_LAUNCH((k_merge<T, N, true>), (unsigned)a.num_split_rows, 512, 0, s, a);
