@@ -210,20 +210,12 @@ __global__ void k_da_vsum(int K, int N, int R, const int32_t* __restrict__ chunk
   }
 }
 
-// dA[r,h,n] = vsum[r][h] . W_r[:,n]  (h = 0: sum dpre x_src, h = 1: sum dpre x_dst); with `apart`
-// (fused backward: sum dpre z per chunk) dA[r,0,n] = sum over the chunks of r of apart[c][n].
+// dA[r,h,n] = vsum[r][h] . W_r[:,n]  (h = 0: sum dpre x_src, h = 1: sum dpre x_dst)
 __global__ void k_da(int K, int N, int R, const float* __restrict__ vsum, const float* __restrict__ W,
-                     float* __restrict__ dA, int round_bf16, const int32_t* __restrict__ chunk_seg,
-                     const float* __restrict__ apart) {
+                     float* __restrict__ dA, int round_bf16) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)R * 2 * N;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(i / (2 * N)), h = (int)((i / N) % 2), n = (int)(i % N);
-    if (h == 0 && apart) {
-      float s = 0.f;
-      for (int c = chunk_seg[r]; c < chunk_seg[r + 1]; ++c) s += apart[(size_t)c * N + n];
-      dA[i] = s;
-      continue;
-    }
     const float* v = vsum + ((size_t)r * 2 + h) * K;
     float s = 0.f;
     for (int k = 0; k < K; ++k) {
@@ -292,8 +284,7 @@ rgnn_status launch_gemm_dw(int prec, int K, int N, const GemmDwArgs& a, cudaStre
 
 rgnn_status launch_dw_reduce(int prec, int K, int N, int R, int64_t num_chunks, const int32_t* chunk_seg,
                              const float* part, const int32_t* cseg, const float* cpart, const float* A,
-                             const float* W, float* dW, float* dA, float* dA_scratch, const float* apart,
-                             cudaStream_t s) {
+                             const float* W, float* dW, float* dA, float* dA_scratch, cudaStream_t s) {
   int64_t total = (int64_t)R * K * N;
   unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16));
   RGNN_LAUNCH(k_dw_reduce, grid, 256, 0, s, K, N, R, num_chunks, chunk_seg, part, cseg, cpart, A, dW);
@@ -302,7 +293,7 @@ rgnn_status launch_dw_reduce(int prec, int K, int N, int R, int64_t num_chunks, 
     unsigned g1 = (unsigned)std::max<int64_t>(1, ((int64_t)R * 2 * K + 127) / 128);
     RGNN_LAUNCH(k_da_vsum, g1, 128, 0, s, K, N, R, chunk_seg, part, cseg, cpart, vsum);
     unsigned g2 = (unsigned)std::max<int64_t>(1, ((int64_t)R * 2 * N + 127) / 128);
-    RGNN_LAUNCH(k_da, g2, 128, 0, s, K, N, R, vsum, W, dA, prec == RGNN_BF16 ? 1 : 0, chunk_seg, apart);
+    RGNN_LAUNCH(k_da, g2, 128, 0, s, K, N, R, vsum, W, dA, prec == RGNN_BF16 ? 1 : 0);
   }
   return RGNN_OK;
 }

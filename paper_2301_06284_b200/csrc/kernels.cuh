@@ -51,8 +51,7 @@ rgnn_status launch_gemm_fwd(int prec, int K, int N, const GemmFwdArgs& a, cudaSt
 rgnn_status launch_gemm_dw(int prec, int K, int N, const GemmDwArgs& a, cudaStream_t s);
 rgnn_status launch_dw_reduce(int prec, int K, int N, int R, int64_t num_chunks, const int32_t* chunk_seg,
                              const float* part, const int32_t* cseg, const float* cpart, const float* A,
-                             const float* W, float* dW, float* dA, float* dA_scratch /* [R*2*K] */,
-                             const float* apart /* [chunks, N] sum dpre z, or null */, cudaStream_t s);
+                             const float* W, float* dW, float* dA, float* dA_scratch /* [R*2*K] */, cudaStream_t s);
 rgnn_status launch_dst_term(int prec, int K, const rgnn_graph* g, const float* dpre, const void* X, float* cpart,
                             cudaStream_t s);
 rgnn_status launch_fold_u(int prec, int R, int K, int N, const float* W, const float* A, float* U, cudaStream_t s);
@@ -102,9 +101,9 @@ rgnn_status launch_bwd_traverse(int prec, int K, int N, const BwdArgs& a, cudaSt
 // tcgen05 path (gemm_tc.cu): returns RGNN_E_UNSUPPORTED if the shape is not covered.
 rgnn_status launch_gemm_fwd_tc(int K, int N, const GemmFwdArgs& a, cudaStream_t s);
 rgnn_status launch_gemm_dw_tc(int K, int N, const GemmDwArgs& a, cudaStream_t s);
-rgnn_status launch_bwd_fused_tc(int K, int N, const rgnn_graph* g, const void* X, const float* W, const float* s_src,
+rgnn_status launch_bwd_fused_tc(int K, int N, const rgnn_graph* g, const void* X, const void* Z, const float* s_src,
                                 const float* lse, const float* Y, const float* dY, const float* U, const float* A,
-                                float slope, float* part, float* cpart, float* apart, cudaStream_t s);
+                                float slope, float* part, float* cpart, cudaStream_t s);
 rgnn_status launch_expand_dz(int64_t E, int N, const int32_t* dst_s, const float* inv_c, const float* G, void* dZ,
                              cudaStream_t s);
 

@@ -23,7 +23,6 @@ struct WsLayout {
   float* dw0part;  // [n0, K*N + K]
   float* cpart;    // RGAT dst term: [num_chunks, K]
   float* vsum;     // RGAT dA vectors: [R, 2, K]
-  float* apart;    // fused backward: sum dpre z per chunk [num_chunks, N]
   void* wt;        // tcgen05: bf16 W^T [R, N, K]
   size_t bytes;
 };
@@ -62,7 +61,6 @@ static WsLayout ws_layout(const rgnn_graph* g, int model, int K, int N, int prec
   w.dw0part = c.take<float>(model == RGNN_RGCN ? (size_t)std::max<int64_t>(dw0_chunks(g), 1) * (K * N + K) : 1);
   w.cpart = c.take<float>((size_t)std::max<int64_t>(g->num_chunks, 1) * K);
   w.vsum = c.take<float>((size_t)g->R * 2 * K);
-  w.apart = c.take<float>((size_t)std::max<int64_t>(g->num_chunks, 1) * N);
   w.bytes = c.off;
   return w;
 }
@@ -203,13 +201,13 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     rgnn_status fst = RGNN_E_UNSUPPORTED;
     if (tc_ok) {  // fused position-order backward: dZ built in smem, dW MMA + dst term in one kernel
       Phase ph("bwd_fused", s);
-      fst = launch_bwd_fused_tc(K, N, g, X, W, sv.s_src, sv.lse, Y, dY, w.U, A, slope, w.dwpart, w.cpart, w.apart, s);
+      fst = launch_bwd_fused_tc(K, N, g, X, sv.Z, sv.s_src, sv.lse, Y, dY, w.U, A, slope, w.dwpart, w.cpart, s);
       if (fst != RGNN_OK && fst != RGNN_E_UNSUPPORTED) return fst;
     }
     if (fst == RGNN_OK) {
       Phase ph("dw_reduce", s);
       RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, g->chunk_seg, w.cpart, A, W,
-                                dW, dA, w.vsum, w.apart, s));
+                                dW, dA, w.vsum, s));
     } else {
     BwdArgs ba{};
     ba.items = g->items; ba.num_items = g->num_items; ba.pos = g->pos; ba.et_slot = g->et_slot; ba.Z = sv.Z;
@@ -219,14 +217,14 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     { Phase ph("dst_term", s); RGNN_TRY(launch_dst_term(prec, K, g, w.dpre, X, w.cpart, s)); }
     da.Bz = w.dZ; da.dpre = w.dpre; da.dst_local = g->dst_s; da.v0 = g->v0;
     { Phase ph("gemm_dw", s); RGNN_TRY(dw_gemm(da)); }
-    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, g->chunk_seg, w.cpart, A, W, dW, dA, w.vsum, nullptr, s)); }
+    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, g->chunk_seg, w.cpart, A, W, dW, dA, w.vsum, s)); }
     }
   } else {
     rgnn_status fst = RGNN_E_UNSUPPORTED;
     if (tc_ok) {  // fused: dZ rows = G_v / c built in smem, tensor-core dW in the same kernel
       Phase ph("bwd_fused", s);
       fst = launch_bwd_fused_tc(K, N, g, X, nullptr, nullptr, nullptr, nullptr, dY, nullptr, nullptr, 0.f, w.dwpart,
-                                w.cpart, w.apart, s);
+                                w.cpart, s);
       if (fst != RGNN_OK && fst != RGNN_E_UNSUPPORTED) return fst;
     }
     if (fst != RGNN_OK) {
@@ -238,7 +236,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
       }
       { Phase ph("gemm_dw", s); RGNN_TRY(dw_gemm(da)); }
     }
-    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, nullptr, nullptr, nullptr, nullptr, dW, nullptr, nullptr, nullptr, s)); }
+    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, nullptr, nullptr, nullptr, nullptr, dW, nullptr, nullptr, s)); }
     if (dW0) {
       Phase ph("gemm_dw0", s);
       GemmDwArgs d0{};
@@ -251,7 +249,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
         d0.Bg = dY;
       }
       RGNN_TRY(dw_gemm(d0));
-      RGNN_TRY(launch_dw_reduce(prec, K, N, 1, d0.num_chunks, nullptr, w.dw0part, nullptr, nullptr, nullptr, nullptr, dW0, nullptr, nullptr, nullptr, s));
+      RGNN_TRY(launch_dw_reduce(prec, K, N, 1, d0.num_chunks, nullptr, w.dw0part, nullptr, nullptr, nullptr, nullptr, dW0, nullptr, nullptr, s));
     }
   }
   if (comm) {
