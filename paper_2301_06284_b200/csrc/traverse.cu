@@ -208,6 +208,195 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
   }
 }
 
+// Same computation as k_aggregate with a per-warp cp.async ring: the Z-row
+// slices (each lane copies exactly the 16-byte slices it will reduce) and the
+// s_src of RING-1 steps ahead are in flight as asynchronous copies into shared
+// memory -- no registers held -- while the current step is reduced.  The warp's
+// items form one continuous stream of B-edge steps, so short rows do not drain
+// the pipeline.  Results are bit-identical to k_aggregate (same per-group edge
+// assignment, same arithmetic order).
+template <typename T, int K, int N, bool RGAT, int RING>
+__global__ void __launch_bounds__(256) k_aggregate_ring(AggArgs a) {
+  using S = WalkShape<T, K, N>;
+  constexpr int EPL = S::EPL, L = S::L, G = S::G, UNR = S::UNR, B = S::B, KPL = S::KPL;
+  extern __shared__ uint4 ring_smem[];
+  const T* Z = static_cast<const T*>(a.Z);
+  const T* X = static_cast<const T*>(a.X);
+  const int lane = threadIdx.x & 31, g = lane / L, l = lane % L, wib = threadIdx.x >> 5;
+  uint4* zring = ring_smem + (size_t)wib * RING * UNR * 32;                          // [RING][UNR][32 lanes]
+  float* sring = reinterpret_cast<float*>(ring_smem + (size_t)(blockDim.x >> 5) * RING * UNR * 32) +
+                 (size_t)wib * RING * 32 * 2;                                          // [RING][32] s_src, [RING][32] r
+  int* rring = reinterpret_cast<int*>(sring + RING * 32);
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+
+  // producer cursor (RING-1 steps ahead of the consumer)
+  int64_t pw = warp0;
+  Item pit = pw < a.num_items ? a.items[pw] : Item{0, 0, 0, -1};
+  int pbase = pit.q0;
+  // (pos, et) of the producer's next step, one step ahead of its copies
+  int np = 0, nr = 0;
+  auto load_idx = [&]() {
+    const int q = pbase + lane;
+    const bool ok = pw < a.num_items && lane < B && q < pit.q1;
+    np = ok ? a.pos[q] : 0;
+    nr = ok ? a.et_slot[q] : 0;
+  };
+  auto advance_producer = [&]() {
+    pbase += B;
+    if (pbase >= pit.q1) {
+      pw += nwarps;
+      if (pw < a.num_items) { pit = a.items[pw]; pbase = pit.q0; }
+    }
+  };
+  int pslot = 0;
+  auto produce = [&]() {  // issue the copies of the producer's current step into ring slot pslot
+    if (pw < a.num_items) {
+      const int myp = np, myr = nr;
+      const int q = pbase + lane;
+      const bool ok = lane < B && q < pit.q1;
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int j = u * G + g;
+        const int p = __shfl_sync(0xffffffffu, myp, j);
+        if (pbase + j < pit.q1)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(
+                           zring + ((size_t)pslot * UNR + u) * 32 + lane)),
+                       "l"(Z + (size_t)p * N + l * EPL)
+                       : "memory");
+      }
+      if (RGAT && ok)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(
+                         sring + pslot * 32 + lane)),
+                     "l"(a.s_src + myp)
+                     : "memory");
+      if (lane < B) rring[pslot * 32 + lane] = myr;
+      advance_producer();
+      load_idx();
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    pslot = pslot + 1 == RING ? 0 : pslot + 1;
+  };
+
+  load_idx();
+#pragma unroll
+  for (int i = 0; i < RING - 1; ++i) produce();
+
+  int cslot = 0;
+  for (int64_t w = warp0; w < a.num_items; w += nwarps) {
+    const Item it = a.items[w];
+    float acc[EPL];
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
+    float m = -CUDART_INF_F, lsum = 0.f;
+    float xv[KPL];
+    if constexpr (RGAT) load_slice<KPL>(X + (a.v0 + it.row) * (int64_t)K + l * KPL, xv);
+    for (int base = it.q0; base < it.q1; base += B) {
+      produce();  // keeps RING-1 steps in flight
+      asm volatile("cp.async.wait_group %0;" ::"n"(RING - 1) : "memory");
+      __syncwarp();
+      uint4 zr[UNR];
+      float sc[UNR];
+      bool val[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int j = u * G + g;
+        val[u] = base + j < it.q1;
+        zr[u] = val[u] ? zring[((size_t)cslot * UNR + u) * 32 + lane] : make_uint4(0, 0, 0, 0);
+        if constexpr (RGAT) {
+          const int r = rring[cslot * 32 + j];
+          const float ss = sring[cslot * 32 + j];
+          const float d = dot_u<KPL>(xv, a.U + (size_t)r * K + l * KPL);
+          sc[u] = l == 0 ? d + ss : d;
+        }
+      }
+      __syncwarp();  // the slot may be refilled by the next produce()
+      cslot = cslot + 1 == RING ? 0 : cslot + 1;
+      if constexpr (RGAT) {
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+#pragma unroll
+          for (int o = L / 2; o > 0; o >>= 1) sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
+          sc[u] = val[u] ? leaky(sc[u], a.slope) : -CUDART_INF_F;
+        }
+        float mnew = m;
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) mnew = fmaxf(mnew, sc[u]);
+        if (mnew != -CUDART_INF_F) {
+          const float corr = __expf(m - mnew);
+          lsum *= corr;
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) acc[i] *= corr;
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) {
+            const float e = val[u] ? __expf(sc[u] - mnew) : 0.f;
+            lsum += e;
+            float zf[EPL];
+            Vec16<T>{zr[u]}.to_float(zf);
+#pragma unroll
+            for (int i = 0; i < EPL; ++i) acc[i] = fmaf(e, zf[i], acc[i]);
+          }
+          m = mnew;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          float zf[EPL];
+          Vec16<T>{zr[u]}.to_float(zf);
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) acc[i] += zf[i];
+        }
+      }
+    }
+#pragma unroll
+    for (int o = L; o < 32; o <<= 1) {
+      if constexpr (RGAT) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        const float l2 = __shfl_xor_sync(0xffffffffu, lsum, o);
+        const float mn = fmaxf(m, m2);
+        const float c1 = mn == -CUDART_INF_F ? 0.f : __expf(m - mn);
+        const float c2 = mn == -CUDART_INF_F ? 0.f : __expf(m2 - mn);
+        lsum = lsum * c1 + l2 * c2;
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) {
+          const float a2 = __shfl_xor_sync(0xffffffffu, acc[i], o);
+          acc[i] = acc[i] * c1 + a2 * c2;
+        }
+        m = mn;
+      } else {
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+      }
+    }
+    if (g == 0) {
+      if (it.part < 0) {
+        float* y = a.Y + (size_t)it.row * N + l * EPL;
+        if constexpr (RGAT) {
+          const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) acc[i] *= inv;
+          if (l == 0) a.lse[it.row] = lsum > 0.f ? m + __logf(lsum) : -CUDART_INF_F;
+        } else if (a.Z0) {
+          float z0[EPL];
+          Vec16<T>{ldg16(static_cast<const T*>(a.Z0) + (size_t)it.row * N + l * EPL)}.to_float(z0);
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) acc[i] += z0[i];
+        }
+#pragma unroll
+        for (int i = 0; i < EPL; i += 4) stg16(y + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]),
+                                                                 __float_as_uint(acc[i + 2]), __float_as_uint(acc[i + 3])));
+      } else {
+        float* pp = a.part + (size_t)it.part * (N + 4);
+#pragma unroll
+        for (int i = 0; i < EPL; i += 4) stg16(pp + l * EPL + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]),
+                                                                           __float_as_uint(acc[i + 2]), __float_as_uint(acc[i + 3])));
+        if (l == 0) { pp[N] = m; pp[N + 1] = lsum; }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // Combine the partial states of each split row: one block per split row, warp w
 // merges parts w, w+16, ... (4 per step), then warp 0 merges the 16 warp states
 // in warp order.  Fixed assignment and order: deterministic.
@@ -429,8 +618,22 @@ static rgnn_status aggregate(bool rgat, const AggArgs& a, cudaStream_t s) {
     RGNN_LAUNCH((k_empty_rows<T, N>), (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, s, a);
   }
   if (a.num_items > 0) {
-    if (rgat) RGNN_LAUNCH((k_aggregate<T, K, N, true>), warps_grid(a.num_items), 256, 0, s, a);
-    else RGNN_LAUNCH((k_aggregate<T, K, N, false>), warps_grid(a.num_items), 256, 0, s, a);
+    // measured (r01): the ring helps d_out = 64 (AM aggregate 0.93 -> 0.84 ms) and costs ~5% at
+    // d_out = 128 (ogbn-mag), where the warp-per-row kernel with index prefetch stays faster
+    static const bool no_ring = getenv("RGNN_WALK_NO_RING") != nullptr;
+    const bool ring = !no_ring && N <= 64;
+    if (ring) {
+      constexpr int RING = 4, UNR = WalkShape<T, K, N>::UNR;
+      const size_t smem = 8 * (RING * UNR * 32 * sizeof(uint4) + RING * 32 * 2 * sizeof(float));
+      auto kt = k_aggregate_ring<T, K, N, true, RING>;
+      auto kf = k_aggregate_ring<T, K, N, false, RING>;
+      RGNN_CUDA_TRY(cudaFuncSetAttribute(rgat ? kt : kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      if (rgat) RGNN_LAUNCH(kt, warps_grid(a.num_items), 256, smem, s, a);
+      else RGNN_LAUNCH(kf, warps_grid(a.num_items), 256, smem, s, a);
+    } else {
+      if (rgat) RGNN_LAUNCH((k_aggregate<T, K, N, true>), warps_grid(a.num_items), 256, 0, s, a);
+      else RGNN_LAUNCH((k_aggregate<T, K, N, false>), warps_grid(a.num_items), 256, 0, s, a);
+    }
   }
   if (a.num_split_rows > 0) {
     if (rgat) RGNN_LAUNCH((k_merge<T, N, true>), (unsigned)a.num_split_rows, 512, 0, s, a);
