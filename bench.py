@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time of the cpu_baseline sample")
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of a captured CUDA graph")
+    ap.add_argument("--materialization", default="auto", choices=["vanilla", "compact", "auto"],
+                    help="per-edge (vanilla) or per-(etype, src) (compact, PAPER.md P:513-531) Z / s_src rows; "
+                         "auto = compact when U <= E/2")
     return ap.parse_args()
 
 
@@ -86,19 +89,21 @@ def config_json(cfg, model, prec, g, world):
 
 
 # --------------------------------------------------------------------- algorithmic bytes
-def algorithmic_bytes(phase, model, prec, K, N, E, V_own, J, num_items):
-    """Bytes the method must move per launch of each phase (no L2 reuse assumed)."""
+def algorithmic_bytes(phase, model, prec, K, N, E, V_own, J, num_items, U=None):
+    """Bytes the method must move per launch of each phase (no L2 reuse assumed).
+    U = compact rows (compact materialisation): the GEMM runs over U rows, the
+    walks read Z through a per-slot row index (plus 1/c per slot for RGCN)."""
     b = 2 if prec == "bf16" else 4
     if phase == "gemm_fwd":  # gather X rows, write Z, read src index (+ s_src write for RGAT, + 1/c read for RGCN)
-        return E * (K * b + N * b + 4 + 4)
+        return (E if U is None else U) * (K * b + N * b + 4 + 4)
     if phase == "aggregate":  # read pos, et, Z row (+ s_src) per edge; X_dst, Y, lse, item per row
-        per_e = N * b + 8 + (4 if model == "rgat" else 0)
+        per_e = N * b + 8 + (4 if model == "rgat" or U is not None else 0)
         per_v = (K * b + N * 4 + 4 + 16) if model == "rgat" else (N * 4 + 16)
         return E * per_e + num_items * per_v
     if phase == "bwd_traverse":  # read pos, et, s_src, Z; write dZ, dpre; per row X, Y, dY, lse, item
         return E * (2 * N * b + 16) + num_items * (K * b + 2 * N * 4 + 4 + 16)
-    if phase == "bwd_fused":  # read Z, s_src, dst, src per edge, gather X_src; per (etype,dst) run G_v, Y_v, X_v, lse
-        return E * (N * b + K * b + 12) + J * (8 * N + K * b + 4)
+    if phase == "bwd_fused":  # read Z, s_src, dst, src (+ compact row) per edge, gather X_src; per run G_v, Y_v, X_v, lse
+        return E * (N * b + K * b + 12 + (4 if U is not None else 0)) + J * (8 * N + K * b + 4)
     if phase == "gemm_dw":  # gather X rows, read dZ (RGAT) or gather G rows (RGCN), indices; dst term per run
         if model == "rgat":
             return E * (K * b + N * b + 4 + 4 + 4) + J * K * b
@@ -255,7 +260,7 @@ def run_ours(args):
     et = torch.from_numpy(g.etype).to(dev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    G = m.Graph(g.V, src, dst, et, g.R, dst_begin=v0, dst_end=v1, device=dev)
+    G = m.Graph(g.V, src, dst, et, g.R, dst_begin=v0, dst_end=v1, materialization=args.materialization, device=dev)
     torch.cuda.synchronize()
     prep_ms = 1e3 * (time.perf_counter() - t0)
     del src, dst, et
@@ -408,7 +413,7 @@ def run_ours(args):
         dom = max(cand, key=lambda k: cand[k][0])
         per_launch_ms = phases[dom][0] / max(phases[dom][1], 1)
         byts = algorithmic_bytes(dom, model, prec, K, N, int(v.E_own), int(v.V_own), int(v.num_runs),
-                                 int(v.num_items))
+                                 int(v.num_items), U=int(v.num_compact) if int(v.num_compact) > 0 else None)
         ach = byts / (per_launch_ms * 1e-3) / 1e9
         traffic = None
         try:
@@ -433,7 +438,10 @@ def run_ours(args):
                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": prec, "data": "synthetic (seeded generator, random-init weights)",
                "config": dict(config_json(cfg, model, prec, g, world),
-                              launch="CUDA graph of the step" if use_graph else "eager"),
+                              launch="CUDA graph of the step" if use_graph else "eager",
+                              materialization=("compact" if G.num_compact > 0 else "vanilla") + (
+                                  " (auto)" if args.materialization == "auto" else ""),
+                              compact_rows=int(G.num_compact)),
                "clocks": clocks, "e2e": e2e,
                "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu,
                "phases_ms_per_step": {k: round(x[0], 4) for k, x in sorted(step_phase.items())},

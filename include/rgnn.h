@@ -66,6 +66,14 @@ typedef enum { RGNN_NORM_REL_INDEG = 0, RGNN_NORM_NONE = 1, RGNN_NORM_EDGE = 2 }
 
 typedef enum { RGNN_RGCN = 0, RGNN_RGAT = 1 } rgnn_model;
 
+/* Where per-edge tensors (Z, s_src) live (Sec. 3.1.3).
+ * VANILLA: one row per edge (the row number is the edge's position).
+ * COMPACT: one row per unique (etype, src) pair, numbered lexicographically
+ * (reading O15); the typed GEMM then runs over U_src rows instead of E.     */
+/* AUTO: compact when the unique pairs are at most half the edges (U <= E/2),
+ * vanilla otherwise; rgnn_graph_view.num_compact > 0 tells which was taken. */
+typedef enum { RGNN_MAT_VANILLA = 0, RGNN_MAT_COMPACT = 1, RGNN_MAT_AUTO = 2 } rgnn_materialization;
+
 typedef struct rgnn_graph rgnn_graph;
 typedef struct rgnn_comm rgnn_comm;
 
@@ -85,6 +93,8 @@ typedef struct {
   int32_t row_split_cap;     /* max in-edges per work item; 0 = 256          */
   int64_t dst_begin;         /* owned destination range [dst_begin, dst_end) */
   int64_t dst_end;           /* (0, V) on one GPU                            */
+  int32_t materialization;   /* rgnn_materialization (0 = vanilla)           */
+  int32_t reserved;          /* must be 0                                    */
 } rgnn_graph_desc;
 
 /* What the preprocessing built (device pointers into the caller's graph
@@ -105,6 +115,10 @@ typedef struct {
   const int32_t* run_ptr;  /* [num_runs+1] (etype,dst) runs, position space */
   const int32_t* rseg;     /* [R+1]   runs of relation r                    */
   const int32_t* seg_host; /* [host, R+1] copy of seg                       */
+  int64_t num_compact;     /* compact rows (0 when vanilla)                 */
+  const int32_t* crow_of_pos; /* [E_own] compact row of position p          */
+  const int32_t* csrc;     /* [num_compact] src node of compact row         */
+  const int32_t* cseg;     /* [R+1] compact rows of relation r              */
 } rgnn_graph_view;
 
 /* Sizes of the caller-owned graph storage (kept for the handle's life) and

@@ -105,6 +105,37 @@ def preprocess(V: int, R: int, src, dst, et, v0: int = 0, v1: Optional[int] = No
     return Preprocessed(n, perm[:n], src_s[:n], seg, row_ptr, pos[:n], et_slot[:n], cnt[:n])
 
 
+class Compaction:
+    """Compact materialisation tables (Sec. 3.1.3)."""
+
+    def __init__(self, crow_of_pos, csrc, crel, cseg):
+        self.crow_of_pos, self.csrc, self.crel, self.cseg = crow_of_pos, csrc, crel, cseg
+
+    @property
+    def num_compact(self) -> int:
+        return int(self.csrc.shape[0])
+
+
+def compaction(R: int, pre: Preprocessed) -> Compaction:
+    """Compact materialisation: data "merely determined by source
+    node features and edge types" is stored "once for each (edge type, unique node
+    index) pair", each pair getting "a unique nonnegative integer".
+    Reading O15: the integers number the pairs present among the owned edges in
+    lexicographic (etype, src) order.  Written out with Python sets and dicts.
+
+    Returns crow_of_pos[p] (compact row of position p), csrc[c] / crel[c] (the
+    pair of compact row c) and cseg[r] (compact rows of relation < r)."""
+    et_p = np.repeat(np.arange(R, dtype=np.int64), np.diff(pre.seg.astype(np.int64)))  # etype of position p
+    keys = list(zip(et_p.tolist(), pre.src_s.tolist()))
+    pairs = sorted(set(keys))
+    number = {pair: i for i, pair in enumerate(pairs)}
+    crow = np.array([number[k] for k in keys], dtype=np.int32)
+    csrc = np.array([s for _, s in pairs], dtype=np.int32)
+    crel = np.array([r for r, _ in pairs], dtype=np.int32)
+    cseg = np.array([sum(1 for r2, _ in pairs if r2 < r) for r in range(R + 1)], dtype=np.int32)
+    return Compaction(crow, csrc, crel, cseg)
+
+
 def _rows(V: int, rows) -> np.ndarray:
     if rows is None:
         return np.arange(V, dtype=np.int64)

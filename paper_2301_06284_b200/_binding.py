@@ -16,6 +16,7 @@ RGNN_OK, RGNN_E_INVALID_ARG, RGNN_E_RANGE, RGNN_E_UNSUPPORTED, RGNN_E_WORKSPACE,
 RGNN_F32, RGNN_BF16 = 0, 1
 RGNN_NORM_REL_INDEG, RGNN_NORM_NONE, RGNN_NORM_EDGE = 0, 1, 2
 RGNN_RGCN, RGNN_RGAT = 0, 1
+RGNN_MAT_VANILLA, RGNN_MAT_COMPACT, RGNN_MAT_AUTO = 0, 1, 2
 
 STATUS_NAMES = {0: "RGNN_OK", 1: "RGNN_E_INVALID_ARG", 2: "RGNN_E_RANGE", 3: "RGNN_E_UNSUPPORTED",
                 4: "RGNN_E_WORKSPACE", 5: "RGNN_E_CUDA", 6: "RGNN_E_NCCL"}
@@ -25,7 +26,8 @@ class rgnn_graph_desc(C.Structure):
     _fields_ = [("num_nodes", C.c_int64), ("num_edges", C.c_int64), ("num_etypes", C.c_int32),
                 ("num_ntypes", C.c_int32), ("src", C.c_void_p), ("dst", C.c_void_p), ("etype", C.c_void_p),
                 ("row_ptr", C.c_void_p), ("ntype", C.c_void_p), ("edge_norm", C.c_void_p), ("norm", C.c_int32),
-                ("row_split_cap", C.c_int32), ("dst_begin", C.c_int64), ("dst_end", C.c_int64)]
+                ("row_split_cap", C.c_int32), ("dst_begin", C.c_int64), ("dst_end", C.c_int64),
+                ("materialization", C.c_int32), ("reserved", C.c_int32)]
 
 
 class rgnn_graph_view(C.Structure):
@@ -34,7 +36,8 @@ class rgnn_graph_view(C.Structure):
                 ("num_split_rows", C.c_int64), ("R", C.c_int32),
                 ("perm", C.c_void_p), ("src_s", C.c_void_p), ("dst_s", C.c_void_p), ("seg", C.c_void_p),
                 ("row_ptr", C.c_void_p), ("pos", C.c_void_p), ("et_slot", C.c_void_p), ("inv_c", C.c_void_p),
-                ("run_ptr", C.c_void_p), ("rseg", C.c_void_p), ("seg_host", C.POINTER(C.c_int32))]
+                ("run_ptr", C.c_void_p), ("rseg", C.c_void_p), ("seg_host", C.POINTER(C.c_int32)),
+                ("num_compact", C.c_int64), ("crow_of_pos", C.c_void_p), ("csrc", C.c_void_p), ("cseg", C.c_void_p)]
 
 
 class RgnnError(RuntimeError):

@@ -58,6 +58,7 @@ struct BwdFusedParams {
   const int32_t* dst_s;
   const float* s_src;
   const __nv_bfloat16* Z;
+  const int32_t* zmap;  // compact: Z / s_src row of position p (null = p)
   const __nv_bfloat16* X;
   const float* lse;
   const float* Y;
@@ -74,7 +75,7 @@ struct BwdFusedParams {
 __device__ __forceinline__ float leaky_f(float x, float s) { return x > 0.f ? x : s * x; }
 
 // GAT = true: RGAT (dZ = alpha G_v + dpre A[r,0], bvec, dst term); false: RGCN (dZ = G_v / c_{v,r}).
-template <int K, int N, bool GAT>
+template <int K, int N, bool GAT, bool CM>
 __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
     k_bwd_fused_tc(BwdFusedParams pr) {
   using C = BfCfg<K, N>;
@@ -206,27 +207,34 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
     int cur_v = -1;
     float gv[EPL], xv[KPL], Sv = 0.f, dsc = 0.f, lse = 0.f;
     const uint32_t gmask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (g * L));
-    // dst and s_src of the warp's positions (lanes < PPW), loaded one stage ahead; Z rows of the
-    // group's positions one stage ahead as well (their latency overlaps the current stage)
-    auto load_pos = [&](int it, int& v, float& sv) {
+    // Per position (lanes < PPW): dst and s_src one stage ahead; the Z rows of the group's
+    // positions one stage ahead as well (their latency overlaps the current stage).  Compact
+    // rows (CM): the Z row index is loaded two stages ahead, s_src and Z one stage ahead.
+    auto load_idx = [&](int it, int& v, int& zr) {
       const int pl = row0 + it * C::MT + cw * C::PPW + (lane % C::PPW);
       const bool okl = lane < C::PPW && pl < row1;
       v = okl ? __ldg(pr.dst_s + pl) : -1;
-      sv = okl ? __ldg((GAT ? pr.s_src : pr.inv_c) + pl) : 0.f;
+      if constexpr (CM) zr = okl ? __ldg(pr.zmap + pl) : 0;
     };
-    auto load_z = [&](int it, uint4* z) {
-      if constexpr (!GAT) return;
+    auto load_sz = [&](int it, int zrow, float& sv, uint4* z) {
       const int pbase = row0 + it * C::MT + cw * C::PPW;
+      const int pl = pbase + (lane % C::PPW);
+      const bool okl = lane < C::PPW && pl < row1;
+      sv = okl ? __ldg(GAT ? pr.s_src + (CM ? zrow : pl) : pr.inv_c + pl) : 0.f;
+      if constexpr (!GAT) return;
 #pragma unroll
       for (int i = 0; i < PG; ++i) {
         const int p = pbase + g * PG + i;
-        z[i] = p < row1 ? ldg_nc16(pr.Z + (size_t)p * N + l * EPL) : make_uint4(0, 0, 0, 0);
+        int zr = p;
+        if constexpr (CM) zr = __shfl_sync(0xffffffffu, zrow, g * PG + i);
+        z[i] = p < row1 ? ldg_nc16(pr.Z + (size_t)zr * N + l * EPL) : make_uint4(0, 0, 0, 0);
       }
     };
-    int nv = -1;
+    int nv = -1, nzr = 0, nnv = -1, nnzr = 0;
     float ns = 0.f;
     uint4 nz[PG];
-    if (nsub > 0) { load_pos(0, nv, ns); load_z(0, nz); }
+    if (nsub > 0) { load_idx(0, nv, nzr); load_sz(0, nzr, ns, nz); }
+    if (CM && nsub > 1) load_idx(1, nnv, nnzr);
     for (int it = 0; it < nsub; ++it) {
       const int st = it % C::STAGES;
       const uint32_t use = (uint32_t)(it / C::STAGES);
@@ -235,7 +243,16 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
       uint4 zr[PG];
 #pragma unroll
       for (int i = 0; i < PG; ++i) zr[i] = nz[i];
-      if (it + 1 < nsub) { load_pos(it + 1, nv, ns); load_z(it + 1, nz); }
+      if (it + 1 < nsub) {
+        if constexpr (CM) {
+          nv = nnv; nzr = nnzr;
+          load_sz(it + 1, nzr, ns, nz);
+          if (it + 2 < nsub) load_idx(it + 2, nnv, nnzr);
+        } else {
+          load_idx(it + 1, nv, nzr);
+          load_sz(it + 1, nzr, ns, nz);
+        }
+      }
       if (use > 0) tc::mbar_wait(&empty[st], (use - 1) & 1);
       uint8_t* b = sB(st);
       uint8_t* b2 = sB2(st);
@@ -380,7 +397,8 @@ static rgnn_status bwd_fused(const rgnn_graph* g, const BwdFusedParams& p0, cons
   using C = BfCfg<K, N>;
   if (g->num_chunks == 0) return RGNN_OK;
   (void)X;
-  auto kern = p0.s_src ? k_bwd_fused_tc<K, N, true> : k_bwd_fused_tc<K, N, false>;
+  auto kern = !p0.s_src ? k_bwd_fused_tc<K, N, false, false>
+              : p0.zmap ? k_bwd_fused_tc<K, N, true, true> : k_bwd_fused_tc<K, N, true, false>;
   RGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   RGNN_LAUNCH(kern, (unsigned)g->num_chunks, C::THREADS, C::SMEM, s, p0);
   return RGNN_OK;
@@ -389,12 +407,13 @@ static rgnn_status bwd_fused(const rgnn_graph* g, const BwdFusedParams& p0, cons
 bool tc_disabled();
 
 // RGAT when s_src != null, RGCN (dZ = G_v / c_{v,r}) otherwise.
-rgnn_status launch_bwd_fused_tc(int K, int N, const rgnn_graph* g, const void* X, const void* Z, const float* s_src,
+rgnn_status launch_bwd_fused_tc(int K, int N, const rgnn_graph* g, const void* X, const void* Z, const int32_t* zmap,
+                                const float* s_src,
                                 const float* lse, const float* Y, const float* dY, const float* U, const float* A,
                                 float slope, float* part, float* cpart, cudaStream_t s) {
   if (tc_disabled()) return RGNN_E_UNSUPPORTED;
   if (getenv("RGNN_DISABLE_FUSED_BWD")) return RGNN_E_UNSUPPORTED;
-  BwdFusedParams p{g->chunks, g->src_s, g->dst_s, s_src, static_cast<const __nv_bfloat16*>(Z),
+  BwdFusedParams p{g->chunks, g->src_s, g->dst_s, s_src, static_cast<const __nv_bfloat16*>(Z), zmap,
                    static_cast<const __nv_bfloat16*>(X), lse, Y, dY, U, A, g->inv_c, slope, g->v0, part, cpart};
   if (K == 64 && N == 64) return bwd_fused<64, 64>(g, p, X, s);
   if (K == 64 && N == 128) return bwd_fused<64, 128>(g, p, X, s);

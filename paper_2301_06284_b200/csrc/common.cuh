@@ -89,6 +89,12 @@ struct rgnn_graph {
   rgnn::SplitRow* split_rows;
   int32_t* empty_rows;  // rows without in-edges (no work item)
   int64_t num_empty;
+  // compact materialisation (NEXT-1): Z rows per unique (etype, src)
+  bool compact;
+  int64_t num_compact, num_ctiles;
+  int32_t *crow_of_pos, *zrow_slot, *csrc, *cseg;
+  float* invc_slot;
+  rgnn::Tile* ctiles;
   rgnn::Tile* tiles;   // 128-row GEMM tiles (never straddle relations)
   rgnn::Tile* chunks;  // dW split-K chunks (never straddle relations)
   int32_t* chunk_seg;  // [R+1] chunks of relation r

@@ -18,12 +18,12 @@
 namespace rgnn {
 
 struct Counters {
-  int32_t bad_edge, bad_node, E_own, J, num_items, num_parts, num_split_rows, num_empty;
+  int32_t bad_edge, bad_node, E_own, J, num_items, num_parts, num_split_rows, num_empty, num_compact, pad[3];
 };
 
 __global__ void k_init_counters(Counters* c, int32_t big) {
   c->bad_edge = big; c->bad_node = big; c->E_own = 0; c->J = 0;
-  c->num_items = 0; c->num_parts = 0; c->num_split_rows = 0; c->num_empty = 0;
+  c->num_items = 0; c->num_parts = 0; c->num_split_rows = 0; c->num_empty = 0; c->num_compact = 0;
 }
 
 // CSR-by-dst input: dst of every edge from row_ptr (one warp per row).
@@ -203,6 +203,44 @@ __global__ void k_fill_items(int64_t V_own, const int32_t* __restrict__ row_ptr,
   }
 }
 
+// ---------------------------------------------------------------- compact materialisation (NEXT-1)
+// Compact rows = unique (etype, src) pairs of the owned edges, numbered
+// lexicographically (reading O15; Sec. 3.1.3: "once for each
+// (edge type, unique node index) pair ... stored in a CSR-like format").
+__global__ void k_ckeys(int64_t n, const int32_t* __restrict__ et_s, const int32_t* __restrict__ src_s, int64_t V,
+                        uint32_t* __restrict__ k, uint32_t* __restrict__ v) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    k[p] = (uint32_t)((int64_t)et_s[p] * V + src_s[p]);
+    v[p] = (uint32_t)p;
+  }
+}
+__global__ void k_cheads(int64_t n, const uint32_t* __restrict__ k, int32_t* __restrict__ head) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    head[i] = (i == 0 || k[i - 1] != k[i]) ? 1 : 0;
+}
+__global__ void k_crows(int64_t n, const uint32_t* __restrict__ k, const uint32_t* __restrict__ pidx,
+                        const int32_t* __restrict__ head, const int32_t* __restrict__ cex, int64_t V,
+                        int32_t* __restrict__ crow_of_pos, int32_t* __restrict__ csrc, int32_t* __restrict__ crel) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = cex[i] + head[i] - 1;
+    crow_of_pos[pidx[i]] = c;
+    if (head[i]) {
+      csrc[c] = (int32_t)(k[i] % (uint32_t)V);
+      crel[c] = (int32_t)(k[i] / (uint32_t)V);
+    }
+  }
+}
+// slot-ordered views used by the walks: Z row of slot q, and (RGCN) the 1/c of slot q
+__global__ void k_cslots(int64_t n, const int32_t* __restrict__ pos, const int32_t* __restrict__ crow_of_pos,
+                         const float* __restrict__ inv_c, int32_t* __restrict__ zrow_slot,
+                         float* __restrict__ invc_slot) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = pos[q];
+    zrow_slot[q] = crow_of_pos[p];
+    invc_slot[q] = inv_c[p];
+  }
+}
+
 static int bits_for(uint64_t maxval) {
   int b = 0;
   while (b < 64 && (maxval >> b) != 0) ++b;
@@ -216,12 +254,15 @@ struct GraphLayout {
   Item* items;
   SplitRow* split_rows;
   int32_t* empty_rows;
+  int32_t *crow_of_pos, *zrow_slot, *csrc, *cseg;
+  float* invc_slot;
+  Tile* ctiles;
   Tile *tiles, *chunks;
   int32_t* chunk_seg;
   size_t dev_bytes;
   // scratch
   Counters* ctr;
-  int32_t *dst_tmp, *flags, *head, *run_ex, *et_s, *n_items, *n_parts, *n_split, *n_empty, *rseg_cnt;
+  int32_t *dst_tmp, *flags, *head, *run_ex, *et_s, *n_items, *n_parts, *n_split, *n_empty, *rseg_cnt, *crel;
   uint32_t *k0, *v0, *k1, *v1;
   void* prim;
   size_t prim_bytes, scratch_bytes;
@@ -249,6 +290,13 @@ static GraphLayout layout(const rgnn_graph_desc* d, void* dev, void* scr) {
   L.items = c.take<Item>(V_own + Ec / cap + 1);
   L.split_rows = c.take<SplitRow>(Ec / cap + 1);
   L.empty_rows = c.take<int32_t>(V_own + 1);
+  const bool cm = d->materialization != RGNN_MAT_VANILLA;
+  L.crow_of_pos = c.take<int32_t>(cm ? Ec : 1);
+  L.zrow_slot = c.take<int32_t>(cm ? Ec : 1);
+  L.invc_slot = c.take<float>(cm ? Ec : 1);
+  L.csrc = c.take<int32_t>(cm ? Ec : 1);
+  L.cseg = c.take<int32_t>(R + 1);
+  L.ctiles = c.take<Tile>(cm ? Ec / kTileRows + R + 1 : 1);
   L.tiles = c.take<Tile>(Ec / kTileRows + R + 1);
   L.chunks = c.take<Tile>(max_chunks(E, R));
   L.chunk_seg = c.take<int32_t>(R + 1);
@@ -265,6 +313,7 @@ static GraphLayout layout(const rgnn_graph_desc* d, void* dev, void* scr) {
   L.n_split = s.take<int32_t>(V_own + 1);
   L.n_empty = s.take<int32_t>(V_own + 1);
   L.rseg_cnt = s.take<int32_t>(R + 1);
+  L.crel = s.take<int32_t>(d->materialization != RGNN_MAT_VANILLA ? Ec : 1);
   L.k0 = s.take<uint32_t>(Ec);
   L.v0 = s.take<uint32_t>(Ec);
   L.k1 = s.take<uint32_t>(Ec);
@@ -295,6 +344,12 @@ static rgnn_status check_desc(const rgnn_graph_desc* d) {
     return set_error(RGNN_E_INVALID_ARG, "edge_norm required for RGNN_NORM_EDGE");
   if (d->ntype && d->num_ntypes < 1) return set_error(RGNN_E_INVALID_ARG, "num_ntypes must be >= 1");
   if (d->row_split_cap < 0) return set_error(RGNN_E_INVALID_ARG, "row_split_cap < 0");
+  if (d->materialization != RGNN_MAT_VANILLA && d->materialization != RGNN_MAT_COMPACT &&
+      d->materialization != RGNN_MAT_AUTO)
+    return set_error(RGNN_E_INVALID_ARG, "bad materialization %d", d->materialization);
+  if (d->materialization != RGNN_MAT_VANILLA &&
+      (uint64_t)d->num_etypes * (uint64_t)(d->num_nodes > 0 ? d->num_nodes : 1) > 0xffffffffull)
+    return set_error(RGNN_E_UNSUPPORTED, "compact materialisation needs R * V < 2^32 (sort key)");
   return RGNN_OK;
 }
 
@@ -399,10 +454,28 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
     RGNN_LAUNCH(k_fill_items, grid_for(V_own), T, 0, s, V_own, L.row_ptr, cap, L.n_items, L.n_parts, L.n_split,
                 L.items, L.split_rows);
   }
+  // Compact materialisation: unique (etype, src) rows, lexicographic.
+  const bool cm = d->materialization != RGNN_MAT_VANILLA;
+  if (cm && n > 0) {
+    RGNN_LAUNCH(k_ckeys, grid_for(n), T, 0, s, n, L.et_s, L.src_s, V, L.k0, L.v0);
+    RGNN_TRY(radix_sort_pairs(L.k0, L.v0, L.k1, L.v1, n, bits_for((uint64_t)R * (uint64_t)V - 1), L.prim,
+                              L.prim_bytes, s, &alt));
+    uint32_t* ck = alt ? L.k1 : L.k0;
+    uint32_t* cv = alt ? L.v1 : L.v0;
+    RGNN_LAUNCH(k_cheads, grid_for(n), T, 0, s, n, ck, L.head);
+    RGNN_TRY(scan_exclusive(L.head, L.run_ex, n, &L.ctr->num_compact, L.prim, L.prim_bytes, s));
+    RGNN_LAUNCH(k_crows, grid_for(n), T, 0, s, n, ck, cv, L.head, L.run_ex, V, L.crow_of_pos, L.csrc, L.crel);
+    RGNN_LAUNCH(k_cslots, grid_for(n), T, 0, s, n, L.pos, L.crow_of_pos, L.inv_c, L.zrow_slot, L.invc_slot);
+  }
   // The single readback: counts + relation segments.
-  std::vector<int32_t> seg_h(R + 1);
+  std::vector<int32_t> seg_h(R + 1), cseg_h(R + 1, 0);
   RGNN_CUDA_TRY(cudaMemcpyAsync(&h, L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
   RGNN_CUDA_TRY(cudaMemcpyAsync(seg_h.data(), L.seg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
+  RGNN_CUDA_TRY(cudaStreamSynchronize(s));
+  if (cm) {  // compact segments: first compact row of each relation
+    RGNN_LAUNCH(k_bounds<int32_t>, grid_for(R + 1), T, 0, s, (int64_t)h.num_compact, L.crel, (int64_t)R, L.cseg);
+    RGNN_CUDA_TRY(cudaMemcpyAsync(cseg_h.data(), L.cseg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
+  }
   RGNN_CUDA_TRY(cudaStreamSynchronize(s));
   int dev_id = 0, sms = 148;
   RGNN_CUDA_TRY(cudaGetDevice(&dev_id));
@@ -421,6 +494,13 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
       chunks.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + chunk_rows, seg_h[r + 1]), 0});
   }
   chunk_seg[R] = (int32_t)chunks.size();
+  std::vector<Tile> ctiles;
+  if (cm)
+    for (int32_t r = 0; r < R; ++r)
+      for (int64_t a = cseg_h[r]; a < cseg_h[r + 1]; a += kTileRows)
+        ctiles.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + kTileRows, cseg_h[r + 1]), 0});
+  if (!ctiles.empty())
+    RGNN_CUDA_TRY(cudaMemcpyAsync(L.ctiles, ctiles.data(), sizeof(Tile) * ctiles.size(), cudaMemcpyHostToDevice, s));
   if ((int64_t)chunks.size() > max_chunks(E, R))
     return set_error(RGNN_E_CUDA, "internal: chunk table overflow");
   if (!tiles.empty())
@@ -439,6 +519,13 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   g->pos = L.pos; g->et_slot = L.et_slot; g->run_ptr = L.run_ptr; g->rseg = L.rseg; g->inv_c = L.inv_c;
   g->items = L.items; g->split_rows = L.split_rows; g->tiles = L.tiles; g->chunks = L.chunks;
   g->empty_rows = L.empty_rows; g->num_empty = h.num_empty;
+  // AUTO keeps the compact rows only when they at least halve the GEMM rows (measured r01:
+  // ogbn-mag U/E = 0.15 gains ~1 ms/step; AM U/E = 0.56 loses, the backward then gathers Z
+  // rows at random instead of streaming them in position order).
+  const bool use_c = cm && (d->materialization == RGNN_MAT_COMPACT || 2 * (int64_t)h.num_compact <= n);
+  g->compact = use_c; g->num_compact = use_c ? h.num_compact : 0; g->crow_of_pos = L.crow_of_pos; g->zrow_slot = L.zrow_slot;
+  g->invc_slot = L.invc_slot; g->csrc = L.csrc; g->cseg = L.cseg; g->ctiles = L.ctiles;
+  g->num_ctiles = (int64_t)ctiles.size();
   g->chunk_seg = L.chunk_seg;
   g->seg_host = seg_h;
   g->chunk_seg_host = chunk_seg;
@@ -455,6 +542,7 @@ rgnn_status rgnn_graph_export(const rgnn_graph* g, rgnn_graph_view* v) {
   v->perm = g->perm; v->src_s = g->src_s; v->dst_s = g->dst_s; v->seg = g->seg; v->row_ptr = g->row_ptr;
   v->pos = g->pos; v->et_slot = g->et_slot; v->inv_c = g->inv_c; v->run_ptr = g->run_ptr; v->rseg = g->rseg;
   v->seg_host = g->seg_host.data();
+  v->num_compact = g->num_compact; v->crow_of_pos = g->crow_of_pos; v->csrc = g->csrc; v->cseg = g->cseg;
   return RGNN_OK;
 }
 

@@ -68,6 +68,8 @@ struct AggArgs {
   const float* U;
   float slope;
   const void* Z0;        // RGCN self-loop rows [V_own, N] T or null
+  const float* slot_scale;  // RGCN compact: 1/c of slot q (Z rows unscaled), or null
+  bool cache_dst;        // RGAT: long (etype, dst) runs -> x_dst . U[r] once per run
   float* Y;
   float* lse;
   float* part;           // [num_parts, N+4]
@@ -82,6 +84,7 @@ struct BwdArgs {
   const Item* items;
   int64_t num_items;
   const int32_t* pos;
+  const int32_t* zrow;   // compact: Z / s_src row of slot q (null: pos[q])
   const int32_t* et_slot;
   const void* Z;
   const float* s_src;
@@ -101,7 +104,9 @@ rgnn_status launch_bwd_traverse(int prec, int K, int N, const BwdArgs& a, cudaSt
 // tcgen05 path (gemm_tc.cu): returns RGNN_E_UNSUPPORTED if the shape is not covered.
 rgnn_status launch_gemm_fwd_tc(int K, int N, const GemmFwdArgs& a, cudaStream_t s);
 rgnn_status launch_gemm_dw_tc(int K, int N, const GemmDwArgs& a, cudaStream_t s);
-rgnn_status launch_bwd_fused_tc(int K, int N, const rgnn_graph* g, const void* X, const void* Z, const float* s_src,
+// zmap (compact): Z / s_src row of position p, null = p.
+rgnn_status launch_bwd_fused_tc(int K, int N, const rgnn_graph* g, const void* X, const void* Z, const int32_t* zmap,
+                                const float* s_src,
                                 const float* lse, const float* Y, const float* dY, const float* U, const float* A,
                                 float slope, float* part, float* cpart, cudaStream_t s);
 rgnn_status launch_expand_dz(int64_t E, int N, const int32_t* dst_s, const float* inv_c, const float* G, void* dZ,

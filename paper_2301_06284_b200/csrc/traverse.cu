@@ -7,7 +7,8 @@
 //   divide of Listing 1's edge_softmax are fused with the
 //   attention score and the alpha-weighted aggregation into one
 //   pass with an online (running max) softmax -- exact in real arithmetic
-//   (reading O5).  RGAT score: pre_e = s_src[p] + x_dst . U[r]  where
+//   (reading O5).  RGAT score: pre_e = s_src[p] + x_dst . U[r]  (the second
+//   term computed once per (dst, relation) run of the row) where
 //   s_src[p] = A[r,0].Z[p] came from the GEMM epilogue and U[r] = W_r A[r,1]
 //   (linear-operator fusion, Sec. 3.4.1).
 // One warp per work item (a row or a <= cap-edge chunk of a long row).  A Z
@@ -71,7 +72,39 @@ __device__ __forceinline__ float dot_u(const float* xv, const float* Ur) {
   return d;
 }
 
-template <typename T, int K, int N, bool RGAT>
+// pre_u = s_src_u + x_dst . U[r_u] for the UNR edges of a lane group (same expression as the
+// backward's pre).  CACHE: the slots of a row come grouped by relation ((etype, dst) positions
+// in ascending order) and x_dst . U[r] depends only on (dst, r), so it is recomputed only when
+// some group's relation changes (warp-uniform vote: no divergence) -- chosen for graphs with
+// long (etype, dst) runs.  Otherwise one dot per edge, UNR independent chains.
+template <int K, int L, int KPL, int UNR, bool CACHE>
+__device__ __forceinline__ void dst_scores(const float* xv, const float* U, int l, const int* rr, const float* ssv,
+                                           int& cr, float& cd, float* sc) {
+  if constexpr (CACHE) {
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      if (__any_sync(0xffffffffu, rr[u] != cr)) {
+        float d = dot_u<KPL>(xv, U + (size_t)rr[u] * K + l * KPL);
+#pragma unroll
+        for (int o = L / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        cd = d;
+        cr = rr[u];
+      }
+      sc[u] = ssv[u] + cd;
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) sc[u] = dot_u<KPL>(xv, U + (size_t)rr[u] * K + l * KPL);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+#pragma unroll
+      for (int o = L / 2; o > 0; o >>= 1) sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
+      sc[u] = ssv[u] + sc[u];
+    }
+  }
+}
+
+template <typename T, int K, int N, bool RGAT, bool CACHE>
 __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
   using S = WalkShape<T, K, N>;
   constexpr int EPL = S::EPL, L = S::L, G = S::G, UNR = S::UNR, B = S::B, KPL = S::KPL;
@@ -89,6 +122,8 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
     for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
     float m = -CUDART_INF_F, lsum = 0.f;
     float xv[KPL];
+    int cr = -1;     // relation of the cached dst score (per lane group)
+    float cd = 0.f;  // x_dst . U[cr]
     if constexpr (RGAT) {
       if (it.q1 > it.q0) load_slice<KPL>(X + (a.v0 + it.row) * (int64_t)K + l * KPL, xv);
     }
@@ -103,33 +138,32 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
       const int myr = nr;
       float mys = 0.f;
       if constexpr (RGAT) mys = ok ? a.s_src[myp] : 0.f;
+      else mys = (ok && a.slot_scale) ? a.slot_scale[base + lane] : 1.f;  // compact RGCN: 1/c per slot
       nq = base + B + lane;
       nok = lane < B && nq < it.q1;
       np = nok ? a.pos[nq] : 0;
       nr = nok ? a.et_slot[nq] : 0;
       uint4 zr[UNR];
-      float sc[UNR];
+      float sc[UNR], ssv[UNR];
+      int rr[UNR];
       bool val[UNR];
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) {
+      for (int u = 0; u < UNR; ++u) {  // all Z-row loads of the step first
         const int j = u * G + g;
         const int p = __shfl_sync(0xffffffffu, myp, j);
-        const int r = __shfl_sync(0xffffffffu, myr, j);
-        const float ss = __shfl_sync(0xffffffffu, mys, j);
+        rr[u] = __shfl_sync(0xffffffffu, myr, j);
+        ssv[u] = __shfl_sync(0xffffffffu, mys, j);
         val[u] = base + j < it.q1;
         zr[u] = val[u] ? ldg16(Z + (size_t)p * N + l * EPL) : make_uint4(0, 0, 0, 0);
-        if constexpr (RGAT) {
-          const float d = dot_u<KPL>(xv, a.U + (size_t)r * K + l * KPL);
-          sc[u] = l == 0 ? d + ss : d;  // lane partial; s_src added once, then reduced
-        }
+      }
+      if constexpr (RGAT) dst_scores<K, L, KPL, UNR, CACHE>(xv, a.U, l, rr, ssv, cr, cd, sc);
+      else {
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) sc[u] = ssv[u];  // edge weight (1 when Z rows are pre-scaled)
       }
       if constexpr (RGAT) {
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-#pragma unroll
-          for (int o = L / 2; o > 0; o >>= 1) sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
-          sc[u] = val[u] ? leaky(sc[u], a.slope) : -CUDART_INF_F;
-        }
+        for (int u = 0; u < UNR; ++u) sc[u] = val[u] ? leaky(sc[u], a.slope) : -CUDART_INF_F;
         float mnew = m;
 #pragma unroll
         for (int u = 0; u < UNR; ++u) mnew = fmaxf(mnew, sc[u]);
@@ -155,7 +189,7 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
           float zf[EPL];
           Vec16<T>{zr[u]}.to_float(zf);
 #pragma unroll
-          for (int i = 0; i < EPL; ++i) acc[i] += zf[i];
+          for (int i = 0; i < EPL; ++i) acc[i] = fmaf(sc[u], zf[i], acc[i]);  // fma(1, z, acc) == acc + z
         }
       }
     }
@@ -215,7 +249,7 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
 // items form one continuous stream of B-edge steps, so short rows do not drain
 // the pipeline.  Results are bit-identical to k_aggregate (same per-group edge
 // assignment, same arithmetic order).
-template <typename T, int K, int N, bool RGAT, int RING>
+template <typename T, int K, int N, bool RGAT, int RING, bool CACHE>
 __global__ void __launch_bounds__(256) k_aggregate_ring(AggArgs a) {
   using S = WalkShape<T, K, N>;
   constexpr int EPL = S::EPL, L = S::L, G = S::G, UNR = S::UNR, B = S::B, KPL = S::KPL;
@@ -265,10 +299,10 @@ __global__ void __launch_bounds__(256) k_aggregate_ring(AggArgs a) {
                        "l"(Z + (size_t)p * N + l * EPL)
                        : "memory");
       }
-      if (RGAT && ok)
+      if (ok && (RGAT || a.slot_scale))  // RGAT: s_src of the Z row; compact RGCN: 1/c of the slot
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(
                          sring + pslot * 32 + lane)),
-                     "l"(a.s_src + myp)
+                     "l"(RGAT ? a.s_src + myp : a.slot_scale + q)
                      : "memory");
       if (lane < B) rring[pslot * 32 + lane] = myr;
       advance_producer();
@@ -290,13 +324,16 @@ __global__ void __launch_bounds__(256) k_aggregate_ring(AggArgs a) {
     for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
     float m = -CUDART_INF_F, lsum = 0.f;
     float xv[KPL];
+    int cr = -1;
+    float cd = 0.f;
     if constexpr (RGAT) load_slice<KPL>(X + (a.v0 + it.row) * (int64_t)K + l * KPL, xv);
     for (int base = it.q0; base < it.q1; base += B) {
       produce();  // keeps RING-1 steps in flight
       asm volatile("cp.async.wait_group %0;" ::"n"(RING - 1) : "memory");
       __syncwarp();
       uint4 zr[UNR];
-      float sc[UNR];
+      float sc[UNR], ssv[UNR];
+      int rr[UNR];
       bool val[UNR];
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
@@ -304,21 +341,18 @@ __global__ void __launch_bounds__(256) k_aggregate_ring(AggArgs a) {
         val[u] = base + j < it.q1;
         zr[u] = val[u] ? zring[((size_t)cslot * UNR + u) * 32 + lane] : make_uint4(0, 0, 0, 0);
         if constexpr (RGAT) {
-          const int r = rring[cslot * 32 + j];
-          const float ss = sring[cslot * 32 + j];
-          const float d = dot_u<KPL>(xv, a.U + (size_t)r * K + l * KPL);
-          sc[u] = l == 0 ? d + ss : d;
+          rr[u] = rring[cslot * 32 + j];
+          ssv[u] = sring[cslot * 32 + j];
+        } else {
+          sc[u] = (a.slot_scale && val[u]) ? sring[cslot * 32 + j] : 1.f;  // stale slots never multiply
         }
       }
+      if constexpr (RGAT) dst_scores<K, L, KPL, UNR, CACHE>(xv, a.U, l, rr, ssv, cr, cd, sc);
       __syncwarp();  // the slot may be refilled by the next produce()
       cslot = cslot + 1 == RING ? 0 : cslot + 1;
       if constexpr (RGAT) {
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-#pragma unroll
-          for (int o = L / 2; o > 0; o >>= 1) sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
-          sc[u] = val[u] ? leaky(sc[u], a.slope) : -CUDART_INF_F;
-        }
+        for (int u = 0; u < UNR; ++u) sc[u] = val[u] ? leaky(sc[u], a.slope) : -CUDART_INF_F;
         float mnew = m;
 #pragma unroll
         for (int u = 0; u < UNR; ++u) mnew = fmaxf(mnew, sc[u]);
@@ -344,7 +378,7 @@ __global__ void __launch_bounds__(256) k_aggregate_ring(AggArgs a) {
           float zf[EPL];
           Vec16<T>{zr[u]}.to_float(zf);
 #pragma unroll
-          for (int i = 0; i < EPL; ++i) acc[i] += zf[i];
+          for (int i = 0; i < EPL; ++i) acc[i] = fmaf(sc[u], zf[i], acc[i]);  // fma(1, z, acc) == acc + z
         }
       }
     }
@@ -534,10 +568,11 @@ __global__ void __launch_bounds__(256) k_bwd_rgat(BwdArgs a) {
       const int q = base + lane;
       const bool ok = lane < B && q < it.q1;
       const int myp = ok ? a.pos[q] : 0;
+      const int myz = ok ? (a.zrow ? a.zrow[q] : myp) : 0;  // row of Z / s_src (compact: (etype, src) row)
       const int myr = ok ? a.et_slot[q] : 0;
-      const float mys = ok ? a.s_src[myp] : 0.f;
+      const float mys = ok ? a.s_src[myz] : 0.f;
       uint4 zr[UNR];
-      float sc[UNR], da[UNR];
+      float sc[UNR], da[UNR], sv[UNR];
       int pp[UNR], rr[UNR];
       bool val[UNR];
 #pragma unroll
@@ -545,11 +580,12 @@ __global__ void __launch_bounds__(256) k_bwd_rgat(BwdArgs a) {
         const int j = u * G + g;
         pp[u] = __shfl_sync(0xffffffffu, myp, j);
         rr[u] = __shfl_sync(0xffffffffu, myr, j);
+        const int zz = __shfl_sync(0xffffffffu, myz, j);
         const float ss = __shfl_sync(0xffffffffu, mys, j);
         val[u] = base + j < it.q1;
-        zr[u] = val[u] ? ldg16(Z + (size_t)pp[u] * N + l * EPL) : make_uint4(0, 0, 0, 0);
-        const float d = dot_u<KPL>(xv, a.U + (size_t)rr[u] * K + l * KPL);
-        sc[u] = l == 0 ? d + ss : d;
+        zr[u] = val[u] ? ldg16(Z + (size_t)zz * N + l * EPL) : make_uint4(0, 0, 0, 0);
+        sc[u] = dot_u<KPL>(xv, a.U + (size_t)rr[u] * K + l * KPL);
+        sv[u] = ss;
       }
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
@@ -571,7 +607,7 @@ __global__ void __launch_bounds__(256) k_bwd_rgat(BwdArgs a) {
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
         if (!val[u]) continue;
-        const float pre = sc[u];
+        const float pre = sv[u] + sc[u];  // s_src + x_dst . U[r], as in the forward walk
         const float alpha = __expf(leaky(pre, a.slope) - lse);
         const float dpre = alpha * (da[u] - Sv) * (pre > 0.f ? 1.f : a.slope);
         const float* A0 = a.A + (size_t)rr[u] * 2 * N + l * EPL;
@@ -625,14 +661,14 @@ static rgnn_status aggregate(bool rgat, const AggArgs& a, cudaStream_t s) {
     if (ring) {
       constexpr int RING = 4, UNR = WalkShape<T, K, N>::UNR;
       const size_t smem = 8 * (RING * UNR * 32 * sizeof(uint4) + RING * 32 * 2 * sizeof(float));
-      auto kt = k_aggregate_ring<T, K, N, true, RING>;
-      auto kf = k_aggregate_ring<T, K, N, false, RING>;
-      RGNN_CUDA_TRY(cudaFuncSetAttribute(rgat ? kt : kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      if (rgat) RGNN_LAUNCH(kt, warps_grid(a.num_items), 256, smem, s, a);
-      else RGNN_LAUNCH(kf, warps_grid(a.num_items), 256, smem, s, a);
+      auto kern = !rgat ? k_aggregate_ring<T, K, N, false, RING, false>
+                  : a.cache_dst ? k_aggregate_ring<T, K, N, true, RING, true> : k_aggregate_ring<T, K, N, true, RING, false>;
+      RGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      RGNN_LAUNCH(kern, warps_grid(a.num_items), 256, smem, s, a);
     } else {
-      if (rgat) RGNN_LAUNCH((k_aggregate<T, K, N, true>), warps_grid(a.num_items), 256, 0, s, a);
-      else RGNN_LAUNCH((k_aggregate<T, K, N, false>), warps_grid(a.num_items), 256, 0, s, a);
+      auto kern = !rgat ? k_aggregate<T, K, N, false, false>
+                  : a.cache_dst ? k_aggregate<T, K, N, true, true> : k_aggregate<T, K, N, true, false>;
+      RGNN_LAUNCH(kern, warps_grid(a.num_items), 256, 0, s, a);
     }
   }
   if (a.num_split_rows > 0) {

@@ -38,6 +38,12 @@ def _prec(p) -> int:
     return PREC[p] if isinstance(p, str) else int(p)
 
 
+def _mat(m) -> int:
+    if isinstance(m, str):
+        return {"vanilla": B.RGNN_MAT_VANILLA, "compact": B.RGNN_MAT_COMPACT, "auto": B.RGNN_MAT_AUTO}[m]
+    return int(m)
+
+
 def _model(m) -> int:
     return MODEL[m] if isinstance(m, str) else int(m)
 
@@ -47,7 +53,8 @@ class Graph:
 
     def __init__(self, num_nodes: int, src, dst, etype, num_etypes: int, *, row_ptr=None, ntype=None,
                  num_ntypes: int = 0, norm: int = B.RGNN_NORM_REL_INDEG, edge_norm=None, row_split_cap: int = 0,
-                 dst_begin: int = 0, dst_end: Optional[int] = None, device="cuda", stream=None):
+                 dst_begin: int = 0, dst_end: Optional[int] = None, materialization="vanilla", device="cuda",
+                 stream=None):
         self.device = torch.device(device)
         self.V, self.R = int(num_nodes), int(num_etypes)
         self.src = _dev_i32(src, self.device)
@@ -64,7 +71,7 @@ class Graph:
                               src=_ptr(self.src), dst=_ptr(self.dst), etype=_ptr(self.etype),
                               row_ptr=_ptr(self.row_ptr_in), ntype=_ptr(self.ntype), edge_norm=_ptr(self.edge_norm),
                               norm=int(norm), row_split_cap=int(row_split_cap), dst_begin=self.dst_begin,
-                              dst_end=self.dst_end)
+                              dst_end=self.dst_end, materialization=_mat(materialization))
         self._desc = d
         dev_b, scr_b = C.c_size_t(), C.c_size_t()
         B.call("rgnn_graph_bytes", C.byref(d), C.byref(dev_b), C.byref(scr_b))
@@ -80,6 +87,7 @@ class Graph:
         B.call("rgnn_graph_export", h, C.byref(v))
         self.view = v
         self.V_own, self.E_own = int(v.V_own), int(v.E_own)
+        self.num_compact = int(v.num_compact)
 
     @property
     def handle(self):
@@ -105,6 +113,14 @@ class Graph:
                 "row_ptr": self._arr(v.row_ptr, Vo + 1, i32), "pos": self._arr(v.pos, E, i32),
                 "et_slot": self._arr(v.et_slot, E, i32), "inv_c": self._arr(v.inv_c, E, f32),
                 "run_ptr": self._arr(v.run_ptr, int(v.num_runs) + 1, i32), "rseg": self._arr(v.rseg, R + 1, i32)}
+
+    def compact_arrays(self) -> dict:
+        """Compact materialisation tables (graph created with materialization="compact")."""
+        v = self.view
+        E, U, R = int(v.E_own), int(v.num_compact), int(v.R)
+        i32 = torch.int32
+        return {"crow_of_pos": self._arr(v.crow_of_pos, E, i32), "csrc": self._arr(v.csrc, U, i32),
+                "cseg": self._arr(v.cseg, R + 1, i32)}
 
 
 class Comm:

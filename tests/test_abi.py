@@ -39,3 +39,26 @@ def test_host_only_entry_points():
     from paper_2301_06284_b200 import _binding as B
     st = B.lib.rgnn_graph_bytes(None, None, None)
     assert st == B.RGNN_E_INVALID_ARG and b"desc" in B.lib.rgnn_last_error()
+
+
+def test_binding_struct_layouts_match_header(tmp_path):
+    """ctypes mirrors of rgnn_graph_desc / rgnn_graph_view have the C layout (size and every offset)."""
+    import subprocess
+    from paper_2301_06284_b200 import _binding as B
+    structs = {"rgnn_graph_desc": B.rgnn_graph_desc, "rgnn_graph_view": B.rgnn_graph_view}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "rgnn.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'  printf("{name} size %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            lines.append(f'  printf("{name} {f} %zu\\n", offsetof({name}, {f}));')
+    lines.append("  return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for name, cls in structs.items():
+        assert got[(name, "size")] == ctypes.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert got[(name, f)] == getattr(cls, f).offset, (name, f)

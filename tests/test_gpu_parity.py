@@ -21,9 +21,9 @@ def _check(m, g, t, model, prec, **kw):
     ref = run_oracle(oracle, g, t, model, prec=prec, **okw)
     assert_close(gpu["Y"], ref["Y"], prec, f"{model}/{prec} Y")
     if kw.get("backward", True):
-        assert_close(gpu["dW"], ref["dW"], prec, f"{model}/{prec} dW")
+        assert_close(gpu["dW"], ref["dW"], prec, f"{model}/{prec} dW", per_slice=True)
         if model == "rgat":
-            assert_close(gpu["dA"], ref["dA"], prec, f"{model}/{prec} dA")
+            assert_close(gpu["dA"], ref["dA"], prec, f"{model}/{prec} dA", per_slice=True)
         if kw.get("with_w0"):
             assert_close(gpu["dW0"], ref["dW0"], prec, f"{model}/{prec} dW0")
     return gpu, ref
@@ -195,4 +195,4 @@ def test_determinism_and_simulated_shards(rgnn):
         ys.append(r["Y"]); dws.append(r["dW"])
     np.testing.assert_array_equal(np.concatenate(ys), a["Y"])
     ref = run_oracle(oracle, g, t, "rgat", prec="bf16")
-    assert_close(sum(dws), ref["dW"], "bf16", "sharded dW sum")
+    assert_close(sum(dws), ref["dW"], "bf16", "sharded dW sum", per_slice=True)

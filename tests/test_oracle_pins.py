@@ -357,3 +357,38 @@ def test_dst_shards_sum_to_full_gradient():
     dW1, dA1 = oracle.rgat_backward(V, R, g.src, g.dst, g.etype, t.X, t.W, t.A, G, rels=[1])
     np.testing.assert_allclose(dW1[1], dW[1], rtol=1e-12, atol=1e-14)
     assert not dW1[0].any() and not dW1[2].any()
+
+
+# ---------------------------------------------------------------- compact materialisation
+def test_golden_compact_toy():
+    with open(os.path.join(os.path.dirname(__file__), "golden", "compact_toy.json")) as f:
+        t = json.load(f)
+    e = np.array(t["edges_src_dst_etype"])
+    pre = oracle.preprocess(t["V"], t["R"], e[:, 0], e[:, 1], e[:, 2])
+    c = oracle.compaction(t["R"], pre)
+    assert pre.E_own == t["vanilla_rows"] and c.num_compact == t["compact_rows"]
+    assert pre.perm.tolist() == t["perm"]
+    assert c.crow_of_pos.tolist() == t["crow_of_pos"]
+    assert c.csrc.tolist() == t["csrc"] and c.cseg.tolist() == t["cseg"]
+
+
+@pytest.mark.parametrize("seed,V,E,R,shard", [(0, 50, 400, 3, False), (1, 300, 2000, 7, True), (2, 5, 0, 2, False),
+                                              (3, 1, 30, 1, False)])
+def test_compaction_bruteforce(seed, V, E, R, shard):
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, V, E); dst = rng.integers(0, V, E); et = rng.integers(0, R, E)
+    v0, v1 = (V // 3, 2 * V // 3) if shard else (0, V)
+    pre = oracle.preprocess(V, R, src, dst, et, v0, v1)
+    c = oracle.compaction(R, pre)
+    own = (dst >= v0) & (dst < v1)
+    # U = number of distinct (etype, src) pairs of the owned edges, counted another way
+    assert c.num_compact == np.unique(et[own].astype(np.int64) * V + src[own]).size
+    # every position's compact row holds exactly its (etype, src)
+    et_p = et[pre.perm]
+    assert (c.csrc[c.crow_of_pos] == src[pre.perm]).all() and (c.crel[c.crow_of_pos] == et_p).all()
+    # rows strictly increasing in (etype, src); cseg brackets each relation
+    key = c.crel.astype(np.int64) * V + c.csrc
+    assert (np.diff(key) > 0).all()
+    for r in range(R):
+        assert (c.crel[c.cseg[r]:c.cseg[r + 1]] == r).all()
+    assert c.cseg[0] == 0 and c.cseg[R] == c.num_compact
