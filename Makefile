@@ -4,7 +4,7 @@ PKG      := paper_2301_06284_b200
 NCCL_DIR ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -Iinclude -I$(NCCL_DIR)/include \
-            --expt-relaxed-constexpr -Xptxas -warn-spills
+            --expt-relaxed-constexpr -Xptxas -warn-spills $(EXTRA)
 SRCS     := $(wildcard $(PKG)/csrc/*.cu)
 OBJS     := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
 HDRS     := $(wildcard $(PKG)/csrc/*.cuh) include/rgnn.h

@@ -412,8 +412,9 @@ def run_ours(args):
     if cand:
         dom = max(cand, key=lambda k: cand[k][0])
         per_launch_ms = phases[dom][0] / max(phases[dom][1], 1)
+        zr = G.zrows(model)
         byts = algorithmic_bytes(dom, model, prec, K, N, int(v.E_own), int(v.V_own), int(v.num_runs),
-                                 int(v.num_items), U=int(v.num_compact) if int(v.num_compact) > 0 else None)
+                                 int(v.num_items), U=zr if zr != int(v.E_own) else None)
         ach = byts / (per_launch_ms * 1e-3) / 1e9
         traffic = None
         try:
@@ -439,9 +440,9 @@ def run_ours(args):
                "vs_baseline": None, "dtype": prec, "data": "synthetic (seeded generator, random-init weights)",
                "config": dict(config_json(cfg, model, prec, g, world),
                               launch="CUDA graph of the step" if use_graph else "eager",
-                              materialization=("compact" if G.num_compact > 0 else "vanilla") + (
+                              materialization=("compact" if G.zrows(model) != G.E_own else "vanilla") + (
                                   " (auto)" if args.materialization == "auto" else ""),
-                              compact_rows=int(G.num_compact)),
+                              z_rows=G.zrows(model), compact_rows=int(G.num_compact)),
                "clocks": clocks, "e2e": e2e,
                "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu,
                "phases_ms_per_step": {k: round(x[0], 4) for k, x in sorted(step_phase.items())},

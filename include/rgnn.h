@@ -70,8 +70,11 @@ typedef enum { RGNN_RGCN = 0, RGNN_RGAT = 1 } rgnn_model;
  * VANILLA: one row per edge (the row number is the edge's position).
  * COMPACT: one row per unique (etype, src) pair, numbered lexicographically
  * (reading O15); the typed GEMM then runs over U_src rows instead of E.     */
-/* AUTO: compact when the unique pairs are at most half the edges (U <= E/2),
- * vanilla otherwise; rgnn_graph_view.num_compact > 0 tells which was taken. */
+/* AUTO: the compact tables are built, and each layer call picks per model:
+ * RGCN compact whenever U < E_own (its backward never reads Z); RGAT compact
+ * when U <= E_own / 2 (its backward then gathers Z rows at random instead of
+ * streaming them -- measured r01: ogbn-mag U/E = 0.15 wins, AM 0.56 loses).
+ * rgnn_zrows() reports the choice.                                          */
 typedef enum { RGNN_MAT_VANILLA = 0, RGNN_MAT_COMPACT = 1, RGNN_MAT_AUTO = 2 } rgnn_materialization;
 
 typedef struct rgnn_graph rgnn_graph;
@@ -115,7 +118,7 @@ typedef struct {
   const int32_t* run_ptr;  /* [num_runs+1] (etype,dst) runs, position space */
   const int32_t* rseg;     /* [R+1]   runs of relation r                    */
   const int32_t* seg_host; /* [host, R+1] copy of seg                       */
-  int64_t num_compact;     /* compact rows (0 when vanilla)                 */
+  int64_t num_compact;     /* unique (etype, src) pairs U (0: not built)    */
   const int32_t* crow_of_pos; /* [E_own] compact row of position p          */
   const int32_t* csrc;     /* [num_compact] src node of compact row         */
   const int32_t* cseg;     /* [R+1] compact rows of relation r              */
@@ -136,6 +139,11 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* desc, void* dev, size_t dev
                               size_t scratch_bytes, void* stream, rgnn_graph** out);
 rgnn_status rgnn_graph_export(const rgnn_graph* g, rgnn_graph_view* view /* [host] */);
 void rgnn_graph_destroy(rgnn_graph* g); /* frees the host struct only */
+
+/* Rows of the per-edge tensors (Z, s_src) a layer of `model` materialises on
+ * this graph: U = number of unique (etype, src) pairs when compact rows are
+ * used, else E_own.  [host] rows.                      */
+rgnn_status rgnn_zrows(const rgnn_graph* g, rgnn_model model, int64_t* rows);
 
 /* Workspace and saved-activation sizes for one layer call.  `saved` links a
  * forward to its backward (RGAT: Z, s_src, lse; RGCN: nothing).          */

@@ -64,6 +64,7 @@ _SIGS = {
     "rgnn_comm_unique_id": [_vp],
     "rgnn_comm_create": [_vp, C.c_int, C.c_int, C.POINTER(_i64), C.POINTER(_vp)],
     "rgnn_partition_dst": [_i64, C.POINTER(_i64), C.c_int, C.POINTER(_i64)],
+    "rgnn_zrows": [_vp, C.c_int, C.POINTER(_i64)],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(lib, _name)

@@ -27,19 +27,29 @@ namespace rgnn {
 
 template <int K, int N>
 struct BfCfg {
-  static constexpr int MT = 128;                             // positions per stage
+#ifndef RGNN_BWD_MT
+#define RGNN_BWD_MT 64
+#endif
+  static constexpr int MT = RGNN_BWD_MT;                     // positions per stage
   static constexpr int A_BYTES = MT * K * 2;
   static constexpr int B_BYTES = MT * N * 2;
   static constexpr int B2_BYTES = MT * 16 * 2;
-  static constexpr int STAGE = A_BYTES + B_BYTES + B2_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE > 6 ? 6 : (200 * 1024) / STAGE;
-  static constexpr int CW = 16;                              // compute warps
-  static constexpr int PW = 2;                               // cp.async producer warps
+  static constexpr int STAGE = A_BYTES + B_BYTES + B2_BYTES;  // multiple of 1024 (SW128 bases)
+  static constexpr int SC_STAGE = MT * 8;                     // per position: local dst (int), s_src or 1/c (float)
+  static constexpr int STAGES = (200 * 1024) / (STAGE + SC_STAGE) > 6 ? 6 : (200 * 1024) / (STAGE + SC_STAGE);
+#ifndef RGNN_BWD_CW
+#define RGNN_BWD_CW 16
+#endif
+  static constexpr int CW = RGNN_BWD_CW;                     // compute warps
+  static constexpr int PW = 4;                               // cp.async producer warps
   static constexpr int THREADS = 32 + PW * 32 + CW * 32;     // MMA warp, producers, compute warps
   static constexpr int DEPTH = STAGES - 1;                   // cp.async groups in flight per producer thread
   static constexpr int CPR = K * 2 / 16;                     // 16-byte chunks per X row
   static constexpr int RPI = 32 / CPR;                       // X rows per warp-wide cp.async
-  static constexpr int SMEM = 1024 + STAGES * STAGE + CW * K * 4 + 256;
+  static constexpr int ZCPR = N * 2 / 16;                    // 16-byte chunks per Z row
+  static constexpr int ZRPI = 32 / ZCPR;                     // Z rows per warp-wide cp.async
+  static constexpr int RPW = MT / PW;                        // stage rows per producer warp
+  static constexpr int SMEM = 1024 + STAGES * (STAGE + SC_STAGE) + CW * K * 4 + 256;
   static constexpr int NCOLS = (N + 16) <= 32 ? 32 : (N + 16) <= 64 ? 64 : (N + 16) <= 128 ? 128 : 256;
   static constexpr uint32_t IDESC = tc::idesc_bf16(K, N, 1, 1);
   static constexpr uint32_t IDESC_B = tc::idesc_bf16(K, 16, 1, 1);
@@ -47,9 +57,10 @@ struct BfCfg {
   static constexpr int EPL = 8;
   static constexpr int L = N / EPL;
   static constexpr int G = 32 / L;
-  static constexpr int PPW = MT / CW;                        // positions per warp per stage (8)
+  static constexpr int PPW = MT / CW;                        // positions per warp per stage
   static constexpr int PG = PPW / G;                         // positions per lane group
   static constexpr int KPL = K / L;                          // x_v features per lane
+  static_assert(STAGE % 1024 == 0 && RPW <= 32 && PG >= 1, "bwd config");
 };
 
 struct BwdFusedParams {
@@ -82,7 +93,8 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
   constexpr int L = C::L, PG = C::PG, KPL = C::KPL, EPL = C::EPL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* s_c = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE);  // [CW][K] dst-term partials
+  uint8_t* sc_base = smem + C::STAGES * C::STAGE;                          // [STAGES][MT] dst, [MT] s
+  float* s_c = reinterpret_cast<float*>(sc_base + C::STAGES * C::SC_STAGE);  // [CW][K] dst-term partials
   uint64_t* bar = reinterpret_cast<uint64_t*>(s_c + C::CW * K);
   uint64_t* a_full = bar;
   uint64_t* b_full = a_full + C::STAGES;
@@ -92,11 +104,22 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
   auto sA = [&](int s) { return smem + s * C::STAGE; };
   auto sB = [&](int s) { return smem + s * C::STAGE + C::A_BYTES; };
   auto sB2 = [&](int s) { return smem + s * C::STAGE + C::A_BYTES + C::B_BYTES; };
+  auto sDst = [&](int s) { return reinterpret_cast<int*>(sc_base + s * C::SC_STAGE); };
+  auto sSs = [&](int s) { return reinterpret_cast<float*>(sc_base + s * C::SC_STAGE + C::MT * 4); };
+  // swizzled A / B (and staged Z) offset of 16-byte chunk `c` of stage row `lp` (MN-major SW128)
+  auto b_off = [&](int c, int lp) { return (c >> 3) * (C::MT * 128) + lp * 128 + (((c & 7) ^ (lp & 7)) << 4); };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Tile ch = pr.chunks[blockIdx.x];
   const int r = ch.r, row0 = ch.row0, row1 = ch.row1;
   const int nsub = (row1 - row0 + C::MT - 1) / C::MT;
+  // Stage row lp of stage `it` holds position pmap(lp, it): the chunk is cut into MT / PG
+  // contiguous segments of PG * nsub positions, one per compute lane group, and each stage
+  // takes the next PG positions of every segment.  A lane group therefore walks one run of
+  // consecutive positions, and its per-destination values (G_v, Y_v, x_v, lse_v) are reloaded
+  // only when the destination changes, not at every stage.  (The dW sum is order-free; the
+  // mapping is fixed, so results stay deterministic.)  Positions >= row1 are padding rows.
+  auto pmap = [&](int lp, int it) { return row0 + (lp / C::PG) * (C::PG * nsub) + C::PG * it + (lp % C::PG); };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::STAGES; ++i) {
@@ -122,46 +145,58 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp >= 1 && warp <= C::PW) {
-    // ------------------------------------------------------------ producers: X_src rows by cp.async
-    const int pw = warp - 1;                      // rows pw*64 .. pw*64+63 of each stage
-    auto load_idx = [&](int it, int* out) {
-      const int p0 = row0 + it * C::MT + pw * 64;
-      out[0] = __ldg(pr.src_s + min(p0 + lane, row1 - 1));
-      out[1] = __ldg(pr.src_s + min(p0 + 32 + lane, row1 - 1));
+    // ------------------------------------------------------------ producers (cp.async, 16 B / 4 B):
+    // X[src] rows -> A, Z rows -> B (overwritten in place by dZ), dst and s_src (1/c) -> scalars.
+    const int pw = warp - 1;                      // rows pw*RPW .. pw*RPW+RPW-1 of each stage
+    constexpr int RPW = C::RPW;
+    auto load_idx = [&](int it, int& src, int& zr, int& p) {
+      p = pmap(pw * RPW + (lane % RPW), it);
+      const int pc = min(p, row1 - 1);
+      src = __ldg(pr.src_s + pc);
+      zr = CM ? __ldg(pr.zmap + pc) : pc;
     };
-    int idx[2] = {0, 0};
-    if (nsub > 0) load_idx(0, idx);
-    int pub = 0;
+    int src = 0, zr = 0, p = 0;
+    if (nsub > 0) load_idx(0, src, zr, p);
     for (int it = 0; it < nsub; ++it) {
       const int st = it % C::STAGES;
       const uint32_t use = (uint32_t)(it / C::STAGES);
-      int nidx[2] = {0, 0};
-      if (it + 1 < nsub) load_idx(it + 1, nidx);
+      int nsrc = 0, nzr = 0, np = 0;
+      if (it + 1 < nsub) load_idx(it + 1, nsrc, nzr, np);
       if (use > 0) tc::mbar_wait(&empty[st], (use - 1) & 1);
       uint8_t* a = sA(st);
 #pragma unroll 4
-      for (int i = 0; i < 64 / C::RPI; ++i) {
-        const int rr = i * C::RPI + lane / C::CPR;  // row within this warp's 64
+      for (int i = 0; i < RPW / C::RPI; ++i) {
+        const int rr = i * C::RPI + lane / C::CPR;  // row within this warp's RPW
         const int c = lane % C::CPR;
-        const int row = pw * 64 + rr;
-        const int xr = __shfl_sync(0xffffffffu, rr < 32 ? idx[0] : idx[1], rr & 31);
-        // MN-major SW128: feature block c/8 at (MT*128), line `row`, chunk (c%8) ^ (row%8)
-        tc::cp_async16(a + (c >> 3) * (C::MT * 128) + row * 128 + (((c & 7) ^ (row & 7)) << 4),
-                       pr.X + (size_t)xr * K + c * 8);
+        const int row = pw * RPW + rr;
+        const int xr = __shfl_sync(0xffffffffu, src, rr);
+        tc::cp_async16(a + b_off(c, row), pr.X + (size_t)xr * K + c * 8);
       }
-      tc::cp_async_commit();
-      if (it - pub >= C::DEPTH) {
-        tc::cp_async_wait<C::DEPTH>();
-        tc::fence_proxy_async_smem();
-        tc::mbar_arrive(&a_full[pub % C::STAGES]);
-        ++pub;
+      if constexpr (GAT) {
+        uint8_t* b = sB(st);
+#pragma unroll 4
+        for (int i = 0; i < RPW / C::ZRPI; ++i) {
+          const int rr = i * C::ZRPI + lane / C::ZCPR;
+          const int c = lane % C::ZCPR;
+          const int row = pw * RPW + rr;
+          const int zz = __shfl_sync(0xffffffffu, zr, rr);
+          tc::cp_async16(b + b_off(c, row), pr.Z + (size_t)zz * N + c * 8);
+        }
       }
-      idx[0] = nidx[0];
-      idx[1] = nidx[1];
+      if (lane < RPW && p < row1) {  // padding rows are recognised by position, not staged
+        const int row = pw * RPW + lane;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tc::smem_u32(sDst(st) + row)),
+                     "l"(pr.dst_s + p) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tc::smem_u32(sSs(st) + row)),
+                     "l"(GAT ? pr.s_src + zr : pr.inv_c + p) : "memory");
+      }
+      // the stage is published by the copy engine itself: the arrive fires when all of this
+      // thread's prior cp.async have landed (no wait, no publication lag)
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&a_full[st]))
+                   : "memory");
+      src = nsrc; zr = nzr; p = np;
     }
     tc::cp_async_wait<0>();
-    tc::fence_proxy_async_smem();
-    for (; pub < nsub; ++pub) tc::mbar_arrive(&a_full[pub % C::STAGES]);
   } else if (warp == 0) {
     // ------------------------------------------------------------ MMA issuer
     for (int it = 0; it < nsub; ++it) {
@@ -169,6 +204,7 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
       const uint32_t ph = (uint32_t)(it / C::STAGES) & 1;
       tc::mbar_wait(&a_full[st], ph);
       tc::mbar_wait(&b_full[st], ph);
+      tc::fence_proxy_async_smem();  // cp.async (generic proxy) data of A -> tcgen05 (async proxy)
       tc::tc_fence_after();
       if (lane == 0) {
         const uint32_t a0 = tc::smem_u32(sA(st)), b0 = tc::smem_u32(sB(st)), c0 = tc::smem_u32(sB2(st));
@@ -207,61 +243,21 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
     int cur_v = -1;
     float gv[EPL], xv[KPL], Sv = 0.f, dsc = 0.f, lse = 0.f;
     const uint32_t gmask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (g * L));
-    // Per position (lanes < PPW): dst and s_src one stage ahead; the Z rows of the group's
-    // positions one stage ahead as well (their latency overlaps the current stage).  Compact
-    // rows (CM): the Z row index is loaded two stages ahead, s_src and Z one stage ahead.
-    auto load_idx = [&](int it, int& v, int& zr) {
-      const int pl = row0 + it * C::MT + cw * C::PPW + (lane % C::PPW);
-      const bool okl = lane < C::PPW && pl < row1;
-      v = okl ? __ldg(pr.dst_s + pl) : -1;
-      if constexpr (CM) zr = okl ? __ldg(pr.zmap + pl) : 0;
-    };
-    auto load_sz = [&](int it, int zrow, float& sv, uint4* z) {
-      const int pbase = row0 + it * C::MT + cw * C::PPW;
-      const int pl = pbase + (lane % C::PPW);
-      const bool okl = lane < C::PPW && pl < row1;
-      sv = okl ? __ldg(GAT ? pr.s_src + (CM ? zrow : pl) : pr.inv_c + pl) : 0.f;
-      if constexpr (!GAT) return;
-#pragma unroll
-      for (int i = 0; i < PG; ++i) {
-        const int p = pbase + g * PG + i;
-        int zr = p;
-        if constexpr (CM) zr = __shfl_sync(0xffffffffu, zrow, g * PG + i);
-        z[i] = p < row1 ? ldg_nc16(pr.Z + (size_t)zr * N + l * EPL) : make_uint4(0, 0, 0, 0);
-      }
-    };
-    int nv = -1, nzr = 0, nnv = -1, nnzr = 0;
-    float ns = 0.f;
-    uint4 nz[PG];
-    if (nsub > 0) { load_idx(0, nv, nzr); load_sz(0, nzr, ns, nz); }
-    if (CM && nsub > 1) load_idx(1, nnv, nnzr);
+    // Everything per position comes from the stage in shared memory (staged by the producers
+    // several stages ahead); only the per-destination rows are read from global memory, once
+    // per destination change.
     for (int it = 0; it < nsub; ++it) {
       const int st = it % C::STAGES;
-      const uint32_t use = (uint32_t)(it / C::STAGES);
-      const int myv = nv;
-      const float mys = ns;
-      uint4 zr[PG];
-#pragma unroll
-      for (int i = 0; i < PG; ++i) zr[i] = nz[i];
-      if (it + 1 < nsub) {
-        if constexpr (CM) {
-          nv = nnv; nzr = nnzr;
-          load_sz(it + 1, nzr, ns, nz);
-          if (it + 2 < nsub) load_idx(it + 2, nnv, nnzr);
-        } else {
-          load_idx(it + 1, nv, nzr);
-          load_sz(it + 1, nzr, ns, nz);
-        }
-      }
-      if (use > 0) tc::mbar_wait(&empty[st], (use - 1) & 1);
+      tc::mbar_wait(&a_full[st], (uint32_t)(it / C::STAGES) & 1);
       uint8_t* b = sB(st);
       uint8_t* b2 = sB2(st);
 #pragma unroll
       for (int i = 0; i < PG; ++i) {
-        const int lp = cw * C::PPW + g * PG + i;  // row of the stage (0..127)
-        const int src_lane = g * PG + i;
-        const int v = __shfl_sync(0xffffffffu, myv, src_lane);
-        const float ss = __shfl_sync(0xffffffffu, mys, src_lane);
+        const int lp = cw * C::PPW + g * PG + i;  // row of the stage
+        const bool pv = pmap(lp, it) < row1;
+        const int v = pv ? sDst(st)[lp] : -1;
+        const float ss = pv ? sSs(st)[lp] : 0.f;
+        uint4* bz = reinterpret_cast<uint4*>(b + b_off(l, lp));  // staged Z chunk; dZ goes to the same place
         float dz[EPL];
         float dpre = 0.f;
         if (v >= 0 && !GAT) {  // RGCN: dZ[p] = G_v / c_{v,r}
@@ -309,7 +305,7 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
             cur_v = v;
           }
           float zf[EPL];
-          Vec16<__nv_bfloat16>{zr[i]}.to_float(zf);
+          Vec16<__nv_bfloat16>{*bz}.to_float(zf);
           float da = 0.f;
 #pragma unroll
           for (int j = 0; j < EPL; ++j) da = fmaf(gv[j], zf[j], da);
@@ -330,7 +326,7 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
         uint4 o;
         o.x = tc::pack_bf16(dz[0], dz[1]); o.y = tc::pack_bf16(dz[2], dz[3]);
         o.z = tc::pack_bf16(dz[4], dz[5]); o.w = tc::pack_bf16(dz[6], dz[7]);
-        *reinterpret_cast<uint4*>(b + (l >> 3) * (C::MT * 128) + lp * 128 + (((l & 7) ^ (lp & 7)) << 4)) = o;
+        *bz = o;
         if (GAT && l == 0)
           *reinterpret_cast<__nv_bfloat16*>(b2 + (lp >> 3) * 256 + (lp & 7) * 16) = __float2bfloat16_rn(dpre);
       }

@@ -90,7 +90,8 @@ struct rgnn_graph {
   int32_t* empty_rows;  // rows without in-edges (no work item)
   int64_t num_empty;
   // compact materialisation (NEXT-1): Z rows per unique (etype, src)
-  bool compact;
+  bool has_compact;  // compact tables built (COMPACT or AUTO)
+  int mat_mode;      // rgnn_materialization requested
   int64_t num_compact, num_ctiles;
   int32_t *crow_of_pos, *zrow_slot, *csrc, *cseg;
   float* invc_slot;
@@ -101,6 +102,14 @@ struct rgnn_graph {
   std::vector<int32_t> seg_host, chunk_seg_host;
   int device, num_sms;
 };
+
+// Per-call materialisation choice (include/rgnn.h, rgnn_zrows).
+inline bool use_compact(const rgnn_graph* g, int model) {
+  if (!g->has_compact) return false;
+  if (g->mat_mode == RGNN_MAT_COMPACT) return true;
+  return model == RGNN_RGCN ? g->num_compact < g->E_own : 2 * g->num_compact <= g->E_own;
+}
+
 
 // ---------------------------------------------------------------- device utils
 namespace rgnn {

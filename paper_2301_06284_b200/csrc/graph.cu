@@ -519,11 +519,7 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   g->pos = L.pos; g->et_slot = L.et_slot; g->run_ptr = L.run_ptr; g->rseg = L.rseg; g->inv_c = L.inv_c;
   g->items = L.items; g->split_rows = L.split_rows; g->tiles = L.tiles; g->chunks = L.chunks;
   g->empty_rows = L.empty_rows; g->num_empty = h.num_empty;
-  // AUTO keeps the compact rows only when they at least halve the GEMM rows (measured r01:
-  // ogbn-mag U/E = 0.15 gains ~1 ms/step; AM U/E = 0.56 loses, the backward then gathers Z
-  // rows at random instead of streaming them in position order).
-  const bool use_c = cm && (d->materialization == RGNN_MAT_COMPACT || 2 * (int64_t)h.num_compact <= n);
-  g->compact = use_c; g->num_compact = use_c ? h.num_compact : 0; g->crow_of_pos = L.crow_of_pos; g->zrow_slot = L.zrow_slot;
+  g->has_compact = cm; g->mat_mode = d->materialization; g->num_compact = cm ? h.num_compact : 0; g->crow_of_pos = L.crow_of_pos; g->zrow_slot = L.zrow_slot;
   g->invc_slot = L.invc_slot; g->csrc = L.csrc; g->cseg = L.cseg; g->ctiles = L.ctiles;
   g->num_ctiles = (int64_t)ctiles.size();
   g->chunk_seg = L.chunk_seg;
@@ -547,5 +543,12 @@ rgnn_status rgnn_graph_export(const rgnn_graph* g, rgnn_graph_view* v) {
 }
 
 void rgnn_graph_destroy(rgnn_graph* g) { delete g; }
+
+rgnn_status rgnn_zrows(const rgnn_graph* g, rgnn_model model, int64_t* rows) {
+  if (!g || !rows) return set_error(RGNN_E_INVALID_ARG, "NULL graph or rows");
+  if (model != RGNN_RGCN && model != RGNN_RGAT) return set_error(RGNN_E_INVALID_ARG, "bad model %d", (int)model);
+  *rows = use_compact(g, model) ? g->num_compact : g->E_own;
+  return RGNN_OK;
+}
 
 }  // extern "C"

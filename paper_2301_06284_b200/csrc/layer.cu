@@ -36,7 +36,9 @@ struct SavedLayout {
 static size_t elt(int prec) { return prec == RGNN_BF16 ? 2 : 4; }
 // Rows of the per-edge tensors Z / s_src: one per edge position (vanilla) or one
 // per unique (etype, src) pair (compact materialisation).
-static int64_t zrows(const rgnn_graph* g) { return std::max<int64_t>(g->compact ? g->num_compact : g->E_own, 1); }
+static int64_t zrows(const rgnn_graph* g, int model) {
+  return std::max<int64_t>(use_compact(g, model) ? g->num_compact : g->E_own, 1);
+}
 static int64_t dw0_chunk_rows(const rgnn_graph* g) {
   return std::max<int64_t>(kTileRows, (g->V_own / (2 * g->num_sms) + kTileRows) / kTileRows * kTileRows);
 }
@@ -54,7 +56,7 @@ static WsLayout ws_layout(const rgnn_graph* g, int model, int K, int N, int prec
   w.part = c.take<float>((size_t)std::max<int64_t>(g->num_parts, 1) * (N + 4));
   w.wt = c.take<char>(prec == RGNN_BF16 ? (size_t)g->R * K * N * 2 : 1);
   if (model == RGNN_RGCN) {
-    w.Z = c.take<char>((size_t)std::max(zrows(g), E) * N * e);  // also the bf16 dZ of the unfused dW path
+    w.Z = c.take<char>((size_t)std::max(zrows(g, model), E) * N * e);  // also the bf16 dZ of the unfused dW path
     w.Z0 = c.take<char>((size_t)std::max<int64_t>(g->V_own, 1) * N * e);
   } else {
     w.dZ = c.take<char>((size_t)E * N * e);
@@ -72,8 +74,8 @@ static SavedLayout saved_layout(const rgnn_graph* g, int model, int N, int prec,
   SavedLayout s{};
   Carver c(base);
   if (model == RGNN_RGAT) {
-    s.Z = c.take<char>((size_t)zrows(g) * N * elt(prec));
-    s.s_src = c.take<float>((size_t)zrows(g));
+    s.Z = c.take<char>((size_t)zrows(g, model) * N * elt(prec));
+    s.s_src = c.take<float>((size_t)zrows(g, model));
     s.lse = c.take<float>((size_t)std::max<int64_t>(g->V_own, 1));
   }
   s.bytes = c.off;
@@ -118,7 +120,8 @@ static rgnn_status forward(const rgnn_graph* g, int model, int K, int N, int pre
   ga.num_w = g->R; ga.x_rows = g->V; ga.z_rows = g->E_own;
   AggArgs aa{};
   aa.items = g->items; aa.num_items = g->num_items; aa.pos = g->pos; aa.et_slot = g->et_slot; aa.X = X;
-  if (g->compact) {  // GEMM over the unique (etype, src) rows; the walk reads Z[zrow_slot[q]]
+  const bool cm = use_compact(g, model);
+  if (cm) {  // GEMM over the unique (etype, src) rows; the walk reads Z[zrow_slot[q]]
     ga.tiles = g->ctiles; ga.num_tiles = g->num_ctiles; ga.gather = g->csrc; ga.z_rows = g->num_compact;
     aa.pos = g->zrow_slot;
     if (model == RGNN_RGCN) aa.slot_scale = g->invc_slot;  // 1/c applied per edge in the walk
@@ -134,7 +137,7 @@ static rgnn_status forward(const rgnn_graph* g, int model, int K, int N, int pre
     aa.Z = sv.Z; aa.s_src = sv.s_src; aa.U = w.U; aa.lse = sv.lse;
     { Phase ph("aggregate", s); RGNN_TRY(launch_aggregate(prec, K, N, true, aa, s)); }
   } else {
-    ga.Z = w.Z; ga.row_scale = g->compact ? nullptr : g->inv_c;
+    ga.Z = w.Z; ga.row_scale = cm ? nullptr : g->inv_c;
     if (ga.num_tiles) { Phase ph("gemm_fwd", s); RGNN_TRY(typed_gemm(prec, K, N, ga, s)); }
     if (W0 && g->V_own > 0) {
       GemmFwdArgs g0{};
@@ -211,7 +214,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     rgnn_status fst = RGNN_E_UNSUPPORTED;
     if (tc_ok) {  // fused position-order backward: dZ built in smem, dW MMA + dst term in one kernel
       Phase ph("bwd_fused", s);
-      fst = launch_bwd_fused_tc(K, N, g, X, sv.Z, g->compact ? g->crow_of_pos : nullptr, sv.s_src, sv.lse, Y, dY, w.U, A, slope, w.dwpart, w.cpart, s);
+      fst = launch_bwd_fused_tc(K, N, g, X, sv.Z, use_compact(g, model) ? g->crow_of_pos : nullptr, sv.s_src, sv.lse, Y, dY, w.U, A, slope, w.dwpart, w.cpart, s);
       if (fst != RGNN_OK && fst != RGNN_E_UNSUPPORTED) return fst;
     }
     if (fst == RGNN_OK) {
@@ -222,7 +225,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     BwdArgs ba{};
     ba.items = g->items; ba.num_items = g->num_items; ba.pos = g->pos; ba.et_slot = g->et_slot; ba.Z = sv.Z;
     ba.s_src = sv.s_src; ba.X = X; ba.v0 = g->v0; ba.U = w.U; ba.A = A; ba.slope = slope; ba.Y = Y; ba.dY = dY;
-    ba.lse = sv.lse; ba.dZ = w.dZ; ba.dpre = w.dpre; ba.zrow = g->compact ? g->zrow_slot : nullptr;
+    ba.lse = sv.lse; ba.dZ = w.dZ; ba.dpre = w.dpre; ba.zrow = use_compact(g, model) ? g->zrow_slot : nullptr;
     { Phase ph("bwd_traverse", s); RGNN_TRY(launch_bwd_traverse(prec, K, N, ba, s)); }
     { Phase ph("dst_term", s); RGNN_TRY(launch_dst_term(prec, K, g, w.dpre, X, w.cpart, s)); }
     da.Bz = w.dZ; da.dpre = w.dpre; da.dst_local = g->dst_s; da.v0 = g->v0;

@@ -114,6 +114,12 @@ class Graph:
                 "et_slot": self._arr(v.et_slot, E, i32), "inv_c": self._arr(v.inv_c, E, f32),
                 "run_ptr": self._arr(v.run_ptr, int(v.num_runs) + 1, i32), "rseg": self._arr(v.rseg, R + 1, i32)}
 
+    def zrows(self, model) -> int:
+        """Rows of Z / s_src a layer of `model` materialises (U compact, else E_own)."""
+        r = C.c_int64()
+        B.call("rgnn_zrows", self._handle, _model(model), C.byref(r))
+        return int(r.value)
+
     def compact_arrays(self) -> dict:
         """Compact materialisation tables (graph created with materialization="compact")."""
         v = self.view

@@ -65,7 +65,7 @@ def test_compact_parity(rgnn, case, model, prec):
     t = synth.make_tensors(g.V, g.R, K, N)
     w0 = model == "rgcn"
     gpu = run_gpu(rgnn, g, t, model, prec, with_w0=w0, materialization="compact")
-    assert gpu["graph"].num_compact <= g.E
+    assert gpu["graph"].zrows(model) == gpu["graph"].num_compact <= g.E
     ref = run_oracle(oracle, g, t, model, prec=prec, with_w0=w0)
     assert_close(gpu["Y"], ref["Y"], prec, f"compact {model}/{prec} Y")
     assert_close(gpu["dW"], ref["dW"], prec, f"compact {model}/{prec} dW", per_slice=True)
@@ -113,9 +113,17 @@ def test_compact_rejects_bad_option(rgnn):
 
 @pytest.mark.parametrize("name,mk", _graphs()[1:], ids=[c[0] for c in _graphs()[1:]])
 def test_auto_materialization_rule(rgnn, name, mk):
-    """AUTO takes compact rows iff U <= E_own / 2 (include/rgnn.h)."""
+    """AUTO (include/rgnn.h): RGCN uses compact rows iff U < E_own, RGAT iff U <= E_own / 2;
+    COMPACT always, VANILLA never."""
     g = mk()
-    G = rgnn.Graph(g.V, g.src, g.dst, g.etype, g.R, materialization="auto")
     c = oracle.compaction(g.R, oracle.preprocess(g.V, g.R, g.src, g.dst, g.etype))
-    want = c.num_compact if 2 * c.num_compact <= G.E_own and G.E_own > 0 else 0
-    assert G.num_compact == want
+    U = c.num_compact
+    Ga = rgnn.Graph(g.V, g.src, g.dst, g.etype, g.R, materialization="auto")
+    assert Ga.num_compact == U
+    E = Ga.E_own
+    assert Ga.zrows("rgcn") == (U if U < E else E)
+    assert Ga.zrows("rgat") == (U if 2 * U <= E else E)
+    Gc = rgnn.Graph(g.V, g.src, g.dst, g.etype, g.R, materialization="compact")
+    assert Gc.zrows("rgcn") == U and Gc.zrows("rgat") == U
+    Gv = rgnn.Graph(g.V, g.src, g.dst, g.etype, g.R)
+    assert Gv.zrows("rgcn") == E and Gv.zrows("rgat") == E and Gv.num_compact == 0
