@@ -149,19 +149,38 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
     // X[src] rows -> A, Z rows -> B (overwritten in place by dZ), dst and s_src (1/c) -> scalars.
     const int pw = warp - 1;                      // rows pw*RPW .. pw*RPW+RPW-1 of each stage
     constexpr int RPW = C::RPW;
-    auto load_idx = [&](int it, int& src, int& zr, int& p) {
+    auto load_idx = [&](int it, int& src, int& zr, int& p, int& v) {
       p = pmap(pw * RPW + (lane % RPW), it);
       const int pc = min(p, row1 - 1);
       src = __ldg(pr.src_s + pc);
       zr = CM ? __ldg(pr.zmap + pc) : pc;
+      v = __ldg(pr.dst_s + pc);
     };
-    int src = 0, zr = 0, p = 0;
-    if (nsub > 0) load_idx(0, src, zr, p);
+    // L2 prefetch of the per-destination rows (G_v, Y_v, x_v) the compute warps will load when
+    // they reach these positions, STAGES-1 stages from now (one lane per run start).
+    auto prefetch_dst = [&](int p, int v) {
+      const int vp = __shfl_up_sync(0xffffffffu, v, 1);
+      if (lane < RPW && p < row1 && (lane == 0 || vp != v)) {
+        const char* gp = reinterpret_cast<const char*>(pr.dY + (size_t)v * N);
+#pragma unroll
+        for (int o = 0; o < N * 4; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(gp + o));
+        if constexpr (GAT) {
+          const char* yp = reinterpret_cast<const char*>(pr.Y + (size_t)v * N);
+          const char* xp = reinterpret_cast<const char*>(pr.X + (pr.v0 + v) * (int64_t)K);
+#pragma unroll
+          for (int o = 0; o < N * 4; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(yp + o));
+#pragma unroll
+          for (int o = 0; o < K * 2; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(xp + o));
+        }
+      }
+    };
+    int src = 0, zr = 0, p = 0, v = 0;
+    if (nsub > 0) load_idx(0, src, zr, p, v);
     for (int it = 0; it < nsub; ++it) {
       const int st = it % C::STAGES;
       const uint32_t use = (uint32_t)(it / C::STAGES);
-      int nsrc = 0, nzr = 0, np = 0;
-      if (it + 1 < nsub) load_idx(it + 1, nsrc, nzr, np);
+      int nsrc = 0, nzr = 0, np = 0, nv = 0;
+      if (it + 1 < nsub) load_idx(it + 1, nsrc, nzr, np, nv);
       if (use > 0) tc::mbar_wait(&empty[st], (use - 1) & 1);
       uint8_t* a = sA(st);
 #pragma unroll 4
@@ -194,7 +213,8 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
       // thread's prior cp.async have landed (no wait, no publication lag)
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&a_full[st]))
                    : "memory");
-      src = nsrc; zr = nzr; p = np;
+      prefetch_dst(p, v);
+      src = nsrc; zr = nzr; p = np; v = nv;
     }
     tc::cp_async_wait<0>();
   } else if (warp == 0) {

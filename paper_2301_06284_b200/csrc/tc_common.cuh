@@ -36,12 +36,24 @@ __device__ __forceinline__ uint64_t global_ns() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-// Spin on an mbarrier phase.  Watchdog: a wait longer than 10 s means a pipeline
+// try_wait with a suspend-time hint: the warp sleeps in hardware until the phase
+// completes or the hint (ns) elapses, instead of spinning and taking issue slots
+// from the warps that do the work.
+__device__ __forceinline__ bool mbar_try_sleep(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
+// Wait for an mbarrier phase.  Watchdog: a wait longer than 10 s means a pipeline
 // bug (deadlock); trap so the launch fails instead of hanging the device.
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   if (mbar_try(b, parity)) return;
   const uint64_t t0 = global_ns();
-  while (!mbar_try(b, parity)) {
+  while (!mbar_try_sleep(b, parity)) {
     if (global_ns() - t0 > 10000000000ull) {
       printf("rgnn watchdog: block %d thread %d stuck on mbarrier smem+0x%x parity %u\n", blockIdx.x, threadIdx.x,
              smem_u32(b), parity);

@@ -657,7 +657,8 @@ static rgnn_status aggregate(bool rgat, const AggArgs& a, cudaStream_t s) {
     // measured (r01): the ring helps d_out = 64 (AM aggregate 0.93 -> 0.84 ms) and costs ~5% at
     // d_out = 128 (ogbn-mag), where the warp-per-row kernel with index prefetch stays faster
     static const bool no_ring = getenv("RGNN_WALK_NO_RING") != nullptr;
-    const bool ring = !no_ring && N <= 64;
+    static const bool force_ring = getenv("RGNN_WALK_RING") != nullptr;
+    const bool ring = !no_ring && (N <= 64 || force_ring);
     if (ring) {
       constexpr int RING = 4, UNR = WalkShape<T, K, N>::UNR;
       const size_t smem = 8 * (RING * UNR * 32 * sizeof(uint4) + RING * 32 * 2 * sizeof(float));
