@@ -104,8 +104,13 @@ __device__ __forceinline__ void dst_scores(const float* xv, const float* U, int 
   }
 }
 
+// 4 resident blocks (64 registers): measured r01 on ogbn-mag d=128, the walk is
+// latency bound and 32 warps / SM beat 24 warps with fewer spills (1.85 vs 2.43 ms)
+#ifndef RGNN_AGG_MINB
+#define RGNN_AGG_MINB 4
+#endif
 template <typename T, int K, int N, bool RGAT, bool CACHE>
-__global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
+__global__ void __launch_bounds__(256, RGNN_AGG_MINB) k_aggregate(AggArgs a) {
   using S = WalkShape<T, K, N>;
   constexpr int EPL = S::EPL, L = S::L, G = S::G, UNR = S::UNR, B = S::B, KPL = S::KPL;
   const T* Z = static_cast<const T*>(a.Z);
@@ -654,11 +659,11 @@ static rgnn_status aggregate(bool rgat, const AggArgs& a, cudaStream_t s) {
     RGNN_LAUNCH((k_empty_rows<T, N>), (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, s, a);
   }
   if (a.num_items > 0) {
-    // measured (r01): the ring helps d_out = 64 (AM aggregate 0.93 -> 0.84 ms) and costs ~5% at
-    // d_out = 128 (ogbn-mag), where the warp-per-row kernel with index prefetch stays faster
     static const bool no_ring = getenv("RGNN_WALK_NO_RING") != nullptr;
     static const bool force_ring = getenv("RGNN_WALK_RING") != nullptr;
-    const bool ring = !no_ring && (N <= 64 || force_ring);
+    // measured r01: with 4 resident blocks the plain walk wins for RGAT at every width (AM d=64
+    // 0.805 vs 0.836 ms); the ring still wins for RGCN at d_out = 64 (wikikg2 1.00 vs 1.26 ms)
+    const bool ring = !no_ring && ((N <= 64 && !rgat) || force_ring);
     if (ring) {
       constexpr int RING = 4, UNR = WalkShape<T, K, N>::UNR;
       const size_t smem = 8 * (RING * UNR * 32 * sizeof(uint4) + RING * 32 * 2 * sizeof(float));
