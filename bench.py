@@ -102,7 +102,10 @@ def algorithmic_bytes(phase, model, prec, K, N, E, V_own, J, num_items, U=None):
         return E * per_e + num_items * per_v
     if phase == "bwd_traverse":  # read pos, et, s_src, Z; write dZ, dpre; per row X, Y, dY, lse, item
         return E * (2 * N * b + 16) + num_items * (K * b + 2 * N * 4 + 4 + 16)
-    if phase == "bwd_fused":  # read Z, s_src, dst, src (+ compact row) per edge, gather X_src; per run G_v, Y_v, X_v, lse
+    if phase == "bwd_fused":
+        if model == "rgcn":  # gather X_src, read src, dst, 1/c per edge; G_v per (etype, dst) run
+            return E * (K * b + 12) + J * 4 * N
+        # read Z, s_src, dst, src (+ compact row) per edge, gather X_src; per run G_v, Y_v, X_v, lse
         return E * (N * b + K * b + 12 + (4 if U is not None else 0)) + J * (8 * N + K * b + 4)
     if phase == "gemm_dw":  # gather X rows, read dZ (RGAT) or gather G rows (RGCN), indices; dst term per run
         if model == "rgat":
@@ -419,7 +422,8 @@ def run_ours(args):
         traffic = None
         try:
             tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-            traffic = tj.get(f"{cfg.name}:{model}:{prec}:{dom}")
+            mat = "compact" if zr != int(v.E_own) else "vanilla"
+            traffic = tj.get(f"{cfg.name}:{model}:{prec}:{mat}:{dom}")
         except Exception:
             pass
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
