@@ -51,6 +51,10 @@ def _load():
         _lib.oracle_rgat_backward.argtypes = [i64, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, f64, vp, i64, i64,
                                               vp, vp, vp]
         _lib.oracle_rgcn_backward.restype = None
+        _lib.oracle_rgat_dx.argtypes = [i64, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, f64, vp, i64, i64, vp]
+        _lib.oracle_rgat_dx.restype = None
+        _lib.oracle_rgcn_dx.argtypes = [i64, i64, i32, i32, i32, vp, vp, vp, vp, vp, i32, vp, vp, i64, i64, vp]
+        _lib.oracle_rgcn_dx.restype = None
         _lib.oracle_rgcn_backward.argtypes = [i64, i64, i32, i32, i32, vp, vp, vp, vp, i32, vp, vp, i64, i64, vp,
                                               vp, vp]
         _lib.oracle_num_threads.restype = C.c_int
@@ -193,6 +197,33 @@ def rgat_backward(V: int, R: int, src, dst, et, X, W, A, G, slope: float = 0.2, 
     lib.oracle_rgat_backward(V, src.shape[0], R, K, N, _p(src), _p(dst), _p(et), _p(X), _p(W), _p(A),
                              float(slope), _p(G), v0, v1, _p(m), _p(dW), _p(dA))
     return dW, dA
+
+
+def rgat_dx(V: int, R: int, src, dst, et, X, W, A, G, slope: float = 0.2, v0: int = 0, v1=None) -> np.ndarray:
+    """dX [V, K] of L = <Y, G> restricted to dst in [v0, v1) (NEXT-2), fp64."""
+    lib = _load()
+    src, dst, et = _i32(src), _i32(dst), _i32(et)
+    X, W, A, G = _f64(X), _f64(W), _f64(A), _f64(G)
+    R_, K, N = W.shape
+    v1 = V if v1 is None else v1
+    dX = np.empty((V, K), np.float64)
+    lib.oracle_rgat_dx(V, src.shape[0], R, K, N, _p(src), _p(dst), _p(et), _p(X), _p(W), _p(A), float(slope),
+                       _p(G), v0, v1, _p(dX))
+    return dX
+
+
+def rgcn_dx(V: int, R: int, src, dst, et, W, G, W0=None, norm: int = NORM_REL_INDEG, edge_norm=None, v0: int = 0,
+            v1=None) -> np.ndarray:
+    """dX [V, K] of the RGCN layer's L = <Y, G> restricted to dst in [v0, v1) (NEXT-2), fp64."""
+    lib = _load()
+    src, dst, et = _i32(src), _i32(dst), _i32(et)
+    W, W0, G, en = _f64(W), _f64(W0), _f64(G), _f64(edge_norm)
+    R_, K, N = W.shape
+    v1 = V if v1 is None else v1
+    dX = np.empty((V, K), np.float64)
+    lib.oracle_rgcn_dx(V, src.shape[0], R, K, N, _p(src), _p(dst), _p(et), _p(W), _p(W0), norm, _p(en), _p(G),
+                       v0, v1, _p(dX))
+    return dX
 
 
 def rgcn_backward(V: int, R: int, src, dst, et, X, G, K: int, N: int, norm: int = NORM_REL_INDEG, edge_norm=None,

@@ -425,4 +425,131 @@ void oracle_rgcn_backward(int64_t V, int64_t E, int32_t R, int32_t K, int32_t N,
   free(in_eid);
 }
 
+/* ------------------------------------------------------------------ */
+/* Input-feature gradient dX ("required       */
+/* gradients"), written out by the chain rule from the forward above.  */
+/* ------------------------------------------------------------------ */
+
+/* y += W_r d : W_r [K,N] row major, d [N] -> y [K]  (d z W_r^T for z = x W_r) */
+static void matvec_t(int K, int N, const double* Wr, const double* d, double* y) {
+  for (int k = 0; k < K; ++k) {
+    double acc = 0.0;
+    for (int n = 0; n < N; ++n) acc += Wr[(size_t)k * N + n] * d[n];
+    y[k] += acc;
+  }
+}
+
+/* RGAT dX [V, K] of L = <Y, G> restricted to dst in [v0, v1):
+ *   zi_e = x_src W_r, zj_e = x_dst W_r, pre_e = A[r,0].zi + A[r,1].zj (Listing 1)
+ *   dzi_e = alpha_e G_v + dpre_e A[r,0]   ->  dX[src] += dzi_e W_r^T
+ *   dzj_e = dpre_e A[r,1]                 ->  dX[dst] += dzj_e W_r^T
+ * with alpha, dpre exactly as in oracle_rgat_backward.  Thread partials of dX
+ * are summed in thread order.                                              */
+void oracle_rgat_dx(int64_t V, int64_t E, int32_t R, int32_t K, int32_t N, const int32_t* src, const int32_t* dst,
+                    const int32_t* et, const double* X, const double* W, const double* A, double slope,
+                    const double* G, int64_t v0, int64_t v1, double* dX) {
+  int64_t* in_ptr;
+  int32_t* in_eid;
+  build_in_lists(V, E, dst, &in_ptr, &in_eid);
+  int nt = omp_get_max_threads();
+  size_t xsz = (size_t)V * K;
+  double* tdX = (double*)calloc((size_t)nt * xsz + 1, sizeof(double));
+#pragma omp parallel
+  {
+    double* mydX = tdX + (size_t)omp_get_thread_num() * xsz;
+    double* zi = (double*)malloc(sizeof(double) * (size_t)N);
+    double* zj = (double*)malloc(sizeof(double) * (size_t)N);
+    double* dz = (double*)malloc(sizeof(double) * (size_t)N);
+    int64_t cap = 0;
+    double *pre = NULL, *al = NULL, *da = NULL;
+#pragma omp for schedule(dynamic, 16)
+    for (int64_t v = v0; v < v1; ++v) {
+      int64_t lo = in_ptr[v], hi = in_ptr[v + 1], deg = hi - lo;
+      if (deg == 0) continue;
+      if (deg > cap) {
+        cap = deg;
+        pre = (double*)realloc(pre, sizeof(double) * (size_t)cap);
+        al = (double*)realloc(al, sizeof(double) * (size_t)cap);
+        da = (double*)realloc(da, sizeof(double) * (size_t)cap);
+      }
+      const double* Gv = G + (size_t)v * N;
+      double m = -INFINITY;
+      for (int64_t q = lo; q < hi; ++q) {
+        int32_t e = in_eid[q], r = et[e];
+        const double* Wr = W + (size_t)r * K * N;
+        vecmat(K, N, X + (size_t)src[e] * K, Wr, zi);
+        vecmat(K, N, X + (size_t)v * K, Wr, zj);
+        pre[q - lo] = dot(N, A + (size_t)r * 2 * N, zi) + dot(N, A + (size_t)r * 2 * N + N, zj);
+        double s = leaky(pre[q - lo], slope);
+        if (s > m) m = s;
+        da[q - lo] = dot(N, Gv, zi);
+      }
+      double l = 0.0;
+      for (int64_t q = lo; q < hi; ++q) { al[q - lo] = exp(leaky(pre[q - lo], slope) - m); l += al[q - lo]; }
+      double S = 0.0;
+      for (int64_t q = lo; q < hi; ++q) { al[q - lo] /= l; S += al[q - lo] * da[q - lo]; }
+      for (int64_t q = lo; q < hi; ++q) {
+        int32_t e = in_eid[q], r = et[e];
+        const double* Wr = W + (size_t)r * K * N;
+        const double* A0 = A + (size_t)r * 2 * N;
+        const double* A1 = A0 + N;
+        double a = al[q - lo];
+        double dpre = a * (da[q - lo] - S) * leaky_grad(pre[q - lo], slope);
+        for (int n = 0; n < N; ++n) dz[n] = a * Gv[n] + dpre * A0[n];
+        matvec_t(K, N, Wr, dz, mydX + (size_t)src[e] * K);
+        for (int n = 0; n < N; ++n) dz[n] = dpre * A1[n];
+        matvec_t(K, N, Wr, dz, mydX + (size_t)v * K);
+      }
+    }
+    free(zi); free(zj); free(dz); free(pre); free(al); free(da);
+  }
+  memset(dX, 0, sizeof(double) * xsz);
+  for (int t = 0; t < nt; ++t)
+    for (size_t i = 0; i < xsz; ++i) dX[i] += tdX[(size_t)t * xsz + i];
+  free(tdX);
+  free(in_ptr);
+  free(in_eid);
+}
+
+/* RGCN dX [V, K] of L = <Y, G> restricted to dst in [v0, v1):
+ *   dX[src] += (1/c_{v,r}) G_v W_r^T  for every edge (src -> v, r),
+ *   dX[v]   += G_v W0^T               (self loop, if W0 != NULL).          */
+void oracle_rgcn_dx(int64_t V, int64_t E, int32_t R, int32_t K, int32_t N, const int32_t* src, const int32_t* dst,
+                    const int32_t* et, const double* W, const double* W0, int32_t norm, const double* edge_norm,
+                    const double* G, int64_t v0, int64_t v1, double* dX) {
+  int64_t* in_ptr;
+  int32_t* in_eid;
+  build_in_lists(V, E, dst, &in_ptr, &in_eid);
+  int nt = omp_get_max_threads();
+  size_t xsz = (size_t)V * K;
+  double* tdX = (double*)calloc((size_t)nt * xsz + 1, sizeof(double));
+#pragma omp parallel
+  {
+    double* mydX = tdX + (size_t)omp_get_thread_num() * xsz;
+    double* dz = (double*)malloc(sizeof(double) * (size_t)N);
+    int64_t* cnt = (int64_t*)calloc((size_t)R, sizeof(int64_t));
+#pragma omp for schedule(dynamic, 64)
+    for (int64_t v = v0; v < v1; ++v) {
+      const double* Gv = G + (size_t)v * N;
+      if (W0) matvec_t(K, N, W0, Gv, mydX + (size_t)v * K);
+      row_count(in_ptr[v], in_ptr[v + 1], in_eid, et, cnt);
+      for (int64_t q = in_ptr[v]; q < in_ptr[v + 1]; ++q) {
+        int32_t e = in_eid[q], r = et[e];
+        double f = rgcn_factor(norm, edge_norm, cnt, et, e);
+        for (int n = 0; n < N; ++n) dz[n] = f * Gv[n];
+        matvec_t(K, N, W + (size_t)r * K * N, dz, mydX + (size_t)src[e] * K);
+      }
+      row_count_clear(in_ptr[v], in_ptr[v + 1], in_eid, et, cnt);
+    }
+    free(dz);
+    free(cnt);
+  }
+  memset(dX, 0, sizeof(double) * xsz);
+  for (int t = 0; t < nt; ++t)
+    for (size_t i = 0; i < xsz; ++i) dX[i] += tdX[(size_t)t * xsz + i];
+  free(tdX);
+  free(in_ptr);
+  free(in_eid);
+}
+
 int oracle_num_threads(void) { return omp_get_max_threads(); }

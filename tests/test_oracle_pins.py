@@ -392,3 +392,77 @@ def test_compaction_bruteforce(seed, V, E, R, shard):
     for r in range(R):
         assert (c.crel[c.cseg[r]:c.cseg[r + 1]] == r).all()
     assert c.cseg[0] == 0 and c.cseg[R] == c.num_compact
+
+
+# ---------------------------------------------------------------- dX (NEXT-2)
+@pytest.mark.parametrize("slope", [0.2, 0.01])
+def test_rgat_dx_vs_torch_autograd(slope):
+    """oracle.rgat_dx equals the X-gradient of the independent torch RGAT (_torch_rgat)."""
+    torch = pytest.importorskip("torch")
+    V, E, R, K, N = 9, 40, 3, 5, 4
+    g = synth.random_graph(V, E, R, seed=22)
+    t = synth.make_tensors(V, R, K, N)
+    X = torch.tensor(t.X, dtype=torch.float64, requires_grad=True)
+    W = torch.tensor(t.W, dtype=torch.float64)
+    A = torch.tensor(t.A, dtype=torch.float64)
+    G = torch.tensor(t.dY[:, :N], dtype=torch.float64)
+    (_torch_rgat(V, g.src, g.dst, g.etype, X, W, A, slope) * G).sum().backward()
+    dX = oracle.rgat_dx(V, R, g.src, g.dst, g.etype, t.X, t.W, t.A, G.numpy(), slope=slope)
+    np.testing.assert_allclose(dX, X.grad.numpy(), rtol=1e-11, atol=1e-13)
+
+
+def test_fd_gradients_dx():
+    V, E, R, K, N = 7, 25, 2, 3, 3
+    g = synth.random_graph(V, E, R, seed=33)
+    t = synth.make_tensors(V, R, K, N)
+    X, W, W0, A, G = (a.astype(float) for a in (t.X, t.W, t.W0, t.A, t.dY[:, :N]))
+
+    def Lgat(X_):
+        Y, _, _ = oracle.rgat_forward(V, R, g.src, g.dst, g.etype, X_, W, A)
+        return float((Y * G).sum())
+
+    def Lgcn(X_):
+        return float((oracle.rgcn_forward(V, R, g.src, g.dst, g.etype, X_, W, W0) * G).sum())
+
+    dXa = oracle.rgat_dx(V, R, g.src, g.dst, g.etype, X, W, A, G)
+    dXc = oracle.rgcn_dx(V, R, g.src, g.dst, g.etype, W, G, W0=W0)
+    rng = np.random.default_rng(1)
+    for _ in range(10):
+        idx = tuple(rng.integers(0, s) for s in X.shape)
+        n = _fd(Lgat, X, idx)
+        assert abs(dXa[idx] - n) / max(abs(dXa[idx]), abs(n), 1e-8) < 1e-4
+        n = _fd(Lgcn, X, idx)
+        assert abs(dXc[idx] - n) / max(abs(dXc[idx]), abs(n), 1e-8) < 1e-4
+
+
+@pytest.mark.parametrize("norm", [0, 1, 2])
+def test_rgcn_dx_closed_form(norm):
+    """dX = sum_r A_r^T G W_r^T + G W0^T with the dense normalised adjacency A_r (NumPy)."""
+    V, E, R, K, N = 20, 150, 3, 4, 5
+    g = synth.random_graph(V, E, R, seed=34)
+    t = synth.make_tensors(V, R, K, N)
+    en = np.random.default_rng(2).uniform(0.1, 1, E)
+    G = t.dY[:, :N].astype(float)
+    ref = G @ t.W0.astype(float).T
+    for r in range(R):
+        Ar = np.zeros((V, V))
+        m = g.etype == r
+        np.add.at(Ar, (g.dst[m], g.src[m]), en[m] if norm == 2 else 1.0)
+        if norm == 0:
+            c = np.bincount(g.dst[m], minlength=V).astype(float)
+            Ar = Ar / np.maximum(c, 1)[:, None]
+        ref += Ar.T @ G @ t.W[r].astype(float).T
+    got = oracle.rgcn_dx(V, R, g.src, g.dst, g.etype, t.W, G, W0=t.W0, norm=norm,
+                         edge_norm=en if norm == 2 else None)
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
+
+
+def test_dx_dst_shards_sum_to_full():
+    V, E, R, K, N = 30, 300, 4, 4, 4
+    g = synth.random_graph(V, E, R, seed=35)
+    t = synth.make_tensors(V, R, K, N)
+    G = t.dY[:, :N]
+    full = oracle.rgat_dx(V, R, g.src, g.dst, g.etype, t.X, t.W, t.A, G)
+    parts = sum(oracle.rgat_dx(V, R, g.src, g.dst, g.etype, t.X, t.W, t.A, G, v0=a, v1=b)
+                for a, b in [(0, 11), (11, 12), (12, 30)])
+    np.testing.assert_allclose(parts, full, rtol=1e-12, atol=1e-13)
