@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time of the cpu_baseline sample")
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of a captured CUDA graph")
+    ap.add_argument("--dx", action="store_true", help="also compute the input-feature gradient dX (NEXT-2)")
     ap.add_argument("--materialization", default="auto", choices=["vanilla", "compact", "auto"],
                     help="per-edge (vanilla) or per-(etype, src) (compact, PAPER.md P:513-531) Z / s_src rows; "
                          "auto = compact when U <= E/2")
@@ -263,7 +264,8 @@ def run_ours(args):
     et = torch.from_numpy(g.etype).to(dev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    G = m.Graph(g.V, src, dst, et, g.R, dst_begin=v0, dst_end=v1, materialization=args.materialization, device=dev)
+    G = m.Graph(g.V, src, dst, et, g.R, dst_begin=v0, dst_end=v1, materialization=args.materialization,
+                build_dx=args.dx, device=dev)
     torch.cuda.synchronize()
     prep_ms = 1e3 * (time.perf_counter() - t0)
     del src, dst, et
@@ -273,7 +275,8 @@ def run_ours(args):
     W = torch.from_numpy(t.W).to(dev)
     A = torch.from_numpy(t.A).to(dev)
     dY = torch.from_numpy(np.ascontiguousarray(t.dY[v0:v1])).to(dev)
-    ws = m.Workspace(G, model, K, N, prec)
+    ws = m.Workspace(G, model, K, N, prec, dx=args.dx)
+    dX = torch.empty(g.V, K, dtype=torch.float32, device=dev) if args.dx else None
     Y_full = torch.empty(g.V, N, dtype=torch.float32, device=dev) if world > 1 else None
     Y = Y_full[v0:v1] if world > 1 else torch.empty(v1 - v0, N, dtype=torch.float32, device=dev)
     dW = torch.empty(g.R, K, N, dtype=torch.float32, device=dev)
@@ -287,7 +290,7 @@ def run_ours(args):
         else:
             m.rgcn_forward(G, Xs, Ws, prec=prec, ws=ws, Y=Y, comm=comm, Y_full=Y_full)
         m.rgnn_backward(G, model, Xs, Ws, dYs, ws, A=As if model == "rgat" else None, slope=args.slope, Y=Y,
-                        prec=prec, comm=comm, dW=dW, dA=dA)
+                        prec=prec, comm=comm, dW=dW, dA=dA, want_dx=args.dx, dX=dX)
 
     def barrier():
         torch.cuda.synchronize()
@@ -379,7 +382,9 @@ def run_ours(args):
         odA = torch.empty(g.R, 2, N, dtype=torch.float32).pin_memory() if dA is not None else None
         dX_, dW_, dA_, ddY = torch.empty_like(X), torch.empty_like(W), torch.empty_like(A), torch.empty_like(dY)
         h2d = hX.numel() * hX.element_size() + hW.numel() * 4 + hA.numel() * 4 + hdY.numel() * 4
-        d2h = oY.numel() * 4 + odW.numel() * 4 + (odA.numel() * 4 if odA is not None else 0)
+        odX = torch.empty(g.V, K, dtype=torch.float32).pin_memory() if args.dx else None
+        d2h = oY.numel() * 4 + odW.numel() * 4 + (odA.numel() * 4 if odA is not None else 0) + (
+            odX.numel() * 4 if odX is not None else 0)
         n_e2e = max(1, min(args.steps, 5))
 
         def e2e_step():
@@ -389,6 +394,8 @@ def run_ours(args):
             oY.copy_(Y, non_blocking=True); odW.copy_(dW, non_blocking=True)
             if odA is not None:
                 odA.copy_(dA, non_blocking=True)
+            if odX is not None:
+                odX.copy_(dX, non_blocking=True)
             torch.cuda.current_stream().synchronize()  # the host reads the result every step
 
         e2e_step()
@@ -444,6 +451,8 @@ def run_ours(args):
                "vs_baseline": None, "dtype": prec, "data": "synthetic (seeded generator, random-init weights)",
                "config": dict(config_json(cfg, model, prec, g, world),
                               launch="CUDA graph of the step" if use_graph else "eager",
+                              backward="dW, dA" + (", dX (NEXT-2)" if args.dx else "") if model == "rgat" else
+                              "dW" + (", dX (NEXT-2)" if args.dx else ""),
                               materialization=("compact" if G.zrows(model) != G.E_own else "vanilla") + (
                                   " (auto)" if args.materialization == "auto" else ""),
                               z_rows=G.zrows(model), compact_rows=int(G.num_compact)),

@@ -77,6 +77,12 @@ typedef enum { RGNN_RGCN = 0, RGNN_RGAT = 1 } rgnn_model;
  * rgnn_zrows() reports the choice.                                          */
 typedef enum { RGNN_MAT_VANILLA = 0, RGNN_MAT_COMPACT = 1, RGNN_MAT_AUTO = 2 } rgnn_materialization;
 
+/* rgnn_graph_desc.flags.  RGNN_GRAPH_DX: also build the tables the input-
+ * feature gradient needs (rgnn_backward with dX != NULL):
+ * run of each position and its destination / relation, and a source-major
+ * CSR over the positions with a split work list (≈ 7 int32 per edge + V).  */
+#define RGNN_GRAPH_DX 1
+
 typedef struct rgnn_graph rgnn_graph;
 typedef struct rgnn_comm rgnn_comm;
 
@@ -97,7 +103,7 @@ typedef struct {
   int64_t dst_begin;         /* owned destination range [dst_begin, dst_end) */
   int64_t dst_end;           /* (0, V) on one GPU                            */
   int32_t materialization;   /* rgnn_materialization (0 = vanilla)           */
-  int32_t reserved;          /* must be 0                                    */
+  int32_t flags;             /* RGNN_GRAPH_* bits (0 = none)                 */
 } rgnn_graph_desc;
 
 /* What the preprocessing built (device pointers into the caller's graph
@@ -146,7 +152,10 @@ void rgnn_graph_destroy(rgnn_graph* g); /* frees the host struct only */
 rgnn_status rgnn_zrows(const rgnn_graph* g, rgnn_model model, int64_t* rows);
 
 /* Workspace and saved-activation sizes for one layer call.  `saved` links a
- * forward to its backward (RGAT: Z, s_src, lse; RGCN: nothing).          */
+ * forward to its backward (RGAT: Z, s_src, lse; RGCN: nothing).
+ * training: 0 inference, 1 training, RGNN_WS_DX (3) training with dX -- the
+ * workspace of a backward that computes dX must be sized with RGNN_WS_DX.  */
+#define RGNN_WS_DX 3
 rgnn_status rgnn_workspace_bytes(const rgnn_graph* g, rgnn_model model, int d_in, int d_out, rgnn_prec prec,
                                  int training, size_t* ws_bytes, size_t* saved_bytes);
 
@@ -173,14 +182,20 @@ rgnn_status rgat_forward(const rgnn_graph* g, int d_in, int d_out, rgnn_prec pre
 
 /* Backward of L = <Y, dY> over the owned rows (Sec. 3.5; reading O17):
  *   dW [R, d_in, d_out] fp32 (required), dA [R, 2, d_out] (RGAT, required),
- *   dW0 [d_in, d_out] (RGCN, iff W0 was used, else NULL).  dX must be NULL
- *   (RGNN_E_UNSUPPORTED otherwise; NEXT-2).  Y is the forward output for the
- *   owned rows and dY [V_own, d_out] fp32.  With comm != NULL, dW / dA / dW0
- *   are all-reduced (sum) in place across ranks.  Outputs are overwritten. */
+ *   dW0 [d_in, d_out] (RGCN, iff W0 was used, else NULL).  Y is the forward
+ *   output for the owned rows and dY [V_own, d_out] fp32.
+ *   dX [V, d_in] fp32 or NULL: input-feature gradient (the
+ *   chain rule of the forward through X_src and, for RGAT, X_dst; DESIGN.md
+ *   Sec. 6 "dX") over ALL V rows -- a shard's contribution from its owned
+ *   edges.  Needs a graph built with RGNN_GRAPH_DX and a workspace sized
+ *   with RGNN_WS_DX (else RGNN_E_UNSUPPORTED / RGNN_E_WORKSPACE); RGCN with a
+ *   self loop also needs W0 [d_in, d_out] (NULL: no self-loop term).
+ *   With comm != NULL, dW / dA / dW0 / dX are all-reduced (sum) in place
+ *   across ranks.  Outputs are overwritten.                                */
 rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int d_in, int d_out, rgnn_prec prec,
-                          const void* X, const float* W, const float* A, float slope, const float* Y,
-                          const float* dY, const void* saved, float* dW, float* dA, float* dW0, float* dX,
-                          void* ws, size_t ws_bytes, rgnn_comm* comm, void* stream);
+                          const void* X, const float* W, const float* W0, const float* A, float slope,
+                          const float* Y, const float* dY, const void* saved, float* dW, float* dA, float* dW0,
+                          float* dX, void* ws, size_t ws_bytes, rgnn_comm* comm, void* stream);
 
 /* Multi-GPU (one process per GPU; dst-range partition).
  * rgnn_comm_unique_id writes a 128-byte NCCL id to `id` [host]; rank 0

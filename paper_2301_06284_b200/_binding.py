@@ -17,6 +17,8 @@ RGNN_F32, RGNN_BF16 = 0, 1
 RGNN_NORM_REL_INDEG, RGNN_NORM_NONE, RGNN_NORM_EDGE = 0, 1, 2
 RGNN_RGCN, RGNN_RGAT = 0, 1
 RGNN_MAT_VANILLA, RGNN_MAT_COMPACT, RGNN_MAT_AUTO = 0, 1, 2
+RGNN_GRAPH_DX = 1
+RGNN_WS_DX = 3
 
 STATUS_NAMES = {0: "RGNN_OK", 1: "RGNN_E_INVALID_ARG", 2: "RGNN_E_RANGE", 3: "RGNN_E_UNSUPPORTED",
                 4: "RGNN_E_WORKSPACE", 5: "RGNN_E_CUDA", 6: "RGNN_E_NCCL"}
@@ -27,7 +29,7 @@ class rgnn_graph_desc(C.Structure):
                 ("num_ntypes", C.c_int32), ("src", C.c_void_p), ("dst", C.c_void_p), ("etype", C.c_void_p),
                 ("row_ptr", C.c_void_p), ("ntype", C.c_void_p), ("edge_norm", C.c_void_p), ("norm", C.c_int32),
                 ("row_split_cap", C.c_int32), ("dst_begin", C.c_int64), ("dst_end", C.c_int64),
-                ("materialization", C.c_int32), ("reserved", C.c_int32)]
+                ("materialization", C.c_int32), ("flags", C.c_int32)]
 
 
 class rgnn_graph_view(C.Structure):
@@ -59,8 +61,8 @@ _SIGS = {
     "rgnn_workspace_bytes": [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_sz), C.POINTER(_sz)],
     "rgcn_forward": [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp, _vp],
     "rgat_forward": [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _f32, _vp, _vp, _vp, _sz, _vp, _vp, _vp],
-    "rgnn_backward": [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _f32, _vp, _vp, _vp, _vp, _vp, _vp,
-                      _vp, _vp, _sz, _vp, _vp],
+    "rgnn_backward": [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _f32, _vp, _vp, _vp, _vp, _vp,
+                      _vp, _vp, _vp, _sz, _vp, _vp],
     "rgnn_comm_unique_id": [_vp],
     "rgnn_comm_create": [_vp, C.c_int, C.c_int, C.POINTER(_i64), C.POINTER(_vp)],
     "rgnn_partition_dst": [_i64, C.POINTER(_i64), C.c_int, C.POINTER(_i64)],

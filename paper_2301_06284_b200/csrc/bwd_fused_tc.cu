@@ -81,6 +81,7 @@ struct BwdFusedParams {
   int64_t v0;
   float* part;
   float* cpart;
+  float2* ad;  // dX: (alpha, dpre) per position, or null
 };
 
 __device__ __forceinline__ float leaky_f(float x, float s) { return x > 0.f ? x : s * x; }
@@ -334,6 +335,7 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
           const float pre = ss + dsc;
           const float alpha = __expf(leaky_f(pre, pr.slope) - lse);
           dpre = alpha * (da - Sv) * (pre > 0.f ? 1.f : pr.slope);
+          if (pr.ad && l == 0) pr.ad[pmap(lp, it)] = make_float2(alpha, dpre);
 #pragma unroll
           for (int j = 0; j < EPL; ++j) dz[j] = fmaf(alpha, gv[j], dpre * a0[j]);
 #pragma unroll
@@ -426,11 +428,11 @@ bool tc_disabled();
 rgnn_status launch_bwd_fused_tc(int K, int N, const rgnn_graph* g, const void* X, const void* Z, const int32_t* zmap,
                                 const float* s_src,
                                 const float* lse, const float* Y, const float* dY, const float* U, const float* A,
-                                float slope, float* part, float* cpart, cudaStream_t s) {
+                                float slope, float* part, float* cpart, float2* ad, cudaStream_t s) {
   if (tc_disabled()) return RGNN_E_UNSUPPORTED;
   if (getenv("RGNN_DISABLE_FUSED_BWD")) return RGNN_E_UNSUPPORTED;
   BwdFusedParams p{g->chunks, g->src_s, g->dst_s, s_src, static_cast<const __nv_bfloat16*>(Z), zmap,
-                   static_cast<const __nv_bfloat16*>(X), lse, Y, dY, U, A, g->inv_c, slope, g->v0, part, cpart};
+                   static_cast<const __nv_bfloat16*>(X), lse, Y, dY, U, A, g->inv_c, slope, g->v0, part, cpart, ad};
   if (K == 64 && N == 64) return bwd_fused<64, 64>(g, p, X, s);
   if (K == 64 && N == 128) return bwd_fused<64, 128>(g, p, X, s);
   if (K == 128 && N == 64) return bwd_fused<128, 64>(g, p, X, s);

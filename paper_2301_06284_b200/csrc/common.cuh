@@ -90,6 +90,15 @@ struct rgnn_graph {
   int32_t* empty_rows;  // rows without in-edges (no work item)
   int64_t num_empty;
   // compact materialisation (NEXT-1): Z rows per unique (etype, src)
+  // dX tables (NEXT-2; RGNN_GRAPH_DX)
+  bool has_dx;
+  int32_t *run_of_pos, *run_dst, *run_rel, *spos, *srun, *srel, *srow;
+  float* sinvc;
+  rgnn::Tile* rtiles;
+  int64_t num_rtiles;
+  rgnn::Item* sitems;      // source work list (rows = global source nodes with out-edges)
+  rgnn::SplitRow* ssplit;
+  int64_t num_sitems, num_ssplit, num_sparts;
   bool has_compact;  // compact tables built (COMPACT or AUTO)
   int mat_mode;      // rgnn_materialization requested
   int64_t num_compact, num_ctiles;

@@ -232,11 +232,11 @@ __global__ void k_da(int K, int N, int R, const float* __restrict__ vsum, const 
 // On the bf16 path W is the RNE-rounded weight (the same values the typed GEMM
 // multiplies), so the score x_dst . U[r] equals A[r,1].(x_dst W_r) of the GEMM's W.
 __global__ void k_fold_u(int R, int K, int N, const float* __restrict__ W, const float* __restrict__ A,
-                         float* __restrict__ U, int round_bf16) {
+                         float* __restrict__ U, int round_bf16, int half) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < R * K; i += gridDim.x * blockDim.x) {
     int r = i / K;
     const float* w = W + (size_t)i * N;
-    const float* a1 = A + (size_t)r * 2 * N + N;
+    const float* a1 = A + (size_t)r * 2 * N + half * N;
     float s = 0.f;
     for (int n = 0; n < N; ++n) {
       float wn = round_bf16 ? __bfloat162float(__float2bfloat16_rn(w[n])) : w[n];
@@ -298,9 +298,10 @@ rgnn_status launch_dw_reduce(int prec, int K, int N, int R, int64_t num_chunks, 
   return RGNN_OK;
 }
 
-rgnn_status launch_fold_u(int prec, int R, int K, int N, const float* W, const float* A, float* U, cudaStream_t s) {
+rgnn_status launch_fold_u(int prec, int R, int K, int N, const float* W, const float* A, float* U, cudaStream_t s,
+                          int half) {
   unsigned grid = (unsigned)std::max(1, (R * K + 255) / 256);
-  RGNN_LAUNCH(k_fold_u, grid, 256, 0, s, R, K, N, W, A, U, prec == RGNN_BF16 ? 1 : 0);
+  RGNN_LAUNCH(k_fold_u, grid, 256, 0, s, R, K, N, W, A, U, prec == RGNN_BF16 ? 1 : 0, half);
   return RGNN_OK;
 }
 

@@ -18,12 +18,14 @@
 namespace rgnn {
 
 struct Counters {
-  int32_t bad_edge, bad_node, E_own, J, num_items, num_parts, num_split_rows, num_empty, num_compact, pad[3];
+  int32_t bad_edge, bad_node, E_own, J, num_items, num_parts, num_split_rows, num_empty, num_compact;
+  int32_t num_sitems, num_sparts, num_ssplit;  // dX source work list
 };
 
 __global__ void k_init_counters(Counters* c, int32_t big) {
   c->bad_edge = big; c->bad_node = big; c->E_own = 0; c->J = 0;
   c->num_items = 0; c->num_parts = 0; c->num_split_rows = 0; c->num_empty = 0; c->num_compact = 0;
+  c->num_sitems = 0; c->num_sparts = 0; c->num_ssplit = 0;
 }
 
 // CSR-by-dst input: dst of every edge from row_ptr (one warp per row).
@@ -157,6 +159,42 @@ __global__ void k_inv_c(int64_t n, int norm, const int32_t* __restrict__ head, c
   }
 }
 
+// ---------------------------------------------------------------- dX tables (NEXT-2)
+// run of each position, and the destination / relation of each run
+__global__ void k_dx_runs(int64_t n, const int32_t* __restrict__ head, const int32_t* __restrict__ run_ex,
+                          const int32_t* __restrict__ dst_s, const int32_t* __restrict__ et_s,
+                          int32_t* __restrict__ run_of_pos, int32_t* __restrict__ run_dst, int32_t* __restrict__ run_rel) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t j = run_ex[p] + head[p] - 1;
+    run_of_pos[p] = j;
+    if (head[p]) {
+      run_dst[j] = dst_s[p];
+      run_rel[j] = et_s[p];
+    }
+  }
+}
+__global__ void k_keys_i32(int64_t n, const int32_t* __restrict__ key, uint32_t* __restrict__ k,
+                           uint32_t* __restrict__ v) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    k[p] = (uint32_t)key[p];
+    v[p] = (uint32_t)p;
+  }
+}
+// source-major slots: position, its run, the run's relation, and 1/c
+__global__ void k_dx_slots(int64_t n, const uint32_t* __restrict__ sorted_pos, const int32_t* __restrict__ run_of_pos,
+                           const int32_t* __restrict__ run_rel, const float* __restrict__ inv_c,
+                           int32_t* __restrict__ spos, int32_t* __restrict__ srun, int32_t* __restrict__ srel,
+                           float* __restrict__ sinvc) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = (int32_t)sorted_pos[q];
+    const int32_t j = run_of_pos[p];
+    spos[q] = p;
+    srun[q] = j;
+    srel[q] = run_rel[j];
+    sinvc[q] = inv_c[p];
+  }
+}
+
 // Work list: rows with more than cap in-edges are split into ceil(deg/cap) chunks;
 // rows without in-edges get no item and go to the empty-row list (Y = 0 / self term).
 __global__ void k_item_counts(int64_t V_own, const int32_t* __restrict__ row_ptr, int cap, int32_t* __restrict__ n_items,
@@ -259,6 +297,11 @@ struct GraphLayout {
   Tile* ctiles;
   Tile *tiles, *chunks;
   int32_t* chunk_seg;
+  int32_t *run_of_pos, *run_dst, *run_rel, *spos, *srun, *srel, *srow;
+  float* sinvc;
+  Tile* rtiles;
+  Item* sitems;
+  SplitRow* ssplit;
   size_t dev_bytes;
   // scratch
   Counters* ctr;
@@ -300,6 +343,19 @@ static GraphLayout layout(const rgnn_graph_desc* d, void* dev, void* scr) {
   L.tiles = c.take<Tile>(Ec / kTileRows + R + 1);
   L.chunks = c.take<Tile>(max_chunks(E, R));
   L.chunk_seg = c.take<int32_t>(R + 1);
+  const bool dx = (d->flags & RGNN_GRAPH_DX) != 0;
+  const int64_t Ex = dx ? Ec : 1;
+  L.run_of_pos = c.take<int32_t>(Ex);
+  L.run_dst = c.take<int32_t>(Ex);
+  L.run_rel = c.take<int32_t>(Ex);
+  L.spos = c.take<int32_t>(Ex);
+  L.srun = c.take<int32_t>(Ex);
+  L.srel = c.take<int32_t>(Ex);
+  L.sinvc = c.take<float>(Ex);
+  L.srow = c.take<int32_t>(dx ? d->num_nodes + 1 : 1);
+  L.rtiles = c.take<Tile>(dx ? Ec / kTileRows + R + 1 : 1);
+  L.sitems = c.take<Item>(dx ? d->num_nodes + Ec / cap + 1 : 1);
+  L.ssplit = c.take<SplitRow>(dx ? Ec / cap + 1 : 1);
   L.dev_bytes = c.off;
   Carver s(scr);
   L.ctr = s.take<Counters>(1);
@@ -308,17 +364,18 @@ static GraphLayout layout(const rgnn_graph_desc* d, void* dev, void* scr) {
   L.head = s.take<int32_t>(Ec);
   L.run_ex = s.take<int32_t>(Ec);
   L.et_s = s.take<int32_t>(Ec);
-  L.n_items = s.take<int32_t>(V_own + 1);
-  L.n_parts = s.take<int32_t>(V_own + 1);
-  L.n_split = s.take<int32_t>(V_own + 1);
-  L.n_empty = s.take<int32_t>(V_own + 1);
+  const int64_t Vw = std::max<int64_t>(V_own, (d->flags & RGNN_GRAPH_DX) ? d->num_nodes : 0);  // work-list rows
+  L.n_items = s.take<int32_t>(Vw + 1);
+  L.n_parts = s.take<int32_t>(Vw + 1);
+  L.n_split = s.take<int32_t>(Vw + 1);
+  L.n_empty = s.take<int32_t>(Vw + 1);
   L.rseg_cnt = s.take<int32_t>(R + 1);
   L.crel = s.take<int32_t>(d->materialization != RGNN_MAT_VANILLA ? Ec : 1);
   L.k0 = s.take<uint32_t>(Ec);
   L.v0 = s.take<uint32_t>(Ec);
   L.k1 = s.take<uint32_t>(Ec);
   L.v1 = s.take<uint32_t>(Ec);
-  L.prim_bytes = std::max(radix_scratch_bytes(Ec), scan_scratch_bytes(std::max<int64_t>(Ec + 1, V_own + 1)));
+  L.prim_bytes = std::max(radix_scratch_bytes(Ec), scan_scratch_bytes(std::max<int64_t>(Ec + 1, Vw + 1)));
   L.prim = s.take<char>(L.prim_bytes);
   L.scratch_bytes = s.off;
   return L;
@@ -347,6 +404,7 @@ static rgnn_status check_desc(const rgnn_graph_desc* d) {
   if (d->materialization != RGNN_MAT_VANILLA && d->materialization != RGNN_MAT_COMPACT &&
       d->materialization != RGNN_MAT_AUTO)
     return set_error(RGNN_E_INVALID_ARG, "bad materialization %d", d->materialization);
+  if (d->flags & ~RGNN_GRAPH_DX) return set_error(RGNN_E_INVALID_ARG, "unknown flags 0x%x", d->flags);
   if (d->materialization != RGNN_MAT_VANILLA &&
       (uint64_t)d->num_etypes * (uint64_t)(d->num_nodes > 0 ? d->num_nodes : 1) > 0xffffffffull)
     return set_error(RGNN_E_UNSUPPORTED, "compact materialisation needs R * V < 2^32 (sort key)");
@@ -442,6 +500,10 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   if (n > 0)
     RGNN_LAUNCH(k_inv_c, grid_for(n), T, 0, s, n, d->norm, L.head, L.run_ex, L.run_ptr, L.perm, d->edge_norm,
                 L.inv_c);
+  const bool dx = (d->flags & RGNN_GRAPH_DX) != 0;
+  if (dx && n > 0)
+    RGNN_LAUNCH(k_dx_runs, grid_for(n), T, 0, s, n, L.head, L.run_ex, L.dst_s, L.et_s, L.run_of_pos, L.run_dst,
+                L.run_rel);
   // Destination-walk work list.
   if (V_own > 0) {
     RGNN_LAUNCH(k_item_counts, grid_for(V_own), T, 0, s, V_own, L.row_ptr, cap, L.n_items, L.n_parts, L.n_split,
@@ -476,6 +538,32 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
     RGNN_LAUNCH(k_bounds<int32_t>, grid_for(R + 1), T, 0, s, (int64_t)h.num_compact, L.crel, (int64_t)R, L.cseg);
     RGNN_CUDA_TRY(cudaMemcpyAsync(cseg_h.data(), L.cseg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
   }
+  std::vector<int32_t> rseg_h(R + 1, 0);
+  if (dx) {
+    // source-major CSR over the positions (stable: ascending position within a source)
+    if (n > 0) {
+      RGNN_LAUNCH(k_keys_i32, grid_for(n), T, 0, s, n, L.src_s, L.k0, L.v0);
+      RGNN_TRY(radix_sort_pairs(L.k0, L.v0, L.k1, L.v1, n, bits_for((uint64_t)(V > 0 ? V - 1 : 0)), L.prim,
+                                L.prim_bytes, s, &alt));
+      RGNN_LAUNCH(k_dx_slots, grid_for(n), T, 0, s, n, alt ? L.v1 : L.v0, L.run_of_pos, L.run_rel, L.inv_c, L.spos,
+                  L.srun, L.srel, L.sinvc);
+    }
+    RGNN_LAUNCH(k_bounds<uint32_t>, grid_for(V + 1), T, 0, s, n, alt ? L.k1 : L.k0, V, L.srow);
+    // source work list: sources with more than cap out-edges are split (partial sums merged in order)
+    if (V > 0) {
+      RGNN_LAUNCH(k_item_counts, grid_for(V), T, 0, s, V, L.srow, cap, L.n_items, L.n_parts, L.n_split, L.n_empty);
+      RGNN_TRY(scan_exclusive(L.n_items, L.n_items, V, &L.ctr->num_sitems, L.prim, L.prim_bytes, s));
+      RGNN_TRY(scan_exclusive(L.n_parts, L.n_parts, V, &L.ctr->num_sparts, L.prim, L.prim_bytes, s));
+      RGNN_TRY(scan_exclusive(L.n_split, L.n_split, V, &L.ctr->num_ssplit, L.prim, L.prim_bytes, s));
+      RGNN_LAUNCH(k_fill_items, grid_for(V), T, 0, s, V, L.srow, cap, L.n_items, L.n_parts, L.n_split, L.sitems,
+                  L.ssplit);
+    }
+    RGNN_CUDA_TRY(cudaMemcpyAsync(rseg_h.data(), L.rseg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
+    Counters h2{};
+    RGNN_CUDA_TRY(cudaMemcpyAsync(&h2, L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+    RGNN_CUDA_TRY(cudaStreamSynchronize(s));
+    h.num_sitems = h2.num_sitems; h.num_sparts = h2.num_sparts; h.num_ssplit = h2.num_ssplit;
+  }
   RGNN_CUDA_TRY(cudaStreamSynchronize(s));
   int dev_id = 0, sms = 148;
   RGNN_CUDA_TRY(cudaGetDevice(&dev_id));
@@ -501,6 +589,13 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
         ctiles.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + kTileRows, cseg_h[r + 1]), 0});
   if (!ctiles.empty())
     RGNN_CUDA_TRY(cudaMemcpyAsync(L.ctiles, ctiles.data(), sizeof(Tile) * ctiles.size(), cudaMemcpyHostToDevice, s));
+  std::vector<Tile> rtiles;  // 128-run GEMM tiles per relation (dX: H = G_v W_r^T per run)
+  if (dx)
+    for (int32_t r = 0; r < R; ++r)
+      for (int64_t a = rseg_h[r]; a < rseg_h[r + 1]; a += kTileRows)
+        rtiles.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + kTileRows, rseg_h[r + 1]), 0});
+  if (!rtiles.empty())
+    RGNN_CUDA_TRY(cudaMemcpyAsync(L.rtiles, rtiles.data(), sizeof(Tile) * rtiles.size(), cudaMemcpyHostToDevice, s));
   if ((int64_t)chunks.size() > max_chunks(E, R))
     return set_error(RGNN_E_CUDA, "internal: chunk table overflow");
   if (!tiles.empty())
@@ -523,6 +618,11 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   g->invc_slot = L.invc_slot; g->csrc = L.csrc; g->cseg = L.cseg; g->ctiles = L.ctiles;
   g->num_ctiles = (int64_t)ctiles.size();
   g->chunk_seg = L.chunk_seg;
+  g->has_dx = dx; g->run_of_pos = L.run_of_pos; g->run_dst = L.run_dst; g->run_rel = L.run_rel; 
+  g->spos = L.spos; g->srun = L.srun; g->srel = L.srel; g->sinvc = L.sinvc; g->srow = L.srow;
+  g->rtiles = L.rtiles; g->num_rtiles = (int64_t)rtiles.size();
+  g->sitems = L.sitems; g->num_sitems = h.num_sitems; g->ssplit = L.ssplit; g->num_ssplit = h.num_ssplit;
+  g->num_sparts = h.num_sparts;
   g->seg_host = seg_h;
   g->chunk_seg_host = chunk_seg;
   RGNN_CUDA_TRY(cudaGetDevice(&g->device));

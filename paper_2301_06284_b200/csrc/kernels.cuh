@@ -54,7 +54,9 @@ rgnn_status launch_dw_reduce(int prec, int K, int N, int R, int64_t num_chunks, 
                              const float* W, float* dW, float* dA, float* dA_scratch /* [R*2*K] */, cudaStream_t s);
 rgnn_status launch_dst_term(int prec, int K, const rgnn_graph* g, const float* dpre, const void* X, float* cpart,
                             cudaStream_t s);
-rgnn_status launch_fold_u(int prec, int R, int K, int N, const float* W, const float* A, float* U, cudaStream_t s);
+// U[r] = W_r A[r, half] (half = 1: the destination fold of the forward; 0: the source half, dX)
+rgnn_status launch_fold_u(int prec, int R, int K, int N, const float* W, const float* A, float* U, cudaStream_t s,
+                          int half = 1);
 
 struct AggArgs {
   const Item* items;
@@ -98,6 +100,7 @@ struct BwdArgs {
   const float* lse;
   void* dZ;
   float* dpre;
+  float2* ad;            // dX: (alpha, dpre) per position, or null
 };
 rgnn_status launch_bwd_traverse(int prec, int K, int N, const BwdArgs& a, cudaStream_t s);
 
@@ -108,9 +111,35 @@ rgnn_status launch_gemm_dw_tc(int K, int N, const GemmDwArgs& a, cudaStream_t s)
 rgnn_status launch_bwd_fused_tc(int K, int N, const rgnn_graph* g, const void* X, const void* Z, const int32_t* zmap,
                                 const float* s_src,
                                 const float* lse, const float* Y, const float* dY, const float* U, const float* A,
-                                float slope, float* part, float* cpart, cudaStream_t s);
+                                float slope, float* part, float* cpart, float2* ad, cudaStream_t s);
 rgnn_status launch_expand_dz(int64_t E, int N, const int32_t* dst_s, const float* inv_c, const float* G, void* dZ,
                              cudaStream_t s);
+
+// dX (dx.cu, NEXT-2)
+struct DxArgs {
+  int64_t V, V_own, v0;
+  const Item* items;                          // source work list (row = source node)
+  int64_t num_items;
+  const SplitRow* split;                      // split sources
+  int64_t num_split;
+  float* part;                                // [num_parts, K] partial rows of split sources
+  const int32_t *srow, *spos, *srun, *srel;  // source-major CSR over the positions
+  const float* sinvc;                         // RGCN: 1/c per source slot
+  const float2* ad;                           // RGAT: (alpha, dpre) per position
+  const void* H;                              // [J, K] fp32: G_v W_r^T per (etype, dst) run
+  const float* U0;                            // RGAT: [R, K] W_r A[r,0]
+  const float* U1;                            // RGAT: [R, K] W_r A[r,1]
+  const Item* ditems;                         // RGAT destination terms: the dst work list
+  int64_t num_ditems;
+  const SplitRow* dsplit;
+  int64_t num_dsplit;
+  float* dpart;                               // [num_parts, K]
+  const int32_t *pos, *et_slot;               // CSR-by-dst slots
+  const void* H0;                             // RGCN self loop: [V_own, K] fp32 (G W0^T) or null
+  float* dX;                                  // [V, K] fp32
+};
+rgnn_status launch_transpose_w(int prec, int R, int K, int N, const float* W, float* Wt, cudaStream_t s);
+rgnn_status launch_dx_walk(int K, bool rgat, const DxArgs& a, cudaStream_t s);
 
 }  // namespace rgnn
 

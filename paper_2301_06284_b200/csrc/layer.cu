@@ -24,6 +24,14 @@ struct WsLayout {
   float* cpart;    // RGAT dst term: [num_chunks, K]
   float* vsum;     // RGAT dA vectors: [R, 2, K]
   void* wt;        // tcgen05: bf16 W^T [R, N, K]
+  // dX (with_dx)
+  float2* ad;      // RGAT: (alpha, dpre) per position [E_own]
+  float* dpart;    // RGAT: [num_parts, K] split-row partial destination terms
+  float* Wt;       // [R, N, K] fp32 W^T (and W0^T after it for RGCN)
+  void* H;         // [J, K] fp32
+  void* H0;        // RGCN self loop: [V_own, K] fp32
+  float* U0;       // RGAT: [R, K]
+  float* xpart;    // [num_sparts, K] split-source partial rows
   size_t bytes;
 };
 struct SavedLayout {
@@ -47,7 +55,7 @@ static int64_t dw0_chunks(const rgnn_graph* g) {
   return (g->V_own + cr - 1) / cr;
 }
 
-static WsLayout ws_layout(const rgnn_graph* g, int model, int K, int N, int prec, void* base) {
+static WsLayout ws_layout(const rgnn_graph* g, int model, int K, int N, int prec, void* base, bool with_dx = false) {
   WsLayout w{};
   Carver c(base);
   const size_t e = elt(prec);
@@ -66,6 +74,16 @@ static WsLayout ws_layout(const rgnn_graph* g, int model, int K, int N, int prec
   w.dw0part = c.take<float>(model == RGNN_RGCN ? (size_t)std::max<int64_t>(dw0_chunks(g), 1) * (K * N + K) : 1);
   w.cpart = c.take<float>((size_t)std::max<int64_t>(g->num_chunks, 1) * K);
   w.vsum = c.take<float>((size_t)g->R * 2 * K);
+  if (with_dx) {
+    const int64_t J = std::max<int64_t>(g->J, 1);
+    w.ad = c.take<float2>(model == RGNN_RGAT ? (size_t)E : 1);
+    w.dpart = c.take<float>(model == RGNN_RGAT ? (size_t)std::max<int64_t>(g->num_parts, 1) * K : 1);
+    w.Wt = c.take<float>((size_t)g->R * N * K + (size_t)N * K);
+    w.H = c.take<char>((size_t)J * K * 4);
+    w.H0 = c.take<char>(model == RGNN_RGCN ? (size_t)std::max<int64_t>(g->V_own, 1) * K * 4 : 1);
+    w.U0 = c.take<float>((size_t)g->R * K);
+    w.xpart = c.take<float>((size_t)std::max<int64_t>(g->num_sparts, 1) * K);
+  }
   w.bytes = c.off;
   return w;
 }
@@ -164,7 +182,7 @@ rgnn_status rgnn_workspace_bytes(const rgnn_graph* g, rgnn_model model, int d_in
   (void)training;
   if (!g) return set_error(RGNN_E_INVALID_ARG, "graph is NULL");
   if (!width_ok(d_in) || !width_ok(d_out)) return set_error(RGNN_E_UNSUPPORTED, "widths not in {32,64,128}");
-  if (ws_bytes) *ws_bytes = ws_layout(g, model, d_in, d_out, prec, nullptr).bytes;
+  if (ws_bytes) *ws_bytes = ws_layout(g, model, d_in, d_out, prec, nullptr, training == RGNN_WS_DX).bytes;
   if (saved_bytes) *saved_bytes = saved_layout(g, model, d_out, prec, nullptr).bytes;
   return RGNN_OK;
 }
@@ -184,18 +202,21 @@ rgnn_status rgat_forward(const rgnn_graph* g, int d_in, int d_out, rgnn_prec pre
 }
 
 rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, rgnn_prec prec, const void* X,
-                          const float* W, const float* A, float slope, const float* Y, const float* dY,
-                          const void* saved, float* dW, float* dA, float* dW0, float* dX, void* ws, size_t ws_bytes,
-                          rgnn_comm* comm, void* stream) {
-  const WsLayout need = ws_layout(g, model, K, N, prec, nullptr);
+                          const float* W, const float* W0, const float* A, float slope, const float* Y,
+                          const float* dY, const void* saved, float* dW, float* dA, float* dW0, float* dX, void* ws,
+                          size_t ws_bytes, rgnn_comm* comm, void* stream) {
+  const bool want_dx = dX != nullptr;
+  if (want_dx && g && !g->has_dx)
+    return set_error(RGNN_E_UNSUPPORTED, "dX needs a graph built with RGNN_GRAPH_DX");
+  const WsLayout need = ws_layout(g, model, K, N, prec, nullptr, want_dx);
   RGNN_TRY(check_common(g, K, N, prec, ws, ws_bytes, need));
-  if (dX) return set_error(RGNN_E_UNSUPPORTED, "dX is not computed in v1 (NEXT-2)");
   if (!X || !dY || !dW) return set_error(RGNN_E_INVALID_ARG, "X, dY, dW must not be NULL");
+  if (want_dx && !W) return set_error(RGNN_E_INVALID_ARG, "dX needs W");
   if (model == RGNN_RGAT && (!W || !A || !Y || !saved || !dA))
     return set_error(RGNN_E_INVALID_ARG, "RGAT backward needs W, A, Y, saved and dA");
   if (comm) RGNN_TRY(comm_check_range(comm, g->v0, g->v0 + g->V_own));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  WsLayout w = ws_layout(g, model, K, N, prec, ws);
+  WsLayout w = ws_layout(g, model, K, N, prec, ws, want_dx);
   SavedLayout sv = saved_layout(g, model, N, prec, const_cast<void*>(saved));
 
   GemmDwArgs da{};
@@ -214,7 +235,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     rgnn_status fst = RGNN_E_UNSUPPORTED;
     if (tc_ok) {  // fused position-order backward: dZ built in smem, dW MMA + dst term in one kernel
       Phase ph("bwd_fused", s);
-      fst = launch_bwd_fused_tc(K, N, g, X, sv.Z, use_compact(g, model) ? g->crow_of_pos : nullptr, sv.s_src, sv.lse, Y, dY, w.U, A, slope, w.dwpart, w.cpart, s);
+      fst = launch_bwd_fused_tc(K, N, g, X, sv.Z, use_compact(g, model) ? g->crow_of_pos : nullptr, sv.s_src, sv.lse, Y, dY, w.U, A, slope, w.dwpart, w.cpart, want_dx ? w.ad : nullptr, s);
       if (fst != RGNN_OK && fst != RGNN_E_UNSUPPORTED) return fst;
     }
     if (fst == RGNN_OK) {
@@ -226,6 +247,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     ba.items = g->items; ba.num_items = g->num_items; ba.pos = g->pos; ba.et_slot = g->et_slot; ba.Z = sv.Z;
     ba.s_src = sv.s_src; ba.X = X; ba.v0 = g->v0; ba.U = w.U; ba.A = A; ba.slope = slope; ba.Y = Y; ba.dY = dY;
     ba.lse = sv.lse; ba.dZ = w.dZ; ba.dpre = w.dpre; ba.zrow = use_compact(g, model) ? g->zrow_slot : nullptr;
+    ba.ad = want_dx ? w.ad : nullptr;
     { Phase ph("bwd_traverse", s); RGNN_TRY(launch_bwd_traverse(prec, K, N, ba, s)); }
     { Phase ph("dst_term", s); RGNN_TRY(launch_dst_term(prec, K, g, w.dpre, X, w.cpart, s)); }
     da.Bz = w.dZ; da.dpre = w.dpre; da.dst_local = g->dst_s; da.v0 = g->v0;
@@ -237,7 +259,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     if (tc_ok) {  // fused: dZ rows = G_v / c built in smem, tensor-core dW in the same kernel
       Phase ph("bwd_fused", s);
       fst = launch_bwd_fused_tc(K, N, g, X, nullptr, nullptr, nullptr, nullptr, nullptr, dY, nullptr, nullptr, 0.f, w.dwpart,
-                                w.cpart, s);
+                                w.cpart, nullptr, s);
       if (fst != RGNN_OK && fst != RGNN_E_UNSUPPORTED) return fst;
     }
     if (fst != RGNN_OK) {
@@ -265,11 +287,48 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
       RGNN_TRY(launch_dw_reduce(prec, K, N, 1, d0.num_chunks, nullptr, w.dw0part, nullptr, nullptr, nullptr, nullptr, dW0, nullptr, nullptr, s));
     }
   }
+  if (want_dx) {
+    // dX (dx.cu): H = G_v W_r^T per (etype, dst) run by one typed GEMM, then the source walk
+    const int64_t J = g->J;
+    { Phase ph("dx_prep", s);
+      RGNN_TRY(launch_transpose_w(prec, g->R, K, N, W, w.Wt, s));
+      if (model == RGNN_RGCN && W0) RGNN_TRY(launch_transpose_w(prec, 1, K, N, W0, w.Wt + (size_t)g->R * N * K, s));
+      if (model == RGNN_RGAT) {
+        RGNN_TRY(launch_fold_u(prec, g->R, K, N, W, A, w.U0, s, 0));
+      }
+    }
+    // fp32 GEMMs (SIMT): G is fp32, and rounding G or H to bf16 is too lossy for dX (dx.cu)
+    if (g->num_rtiles) {
+      Phase ph("dx_gemm", s);
+      GemmFwdArgs gh{};
+      gh.tiles = g->rtiles; gh.num_tiles = g->num_rtiles; gh.X = dY; gh.gather = g->run_dst; gh.W = w.Wt;
+      gh.Z = w.H; gh.wt_bf16 = w.wt; gh.num_w = g->R; gh.x_rows = std::max<int64_t>(g->V_own, 1); gh.z_rows = J;
+      RGNN_TRY(launch_gemm_fwd(RGNN_F32, N, K, gh, s));  // GEMM K = d_out, N = d_in
+    }
+    const bool self = model == RGNN_RGCN && W0 && g->V_own > 0;
+    if (self) {
+      Phase ph("dx_gemm", s);
+      GemmFwdArgs g0{};
+      g0.rows = g->V_own; g0.X = dY; g0.gofs = 0; g0.W = w.Wt + (size_t)g->R * N * K; g0.Z = w.H0;
+      g0.wt_bf16 = w.wt; g0.num_w = 1; g0.x_rows = g->V_own;
+      RGNN_TRY(launch_gemm_fwd(RGNN_F32, N, K, g0, s));
+    }
+    { Phase ph("dx_zero", s); RGNN_CUDA_TRY(cudaMemsetAsync(dX, 0, sizeof(float) * (size_t)g->V * K, s)); }
+    DxArgs xa{};
+    xa.V = g->V; xa.V_own = g->V_own; xa.v0 = g->v0;
+    xa.items = g->sitems; xa.num_items = g->num_sitems; xa.split = g->ssplit; xa.num_split = g->num_ssplit;
+    xa.part = w.xpart; xa.srow = g->srow; xa.spos = g->spos; xa.srun = g->srun;
+    xa.srel = g->srel; xa.sinvc = g->sinvc; xa.ad = w.ad; xa.H = w.H; xa.U0 = w.U0; xa.U1 = w.U;
+    xa.ditems = g->items; xa.num_ditems = g->num_items; xa.dsplit = g->split_rows; xa.num_dsplit = g->num_split_rows;
+    xa.dpart = w.dpart; xa.pos = g->pos; xa.et_slot = g->et_slot; xa.H0 = self ? w.H0 : nullptr;
+    xa.dX = dX;
+    RGNN_TRY(launch_dx_walk(K, model == RGNN_RGAT, xa, s));
+  }
   if (comm) {
-    float* bufs[3] = {dW, model == RGNN_RGAT ? dA : nullptr, model == RGNN_RGCN ? dW0 : nullptr};
-    size_t counts[3] = {(size_t)g->R * K * N, (size_t)g->R * 2 * N, (size_t)K * N};
+    float* bufs[4] = {dW, model == RGNN_RGAT ? dA : nullptr, model == RGNN_RGCN ? dW0 : nullptr, dX};
+    size_t counts[4] = {(size_t)g->R * K * N, (size_t)g->R * 2 * N, (size_t)K * N, (size_t)g->V * K};
     Phase ph("comm", s);
-    RGNN_TRY(comm_allreduce_sum(comm, bufs, counts, 3, s));
+    RGNN_TRY(comm_allreduce_sum(comm, bufs, counts, 4, s));
   }
   return RGNN_OK;
 }

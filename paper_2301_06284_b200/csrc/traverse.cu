@@ -622,7 +622,10 @@ __global__ void __launch_bounds__(256) k_bwd_rgat(BwdArgs a) {
         Vec16<T> v;
         v.from_float(o);
         stg16(dZ + (size_t)pp[u] * N + l * EPL, v.raw);
-        if (l == 0) a.dpre[pp[u]] = dpre;
+        if (l == 0) {
+          a.dpre[pp[u]] = dpre;
+          if (a.ad) a.ad[pp[u]] = make_float2(alpha, dpre);
+        }
       }
     }
   }

@@ -53,8 +53,8 @@ class Graph:
 
     def __init__(self, num_nodes: int, src, dst, etype, num_etypes: int, *, row_ptr=None, ntype=None,
                  num_ntypes: int = 0, norm: int = B.RGNN_NORM_REL_INDEG, edge_norm=None, row_split_cap: int = 0,
-                 dst_begin: int = 0, dst_end: Optional[int] = None, materialization="vanilla", device="cuda",
-                 stream=None):
+                 dst_begin: int = 0, dst_end: Optional[int] = None, materialization="vanilla", build_dx: bool = False,
+                 device="cuda", stream=None):
         self.device = torch.device(device)
         self.V, self.R = int(num_nodes), int(num_etypes)
         self.src = _dev_i32(src, self.device)
@@ -71,7 +71,8 @@ class Graph:
                               src=_ptr(self.src), dst=_ptr(self.dst), etype=_ptr(self.etype),
                               row_ptr=_ptr(self.row_ptr_in), ntype=_ptr(self.ntype), edge_norm=_ptr(self.edge_norm),
                               norm=int(norm), row_split_cap=int(row_split_cap), dst_begin=self.dst_begin,
-                              dst_end=self.dst_end, materialization=_mat(materialization))
+                              dst_end=self.dst_end, materialization=_mat(materialization),
+                              flags=B.RGNN_GRAPH_DX if build_dx else 0)
         self._desc = d
         dev_b, scr_b = C.c_size_t(), C.c_size_t()
         B.call("rgnn_graph_bytes", C.byref(d), C.byref(dev_b), C.byref(scr_b))
@@ -170,10 +171,12 @@ def partition_dst(indeg_prefix, nparts: int):
 class Workspace:
     """Workspace + saved buffers sized by rgnn_workspace_bytes (reused across calls)."""
 
-    def __init__(self, g: Graph, model, d_in: int, d_out: int, prec, training: bool = True):
+    def __init__(self, g: Graph, model, d_in: int, d_out: int, prec, training: bool = True, dx: bool = False):
         ws, sv = C.c_size_t(), C.c_size_t()
-        B.call("rgnn_workspace_bytes", g.handle, _model(model), d_in, d_out, _prec(prec), int(training),
+        mode = B.RGNN_WS_DX if dx else int(training)
+        B.call("rgnn_workspace_bytes", g.handle, _model(model), d_in, d_out, _prec(prec), mode,
                C.byref(ws), C.byref(sv))
+        self.dx = dx
         self.ws = torch.empty(max(ws.value, 256), dtype=torch.uint8, device=g.device)
         self.saved = torch.empty(max(sv.value, 256), dtype=torch.uint8, device=g.device)
         self.key = (_model(model), d_in, d_out, _prec(prec))
@@ -213,8 +216,9 @@ def rgat_forward(g: Graph, X: torch.Tensor, W: torch.Tensor, A: torch.Tensor, sl
 
 def rgnn_backward(g: Graph, model, X: torch.Tensor, W: torch.Tensor, dY: torch.Tensor, ws: Workspace, *,
                   A: Optional[torch.Tensor] = None, slope: float = 0.2, Y: Optional[torch.Tensor] = None,
-                  with_w0: bool = False, prec="bf16", comm: Optional[Comm] = None, dW=None, dA=None, dW0=None,
-                  stream=None):
+                  with_w0: bool = False, W0: Optional[torch.Tensor] = None, want_dx: bool = False, prec="bf16",
+                  comm: Optional[Comm] = None, dW=None, dA=None, dW0=None, dX=None, stream=None):
+    """rgnn_backward.  Returns (dW, dA, dW0) or, with want_dx, (dW, dA, dW0, dX [V, d_in])."""
     p, m = _prec(prec), _model(model)
     R, K, N = W.shape
     dW = dW if dW is not None else torch.empty(R, K, N, dtype=torch.float32, device=g.device)
@@ -222,7 +226,9 @@ def rgnn_backward(g: Graph, model, X: torch.Tensor, W: torch.Tensor, dY: torch.T
         dA = torch.empty(R, 2, N, dtype=torch.float32, device=g.device)
     if with_w0 and dW0 is None:
         dW0 = torch.empty(K, N, dtype=torch.float32, device=g.device)
-    B.call("rgnn_backward", g.handle, m, K, N, p, _ptr(X), _ptr(W), _ptr(A), float(slope), _ptr(Y), _ptr(dY),
-           _ptr(ws.saved), _ptr(dW), _ptr(dA), _ptr(dW0) if with_w0 else None, None, _ptr(ws.ws), ws.ws.numel(),
-           comm.handle if comm else None, _stream(stream))
-    return dW, dA, dW0
+    if want_dx and dX is None:
+        dX = torch.empty(g.V, K, dtype=torch.float32, device=g.device)
+    B.call("rgnn_backward", g.handle, m, K, N, p, _ptr(X), _ptr(W), _ptr(W0), _ptr(A), float(slope), _ptr(Y),
+           _ptr(dY), _ptr(ws.saved), _ptr(dW), _ptr(dA), _ptr(dW0) if with_w0 else None,
+           _ptr(dX) if want_dx else None, _ptr(ws.ws), ws.ws.numel(), comm.handle if comm else None, _stream(stream))
+    return (dW, dA, dW0, dX) if want_dx else (dW, dA, dW0)

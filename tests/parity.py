@@ -40,13 +40,13 @@ def assert_close(got, ref, prec: str, what: str = "", per_slice: bool = False):
 
 
 def run_gpu(m, g, t, model: str, prec: str, *, slope=0.2, with_w0=False, norm=0, edge_norm=None,
-            split_cap=0, dst_range=None, backward=True, materialization="vanilla"):
+            split_cap=0, dst_range=None, backward=True, materialization="vanilla", want_dx=False):
     """Build the graph and run fwd (+bwd) on the GPU. Returns dict of numpy arrays."""
     import torch
     dev = "cuda"
     v0, v1 = dst_range or (0, g.V)
     G = m.Graph(g.V, g.src, g.dst, g.etype, g.R, norm=norm, edge_norm=edge_norm, row_split_cap=split_cap,
-                dst_begin=v0, dst_end=v1, materialization=materialization)
+                dst_begin=v0, dst_end=v1, materialization=materialization, build_dx=want_dx)
     Xt = torch.from_numpy(t.X).to(dev)
     X = Xt.to(torch.bfloat16) if prec == "bf16" else Xt
     W = torch.from_numpy(t.W).to(dev)
@@ -54,15 +54,19 @@ def run_gpu(m, g, t, model: str, prec: str, *, slope=0.2, with_w0=False, norm=0,
     W0 = torch.from_numpy(t.W0).to(dev) if with_w0 else None
     dY = torch.from_numpy(np.ascontiguousarray(t.dY[v0:v1])).to(dev)
     out = {"graph": G}
+    K, N = t.W.shape[1], t.W.shape[2]
+    ws = m.Workspace(G, model, K, N, prec, dx=want_dx)
     if model == "rgat":
-        Y, ws = m.rgat_forward(G, X, W, A, slope, prec=prec)
+        Y, ws = m.rgat_forward(G, X, W, A, slope, prec=prec, ws=ws)
     else:
-        Y, ws = m.rgcn_forward(G, X, W, W0, prec=prec)
+        Y, ws = m.rgcn_forward(G, X, W, W0, prec=prec, ws=ws)
     out["Y"] = Y
     if backward:
-        dW, dA, dW0 = m.rgnn_backward(G, model, X, W, dY, ws, A=A if model == "rgat" else None, slope=slope, Y=Y,
-                                      with_w0=with_w0, prec=prec)
-        out.update(dW=dW, dA=dA, dW0=dW0)
+        res = m.rgnn_backward(G, model, X, W, dY, ws, A=A if model == "rgat" else None, slope=slope, Y=Y,
+                              with_w0=with_w0, W0=W0, want_dx=want_dx, prec=prec)
+        out.update(dW=res[0], dA=res[1], dW0=res[2])
+        if want_dx:
+            out["dX"] = res[3]
     torch.cuda.synchronize()
     res = {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in out.items() if v is not None}
     res["ws"] = ws
@@ -85,7 +89,7 @@ def bf16_inputs(t):
 
 
 def run_oracle(oracle, g, t, model: str, *, slope=0.2, with_w0=False, norm=0, edge_norm=None, dst_range=None,
-               backward=True, rels=None, prec="f32"):
+               backward=True, rels=None, prec="f32", want_dx=False):
     if prec == "bf16":
         t = bf16_inputs(t)
     v0, v1 = dst_range or (0, g.V)
@@ -106,4 +110,10 @@ def run_oracle(oracle, g, t, model: str, *, slope=0.2, with_w0=False, norm=0, ed
             out["dW"], out["dW0"] = oracle.rgcn_backward(g.V, g.R, g.src, g.dst, g.etype, t.X, G, K, N, norm=norm,
                                                          edge_norm=edge_norm, with_w0=with_w0, v0=v0, v1=v1,
                                                          rels=rels)
+    if want_dx:
+        if model == "rgat":
+            out["dX"] = oracle.rgat_dx(g.V, g.R, g.src, g.dst, g.etype, t.X, t.W, t.A, G, slope=slope, v0=v0, v1=v1)
+        else:
+            out["dX"] = oracle.rgcn_dx(g.V, g.R, g.src, g.dst, g.etype, t.W, G, W0=t.W0 if with_w0 else None,
+                                       norm=norm, edge_norm=edge_norm, v0=v0, v1=v1)
     return out
