@@ -55,6 +55,9 @@ def _load():
         _lib.oracle_rgat_dx.restype = None
         _lib.oracle_rgcn_dx.argtypes = [i64, i64, i32, i32, i32, vp, vp, vp, vp, vp, i32, vp, vp, i64, i64, vp]
         _lib.oracle_rgcn_dx.restype = None
+        _lib.oracle_hgt_forward.argtypes = [i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                            i64, vp, vp, vp]
+        _lib.oracle_hgt_forward.restype = None
         _lib.oracle_rgcn_backward.argtypes = [i64, i64, i32, i32, i32, vp, vp, vp, vp, i32, vp, vp, i64, i64, vp,
                                               vp, vp]
         _lib.oracle_num_threads.restype = C.c_int
@@ -197,6 +200,20 @@ def rgat_backward(V: int, R: int, src, dst, et, X, W, A, G, slope: float = 0.2, 
     lib.oracle_rgat_backward(V, src.shape[0], R, K, N, _p(src), _p(dst), _p(et), _p(X), _p(W), _p(A),
                              float(slope), _p(G), v0, v1, _p(m), _p(dW), _p(dA))
     return dW, dA
+
+
+def hgt_forward(V: int, R: int, src, dst, et, ntype, X, WK, WQ, WV, Wa, Wm, rows=None):
+    """(Y[rows], lse[rows]) of the HGT layer (NEXT-3, reading O23), fp64."""
+    lib = _load()
+    src, dst, et, nt = _i32(src), _i32(dst), _i32(et), _i32(ntype)
+    X, WK, WQ, WV, Wa, Wm = (_f64(a) for a in (X, WK, WQ, WV, Wa, Wm))
+    T, K, N = WK.shape
+    rr = _rows(V, rows)
+    Y = np.empty((rr.shape[0], N), np.float64)
+    lse = np.empty(rr.shape[0], np.float64)
+    lib.oracle_hgt_forward(V, src.shape[0], R, T, K, N, _p(src), _p(dst), _p(et), _p(nt), _p(X), _p(WK), _p(WQ),
+                           _p(WV), _p(Wa), _p(Wm), rr.shape[0], _p(rr), _p(Y), _p(lse))
+    return Y, lse
 
 
 def rgat_dx(V: int, R: int, src, dst, et, X, W, A, G, slope: float = 0.2, v0: int = 0, v1=None) -> np.ndarray:

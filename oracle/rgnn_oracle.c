@@ -552,4 +552,65 @@ void oracle_rgcn_dx(int64_t V, int64_t E, int32_t R, int32_t K, int32_t N, const
   free(in_eid);
 }
 
+/* ------------------------------------------------------------------ */
+/* HGT layer         */
+/* ------------------------------------------------------------------ */
+/* Forward, for each destination t and incoming edge e = (s -> t, r):
+ *   k_e = x_s WK[tau(s)],  q_t = x_t WQ[tau(t)],  v_e = x_s WV[tau(s)]   (typed linear W_tau(n))
+ *   a_e = k_e^T W_{a,r} q_t = sum_{m,n} k_e[m] Wa[r][m][n] q_t[n]
+ *   alpha_e = softmax over all incoming edges of t
+ *   m_e = v_e W_{m,r}  ("determined by source node features and edge types")
+ *   Y_t = sum_e alpha_e m_e                                                (reading O23)
+ * WK/WQ/WV [T, K, N]; Wa/Wm [R, N, N] row major.  Zero in-degree: Y = 0, lse = -inf. */
+void oracle_hgt_forward(int64_t V, int64_t E, int32_t R, int32_t T, int32_t K, int32_t N, const int32_t* src,
+                        const int32_t* dst, const int32_t* et, const int32_t* ntype, const double* X,
+                        const double* WK, const double* WQ, const double* WV, const double* Wa, const double* Wm,
+                        int64_t n_rows, const int64_t* rows, double* Y, double* lse) {
+  (void)R; (void)T;
+  int64_t* in_ptr;
+  int32_t* in_eid;
+  build_in_lists(V, E, dst, &in_ptr, &in_eid);
+#pragma omp parallel
+  {
+    double* q = (double*)malloc(sizeof(double) * (size_t)N);
+    double* k = (double*)malloc(sizeof(double) * (size_t)N);
+    double* kw = (double*)malloc(sizeof(double) * (size_t)N);
+    double* vv = (double*)malloc(sizeof(double) * (size_t)N);
+    double* mm = (double*)malloc(sizeof(double) * (size_t)N);
+    int64_t cap = 0;
+    double* s = NULL;
+#pragma omp for schedule(dynamic, 16)
+    for (int64_t i = 0; i < n_rows; ++i) {
+      int64_t t = rows[i];
+      int64_t lo = in_ptr[t], hi = in_ptr[t + 1], deg = hi - lo;
+      double* acc = Y + (size_t)i * N;
+      for (int n = 0; n < N; ++n) acc[n] = 0.0;
+      if (deg == 0) { lse[i] = -INFINITY; continue; }
+      if (deg > cap) { cap = deg; s = (double*)realloc(s, sizeof(double) * (size_t)cap); }
+      vecmat(K, N, X + (size_t)t * K, WQ + (size_t)ntype[t] * K * N, q);
+      double m = -INFINITY;
+      for (int64_t e_ = lo; e_ < hi; ++e_) {
+        int32_t e = in_eid[e_], r = et[e], u = src[e];
+        vecmat(K, N, X + (size_t)u * K, WK + (size_t)ntype[u] * K * N, k);
+        vecmat(N, N, k, Wa + (size_t)r * N * N, kw);
+        s[e_ - lo] = dot(N, kw, q);
+        if (s[e_ - lo] > m) m = s[e_ - lo];
+      }
+      double l = 0.0;
+      for (int64_t e_ = lo; e_ < hi; ++e_) l += exp(s[e_ - lo] - m);
+      for (int64_t e_ = lo; e_ < hi; ++e_) {
+        int32_t e = in_eid[e_], r = et[e], u = src[e];
+        double a = exp(s[e_ - lo] - m) / l;
+        vecmat(K, N, X + (size_t)u * K, WV + (size_t)ntype[u] * K * N, vv);
+        vecmat(N, N, vv, Wm + (size_t)r * N * N, mm);
+        for (int n = 0; n < N; ++n) acc[n] += a * mm[n];
+      }
+      lse[i] = m + log(l);
+    }
+    free(q); free(k); free(kw); free(vv); free(mm); free(s);
+  }
+  free(in_ptr);
+  free(in_eid);
+}
+
 int oracle_num_threads(void) { return omp_get_max_threads(); }

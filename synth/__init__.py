@@ -6,6 +6,6 @@ arithmetic (no GEMM, softmax, aggregation or preprocessing).  Recipe: SURVEY.md
 §8(d) "Synthetic inputs", restated in DESIGN.md §4.
 """
 from .heterograph import (  # noqa: F401
-    CONFIGS, GraphConfig, HeteroGraph, LayerTensors, make_graph, make_tensors,
+    CONFIGS, GraphConfig, HeteroGraph, HgtTensors, LayerTensors, make_graph, make_hgt_tensors, make_tensors,
     random_graph, get_config,
 )

@@ -210,3 +210,31 @@ def make_tensors(V: int, R: int, K: int, N: int, seeds=(X_SEED, W_SEED, A_SEED, 
     A = ra.uniform(-ga, ga, size=(R, 2, N)).astype(np.float32)
     dY = rd.uniform(-1.0, 1.0, size=(V, N)).astype(np.float32)
     return LayerTensors(X=X, W=W, A=A, W0=W0, dY=dY)
+
+
+@dataclasses.dataclass
+class HgtTensors:
+    X: np.ndarray    # fp32 [V, K]
+    WK: np.ndarray   # fp32 [T, K, N]  node-typed key linear
+    WQ: np.ndarray   # fp32 [T, K, N]  node-typed query linear
+    WV: np.ndarray   # fp32 [T, K, N]  node-typed value linear
+    Wa: np.ndarray   # fp32 [R, N, N]  relation attention matrix W_{a,r}
+    Wm: np.ndarray   # fp32 [R, N, N]  relation message matrix W_{m,r}
+    dY: np.ndarray   # fp32 [V, N]
+
+
+def make_hgt_tensors(V: int, R: int, T: int, K: int, N: int, seeds=(X_SEED, W_SEED, A_SEED, DY_SEED)) -> HgtTensors:
+    """Seeded HGT layer inputs (NEXT-3): U(-1,1) features, Glorot-uniform weights."""
+    xs, ws, as_, dys = seeds
+    rx = np.random.Generator(np.random.PCG64(xs))
+    rw = np.random.Generator(np.random.PCG64(ws))
+    ra = np.random.Generator(np.random.PCG64(as_))
+    rd = np.random.Generator(np.random.PCG64(dys))
+    X = rx.uniform(-1.0, 1.0, size=(V, K)).astype(np.float32)
+    g1 = np.sqrt(6.0 / (K + N))
+    WK, WQ, WV = (rw.uniform(-g1, g1, size=(T, K, N)).astype(np.float32) for _ in range(3))
+    g2 = np.sqrt(6.0 / (2 * N))
+    Wa = ra.uniform(-g2, g2, size=(R, N, N)).astype(np.float32)
+    Wm = ra.uniform(-g2, g2, size=(R, N, N)).astype(np.float32)
+    dY = rd.uniform(-1.0, 1.0, size=(V, N)).astype(np.float32)
+    return HgtTensors(X=X, WK=WK, WQ=WQ, WV=WV, Wa=Wa, Wm=Wm, dY=dY)

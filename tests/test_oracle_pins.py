@@ -466,3 +466,72 @@ def test_dx_dst_shards_sum_to_full():
     parts = sum(oracle.rgat_dx(V, R, g.src, g.dst, g.etype, t.X, t.W, t.A, G, v0=a, v1=b)
                 for a, b in [(0, 11), (11, 12), (12, 30)])
     np.testing.assert_allclose(parts, full, rtol=1e-12, atol=1e-13)
+
+
+# ---------------------------------------------------------------- HGT (NEXT-3)
+def _torch_hgt(V, src, dst, et, ntype, X, WK, WQ, WV, Wa, Wm):
+    """Independent vectorised fp64 torch HGT: per-node typed linears, per-edge bilinear score,
+    dense [V, E] masked softmax."""
+    import torch
+    s_, d_, e_ = (torch.as_tensor(a, dtype=torch.long) for a in (src, dst, et))
+    nt = torch.as_tensor(ntype, dtype=torch.long)
+    Kn = torch.einsum("vk,vkn->vn", X, WK[nt])
+    Qn = torch.einsum("vk,vkn->vn", X, WQ[nt])
+    Vn = torch.einsum("vk,vkn->vn", X, WV[nt])
+    a = torch.einsum("em,emn,en->e", Kn[s_], Wa[e_], Qn[d_])
+    msg = torch.einsum("em,emn->en", Vn[s_], Wm[e_])
+    mask = torch.zeros(V, len(src), dtype=torch.bool)
+    mask[d_, torch.arange(len(src))] = True
+    logits = torch.where(mask, a[None, :], torch.full_like(mask, -torch.inf, dtype=torch.float64))
+    has = mask.any(1)
+    alpha = torch.zeros_like(logits)
+    alpha[has] = torch.softmax(logits[has], dim=1)
+    return alpha @ msg
+
+
+def test_hgt_vs_torch():
+    torch = pytest.importorskip("torch")
+    V, E, R, T, K, N = 12, 60, 3, 2, 5, 4
+    g = synth.random_graph(V, E, R, seed=51, T=T)
+    t = synth.make_hgt_tensors(V, R, T, K, N)
+    args = [torch.tensor(a, dtype=torch.float64) for a in (t.X, t.WK, t.WQ, t.WV, t.Wa, t.Wm)]
+    ref = _torch_hgt(V, g.src, g.dst, g.etype, g.ntype, *args).numpy()
+    Y, lse = oracle.hgt_forward(V, R, g.src, g.dst, g.etype, g.ntype, t.X, t.WK, t.WQ, t.WV, t.Wa, t.Wm)
+    np.testing.assert_allclose(Y, ref, rtol=1e-12, atol=1e-14)
+    deg = np.bincount(g.dst, minlength=V)
+    assert np.isneginf(lse[deg == 0]).all() and np.isfinite(lse[deg > 0]).all()
+
+
+def test_hgt_one_type_identity_is_dot_product_attention():
+    """T = R = 1, W_a = W_m = I: graph-masked single-head dot-product attention softmax(Q K^T) V
+    (torch.nn.functional.scaled_dot_product_attention with scale 1 and the adjacency as mask)."""
+    torch = pytest.importorskip("torch")
+    V, E, K, N = 10, 45, 4, 3
+    g = synth.random_graph(V, E, 1, seed=52)
+    t = synth.make_hgt_tensors(V, 1, 1, K, N)
+    I = np.eye(N)[None]
+    Y, _ = oracle.hgt_forward(V, 1, g.src, g.dst, g.etype, np.zeros(V, np.int32), t.X, t.WK, t.WQ, t.WV, I, I)
+    X = torch.tensor(t.X, dtype=torch.float64)
+    Q, Kt, Vt = X @ torch.tensor(t.WQ[0], dtype=torch.float64), X @ torch.tensor(t.WK[0], dtype=torch.float64), \
+        X @ torch.tensor(t.WV[0], dtype=torch.float64)
+    cnt = np.zeros((V, V))
+    np.add.at(cnt, (g.dst, g.src), 1.0)  # multi-edges count twice in the softmax
+    has = cnt.sum(1) > 0
+    bias = torch.tensor(np.where(cnt > 0, np.log(np.maximum(cnt, 1)), -np.inf))
+    out = torch.nn.functional.scaled_dot_product_attention(Q[has][None], Kt[None], Vt[None],
+                                                           attn_mask=bias[has][None], scale=1.0)[0]
+    np.testing.assert_allclose(Y[has], out.numpy(), rtol=1e-12, atol=1e-13)
+    assert not Y[~has].any()
+
+
+def test_hgt_softmax_weights_sum_to_one():
+    """Messages identically 1 (V s = const, W_m chosen so m = 1): Y_t = sum alpha = 1 on rows with in-edges."""
+    V, E, R, T, K, N = 15, 80, 3, 2, 4, 4
+    g = synth.random_graph(V, E, R, seed=53, T=T)
+    t = synth.make_hgt_tensors(V, R, T, K, N)
+    X = t.X.copy(); X[:, 0] = 1.0
+    WV = np.zeros_like(t.WV); WV[:, 0, 0] = 1.0          # v = e_0 for every node
+    Wm = np.zeros_like(t.Wm); Wm[:, 0, :] = 1.0          # m = v W_m = all-ones
+    Y, _ = oracle.hgt_forward(V, R, g.src, g.dst, g.etype, g.ntype, X, t.WK * 5, t.WQ * 5, WV, t.Wa, Wm)
+    deg = np.bincount(g.dst, minlength=V)
+    np.testing.assert_allclose(Y[deg > 0], 1.0, atol=1e-12)
