@@ -64,7 +64,7 @@ typedef enum { RGNN_F32 = 0, RGNN_BF16 = 1 } rgnn_prec;
  * or a caller-supplied per-edge factor edge_norm[e].                        */
 typedef enum { RGNN_NORM_REL_INDEG = 0, RGNN_NORM_NONE = 1, RGNN_NORM_EDGE = 2 } rgnn_norm;
 
-typedef enum { RGNN_RGCN = 0, RGNN_RGAT = 1 } rgnn_model;
+typedef enum { RGNN_RGCN = 0, RGNN_RGAT = 1, RGNN_HGT = 2 } rgnn_model;
 
 /* Where per-edge tensors (Z, s_src) live (Sec. 3.1.3).
  * VANILLA: one row per edge (the row number is the edge's position).
@@ -179,6 +179,20 @@ rgnn_status rgcn_forward(const rgnn_graph* g, int d_in, int d_out, rgnn_prec pre
 rgnn_status rgat_forward(const rgnn_graph* g, int d_in, int d_out, rgnn_prec prec, const void* X, const float* W,
                          const float* A, float slope, float* Y, void* saved, void* ws, size_t ws_bytes,
                          rgnn_comm* comm, float* Y_full, void* stream);
+
+/* HGT forward (reading O23):
+ *   k = x_s WK[tau(s)], q = x_t WQ[tau(t)], v = x_s WV[tau(s)]   (node-typed linears)
+ *   a_e = (k W_{a,r}) . q,  alpha = softmax over ALL incoming edges of t,
+ *   Y_t = sum_e alpha_e (v W_{m,r})     -- one head, no extra scaling
+ *   WK, WQ, WV [T, d_in, d_out] fp32; Wa, Wm [R, d_out, d_out] fp32; X as in
+ *   rgat_forward.  The graph must carry node types (desc.ntype, num_ntypes
+ *   = T; else RGNN_E_UNSUPPORTED).  k W_{a,r} and v W_{m,r} are formed once
+ *   per (etype, src) pair when the graph has compact rows (rgnn_zrows with
+ *   RGNN_HGT), else once per edge.  saved receives lse [V_own].  Forward
+ *   only in this version (rgnn_backward returns RGNN_E_UNSUPPORTED for HGT). */
+rgnn_status hgt_forward(const rgnn_graph* g, int d_in, int d_out, rgnn_prec prec, const void* X, const float* WK,
+                        const float* WQ, const float* WV, const float* Wa, const float* Wm, float* Y, void* saved,
+                        void* ws, size_t ws_bytes, rgnn_comm* comm, float* Y_full, void* stream);
 
 /* Backward of L = <Y, dY> over the owned rows (Sec. 3.5; reading O17):
  *   dW [R, d_in, d_out] fp32 (required), dA [R, 2, d_out] (RGAT, required),

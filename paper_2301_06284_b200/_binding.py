@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "librgnn.so")
 RGNN_OK, RGNN_E_INVALID_ARG, RGNN_E_RANGE, RGNN_E_UNSUPPORTED, RGNN_E_WORKSPACE, RGNN_E_CUDA, RGNN_E_NCCL = range(7)
 RGNN_F32, RGNN_BF16 = 0, 1
 RGNN_NORM_REL_INDEG, RGNN_NORM_NONE, RGNN_NORM_EDGE = 0, 1, 2
-RGNN_RGCN, RGNN_RGAT = 0, 1
+RGNN_RGCN, RGNN_RGAT, RGNN_HGT = 0, 1, 2
 RGNN_MAT_VANILLA, RGNN_MAT_COMPACT, RGNN_MAT_AUTO = 0, 1, 2
 RGNN_GRAPH_DX = 1
 RGNN_WS_DX = 3
@@ -67,6 +67,7 @@ _SIGS = {
     "rgnn_comm_create": [_vp, C.c_int, C.c_int, C.POINTER(_i64), C.POINTER(_vp)],
     "rgnn_partition_dst": [_i64, C.POINTER(_i64), C.c_int, C.POINTER(_i64)],
     "rgnn_zrows": [_vp, C.c_int, C.POINTER(_i64)],
+    "hgt_forward": [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp, _vp],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(lib, _name)

@@ -99,6 +99,12 @@ struct rgnn_graph {
   rgnn::Item* sitems;      // source work list (rows = global source nodes with out-edges)
   rgnn::SplitRow* ssplit;
   int64_t num_sitems, num_ssplit, num_sparts;
+  // node-type segments (HGT)
+  bool has_ntype;
+  int32_t num_ntypes;
+  int32_t *nperm, *ninv;
+  rgnn::Tile* ntiles;
+  int64_t num_ntiles;
   bool has_compact;  // compact tables built (COMPACT or AUTO)
   int mat_mode;      // rgnn_materialization requested
   int64_t num_compact, num_ctiles;
@@ -116,7 +122,8 @@ struct rgnn_graph {
 inline bool use_compact(const rgnn_graph* g, int model) {
   if (!g->has_compact) return false;
   if (g->mat_mode == RGNN_MAT_COMPACT) return true;
-  return model == RGNN_RGCN ? g->num_compact < g->E_own : 2 * g->num_compact <= g->E_own;
+  // RGCN / HGT forward-only use of the rows: compact whenever it saves rows
+  return model == RGNN_RGAT ? 2 * g->num_compact <= g->E_own : g->num_compact < g->E_own;
 }
 
 

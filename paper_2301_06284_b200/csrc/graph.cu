@@ -159,6 +159,17 @@ __global__ void k_inv_c(int64_t n, int norm, const int32_t* __restrict__ head, c
   }
 }
 
+// ---------------------------------------------------------------- node-type segments (D4; HGT)
+// nperm[i] = node at type-sorted row i; ninv[u] = row of node u
+__global__ void k_node_perm(int64_t V, const uint32_t* __restrict__ sorted_nodes, int32_t* __restrict__ nperm,
+                            int32_t* __restrict__ ninv) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = (int32_t)sorted_nodes[i];
+    nperm[i] = u;
+    ninv[u] = (int32_t)i;
+  }
+}
+
 // ---------------------------------------------------------------- dX tables (NEXT-2)
 // run of each position, and the destination / relation of each run
 __global__ void k_dx_runs(int64_t n, const int32_t* __restrict__ head, const int32_t* __restrict__ run_ex,
@@ -302,6 +313,8 @@ struct GraphLayout {
   Tile* rtiles;
   Item* sitems;
   SplitRow* ssplit;
+  int32_t *nperm, *ninv, *nseg;
+  Tile* ntiles;
   size_t dev_bytes;
   // scratch
   Counters* ctr;
@@ -356,6 +369,12 @@ static GraphLayout layout(const rgnn_graph_desc* d, void* dev, void* scr) {
   L.rtiles = c.take<Tile>(dx ? Ec / kTileRows + R + 1 : 1);
   L.sitems = c.take<Item>(dx ? d->num_nodes + Ec / cap + 1 : 1);
   L.ssplit = c.take<SplitRow>(dx ? Ec / cap + 1 : 1);
+  const bool nt = d->ntype != nullptr;
+  const int64_t Vn = nt ? std::max<int64_t>(d->num_nodes, 1) : 1;
+  L.nperm = c.take<int32_t>(Vn);
+  L.ninv = c.take<int32_t>(Vn);
+  L.nseg = c.take<int32_t>(nt ? d->num_ntypes + 1 : 1);
+  L.ntiles = c.take<Tile>(nt ? Vn / kTileRows + d->num_ntypes + 1 : 1);
   L.dev_bytes = c.off;
   Carver s(scr);
   L.ctr = s.take<Counters>(1);
@@ -371,11 +390,12 @@ static GraphLayout layout(const rgnn_graph_desc* d, void* dev, void* scr) {
   L.n_empty = s.take<int32_t>(Vw + 1);
   L.rseg_cnt = s.take<int32_t>(R + 1);
   L.crel = s.take<int32_t>(d->materialization != RGNN_MAT_VANILLA ? Ec : 1);
-  L.k0 = s.take<uint32_t>(Ec);
-  L.v0 = s.take<uint32_t>(Ec);
-  L.k1 = s.take<uint32_t>(Ec);
-  L.v1 = s.take<uint32_t>(Ec);
-  L.prim_bytes = std::max(radix_scratch_bytes(Ec), scan_scratch_bytes(std::max<int64_t>(Ec + 1, Vw + 1)));
+  const int64_t Ek = std::max<int64_t>(Ec, d->ntype ? d->num_nodes : 0);  // sort keys: edges, or nodes (types)
+  L.k0 = s.take<uint32_t>(Ek);
+  L.v0 = s.take<uint32_t>(Ek);
+  L.k1 = s.take<uint32_t>(Ek);
+  L.v1 = s.take<uint32_t>(Ek);
+  L.prim_bytes = std::max(radix_scratch_bytes(Ek), scan_scratch_bytes(std::max<int64_t>(Ek + 1, Vw + 1)));
   L.prim = s.take<char>(L.prim_bytes);
   L.scratch_bytes = s.off;
   return L;
@@ -538,6 +558,18 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
     RGNN_LAUNCH(k_bounds<int32_t>, grid_for(R + 1), T, 0, s, (int64_t)h.num_compact, L.crel, (int64_t)R, L.cseg);
     RGNN_CUDA_TRY(cudaMemcpyAsync(cseg_h.data(), L.cseg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
   }
+  // node-type segments (HGT's node-typed linears, D4): stable sort of node ids by type
+  std::vector<int32_t> nseg_h;
+  if (d->ntype && V > 0) {
+    const int32_t NT = d->num_ntypes;
+    nseg_h.assign(NT + 1, 0);
+    RGNN_LAUNCH(k_keys_i32, grid_for(V), T, 0, s, V, d->ntype, L.k0, L.v0);
+    RGNN_TRY(radix_sort_pairs(L.k0, L.v0, L.k1, L.v1, V, bits_for((uint64_t)(NT > 0 ? NT - 1 : 0)), L.prim,
+                              L.prim_bytes, s, &alt));
+    RGNN_LAUNCH(k_node_perm, grid_for(V), T, 0, s, V, alt ? L.v1 : L.v0, L.nperm, L.ninv);
+    RGNN_LAUNCH(k_bounds<uint32_t>, grid_for(NT + 1), T, 0, s, V, alt ? L.k1 : L.k0, (int64_t)NT, L.nseg);
+    RGNN_CUDA_TRY(cudaMemcpyAsync(nseg_h.data(), L.nseg, sizeof(int32_t) * (NT + 1), cudaMemcpyDeviceToHost, s));
+  }
   std::vector<int32_t> rseg_h(R + 1, 0);
   if (dx) {
     // source-major CSR over the positions (stable: ascending position within a source)
@@ -589,6 +621,12 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
         ctiles.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + kTileRows, cseg_h[r + 1]), 0});
   if (!ctiles.empty())
     RGNN_CUDA_TRY(cudaMemcpyAsync(L.ctiles, ctiles.data(), sizeof(Tile) * ctiles.size(), cudaMemcpyHostToDevice, s));
+  std::vector<Tile> ntiles;  // 128-node GEMM tiles per node type (HGT typed linears)
+  for (int32_t t = 0; t + 1 < (int32_t)nseg_h.size(); ++t)
+    for (int64_t a = nseg_h[t]; a < nseg_h[t + 1]; a += kTileRows)
+      ntiles.push_back(Tile{t, (int32_t)a, (int32_t)std::min<int64_t>(a + kTileRows, nseg_h[t + 1]), 0});
+  if (!ntiles.empty())
+    RGNN_CUDA_TRY(cudaMemcpyAsync(L.ntiles, ntiles.data(), sizeof(Tile) * ntiles.size(), cudaMemcpyHostToDevice, s));
   std::vector<Tile> rtiles;  // 128-run GEMM tiles per relation (dX: H = G_v W_r^T per run)
   if (dx)
     for (int32_t r = 0; r < R; ++r)
@@ -623,6 +661,8 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   g->rtiles = L.rtiles; g->num_rtiles = (int64_t)rtiles.size();
   g->sitems = L.sitems; g->num_sitems = h.num_sitems; g->ssplit = L.ssplit; g->num_ssplit = h.num_ssplit;
   g->num_sparts = h.num_sparts;
+  g->has_ntype = d->ntype != nullptr && V > 0; g->num_ntypes = d->ntype ? d->num_ntypes : 0;
+  g->nperm = L.nperm; g->ninv = L.ninv; g->ntiles = L.ntiles; g->num_ntiles = (int64_t)ntiles.size();
   g->seg_host = seg_h;
   g->chunk_seg_host = chunk_seg;
   RGNN_CUDA_TRY(cudaGetDevice(&g->device));
@@ -646,7 +686,8 @@ void rgnn_graph_destroy(rgnn_graph* g) { delete g; }
 
 rgnn_status rgnn_zrows(const rgnn_graph* g, rgnn_model model, int64_t* rows) {
   if (!g || !rows) return set_error(RGNN_E_INVALID_ARG, "NULL graph or rows");
-  if (model != RGNN_RGCN && model != RGNN_RGAT) return set_error(RGNN_E_INVALID_ARG, "bad model %d", (int)model);
+  if (model != RGNN_RGCN && model != RGNN_RGAT && model != RGNN_HGT)
+    return set_error(RGNN_E_INVALID_ARG, "bad model %d", (int)model);
   *rows = use_compact(g, model) ? g->num_compact : g->E_own;
   return RGNN_OK;
 }

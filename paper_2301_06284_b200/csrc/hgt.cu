@@ -1,0 +1,190 @@
+// hgt.cu -- HGT layer forward (PAPER.md P:280, P:355,
+// P:520-521; reading O23):
+//   k = x_s WK[tau(s)], q = x_t WQ[tau(t)], v = x_s WV[tau(s)]   node-typed linears (segment MM over
+//                                                                 node-type segments)
+//   kw = k W_{a,r},  m = v W_{m,r}        once per (etype, src) pair with compact rows (P:520-521:
+//                                          "determined by source node features and edge types")
+//   a_e = kw . q_t,  alpha = softmax over the incoming edges of t,  Y_t = sum alpha_e m_e
+// The typed linears run on the same typed GEMM as RGCN/RGAT (tcgen05 on the bf16 path); this
+// file holds the destination walk: a_e = kw . q_t is the paper's "edge-wise vector inner
+// product" after the typed linear, fused with the online softmax and the aggregation.
+#include <math_constants.h>
+
+#include "kernels.cuh"
+
+namespace rgnn {
+
+// out[i] = ninv[idx[i]] : GEMM gather rows of the node-typed features (type-sorted rows)
+__global__ void k_map_gather(int64_t n, const int32_t* __restrict__ idx, const int32_t* __restrict__ ninv,
+                             int32_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = ninv[idx[i]];
+}
+
+// fp32 copies for the score path of the bf16 layer: X values (exact) and RNE-rounded weights
+__global__ void k_bf16_to_f32(int64_t n, const __nv_bfloat16* __restrict__ a, float* __restrict__ b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = __bfloat162float(a[i]);
+}
+__global__ void k_round_bf16(int64_t n, const float* __restrict__ a, float* __restrict__ b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = __bfloat162float(__float2bfloat16_rn(a[i]));
+}
+rgnn_status launch_bf16_to_f32(int64_t n, const void* a, float* b, cudaStream_t s) {
+  if (n == 0) return RGNN_OK;
+  RGNN_LAUNCH(k_bf16_to_f32, (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, s, n,
+              static_cast<const __nv_bfloat16*>(a), b);
+  return RGNN_OK;
+}
+rgnn_status launch_round_bf16(int64_t n, const float* a, float* b, cudaStream_t s) {
+  if (n == 0) return RGNN_OK;
+  RGNN_LAUNCH(k_round_bf16, (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, s, n, a, b);
+  return RGNN_OK;
+}
+
+rgnn_status launch_map_gather(int64_t n, const int32_t* idx, const int32_t* ninv, int32_t* out, cudaStream_t s) {
+  if (n == 0) return RGNN_OK;
+  RGNN_LAUNCH(k_map_gather, (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, s, n, idx, ninv, out);
+  return RGNN_OK;
+}
+
+// One warp per work item (a destination row or a chunk of a hub row), as k_aggregate:
+// L = N*sizeof(T)/16 lanes read a 16-byte slice of the kw row and of the m row of an
+// edge; the warp's 32/L lane groups take interleaved edges with their own online
+// (max, sum, acc) state, merged in a fixed xor tree.  Deterministic, no atomics.
+// TS: type of the score factors kw and q (fp32 on both paths: bf16 logits lose ~2-4% of rms(Y)
+// at single elements through exp, measured against the oracle; O23); TM: message type.
+template <typename TS, typename TM, int N>
+__global__ void __launch_bounds__(256) k_aggregate_hgt(HgtAggArgs a) {
+  constexpr int EPL = 16 / sizeof(TM);
+  constexpr int SV = EPL * sizeof(TS) / 16;  // 16-byte vectors of a lane's kw / q slice
+  constexpr int L = N / EPL;
+  constexpr int G = 32 / L;
+  constexpr int UNR = G >= 4 ? 2 : 4;
+  constexpr int B = G * UNR;
+  static_assert(L >= 1 && L <= 32 && B <= 32, "hgt walk shape");
+  const TS* KW = static_cast<const TS*>(a.KW);
+  const TM* M = static_cast<const TM*>(a.M);
+  const TS* Q = static_cast<const TS*>(a.Q);
+  const int lane = threadIdx.x & 31, g = lane / L, l = lane % L;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = warp0; w < a.num_items; w += nwarps) {
+    const Item it = a.items[w];
+    float qf[EPL];
+    {
+      const TS* qp = Q + (size_t)a.ninv[a.v0 + it.row] * N + l * EPL;
+#pragma unroll
+      for (int v = 0; v < SV; ++v) Vec16<TS>{ldg16(qp + v * (16 / sizeof(TS)))}.to_float(qf + v * (16 / sizeof(TS)));
+    }
+    float acc[EPL];
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
+    float m = -CUDART_INF_F, lsum = 0.f;
+    int nq = it.q0 + lane;
+    int np = (lane < B && nq < it.q1) ? a.pos[nq] : 0;
+    for (int base = it.q0; base < it.q1; base += B) {
+      const int myp = np;
+      nq = base + B + lane;
+      np = (lane < B && nq < it.q1) ? a.pos[nq] : 0;
+      uint4 kr[UNR][SV], mr[UNR];
+      bool val[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int j = u * G + g;
+        const int p = __shfl_sync(0xffffffffu, myp, j);
+        val[u] = base + j < it.q1;
+#pragma unroll
+        for (int v = 0; v < SV; ++v)
+          kr[u][v] = val[u] ? ldg16(KW + (size_t)p * N + l * EPL + v * (16 / sizeof(TS))) : make_uint4(0, 0, 0, 0);
+        mr[u] = val[u] ? ldg16(M + (size_t)p * N + l * EPL) : make_uint4(0, 0, 0, 0);
+      }
+      float sc[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        float kf[EPL];
+#pragma unroll
+        for (int v = 0; v < SV; ++v) Vec16<TS>{kr[u][v]}.to_float(kf + v * (16 / sizeof(TS)));
+        float d = 0.f;
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) d = fmaf(kf[i], qf[i], d);
+#pragma unroll
+        for (int o = L / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        sc[u] = val[u] ? d : -CUDART_INF_F;
+      }
+      float mnew = m;
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) mnew = fmaxf(mnew, sc[u]);
+      if (mnew != -CUDART_INF_F) {
+        const float corr = __expf(m - mnew);
+        lsum *= corr;
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) acc[i] *= corr;
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const float e = val[u] ? __expf(sc[u] - mnew) : 0.f;
+          lsum += e;
+          float mf[EPL];
+          Vec16<TM>{mr[u]}.to_float(mf);
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) acc[i] = fmaf(e, mf[i], acc[i]);
+        }
+        m = mnew;
+      }
+    }
+#pragma unroll
+    for (int o = L; o < 32; o <<= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      const float l2 = __shfl_xor_sync(0xffffffffu, lsum, o);
+      const float mn = fmaxf(m, m2);
+      const float c1 = mn == -CUDART_INF_F ? 0.f : __expf(m - mn);
+      const float c2 = mn == -CUDART_INF_F ? 0.f : __expf(m2 - mn);
+      lsum = lsum * c1 + l2 * c2;
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        const float a2 = __shfl_xor_sync(0xffffffffu, acc[i], o);
+        acc[i] = acc[i] * c1 + a2 * c2;
+      }
+      m = mn;
+    }
+    if (g == 0) {
+      if (it.part < 0) {
+        const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+        float* y = a.Y + (size_t)it.row * N + l * EPL;
+#pragma unroll
+        for (int i = 0; i < EPL; i += 4)
+          stg16(y + i, make_uint4(__float_as_uint(acc[i] * inv), __float_as_uint(acc[i + 1] * inv),
+                                  __float_as_uint(acc[i + 2] * inv), __float_as_uint(acc[i + 3] * inv)));
+        if (l == 0) a.lse[it.row] = lsum > 0.f ? m + __logf(lsum) : -CUDART_INF_F;
+      } else {
+        float* pp = a.part + (size_t)it.part * (N + 4);
+#pragma unroll
+        for (int i = 0; i < EPL; i += 4)
+          stg16(pp + l * EPL + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]),
+                                             __float_as_uint(acc[i + 2]), __float_as_uint(acc[i + 3])));
+        if (l == 0) { pp[N] = m; pp[N + 1] = lsum; }
+      }
+    }
+  }
+}
+
+template <typename TM, int N>
+static rgnn_status hgt_walk(const HgtAggArgs& a, cudaStream_t s) {
+  if (a.num_items == 0) return RGNN_OK;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((a.num_items + 7) / 8, 148 * 16));
+  RGNN_LAUNCH((k_aggregate_hgt<float, TM, N>), grid, 256, 0, s, a);
+  return RGNN_OK;
+}
+
+// kw and q are fp32 on both paths; the message rows are bf16 on the bf16 path
+rgnn_status launch_aggregate_hgt(int prec, int N, const HgtAggArgs& a, cudaStream_t s) {
+  const bool bf = prec == RGNN_BF16;
+  switch (N) {
+    case 32: return bf ? hgt_walk<__nv_bfloat16, 32>(a, s) : hgt_walk<float, 32>(a, s);
+    case 64: return bf ? hgt_walk<__nv_bfloat16, 64>(a, s) : hgt_walk<float, 64>(a, s);
+    case 128: return bf ? hgt_walk<__nv_bfloat16, 128>(a, s) : hgt_walk<float, 128>(a, s);
+    default: return set_error(RGNN_E_UNSUPPORTED, "d_out=%d not in {32,64,128}", N);
+  }
+}
+
+}  // namespace rgnn

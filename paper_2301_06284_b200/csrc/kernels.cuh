@@ -141,6 +141,25 @@ struct DxArgs {
 rgnn_status launch_transpose_w(int prec, int R, int K, int N, const float* W, float* Wt, cudaStream_t s);
 rgnn_status launch_dx_walk(int K, bool rgat, const DxArgs& a, cudaStream_t s);
 
+// HGT (hgt.cu, NEXT-3)
+struct HgtAggArgs {
+  const Item* items;
+  int64_t num_items;
+  const int32_t* pos;     // slot -> row of KW / M (compact: zrow_slot)
+  const void* KW;         // [zrows, N] fp32: k W_{a,r}
+  const void* M;          // [zrows, N] T: v W_{m,r}
+  const void* Q;          // [V, N] fp32: q rows in node-type order
+  const int32_t* ninv;    // node -> its row in Q
+  int64_t v0;
+  float* Y;
+  float* lse;
+  float* part;
+};
+rgnn_status launch_map_gather(int64_t n, const int32_t* idx, const int32_t* ninv, int32_t* out, cudaStream_t s);
+rgnn_status launch_bf16_to_f32(int64_t n, const void* a, float* b, cudaStream_t s);
+rgnn_status launch_round_bf16(int64_t n, const float* a, float* b, cudaStream_t s);
+rgnn_status launch_aggregate_hgt(int prec, int N, const HgtAggArgs& a, cudaStream_t s);
+
 }  // namespace rgnn
 
 #define RGNN_DISPATCH_KN(K, N, ...)                                                        \

@@ -55,6 +55,36 @@ static int64_t dw0_chunks(const rgnn_graph* g) {
   return (g->V_own + cr - 1) / cr;
 }
 
+struct HgtWs {
+  float *Kf, *Qf, *KWf;   // score path, fp32 on both paths
+  void *Vn, *M, *wt;      // message path, T
+  float *Xf, *Wr;         // bf16 path: X as fp32, RNE-rounded WK | WQ | Wa
+  int32_t* gather;
+  float* part;
+  size_t bytes;
+};
+static HgtWs hgt_ws_layout(const rgnn_graph* g, int K, int N, int prec, void* base) {
+  HgtWs w{};
+  Carver c(base);
+  const size_t e = prec == RGNN_BF16 ? 2 : 4;
+  const int64_t V = std::max<int64_t>(g->V, 1);
+  const int64_t zr = std::max<int64_t>(use_compact(g, RGNN_HGT) ? g->num_compact : g->E_own, 1);
+  const int64_t T = std::max<int64_t>(g->num_ntypes, 1);
+  w.Kf = c.take<float>((size_t)V * N);
+  w.Qf = c.take<float>((size_t)V * N);
+  w.KWf = c.take<float>((size_t)zr * N);
+  w.Vn = c.take<char>((size_t)V * N * e);
+  w.M = c.take<char>((size_t)zr * N * e);
+  w.gather = c.take<int32_t>((size_t)zr);
+  w.part = c.take<float>((size_t)std::max<int64_t>(g->num_parts, 1) * (N + 4));
+  const int64_t nw = std::max<int64_t>(T * K * N, (int64_t)g->R * N * N);
+  w.wt = c.take<char>(prec == RGNN_BF16 ? (size_t)nw * 2 : 1);
+  w.Xf = c.take<float>(prec == RGNN_BF16 ? (size_t)V * K : 1);
+  w.Wr = c.take<float>(prec == RGNN_BF16 ? (size_t)(2 * T * K * N + (int64_t)g->R * N * N) : 1);
+  w.bytes = c.off;
+  return w;
+}
+
 static WsLayout ws_layout(const rgnn_graph* g, int model, int K, int N, int prec, void* base, bool with_dx = false) {
   WsLayout w{};
   Carver c(base);
@@ -94,6 +124,8 @@ static SavedLayout saved_layout(const rgnn_graph* g, int model, int N, int prec,
   if (model == RGNN_RGAT) {
     s.Z = c.take<char>((size_t)zrows(g, model) * N * elt(prec));
     s.s_src = c.take<float>((size_t)zrows(g, model));
+    s.lse = c.take<float>((size_t)std::max<int64_t>(g->V_own, 1));
+  } else if (model == RGNN_HGT) {
     s.lse = c.take<float>((size_t)std::max<int64_t>(g->V_own, 1));
   }
   s.bytes = c.off;
@@ -182,7 +214,9 @@ rgnn_status rgnn_workspace_bytes(const rgnn_graph* g, rgnn_model model, int d_in
   (void)training;
   if (!g) return set_error(RGNN_E_INVALID_ARG, "graph is NULL");
   if (!width_ok(d_in) || !width_ok(d_out)) return set_error(RGNN_E_UNSUPPORTED, "widths not in {32,64,128}");
-  if (ws_bytes) *ws_bytes = ws_layout(g, model, d_in, d_out, prec, nullptr, training == RGNN_WS_DX).bytes;
+  if (ws_bytes)
+    *ws_bytes = model == RGNN_HGT ? hgt_ws_layout(g, d_in, d_out, prec, nullptr).bytes
+                                  : ws_layout(g, model, d_in, d_out, prec, nullptr, training == RGNN_WS_DX).bytes;
   if (saved_bytes) *saved_bytes = saved_layout(g, model, d_out, prec, nullptr).bytes;
   return RGNN_OK;
 }
@@ -201,10 +235,88 @@ rgnn_status rgat_forward(const rgnn_graph* g, int d_in, int d_out, rgnn_prec pre
                  stream);
 }
 
+rgnn_status hgt_forward(const rgnn_graph* g, int K, int N, rgnn_prec prec, const void* X, const float* WK,
+                        const float* WQ, const float* WV, const float* Wa, const float* Wm, float* Y, void* saved,
+                        void* ws, size_t ws_bytes, rgnn_comm* comm, float* Y_full, void* stream) {
+  if (!g) return set_error(RGNN_E_INVALID_ARG, "graph is NULL");
+  if (!g->has_ntype) return set_error(RGNN_E_UNSUPPORTED, "HGT needs node types (rgnn_graph_desc.ntype)");
+  const HgtWs need = hgt_ws_layout(g, K, N, prec, nullptr);
+  if (!width_ok(K) || !width_ok(N)) return set_error(RGNN_E_UNSUPPORTED, "d_in=%d d_out=%d not in {32,64,128}", K, N);
+  if (prec != RGNN_F32 && prec != RGNN_BF16) return set_error(RGNN_E_INVALID_ARG, "bad precision %d", prec);
+  if (!ws || (uintptr_t)ws % kAlign) return set_error(RGNN_E_INVALID_ARG, "workspace NULL or not 256B aligned");
+  if (ws_bytes < need.bytes) return set_error(RGNN_E_WORKSPACE, "workspace %zu < required %zu", ws_bytes, need.bytes);
+  if (!X || !WK || !WQ || !WV || !Wa || !Wm || !Y || !saved)
+    return set_error(RGNN_E_INVALID_ARG, "X, WK, WQ, WV, Wa, Wm, Y, saved must not be NULL");
+  if (comm) RGNN_TRY(comm_check_range(comm, g->v0, g->v0 + g->V_own));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HgtWs w = hgt_ws_layout(g, K, N, prec, ws);
+  SavedLayout sv = saved_layout(g, RGNN_HGT, N, prec, saved);
+  // Score path (k, q, k W_{a,r}) in fp32 on both paths -- bf16 logits lose too much through the
+  // exponent (O23); the message path (v, v W_{m,r}) on the typed GEMM of the layer's
+  // precision (tcgen05 on the bf16 path).  Node-typed linears run over the node-type segments
+  // (rows in type order), relation-typed ones per (etype, src) pair (or per edge).
+  const bool bf = prec == RGNN_BF16;
+  const int64_t T = g->num_ntypes;
+  const float *WKs = WK, *WQs = WQ, *Was = Wa;
+  const void* Xs = X;
+  if (bf) {
+    Phase ph("hgt_prep", s);
+    RGNN_TRY(launch_bf16_to_f32(g->V * K, X, w.Xf, s));
+    RGNN_TRY(launch_round_bf16(T * K * N, WK, w.Wr, s));
+    RGNN_TRY(launch_round_bf16(T * K * N, WQ, w.Wr + T * K * N, s));
+    RGNN_TRY(launch_round_bf16((int64_t)g->R * N * N, Wa, w.Wr + 2 * T * K * N, s));
+    Xs = w.Xf; WKs = w.Wr; WQs = w.Wr + T * K * N; Was = w.Wr + 2 * T * K * N;
+  }
+  if (g->num_ntiles) {
+    Phase ph("hgt_node_gemm", s);
+    auto node_gemm = [&](int p, const void* Xin, const float* Win, void* out) -> rgnn_status {
+      GemmFwdArgs ga{};
+      ga.tiles = g->ntiles; ga.num_tiles = g->num_ntiles; ga.X = Xin; ga.gather = g->nperm; ga.W = Win;
+      ga.Z = out; ga.wt_bf16 = w.wt; ga.num_w = (int)T; ga.x_rows = g->V; ga.z_rows = g->V;
+      return p == RGNN_F32 ? launch_gemm_fwd(RGNN_F32, K, N, ga, s) : typed_gemm(p, K, N, ga, s);
+    };
+    RGNN_TRY(node_gemm(RGNN_F32, Xs, WKs, w.Kf));
+    RGNN_TRY(node_gemm(RGNN_F32, Xs, WQs, w.Qf));
+    RGNN_TRY(node_gemm(prec, X, WV, w.Vn));
+  }
+  const bool cm = use_compact(g, RGNN_HGT);
+  const int64_t zr = cm ? g->num_compact : g->E_own;
+  const int64_t nt = cm ? g->num_ctiles : g->num_tiles;
+  {
+    Phase ph("hgt_rel_gemm", s);
+    RGNN_TRY(launch_map_gather(zr, cm ? g->csrc : g->src_s, g->ninv, w.gather, s));
+    auto rel_gemm = [&](int p, const void* Xin, const float* Win, void* out) -> rgnn_status {
+      GemmFwdArgs ga{};
+      ga.tiles = cm ? g->ctiles : g->tiles; ga.num_tiles = nt; ga.X = Xin; ga.gather = w.gather; ga.W = Win;
+      ga.Z = out; ga.wt_bf16 = w.wt; ga.num_w = g->R; ga.x_rows = g->V; ga.z_rows = zr;
+      return p == RGNN_F32 ? launch_gemm_fwd(RGNN_F32, N, N, ga, s) : typed_gemm(p, N, N, ga, s);
+    };
+    if (nt) {
+      RGNN_TRY(rel_gemm(RGNN_F32, w.Kf, Was, w.KWf));
+      RGNN_TRY(rel_gemm(prec, w.Vn, Wm, w.M));
+    }
+  }
+  {
+    Phase ph("aggregate", s);
+    HgtAggArgs ha{};
+    ha.items = g->items; ha.num_items = g->num_items; ha.pos = cm ? g->zrow_slot : g->pos; ha.KW = w.KWf;
+    ha.M = w.M; ha.Q = w.Qf; ha.ninv = g->ninv; ha.v0 = g->v0; ha.Y = Y; ha.lse = sv.lse; ha.part = w.part;
+    RGNN_TRY(launch_aggregate_hgt(prec, N, ha, s));
+    // zero rows and split-row merges of the shared walk infrastructure (online-softmax states)
+    AggArgs aa{};
+    aa.num_items = 0; aa.Y = Y; aa.lse = sv.lse; aa.part = w.part; aa.split_rows = g->split_rows;
+    aa.num_split_rows = g->num_split_rows; aa.empty_rows = g->empty_rows; aa.num_empty = g->num_empty;
+    RGNN_TRY(launch_aggregate(prec, N, N, true, aa, s));
+  }
+  if (comm && Y_full) { Phase ph("comm", s); RGNN_TRY(comm_gather_rows(comm, Y, N, Y_full, s)); }
+  return RGNN_OK;
+}
+
 rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, rgnn_prec prec, const void* X,
                           const float* W, const float* W0, const float* A, float slope, const float* Y,
                           const float* dY, const void* saved, float* dW, float* dA, float* dW0, float* dX, void* ws,
                           size_t ws_bytes, rgnn_comm* comm, void* stream) {
+  if (model == RGNN_HGT) return set_error(RGNN_E_UNSUPPORTED, "HGT backward is not implemented (forward only)");
   const bool want_dx = dX != nullptr;
   if (want_dx && g && !g->has_dx)
     return set_error(RGNN_E_UNSUPPORTED, "dX needs a graph built with RGNN_GRAPH_DX");

@@ -16,7 +16,7 @@ import torch
 from . import _binding as B
 
 PREC = {"f32": B.RGNN_F32, "fp32": B.RGNN_F32, "bf16": B.RGNN_BF16}
-MODEL = {"rgcn": B.RGNN_RGCN, "rgat": B.RGNN_RGAT}
+MODEL = {"rgcn": B.RGNN_RGCN, "rgat": B.RGNN_RGAT, "hgt": B.RGNN_HGT}
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -211,6 +211,20 @@ def rgat_forward(g: Graph, X: torch.Tensor, W: torch.Tensor, A: torch.Tensor, sl
     Y = Y if Y is not None else torch.empty(g.V_own, N, dtype=torch.float32, device=g.device)
     B.call("rgat_forward", g.handle, K, N, p, _ptr(X), _ptr(W), _ptr(A), float(slope), _ptr(Y), _ptr(ws.saved),
            _ptr(ws.ws), ws.ws.numel(), comm.handle if comm else None, _ptr(Y_full), _stream(stream))
+    return Y, ws
+
+
+def hgt_forward(g: Graph, X: torch.Tensor, WK: torch.Tensor, WQ: torch.Tensor, WV: torch.Tensor, Wa: torch.Tensor,
+                Wm: torch.Tensor, *, prec="bf16", ws: Optional[Workspace] = None, Y: Optional[torch.Tensor] = None,
+                comm: Optional[Comm] = None, Y_full: Optional[torch.Tensor] = None, stream=None):
+    """hgt_forward (NEXT-3): WK/WQ/WV [T, d_in, d_out], Wa/Wm [R, d_out, d_out]."""
+    p = _prec(prec)
+    _check_x(X, p)
+    T, K, N = WK.shape
+    ws = ws or Workspace(g, "hgt", K, N, p)
+    Y = Y if Y is not None else torch.empty(g.V_own, N, dtype=torch.float32, device=g.device)
+    B.call("hgt_forward", g.handle, K, N, p, _ptr(X), _ptr(WK), _ptr(WQ), _ptr(WV), _ptr(Wa), _ptr(Wm), _ptr(Y),
+           _ptr(ws.saved), _ptr(ws.ws), ws.ws.numel(), comm.handle if comm else None, _ptr(Y_full), _stream(stream))
     return Y, ws
 
 

@@ -1,0 +1,77 @@
+"""HGT forward (reading O23) through the C ABI vs the fp64 oracle
+(oracle.hgt_forward, pinned in test_oracle_pins.py)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from parity import assert_close, bf16_round
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(rgnn, g, t, prec, materialization="auto", dst_range=None, split_cap=0):
+    import torch
+    v0, v1 = dst_range or (0, g.V)
+    G = rgnn.Graph(g.V, g.src, g.dst, g.etype, g.R, ntype=g.ntype, num_ntypes=g.T, dst_begin=v0, dst_end=v1,
+                   materialization=materialization, row_split_cap=split_cap)
+    X = torch.from_numpy(t.X).cuda()
+    X = X.to(torch.bfloat16) if prec == "bf16" else X
+    Ws = [torch.from_numpy(a).cuda() for a in (t.WK, t.WQ, t.WV, t.Wa, t.Wm)]
+    Y, ws = rgnn.hgt_forward(G, X, *Ws, prec=prec)
+    torch.cuda.synchronize()
+    return Y.cpu().numpy(), ws.saved, G
+
+
+def _ref(g, t, prec, dst_range=None):
+    v0, v1 = dst_range or (0, g.V)
+    r = bf16_round if prec == "bf16" else (lambda a: a)
+    Y, lse = oracle.hgt_forward(g.V, g.R, g.src, g.dst, g.etype, g.ntype, r(t.X), r(t.WK), r(t.WQ), r(t.WV),
+                                r(t.Wa), r(t.Wm), rows=np.arange(v0, v1))
+    return Y
+
+
+CASES = [
+    ("rand", lambda: (synth.random_graph(400, 5000, 6, seed=7, T=3), 64, 64)),
+    ("rand-kn", lambda: (synth.random_graph(300, 3000, 5, seed=8, T=2), 128, 64)),
+    ("rand-nk", lambda: (synth.random_graph(300, 3000, 4, seed=9, T=4), 64, 128)),
+    ("mutag/8", lambda: (synth.make_graph(synth.get_config("mutag").scaled(8)), 64, 64)),
+    ("aifb", lambda: (synth.make_graph(synth.get_config("aifb")), 32, 32)),
+]
+
+
+@pytest.mark.parametrize("prec", ["f32", "bf16"])
+@pytest.mark.parametrize("mat", ["compact", "vanilla"])
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_hgt_parity(rgnn, case, mat, prec):
+    g, K, N = case[1]()
+    t = synth.make_hgt_tensors(g.V, g.R, g.T, K, N)
+    Y, _, G = _run(rgnn, g, t, prec, materialization=mat)
+    assert G.zrows("hgt") == (G.num_compact if mat == "compact" else G.E_own)
+    assert_close(Y, _ref(g, t, prec), prec, f"hgt {mat}/{prec} Y")
+
+
+def test_hgt_split_rows_shards_and_determinism(rgnn):
+    g = synth.make_graph(synth.get_config("bgs").scaled(10))
+    t = synth.make_hgt_tensors(g.V, g.R, g.T, 64, 64)
+    Y, _, _ = _run(rgnn, g, t, "f32", split_cap=8)
+    assert_close(Y, _ref(g, t, "f32"), "f32", "hgt split Y")
+    Y2, _, _ = _run(rgnn, g, t, "f32", split_cap=8)
+    np.testing.assert_array_equal(Y, Y2)
+    indeg = np.r_[0, np.cumsum(np.bincount(g.dst, minlength=g.V))]
+    b = rgnn.partition_dst(indeg, 2)
+    for k in range(2):
+        rng = (int(b[k]), int(b[k + 1]))
+        Ys, _, _ = _run(rgnn, g, t, "bf16", dst_range=rng)
+        assert_close(Ys, _ref(g, t, "bf16", rng), "bf16", f"hgt shard {k}")
+
+
+def test_hgt_needs_node_types(rgnn):
+    import torch
+    g = synth.random_graph(40, 200, 3, seed=3, T=2)
+    t = synth.make_hgt_tensors(g.V, g.R, g.T, 32, 32)
+    G = rgnn.Graph(g.V, g.src, g.dst, g.etype, g.R)
+    Ws = [torch.from_numpy(a).cuda() for a in (t.WK, t.WQ, t.WV, t.Wa, t.Wm)]
+    with pytest.raises(rgnn.RgnnError) as ei:
+        rgnn.hgt_forward(G, torch.from_numpy(t.X).cuda(), *Ws, prec="f32")
+    assert ei.value.status == 3
