@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="mag")
-    ap.add_argument("--model", default=None)
+    ap.add_argument("--model", default=None, choices=[None, "rgcn", "rgat", "hgt"])
     ap.add_argument("--prec", default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--slope", type=float, default=0.2)
@@ -82,7 +82,8 @@ def config_json(cfg, model, prec, g, world):
           % (ws / 1e6)) if needs_flush(cfg, prec, g) else (
         "no flush: per-step inputs larger than L2 (X %.0f MB, Z %.0f MB)" % (
             g.V * cfg.K * (2 if prec == "bf16" else 4) / 1e6, g.E * cfg.N * (2 if prec == "bf16" else 4) / 1e6))
-    return {"workload": f"{cfg.name}-shaped heterograph, {model.upper()} layer fwd+bwd, d={cfg.K}",
+    return {"workload": f"{cfg.name}-shaped heterograph, {model.upper()} layer "
+                        f"{'fwd (forward only in this version)' if model == 'hgt' else 'fwd+bwd'}, d={cfg.K}",
             "model": model, "prec": prec, "V": int(g.V), "E": int(g.E), "R": int(g.R), "d_in": cfg.K,
             "d_out": cfg.N, "seeds": "graph 0, X 1, W 2, A 3, dY 4 (synth/)", "l2": l2,
             "parallelism": f"dst-range partition x{world} (NCCL Y gather + dW all-reduce)" if world > 1
@@ -97,6 +98,8 @@ def algorithmic_bytes(phase, model, prec, K, N, E, V_own, J, num_items, U=None):
     b = 2 if prec == "bf16" else 4
     if phase == "gemm_fwd":  # gather X rows, write Z, read src index (+ s_src write for RGAT, + 1/c read for RGCN)
         return (E if U is None else U) * (K * b + N * b + 4 + 4)
+    if phase == "aggregate" and model == "hgt":  # per edge: slot row, kw row (fp32), m row; per row q, Y, lse, item
+        return E * (4 + N * 4 + N * b) + num_items * (N * 4 + N * 4 + 4 + 16)
     if phase == "aggregate":  # read pos, et, Z row (+ s_src) per edge; X_dst, Y, lse, item per row
         per_e = N * b + 8 + (4 if model == "rgat" or U is not None else 0)
         per_v = (K * b + N * 4 + 4 + 16) if model == "rgat" else (N * 4 + 16)
@@ -175,6 +178,14 @@ def oracle_sample(g, t, model, K, N, target_s, slope, prec):
         from parity import bf16_inputs
         tt = bf16_inputs(t)
     X, W, A = (np.ascontiguousarray(a, dtype=np.float64) for a in (tt.X, tt.W, tt.A))
+    hw = None
+    if model == "hgt":
+        h = synth.make_hgt_tensors(g.V, g.R, g.T, K, N)
+        if prec == "bf16":
+            from parity import bf16_round
+            hw = [bf16_round(a).astype(np.float64) for a in (h.WK, h.WQ, h.WV, h.Wa, h.Wm)]
+        else:
+            hw = [a.astype(np.float64) for a in (h.WK, h.WQ, h.WV, h.Wa, h.Wm)]
     W0 = np.ascontiguousarray(tt.W0, dtype=np.float64)
     indeg = np.r_[0, np.cumsum(np.bincount(g.dst, minlength=g.V))]
     a = g.V // 3
@@ -185,7 +196,9 @@ def oracle_sample(g, t, model, K, N, target_s, slope, prec):
         b = max(b, a + 1)
         G[a:b] = t.dY[a:b]
         t0 = time.perf_counter()
-        if model == "rgat":
+        if model == "hgt":
+            oracle.hgt_forward(g.V, g.R, g.src, g.dst, g.etype, g.ntype, X, *hw, rows=np.arange(a, b))
+        elif model == "rgat":
             oracle.rgat_forward(g.V, g.R, g.src, g.dst, g.etype, X, W, A, slope=slope, rows=np.arange(a, b))
             oracle.rgat_backward(g.V, g.R, g.src, g.dst, g.etype, X, W, A, G, slope=slope, v0=a, v1=b)
         else:
@@ -265,7 +278,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     G = m.Graph(g.V, src, dst, et, g.R, dst_begin=v0, dst_end=v1, materialization=args.materialization,
-                build_dx=args.dx, device=dev)
+                build_dx=args.dx, ntype=g.ntype if model == "hgt" else None,
+                num_ntypes=g.T if model == "hgt" else 0, device=dev)
     torch.cuda.synchronize()
     prep_ms = 1e3 * (time.perf_counter() - t0)
     del src, dst, et
@@ -284,7 +298,15 @@ def run_ours(args):
     comm = m.Comm(bounds, rank, world) if world > 1 else None
     stream = torch.cuda.current_stream(dev)
 
-    def step(Xs=X, Ws=W, As=A, dYs=dY):
+    HW = None
+    if model == "hgt":
+        h = synth.make_hgt_tensors(g.V, g.R, g.T, K, N)
+        HW = [torch.from_numpy(a).to(dev) for a in (h.WK, h.WQ, h.WV, h.Wa, h.Wm)]
+
+    def step(Xs=X, Ws=W, As=A, dYs=dY, HWs=None):
+        if model == "hgt":  # forward only (NEXT-3)
+            m.hgt_forward(G, Xs, *(HWs or HW), prec=prec, ws=ws, Y=Y, comm=comm, Y_full=Y_full)
+            return
         if model == "rgat":
             m.rgat_forward(G, Xs, Ws, As, args.slope, prec=prec, ws=ws, Y=Y, comm=comm, Y_full=Y_full)
         else:
@@ -387,8 +409,22 @@ def run_ours(args):
             odX.numel() * 4 if odX is not None else 0)
         n_e2e = max(1, min(args.steps, 5))
 
+        if model == "hgt":
+            hHW = [a.cpu().pin_memory() for a in HW]
+            dHW = [torch.empty_like(a) for a in HW]
+            h2d = hX.numel() * hX.element_size() + sum(a.numel() * 4 for a in hHW)
+            d2h = oY.numel() * 4
+
         def e2e_step():
-            dX_.copy_(hX, non_blocking=True); dW_.copy_(hW, non_blocking=True)
+            dX_.copy_(hX, non_blocking=True)
+            if model == "hgt":
+                for a, b in zip(dHW, hHW):
+                    a.copy_(b, non_blocking=True)
+                step(dX_, HWs=dHW)
+                oY.copy_(Y, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                return
+            dW_.copy_(hW, non_blocking=True)
             dA_.copy_(hA, non_blocking=True); ddY.copy_(hdY, non_blocking=True)
             step(dX_, dW_, dA_, ddY)
             oY.copy_(Y, non_blocking=True); odW.copy_(dW, non_blocking=True)
@@ -451,8 +487,9 @@ def run_ours(args):
                "vs_baseline": None, "dtype": prec, "data": "synthetic (seeded generator, random-init weights)",
                "config": dict(config_json(cfg, model, prec, g, world),
                               launch="CUDA graph of the step" if use_graph else "eager",
-                              backward="dW, dA" + (", dX (NEXT-2)" if args.dx else "") if model == "rgat" else
-                              "dW" + (", dX (NEXT-2)" if args.dx else ""),
+                              backward=("none (HGT forward only)" if model == "hgt" else
+                                        "dW, dA" + (", dX (NEXT-2)" if args.dx else "") if model == "rgat" else
+                                        "dW" + (", dX (NEXT-2)" if args.dx else "")),
                               materialization=("compact" if G.zrows(model) != G.E_own else "vanilla") + (
                                   " (auto)" if args.materialization == "auto" else ""),
                               z_rows=G.zrows(model), compact_rows=int(G.num_compact)),
