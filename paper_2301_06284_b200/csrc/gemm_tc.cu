@@ -38,8 +38,22 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+static rgnn_status make_tmap_2d(CUtensorMapDataType dt, CUtensorMap* map, const void* base, uint64_t cols,
+                                uint64_t rows, uint64_t pitch_bytes, uint32_t box_cols, uint32_t box_rows,
+                                int swizzle_bytes);
 rgnn_status make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch_bytes,
                               uint32_t box_cols, uint32_t box_rows, int swizzle_bytes) {
+  return make_tmap_2d(CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, map, base, cols, rows, pitch_bytes, box_cols, box_rows,
+                      swizzle_bytes);
+}
+rgnn_status make_tmap_2d_f32(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch_bytes,
+                             uint32_t box_cols, uint32_t box_rows, int swizzle_bytes) {
+  return make_tmap_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, map, base, cols, rows, pitch_bytes, box_cols, box_rows,
+                      swizzle_bytes);
+}
+static rgnn_status make_tmap_2d(CUtensorMapDataType dt, CUtensorMap* map, const void* base, uint64_t cols,
+                                uint64_t rows, uint64_t pitch_bytes, uint32_t box_cols, uint32_t box_rows,
+                                int swizzle_bytes) {
   auto fn = encode_fn();
   if (!fn) return set_error(RGNN_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {cols, rows};
@@ -50,7 +64,7 @@ rgnn_status make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t cols,
                           : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                           : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                                 : CU_TENSOR_MAP_SWIZZLE_NONE;
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+  CUresult r = fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(RGNN_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);

@@ -28,6 +28,7 @@ struct WsLayout {
   float2* ad;      // RGAT: (alpha, dpre) per position [E_own]
   float* dpart;    // RGAT: [num_parts, K] split-row partial destination terms
   float* Wt;       // [R, N, K] fp32 W^T (and W0^T after it for RGCN)
+  float* Wr;       // [R, K, N] fp32 W (RNE-rounded on the bf16 path), then W0: the tf32 GEMM's W^T^T
   void* H;         // [J, K] fp32
   void* H0;        // RGCN self loop: [V_own, K] fp32
   float* U0;       // RGAT: [R, K]
@@ -59,6 +60,7 @@ struct HgtWs {
   float *Kf, *Qf, *KWf;   // score path, fp32 on both paths
   void *Vn, *M, *wt;      // message path, T
   float *Xf, *Wr;         // bf16 path: X as fp32, RNE-rounded WK | WQ | Wa
+  float* Wtr;             // tf32 GEMM weights: (rounded) WK^T | WQ^T | Wa^T
   int32_t* gather;
   float* part;
   size_t bytes;
@@ -81,6 +83,7 @@ static HgtWs hgt_ws_layout(const rgnn_graph* g, int K, int N, int prec, void* ba
   w.wt = c.take<char>(prec == RGNN_BF16 ? (size_t)nw * 2 : 1);
   w.Xf = c.take<float>(prec == RGNN_BF16 ? (size_t)V * K : 1);
   w.Wr = c.take<float>(prec == RGNN_BF16 ? (size_t)(2 * T * K * N + (int64_t)g->R * N * N) : 1);
+  w.Wtr = c.take<float>((size_t)(2 * T * K * N + (int64_t)g->R * N * N));
   w.bytes = c.off;
   return w;
 }
@@ -109,6 +112,7 @@ static WsLayout ws_layout(const rgnn_graph* g, int model, int K, int N, int prec
     w.ad = c.take<float2>(model == RGNN_RGAT ? (size_t)E : 1);
     w.dpart = c.take<float>(model == RGNN_RGAT ? (size_t)std::max<int64_t>(g->num_parts, 1) * K : 1);
     w.Wt = c.take<float>((size_t)g->R * N * K + (size_t)N * K);
+    w.Wr = c.take<float>((size_t)g->R * N * K + (size_t)N * K);
     w.H = c.take<char>((size_t)J * K * 4);
     w.H0 = c.take<char>(model == RGNN_RGCN ? (size_t)std::max<int64_t>(g->V_own, 1) * K * 4 : 1);
     w.U0 = c.take<float>((size_t)g->R * K);
@@ -143,6 +147,18 @@ static rgnn_status check_common(const rgnn_graph* g, int K, int N, int prec, con
   if ((uintptr_t)ws % kAlign) return set_error(RGNN_E_INVALID_ARG, "workspace must be 256B aligned");
   if (ws_bytes < need.bytes) return set_error(RGNN_E_WORKSPACE, "workspace %zu < required %zu", ws_bytes, need.bytes);
   return RGNN_OK;
+}
+
+// fp32-output GEMM inside a layer of precision `prec`: on the bf16 layer the tensor cores with
+// fp32 operands (tcgen05 kind::tf32; wt_f32 = W^T [num_w, N, K]) -- exact for the bf16-valued
+// operands, a 10-bit-mantissa truncation of fp32 ones (G, k), well inside the bf16 bound; on the
+// fp32 layer (and without tcgen05) the SIMT fp32 kernel on a.W [num_w, K, N].
+static rgnn_status f32_gemm(int prec, int K, int N, const GemmFwdArgs& a, const float* wt_f32, cudaStream_t s) {
+  if (prec == RGNN_BF16) {
+    rgnn_status st = launch_gemm_fwd_tf32(K, N, a, wt_f32, s);
+    if (st != RGNN_E_UNSUPPORTED) return st;
+  }
+  return launch_gemm_fwd(RGNN_F32, K, N, a, s);
 }
 
 static rgnn_status typed_gemm(int prec, int K, int N, const GemmFwdArgs& a, cudaStream_t s) {
@@ -267,17 +283,23 @@ rgnn_status hgt_forward(const rgnn_graph* g, int K, int N, rgnn_prec prec, const
     RGNN_TRY(launch_round_bf16((int64_t)g->R * N * N, Wa, w.Wr + 2 * T * K * N, s));
     Xs = w.Xf; WKs = w.Wr; WQs = w.Wr + T * K * N; Was = w.Wr + 2 * T * K * N;
   }
+  {
+    Phase ph("hgt_prep", s);
+    RGNN_TRY(launch_transpose_w(prec, (int)T, K, N, WK, w.Wtr, s));
+    RGNN_TRY(launch_transpose_w(prec, (int)T, K, N, WQ, w.Wtr + T * K * N, s));
+    RGNN_TRY(launch_transpose_w(prec, g->R, N, N, Wa, w.Wtr + 2 * T * K * N, s));
+  }
   if (g->num_ntiles) {
     Phase ph("hgt_node_gemm", s);
-    auto node_gemm = [&](int p, const void* Xin, const float* Win, void* out) -> rgnn_status {
+    auto node_gemm = [&](int p, const void* Xin, const float* Win, const float* Wt32, void* out) -> rgnn_status {
       GemmFwdArgs ga{};
       ga.tiles = g->ntiles; ga.num_tiles = g->num_ntiles; ga.X = Xin; ga.gather = g->nperm; ga.W = Win;
       ga.Z = out; ga.wt_bf16 = w.wt; ga.num_w = (int)T; ga.x_rows = g->V; ga.z_rows = g->V;
-      return p == RGNN_F32 ? launch_gemm_fwd(RGNN_F32, K, N, ga, s) : typed_gemm(p, K, N, ga, s);
+      return p == RGNN_F32 ? f32_gemm(prec, K, N, ga, Wt32, s) : typed_gemm(p, K, N, ga, s);
     };
-    RGNN_TRY(node_gemm(RGNN_F32, Xs, WKs, w.Kf));
-    RGNN_TRY(node_gemm(RGNN_F32, Xs, WQs, w.Qf));
-    RGNN_TRY(node_gemm(prec, X, WV, w.Vn));
+    RGNN_TRY(node_gemm(RGNN_F32, Xs, WKs, w.Wtr, w.Kf));
+    RGNN_TRY(node_gemm(RGNN_F32, Xs, WQs, w.Wtr + T * K * N, w.Qf));
+    RGNN_TRY(node_gemm(prec, X, WV, nullptr, w.Vn));
   }
   const bool cm = use_compact(g, RGNN_HGT);
   const int64_t zr = cm ? g->num_compact : g->E_own;
@@ -285,15 +307,15 @@ rgnn_status hgt_forward(const rgnn_graph* g, int K, int N, rgnn_prec prec, const
   {
     Phase ph("hgt_rel_gemm", s);
     RGNN_TRY(launch_map_gather(zr, cm ? g->csrc : g->src_s, g->ninv, w.gather, s));
-    auto rel_gemm = [&](int p, const void* Xin, const float* Win, void* out) -> rgnn_status {
+    auto rel_gemm = [&](int p, const void* Xin, const float* Win, const float* Wt32, void* out) -> rgnn_status {
       GemmFwdArgs ga{};
       ga.tiles = cm ? g->ctiles : g->tiles; ga.num_tiles = nt; ga.X = Xin; ga.gather = w.gather; ga.W = Win;
       ga.Z = out; ga.wt_bf16 = w.wt; ga.num_w = g->R; ga.x_rows = g->V; ga.z_rows = zr;
-      return p == RGNN_F32 ? launch_gemm_fwd(RGNN_F32, N, N, ga, s) : typed_gemm(p, N, N, ga, s);
+      return p == RGNN_F32 ? f32_gemm(prec, N, N, ga, Wt32, s) : typed_gemm(p, N, N, ga, s);
     };
     if (nt) {
-      RGNN_TRY(rel_gemm(RGNN_F32, w.Kf, Was, w.KWf));
-      RGNN_TRY(rel_gemm(prec, w.Vn, Wm, w.M));
+      RGNN_TRY(rel_gemm(RGNN_F32, w.Kf, Was, w.Wtr + 2 * T * K * N, w.KWf));
+      RGNN_TRY(rel_gemm(prec, w.Vn, Wm, nullptr, w.M));
     }
   }
   {
@@ -405,6 +427,16 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     { Phase ph("dx_prep", s);
       RGNN_TRY(launch_transpose_w(prec, g->R, K, N, W, w.Wt, s));
       if (model == RGNN_RGCN && W0) RGNN_TRY(launch_transpose_w(prec, 1, K, N, W0, w.Wt + (size_t)g->R * N * K, s));
+      // the tf32 GEMM reads its weight transposed: (W^T)^T = W, rounded like the SIMT copy
+      if (prec == RGNN_BF16) {
+        RGNN_TRY(launch_round_bf16((int64_t)g->R * K * N, W, w.Wr, s));
+        if (model == RGNN_RGCN && W0) RGNN_TRY(launch_round_bf16((int64_t)K * N, W0, w.Wr + (size_t)g->R * N * K, s));
+      } else {
+        RGNN_CUDA_TRY(cudaMemcpyAsync(w.Wr, W, sizeof(float) * g->R * K * N, cudaMemcpyDeviceToDevice, s));
+        if (model == RGNN_RGCN && W0)
+          RGNN_CUDA_TRY(cudaMemcpyAsync(w.Wr + (size_t)g->R * N * K, W0, sizeof(float) * K * N,
+                                        cudaMemcpyDeviceToDevice, s));
+      }
       if (model == RGNN_RGAT) {
         RGNN_TRY(launch_fold_u(prec, g->R, K, N, W, A, w.U0, s, 0));
       }
@@ -415,7 +447,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
       GemmFwdArgs gh{};
       gh.tiles = g->rtiles; gh.num_tiles = g->num_rtiles; gh.X = dY; gh.gather = g->run_dst; gh.W = w.Wt;
       gh.Z = w.H; gh.wt_bf16 = w.wt; gh.num_w = g->R; gh.x_rows = std::max<int64_t>(g->V_own, 1); gh.z_rows = J;
-      RGNN_TRY(launch_gemm_fwd(RGNN_F32, N, K, gh, s));  // GEMM K = d_out, N = d_in
+      RGNN_TRY(f32_gemm(prec, N, K, gh, w.Wr, s));  // GEMM K = d_out, N = d_in
     }
     const bool self = model == RGNN_RGCN && W0 && g->V_own > 0;
     if (self) {
@@ -423,7 +455,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
       GemmFwdArgs g0{};
       g0.rows = g->V_own; g0.X = dY; g0.gofs = 0; g0.W = w.Wt + (size_t)g->R * N * K; g0.Z = w.H0;
       g0.wt_bf16 = w.wt; g0.num_w = 1; g0.x_rows = g->V_own;
-      RGNN_TRY(launch_gemm_fwd(RGNN_F32, N, K, g0, s));
+      RGNN_TRY(f32_gemm(prec, N, K, g0, w.Wr + (size_t)g->R * N * K, s));
     }
     { Phase ph("dx_zero", s); RGNN_CUDA_TRY(cudaMemsetAsync(dX, 0, sizeof(float) * (size_t)g->V * K, s)); }
     DxArgs xa{};
