@@ -58,6 +58,9 @@ def _load():
         _lib.oracle_hgt_forward.argtypes = [i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                             i64, vp, vp, vp]
         _lib.oracle_hgt_forward.restype = None
+        _lib.oracle_hgt_backward.argtypes = [i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                             vp, i64, i64, vp, vp, vp, vp, vp]
+        _lib.oracle_hgt_backward.restype = None
         _lib.oracle_rgcn_backward.argtypes = [i64, i64, i32, i32, i32, vp, vp, vp, vp, i32, vp, vp, i64, i64, vp,
                                               vp, vp]
         _lib.oracle_num_threads.restype = C.c_int
@@ -214,6 +217,19 @@ def hgt_forward(V: int, R: int, src, dst, et, ntype, X, WK, WQ, WV, Wa, Wm, rows
     lib.oracle_hgt_forward(V, src.shape[0], R, T, K, N, _p(src), _p(dst), _p(et), _p(nt), _p(X), _p(WK), _p(WQ),
                            _p(WV), _p(Wa), _p(Wm), rr.shape[0], _p(rr), _p(Y), _p(lse))
     return Y, lse
+
+
+def hgt_backward(V: int, R: int, src, dst, et, ntype, X, WK, WQ, WV, Wa, Wm, G, v0: int = 0, v1=None):
+    """(dWK, dWQ, dWV, dWa, dWm) of the HGT layer's L = <Y, G> restricted to dst in [v0, v1), fp64."""
+    lib = _load()
+    src, dst, et, nt = _i32(src), _i32(dst), _i32(et), _i32(ntype)
+    X, WK, WQ, WV, Wa, Wm, G = (_f64(a) for a in (X, WK, WQ, WV, Wa, Wm, G))
+    T, K, N = WK.shape
+    v1 = V if v1 is None else v1
+    outs = [np.empty((T, K, N)), np.empty((T, K, N)), np.empty((T, K, N)), np.empty((R, N, N)), np.empty((R, N, N))]
+    lib.oracle_hgt_backward(V, src.shape[0], R, T, K, N, _p(src), _p(dst), _p(et), _p(nt), _p(X), _p(WK), _p(WQ),
+                            _p(WV), _p(Wa), _p(Wm), _p(G), v0, v1, *[_p(o) for o in outs])
+    return tuple(outs)
 
 
 def rgat_dx(V: int, R: int, src, dst, et, X, W, A, G, slope: float = 0.2, v0: int = 0, v1=None) -> np.ndarray:

@@ -613,4 +613,114 @@ void oracle_hgt_forward(int64_t V, int64_t E, int32_t R, int32_t T, int32_t K, i
   free(in_eid);
 }
 
+/* HGT backward (NEXT-3): gradients of L = <Y, G> restricted to dst in [v0, v1) w.r.t.
+ * WK, WQ, WV [T, K, N] and Wa, Wm [R, N, N], by the chain rule of oracle_hgt_forward:
+ *   dm_e = alpha_e G_t,  dalpha_e = G_t . m_e,  S_t = sum_e alpha_e dalpha_e,
+ *   da_e = alpha_e (dalpha_e - S_t),
+ *   dWm[r] += v_e^T dm_e,  dv_e = dm_e Wm[r]^T,  dWV[tau(s)] += x_s^T dv_e
+ *   dkw_e = da_e q_t,  dWa[r] += k_e^T dkw_e,  dk_e = dkw_e Wa[r]^T,  dWK[tau(s)] += x_s^T dk_e
+ *   dq_t = sum_e da_e kw_e,  dWQ[tau(t)] += x_t^T dq_t
+ * Thread partials summed in thread order.                                      */
+void oracle_hgt_backward(int64_t V, int64_t E, int32_t R, int32_t T, int32_t K, int32_t N, const int32_t* src,
+                         const int32_t* dst, const int32_t* et, const int32_t* ntype, const double* X,
+                         const double* WK, const double* WQ, const double* WV, const double* Wa, const double* Wm,
+                         const double* G, int64_t v0, int64_t v1, double* dWK, double* dWQ, double* dWV, double* dWa,
+                         double* dWm) {
+  int64_t* in_ptr;
+  int32_t* in_eid;
+  build_in_lists(V, E, dst, &in_ptr, &in_eid);
+  int nt = omp_get_max_threads();
+  size_t tsz = (size_t)T * K * N, rsz = (size_t)R * N * N, tot = 3 * tsz + 2 * rsz;
+  double* part = (double*)calloc((size_t)nt * tot + 1, sizeof(double));
+#pragma omp parallel
+  {
+    double* my = part + (size_t)omp_get_thread_num() * tot;
+    double *mWK = my, *mWQ = my + tsz, *mWV = my + 2 * tsz, *mWa = my + 3 * tsz, *mWm = my + 3 * tsz + rsz;
+    double* q = (double*)malloc(sizeof(double) * (size_t)N);
+    double* k = (double*)malloc(sizeof(double) * (size_t)N);
+    double* kw = (double*)malloc(sizeof(double) * (size_t)N);
+    double* vv = (double*)malloc(sizeof(double) * (size_t)N);
+    double* mm = (double*)malloc(sizeof(double) * (size_t)N);
+    double* dq = (double*)malloc(sizeof(double) * (size_t)N);
+    double* d1 = (double*)malloc(sizeof(double) * (size_t)N);
+    double* d2 = (double*)malloc(sizeof(double) * (size_t)N);
+    int64_t cap = 0;
+    double *a = NULL, *al = NULL, *da = NULL;
+#pragma omp for schedule(dynamic, 16)
+    for (int64_t t = v0; t < v1; ++t) {
+      int64_t lo = in_ptr[t], hi = in_ptr[t + 1], deg = hi - lo;
+      if (deg == 0) continue;
+      if (deg > cap) {
+        cap = deg;
+        a = (double*)realloc(a, sizeof(double) * (size_t)cap);
+        al = (double*)realloc(al, sizeof(double) * (size_t)cap);
+        da = (double*)realloc(da, sizeof(double) * (size_t)cap);
+      }
+      const double* Gt = G + (size_t)t * N;
+      const double* xt = X + (size_t)t * K;
+      vecmat(K, N, xt, WQ + (size_t)ntype[t] * K * N, q);
+      double m = -INFINITY;
+      for (int64_t e_ = lo; e_ < hi; ++e_) {
+        int32_t e = in_eid[e_], r = et[e], u = src[e];
+        vecmat(K, N, X + (size_t)u * K, WK + (size_t)ntype[u] * K * N, k);
+        vecmat(N, N, k, Wa + (size_t)r * N * N, kw);
+        a[e_ - lo] = dot(N, kw, q);
+        if (a[e_ - lo] > m) m = a[e_ - lo];
+        vecmat(K, N, X + (size_t)u * K, WV + (size_t)ntype[u] * K * N, vv);
+        vecmat(N, N, vv, Wm + (size_t)r * N * N, mm);
+        da[e_ - lo] = dot(N, Gt, mm); /* dalpha_e */
+      }
+      double l = 0.0;
+      for (int64_t e_ = lo; e_ < hi; ++e_) { al[e_ - lo] = exp(a[e_ - lo] - m); l += al[e_ - lo]; }
+      double S = 0.0;
+      for (int64_t e_ = lo; e_ < hi; ++e_) { al[e_ - lo] /= l; S += al[e_ - lo] * da[e_ - lo]; }
+      for (int n = 0; n < N; ++n) dq[n] = 0.0;
+      for (int64_t e_ = lo; e_ < hi; ++e_) {
+        int32_t e = in_eid[e_], r = et[e], u = src[e];
+        const double* xu = X + (size_t)u * K;
+        double aa = al[e_ - lo], dae = aa * (da[e_ - lo] - S);
+        vecmat(K, N, xu, WK + (size_t)ntype[u] * K * N, k);
+        vecmat(N, N, k, Wa + (size_t)r * N * N, kw);
+        vecmat(K, N, xu, WV + (size_t)ntype[u] * K * N, vv);
+        /* message path: dm = alpha G; dWm[r] += v^T dm; dv = dm Wm^T; dWV[tau(u)] += x_u^T dv */
+        double* gWm = mWm + (size_t)r * N * N;
+        for (int i = 0; i < N; ++i)
+          for (int j = 0; j < N; ++j) gWm[(size_t)i * N + j] += vv[i] * aa * Gt[j];
+        for (int i = 0; i < N; ++i) d1[i] = 0.0;
+        for (int j = 0; j < N; ++j) d2[j] = aa * Gt[j];
+        matvec_t(N, N, Wm + (size_t)r * N * N, d2, d1);
+        double* gWV = mWV + (size_t)ntype[u] * K * N;
+        for (int i = 0; i < K; ++i)
+          for (int j = 0; j < N; ++j) gWV[(size_t)i * N + j] += xu[i] * d1[j];
+        /* score path: dkw = da q; dWa[r] += k^T dkw; dk = dkw Wa^T; dWK[tau(u)] += x_u^T dk; dq += da kw */
+        double* gWa = mWa + (size_t)r * N * N;
+        for (int i = 0; i < N; ++i)
+          for (int j = 0; j < N; ++j) gWa[(size_t)i * N + j] += k[i] * dae * q[j];
+        for (int i = 0; i < N; ++i) d1[i] = 0.0;
+        for (int j = 0; j < N; ++j) d2[j] = dae * q[j];
+        matvec_t(N, N, Wa + (size_t)r * N * N, d2, d1);
+        double* gWK = mWK + (size_t)ntype[u] * K * N;
+        for (int i = 0; i < K; ++i)
+          for (int j = 0; j < N; ++j) gWK[(size_t)i * N + j] += xu[i] * d1[j];
+        for (int n = 0; n < N; ++n) dq[n] += dae * kw[n];
+      }
+      double* gWQ = mWQ + (size_t)ntype[t] * K * N;
+      for (int i = 0; i < K; ++i)
+        for (int j = 0; j < N; ++j) gWQ[(size_t)i * N + j] += xt[i] * dq[j];
+    }
+    free(q); free(k); free(kw); free(vv); free(mm); free(dq); free(d1); free(d2); free(a); free(al); free(da);
+  }
+  double* outs[5] = {dWK, dWQ, dWV, dWa, dWm};
+  size_t offs[5] = {0, tsz, 2 * tsz, 3 * tsz, 3 * tsz + rsz};
+  size_t lens[5] = {tsz, tsz, tsz, rsz, rsz};
+  for (int o = 0; o < 5; ++o) {
+    memset(outs[o], 0, sizeof(double) * lens[o]);
+    for (int th = 0; th < nt; ++th)
+      for (size_t i = 0; i < lens[o]; ++i) outs[o][i] += part[(size_t)th * tot + offs[o] + i];
+  }
+  free(part);
+  free(in_ptr);
+  free(in_eid);
+}
+
 int oracle_num_threads(void) { return omp_get_max_threads(); }

@@ -535,3 +535,41 @@ def test_hgt_softmax_weights_sum_to_one():
     Y, _ = oracle.hgt_forward(V, R, g.src, g.dst, g.etype, g.ntype, X, t.WK * 5, t.WQ * 5, WV, t.Wa, Wm)
     deg = np.bincount(g.dst, minlength=V)
     np.testing.assert_allclose(Y[deg > 0], 1.0, atol=1e-12)
+
+
+def test_hgt_backward_vs_torch_autograd():
+    torch = pytest.importorskip("torch")
+    V, E, R, T, K, N = 12, 60, 3, 2, 5, 4
+    g = synth.random_graph(V, E, R, seed=54, T=T)
+    t = synth.make_hgt_tensors(V, R, T, K, N)
+    X = torch.tensor(t.X, dtype=torch.float64)
+    Ws = [torch.tensor(a, dtype=torch.float64, requires_grad=True) for a in (t.WK, t.WQ, t.WV, t.Wa, t.Wm)]
+    G = torch.tensor(t.dY[:, :N], dtype=torch.float64)
+    (_torch_hgt(V, g.src, g.dst, g.etype, g.ntype, X, *Ws) * G).sum().backward()
+    got = oracle.hgt_backward(V, R, g.src, g.dst, g.etype, g.ntype, t.X, t.WK, t.WQ, t.WV, t.Wa, t.Wm, G.numpy())
+    for name, a, w in zip(["dWK", "dWQ", "dWV", "dWa", "dWm"], got, Ws):
+        np.testing.assert_allclose(a, w.grad.numpy(), rtol=1e-11, atol=1e-13, err_msg=name)
+
+
+def test_hgt_backward_fd_and_shards():
+    V, E, R, T, K, N = 8, 30, 2, 2, 3, 3
+    g = synth.random_graph(V, E, R, seed=55, T=T)
+    t = synth.make_hgt_tensors(V, R, T, K, N)
+    Wl = [a.astype(float) for a in (t.WK, t.WQ, t.WV, t.Wa, t.Wm)]
+    G = t.dY[:, :N].astype(float)
+
+    def L(ws):
+        Y, _ = oracle.hgt_forward(V, R, g.src, g.dst, g.etype, g.ntype, t.X, *ws)
+        return float((Y * G).sum())
+
+    got = oracle.hgt_backward(V, R, g.src, g.dst, g.etype, g.ntype, t.X, *Wl, G)
+    rng = np.random.default_rng(2)
+    for wi in range(5):
+        for _ in range(3):
+            idx = tuple(rng.integers(0, s) for s in Wl[wi].shape)
+            n = _fd(lambda w: L(Wl[:wi] + [w] + Wl[wi + 1:]), Wl[wi], idx)
+            assert abs(got[wi][idx] - n) / max(abs(got[wi][idx]), abs(n), 1e-8) < 1e-4, (wi, idx)
+    parts = [oracle.hgt_backward(V, R, g.src, g.dst, g.etype, g.ntype, t.X, *Wl, G, v0=a, v1=b)
+             for a, b in [(0, 3), (3, 8)]]
+    for wi in range(5):
+        np.testing.assert_allclose(parts[0][wi] + parts[1][wi], got[wi], rtol=1e-12, atol=1e-13)
