@@ -83,7 +83,7 @@ def config_json(cfg, model, prec, g, world):
         "no flush: per-step inputs larger than L2 (X %.0f MB, Z %.0f MB)" % (
             g.V * cfg.K * (2 if prec == "bf16" else 4) / 1e6, g.E * cfg.N * (2 if prec == "bf16" else 4) / 1e6))
     return {"workload": f"{cfg.name}-shaped heterograph, {model.upper()} layer "
-                        f"{'fwd (forward only in this version)' if model == 'hgt' else 'fwd+bwd'}, d={cfg.K}",
+                        f"fwd+bwd, d={cfg.K}",
             "model": model, "prec": prec, "V": int(g.V), "E": int(g.E), "R": int(g.R), "d_in": cfg.K,
             "d_out": cfg.N, "seeds": "graph 0, X 1, W 2, A 3, dY 4 (synth/)", "l2": l2,
             "parallelism": f"dst-range partition x{world} (NCCL Y gather + dW all-reduce)" if world > 1
@@ -100,6 +100,8 @@ def algorithmic_bytes(phase, model, prec, K, N, E, V_own, J, num_items, U=None):
         return (E if U is None else U) * (K * b + N * b + 4 + 4)
     if phase == "aggregate" and model == "hgt":  # per edge: slot row, kw row (fp32), m row; per row q, Y, lse, item
         return E * (4 + N * 4 + N * b) + num_items * (N * 4 + N * 4 + 4 + 16)
+    if phase == "hgt_bwd_walk":  # per edge: slot pos (+ row), kw row (fp32), m row, alpha/da writes; per row q, G, Y, dq
+        return E * (4 + (4 if U is not None else 0) + N * 4 + N * b + 8) + num_items * (4 * N * 4 + 4 + 16)
     if phase == "aggregate":  # read pos, et, Z row (+ s_src) per edge; X_dst, Y, lse, item per row
         per_e = N * b + 8 + (4 if model == "rgat" or U is not None else 0)
         per_v = (K * b + N * 4 + 4 + 16) if model == "rgat" else (N * 4 + 16)
@@ -198,6 +200,7 @@ def oracle_sample(g, t, model, K, N, target_s, slope, prec):
         t0 = time.perf_counter()
         if model == "hgt":
             oracle.hgt_forward(g.V, g.R, g.src, g.dst, g.etype, g.ntype, X, *hw, rows=np.arange(a, b))
+            oracle.hgt_backward(g.V, g.R, g.src, g.dst, g.etype, g.ntype, X, *hw, G, v0=a, v1=b)
         elif model == "rgat":
             oracle.rgat_forward(g.V, g.R, g.src, g.dst, g.etype, X, W, A, slope=slope, rows=np.arange(a, b))
             oracle.rgat_backward(g.V, g.R, g.src, g.dst, g.etype, X, W, A, G, slope=slope, v0=a, v1=b)
@@ -278,7 +281,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     G = m.Graph(g.V, src, dst, et, g.R, dst_begin=v0, dst_end=v1, materialization=args.materialization,
-                build_dx=args.dx, ntype=g.ntype if model == "hgt" else None,
+                build_dx=args.dx or model == "hgt", ntype=g.ntype if model == "hgt" else None,
                 num_ntypes=g.T if model == "hgt" else 0, device=dev)
     torch.cuda.synchronize()
     prep_ms = 1e3 * (time.perf_counter() - t0)
@@ -299,13 +302,18 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
 
     HW = None
+    hgrads = None
     if model == "hgt":
         h = synth.make_hgt_tensors(g.V, g.R, g.T, K, N)
         HW = [torch.from_numpy(a).to(dev) for a in (h.WK, h.WQ, h.WV, h.Wa, h.Wm)]
+        dY = torch.from_numpy(np.ascontiguousarray(h.dY[v0:v1])).to(dev)
 
     def step(Xs=X, Ws=W, As=A, dYs=dY, HWs=None):
-        if model == "hgt":  # forward only (NEXT-3)
-            m.hgt_forward(G, Xs, *(HWs or HW), prec=prec, ws=ws, Y=Y, comm=comm, Y_full=Y_full)
+        nonlocal hgrads
+        if model == "hgt":  # forward + backward (dWK, dWQ, dWV, dWa, dWm)
+            hw = HWs or HW
+            m.hgt_forward(G, Xs, *hw, prec=prec, ws=ws, Y=Y, comm=comm, Y_full=Y_full)
+            hgrads = m.hgt_backward(G, Xs, *hw, Y, dYs, ws, prec=prec, comm=comm)
             return
         if model == "rgat":
             m.rgat_forward(G, Xs, Ws, As, args.slope, prec=prec, ws=ws, Y=Y, comm=comm, Y_full=Y_full)
@@ -412,16 +420,21 @@ def run_ours(args):
         if model == "hgt":
             hHW = [a.cpu().pin_memory() for a in HW]
             dHW = [torch.empty_like(a) for a in HW]
-            h2d = hX.numel() * hX.element_size() + sum(a.numel() * 4 for a in hHW)
-            d2h = oY.numel() * 4
+            hdY = dY.cpu().pin_memory()
+            ohg = [torch.empty(a.shape, dtype=torch.float32).pin_memory() for a in HW]
+            h2d = hX.numel() * hX.element_size() + sum(a.numel() * 4 for a in hHW) + hdY.numel() * 4
+            d2h = oY.numel() * 4 + sum(a.numel() * 4 for a in ohg)
 
         def e2e_step():
             dX_.copy_(hX, non_blocking=True)
             if model == "hgt":
                 for a, b in zip(dHW, hHW):
                     a.copy_(b, non_blocking=True)
-                step(dX_, HWs=dHW)
+                ddY.copy_(hdY, non_blocking=True)
+                step(dX_, dYs=ddY, HWs=dHW)
                 oY.copy_(Y, non_blocking=True)
+                for o, gr in zip(ohg, hgrads):
+                    o.copy_(gr, non_blocking=True)
                 torch.cuda.current_stream().synchronize()
                 return
             dW_.copy_(hW, non_blocking=True)
@@ -453,7 +466,7 @@ def run_ours(args):
     v = G.view
     step_phase = {k: (tot / args.steps, n // max(args.steps, 1)) for k, (tot, n) in phases.items()}
     cand = {k: x for k, x in step_phase.items()
-            if k in ("gemm_fwd", "aggregate", "bwd_traverse", "gemm_dw", "bwd_fused")}
+            if k in ("gemm_fwd", "aggregate", "bwd_traverse", "gemm_dw", "bwd_fused", "hgt_bwd_walk")}
     roof = None
     if cand:
         dom = max(cand, key=lambda k: cand[k][0])
@@ -487,7 +500,7 @@ def run_ours(args):
                "vs_baseline": None, "dtype": prec, "data": "synthetic (seeded generator, random-init weights)",
                "config": dict(config_json(cfg, model, prec, g, world),
                               launch="CUDA graph of the step" if use_graph else "eager",
-                              backward=("none (HGT forward only)" if model == "hgt" else
+                              backward=("dWK, dWQ, dWV, dWa, dWm" if model == "hgt" else
                                         "dW, dA" + (", dX (NEXT-2)" if args.dx else "") if model == "rgat" else
                                         "dW" + (", dX (NEXT-2)" if args.dx else "")),
                               materialization=("compact" if G.zrows(model) != G.E_own else "vanilla") + (

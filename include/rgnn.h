@@ -188,11 +188,30 @@ rgnn_status rgat_forward(const rgnn_graph* g, int d_in, int d_out, rgnn_prec pre
  *   rgat_forward.  The graph must carry node types (desc.ntype, num_ntypes
  *   = T; else RGNN_E_UNSUPPORTED).  k W_{a,r} and v W_{m,r} are formed once
  *   per (etype, src) pair when the graph has compact rows (rgnn_zrows with
- *   RGNN_HGT), else once per edge.  saved receives lse [V_own].  Forward
- *   only in this version (rgnn_backward returns RGNN_E_UNSUPPORTED for HGT). */
+ *   RGNN_HGT), else once per edge.  saved (rgnn_workspace_bytes with
+ *   RGNN_HGT) receives lse [V_own] and the typed-linear outputs k, q, v,
+ *   k W_{a,r}, v W_{m,r} that hgt_backward reads.                          */
 rgnn_status hgt_forward(const rgnn_graph* g, int d_in, int d_out, rgnn_prec prec, const void* X, const float* WK,
                         const float* WQ, const float* WV, const float* Wa, const float* Wm, float* Y, void* saved,
                         void* ws, size_t ws_bytes, rgnn_comm* comm, float* Y_full, void* stream);
+
+/* HGT backward (NEXT-3): gradients of L = <Y, dY> over the owned rows w.r.t.
+ * the five weights, by the chain rule of hgt_forward (DESIGN.md Sec. 6 "HGT"):
+ *   da_e = alpha_e (dY_t . m_e - dY_t . Y_t);  dWm[r] = sum_e v_s^T alpha_e dY_t;
+ *   dWa[r] = sum_e k_s^T da_e q_t;  dq_t = sum_e da_e k_s W_{a,r};
+ *   dv_s = sum_{e: src=s} alpha_e dY_t Wm_r^T;  dk_s = sum_e da_e q_t Wa_r^T;
+ *   dWK / dWV / dWQ [tau] = sum over the nodes of type tau of x^T dk / dv / dq.
+ *   dWK, dWQ, dWV [T, d_in, d_out], dWa, dWm [R, d_out, d_out] fp32, overwritten.
+ * Y [V_own, d_out] and saved are the forward's; dY [V_own, d_out] fp32.  The
+ * graph needs node types and RGNN_GRAPH_DX (source-major tables; else
+ * RGNN_E_UNSUPPORTED); the workspace is sized with training = 1 (else
+ * RGNN_E_WORKSPACE).  With comm != NULL the gradients are all-reduced (sum)
+ * in place.  WK, WQ, WV are not read (their gradients need only X and the
+ * saved activations) and may be NULL.                                      */
+rgnn_status hgt_backward(const rgnn_graph* g, int d_in, int d_out, rgnn_prec prec, const void* X, const float* WK,
+                         const float* WQ, const float* WV, const float* Wa, const float* Wm, const float* Y,
+                         const float* dY, const void* saved, float* dWK, float* dWQ, float* dWV, float* dWa,
+                         float* dWm, void* ws, size_t ws_bytes, rgnn_comm* comm, void* stream);
 
 /* Backward of L = <Y, dY> over the owned rows (Sec. 3.5; reading O17):
  *   dW [R, d_in, d_out] fp32 (required), dA [R, 2, d_out] (RGAT, required),

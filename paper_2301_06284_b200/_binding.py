@@ -68,6 +68,7 @@ _SIGS = {
     "rgnn_partition_dst": [_i64, C.POINTER(_i64), C.c_int, C.POINTER(_i64)],
     "rgnn_zrows": [_vp, C.c_int, C.POINTER(_i64)],
     "hgt_forward": [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp, _vp],
+    "hgt_backward": [_vp, C.c_int, C.c_int, C.c_int] + [_vp] * 14 + [_vp, _sz, _vp, _vp],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(lib, _name)

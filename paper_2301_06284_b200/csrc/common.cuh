@@ -105,6 +105,9 @@ struct rgnn_graph {
   int32_t *nperm, *ninv;
   rgnn::Tile* ntiles;
   int64_t num_ntiles;
+  rgnn::Tile* nchunks;   // dW split-K chunks over the node-type segments (HGT backward)
+  int32_t* nchunk_seg;   // [T+1]
+  int64_t num_nchunks;
   bool has_compact;  // compact tables built (COMPACT or AUTO)
   int mat_mode;      // rgnn_materialization requested
   int64_t num_compact, num_ctiles;
@@ -184,6 +187,38 @@ __device__ __forceinline__ float group_sum(float v) {
 #pragma unroll
   for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// Sum of a split row's parts in a fixed order: one block per split row; warp w
+// sums parts w, w+8, ... then warp 0 adds the 8 warp sums in warp order.
+template <int K>
+__device__ __forceinline__ void merge_parts(const float* __restrict__ part, int32_t part0, int32_t nparts, float* out,
+                                            bool add) {
+  constexpr int KL = K / 32;
+  __shared__ float red[8][K];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  float acc[KL];
+#pragma unroll
+  for (int i = 0; i < KL; ++i) acc[i] = 0.f;
+  for (int32_t t = wp; t < nparts; t += 8) {
+    const float* pr = part + (size_t)(part0 + t) * K + lane;
+#pragma unroll
+    for (int i = 0; i < KL; ++i) acc[i] += pr[32 * i];
+  }
+#pragma unroll
+  for (int i = 0; i < KL; ++i) red[wp][lane + 32 * i] = acc[i];
+  __syncthreads();
+  if (wp == 0) {
+#pragma unroll
+    for (int i = 0; i < KL; ++i) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) s += red[w][lane + 32 * i];
+      if (add) out[lane + 32 * i] += s;
+      else out[lane + 32 * i] = s;
+    }
+  }
+  __syncthreads();
 }
 
 }  // namespace rgnn

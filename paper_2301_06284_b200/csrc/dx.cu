@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(256) k_dx_walk(DxArgs a) {
         d = ad.y;
         r = a.srel[q];
       } else {
-        c = a.sinvc[q];
+        c = a.wpos ? a.wpos[a.spos[q]] : a.sinvc[q];
       }
       const float4 h = __ldg(reinterpret_cast<const float4*>(H + (size_t)j * K + l * EPL));
       acc[0] = fmaf(c, h.x, acc[0]); acc[1] = fmaf(c, h.y, acc[1]);
@@ -79,38 +79,6 @@ __global__ void __launch_bounds__(256) k_dx_walk(DxArgs a) {
                                       __float_as_uint(acc[3])));
     }
   }
-}
-
-// Sum of a split row's parts in a fixed order: one block per split row; warp w
-// sums parts w, w+8, ... then warp 0 adds the 8 warp sums in warp order.
-template <int K>
-__device__ __forceinline__ void merge_parts(const float* __restrict__ part, int32_t part0, int32_t nparts, float* out,
-                                            bool add) {
-  constexpr int KL = K / 32;
-  __shared__ float red[8][K];
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  float acc[KL];
-#pragma unroll
-  for (int i = 0; i < KL; ++i) acc[i] = 0.f;
-  for (int32_t t = wp; t < nparts; t += 8) {
-    const float* pr = part + (size_t)(part0 + t) * K + lane;
-#pragma unroll
-    for (int i = 0; i < KL; ++i) acc[i] += pr[32 * i];
-  }
-#pragma unroll
-  for (int i = 0; i < KL; ++i) red[wp][lane + 32 * i] = acc[i];
-  __syncthreads();
-  if (wp == 0) {
-#pragma unroll
-    for (int i = 0; i < KL; ++i) {
-      float s = 0.f;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) s += red[w][lane + 32 * i];
-      if (add) out[lane + 32 * i] += s;
-      else out[lane + 32 * i] = s;
-    }
-  }
-  __syncthreads();
 }
 
 template <int K>

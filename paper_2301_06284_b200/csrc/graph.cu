@@ -314,7 +314,8 @@ struct GraphLayout {
   Item* sitems;
   SplitRow* ssplit;
   int32_t *nperm, *ninv, *nseg;
-  Tile* ntiles;
+  Tile *ntiles, *nchunks;
+  int32_t* nchunk_seg;
   size_t dev_bytes;
   // scratch
   Counters* ctr;
@@ -375,6 +376,8 @@ static GraphLayout layout(const rgnn_graph_desc* d, void* dev, void* scr) {
   L.ninv = c.take<int32_t>(Vn);
   L.nseg = c.take<int32_t>(nt ? d->num_ntypes + 1 : 1);
   L.ntiles = c.take<Tile>(nt ? Vn / kTileRows + d->num_ntypes + 1 : 1);
+  L.nchunks = c.take<Tile>(nt ? Vn / kTileRows + d->num_ntypes + 1 : 1);  // chunks >= 128 rows: <= #ntiles
+  L.nchunk_seg = c.take<int32_t>(nt ? d->num_ntypes + 1 : 1);
   L.dev_bytes = c.off;
   Carver s(scr);
   L.ctr = s.take<Counters>(1);
@@ -627,6 +630,23 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
       ntiles.push_back(Tile{t, (int32_t)a, (int32_t)std::min<int64_t>(a + kTileRows, nseg_h[t + 1]), 0});
   if (!ntiles.empty())
     RGNN_CUDA_TRY(cudaMemcpyAsync(L.ntiles, ntiles.data(), sizeof(Tile) * ntiles.size(), cudaMemcpyHostToDevice, s));
+  // dW split-K chunks over the node-type segments (HGT backward: dWK / dWQ / dWV), never straddling types
+  std::vector<Tile> nchunks;
+  std::vector<int32_t> nchunk_seg(nseg_h.empty() ? 0 : nseg_h.size(), 0);
+  if (!nseg_h.empty()) {
+    const int64_t ncr =
+        std::max<int64_t>(kTileRows, ((V / (2 * sms) + 1) + kTileRows - 1) / kTileRows * kTileRows);
+    for (int32_t t = 0; t + 1 < (int32_t)nseg_h.size(); ++t) {
+      nchunk_seg[t] = (int32_t)nchunks.size();
+      for (int64_t a = nseg_h[t]; a < nseg_h[t + 1]; a += ncr)
+        nchunks.push_back(Tile{t, (int32_t)a, (int32_t)std::min<int64_t>(a + ncr, nseg_h[t + 1]), 0});
+    }
+    nchunk_seg.back() = (int32_t)nchunks.size();
+    if (!nchunks.empty())
+      RGNN_CUDA_TRY(cudaMemcpyAsync(L.nchunks, nchunks.data(), sizeof(Tile) * nchunks.size(), cudaMemcpyHostToDevice, s));
+    RGNN_CUDA_TRY(cudaMemcpyAsync(L.nchunk_seg, nchunk_seg.data(), sizeof(int32_t) * nchunk_seg.size(),
+                                  cudaMemcpyHostToDevice, s));
+  }
   std::vector<Tile> rtiles;  // 128-run GEMM tiles per relation (dX: H = G_v W_r^T per run)
   if (dx)
     for (int32_t r = 0; r < R; ++r)
@@ -663,6 +683,7 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   g->num_sparts = h.num_sparts;
   g->has_ntype = d->ntype != nullptr && V > 0; g->num_ntypes = d->ntype ? d->num_ntypes : 0;
   g->nperm = L.nperm; g->ninv = L.ninv; g->ntiles = L.ntiles; g->num_ntiles = (int64_t)ntiles.size();
+  g->nchunks = L.nchunks; g->nchunk_seg = L.nchunk_seg; g->num_nchunks = (int64_t)nchunks.size();
   g->seg_host = seg_h;
   g->chunk_seg_host = chunk_seg;
   RGNN_CUDA_TRY(cudaGetDevice(&g->device));

@@ -16,9 +16,9 @@ namespace rgnn {
 
 // out[i] = ninv[idx[i]] : GEMM gather rows of the node-typed features (type-sorted rows)
 __global__ void k_map_gather(int64_t n, const int32_t* __restrict__ idx, const int32_t* __restrict__ ninv,
-                             int32_t* __restrict__ out) {
+                             int32_t* __restrict__ out, int64_t ofs) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = ninv[idx[i]];
+    out[i] = ninv[idx[i] + ofs];
 }
 
 // fp32 copies for the score path of the bf16 layer: X values (exact) and RNE-rounded weights
@@ -42,9 +42,22 @@ rgnn_status launch_round_bf16(int64_t n, const float* a, float* b, cudaStream_t 
   return RGNN_OK;
 }
 
-rgnn_status launch_map_gather(int64_t n, const int32_t* idx, const int32_t* ninv, int32_t* out, cudaStream_t s) {
+rgnn_status launch_map_gather(int64_t n, const int32_t* idx, const int32_t* ninv, int32_t* out, cudaStream_t s,
+                              int64_t ofs) {
   if (n == 0) return RGNN_OK;
-  RGNN_LAUNCH(k_map_gather, (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, s, n, idx, ninv, out);
+  RGNN_LAUNCH(k_map_gather, (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, s, n, idx, ninv, out,
+              ofs);
+  return RGNN_OK;
+}
+
+__global__ void k_f32_to_bf16(int64_t n, const float* __restrict__ a, __nv_bfloat16* __restrict__ b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = __float2bfloat16_rn(a[i]);
+}
+rgnn_status launch_f32_to_bf16(int64_t n, const float* a, void* b, cudaStream_t s) {
+  if (n == 0) return RGNN_OK;
+  RGNN_LAUNCH(k_f32_to_bf16, (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, s, n, a,
+              static_cast<__nv_bfloat16*>(b));
   return RGNN_OK;
 }
 
@@ -183,6 +196,124 @@ rgnn_status launch_aggregate_hgt(int prec, int N, const HgtAggArgs& a, cudaStrea
     case 32: return bf ? hgt_walk<__nv_bfloat16, 32>(a, s) : hgt_walk<float, 32>(a, s);
     case 64: return bf ? hgt_walk<__nv_bfloat16, 64>(a, s) : hgt_walk<float, 64>(a, s);
     case 128: return bf ? hgt_walk<__nv_bfloat16, 128>(a, s) : hgt_walk<float, 128>(a, s);
+    default: return set_error(RGNN_E_UNSUPPORTED, "d_out=%d not in {32,64,128}", N);
+  }
+}
+
+// ---------------------------------------------------------------- backward
+// Destination walk of the HGT backward (chain rule of the forward above; the oracle's
+// oracle_hgt_backward states the same formulas):
+//   S_t = G_t . Y_t = sum_e alpha_e (G_t . m_e),  alpha_e = exp(a_e - lse_t),  a_e = kw_e . q_t
+//   da_e = alpha_e (G_t . m_e - S_t)       (d a_e, the score gradient)
+//   dq_t = sum_e da_e kw_e                 (the query gradient, summed along the row: no atomics)
+// alpha_e and da_e are stored by position: the source sums (dk, dv) and the relation dW GEMMs
+// read them.  One warp per work item as the forward walk; a lane group of L = N*sizeof(TM)/16
+// lanes handles one edge, its lanes each holding EPL features of kw, m, q, G and dq.
+template <typename TM, int N>
+__global__ void __launch_bounds__(256) k_hgt_bwd_walk(HgtBwdArgs a) {
+  constexpr int EPL = 16 / sizeof(TM);
+  constexpr int SV = EPL * 4 / 16;  // fp32 16-byte vectors per lane slice (kw, q, G, Y)
+  constexpr int L = N / EPL;
+  constexpr int G = 32 / L;
+  static_assert(L >= 1 && L <= 32, "hgt bwd walk shape");
+  const float* KW = static_cast<const float*>(a.KW);
+  const TM* M = static_cast<const TM*>(a.M);
+  const float* Q = static_cast<const float*>(a.Q);
+  const int lane = threadIdx.x & 31, g = lane / L, l = lane % L;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = warp0; w < a.num_items; w += nwarps) {
+    const Item it = a.items[w];
+    float qf[EPL], gf[EPL], yf[EPL];
+    {
+      const float* qp = Q + (size_t)a.ninv[a.v0 + it.row] * N + l * EPL;
+      const float* gp = a.dY + (size_t)it.row * N + l * EPL;
+      const float* yp = a.Y + (size_t)it.row * N + l * EPL;
+#pragma unroll
+      for (int v = 0; v < SV; ++v) {
+        Vec16<float>{ldg16(qp + 4 * v)}.to_float(qf + 4 * v);
+        Vec16<float>{ldg16(gp + 4 * v)}.to_float(gf + 4 * v);
+        Vec16<float>{ldg16(yp + 4 * v)}.to_float(yf + 4 * v);
+      }
+    }
+    float S = 0.f;
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) S = fmaf(gf[i], yf[i], S);
+    S = group_sum<L>(S);
+    const float lse = a.lse[it.row];
+    float dq[EPL];
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) dq[i] = 0.f;
+    for (int32_t base = it.q0; base < it.q1; base += G) {
+      const int32_t q = base + g;
+      const bool ok = q < it.q1;
+      const int32_t p = ok ? a.pos[q] : 0;
+      const int32_t z = ok ? (a.zrow ? a.zrow[q] : p) : 0;
+      float kf[EPL], mf[EPL];
+      if (ok) {
+#pragma unroll
+        for (int v = 0; v < SV; ++v) Vec16<float>{ldg16(KW + (size_t)z * N + l * EPL + 4 * v)}.to_float(kf + 4 * v);
+        Vec16<TM>{ldg16(M + (size_t)z * N + l * EPL)}.to_float(mf);
+      } else {
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) kf[i] = mf[i] = 0.f;
+      }
+      float sa = 0.f, sd = 0.f;
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        sa = fmaf(kf[i], qf[i], sa);
+        sd = fmaf(gf[i], mf[i], sd);
+      }
+      sa = group_sum<L>(sa);
+      sd = group_sum<L>(sd);
+      const float al = ok ? __expf(sa - lse) : 0.f;
+      const float dae = al * (sd - S);
+      if (ok && l == 0) {
+        a.alpha[p] = al;
+        a.da[p] = dae;
+      }
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) dq[i] = fmaf(dae, kf[i], dq[i]);
+    }
+#pragma unroll
+    for (int o = L; o < 32; o <<= 1)
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) dq[i] += __shfl_xor_sync(0xffffffffu, dq[i], o);
+    if (g == 0) {
+      float* out = it.part < 0 ? a.dQ + (size_t)(a.v0 + it.row) * N : a.part + (size_t)it.part * N;
+#pragma unroll
+      for (int i = 0; i < EPL; i += 4)
+        stg16(out + l * EPL + i, make_uint4(__float_as_uint(dq[i]), __float_as_uint(dq[i + 1]),
+                                            __float_as_uint(dq[i + 2]), __float_as_uint(dq[i + 3])));
+    }
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(256) k_hgt_dq_merge(HgtBwdArgs a) {
+  for (int64_t w = blockIdx.x; w < a.num_split_rows; w += gridDim.x) {
+    const SplitRow sr = a.split_rows[w];
+    merge_parts<N>(a.part, sr.part0, sr.nparts, a.dQ + (size_t)(a.v0 + sr.row) * N, false);
+  }
+}
+
+template <typename TM, int N>
+static rgnn_status hgt_bwd_walk(const HgtBwdArgs& a, cudaStream_t s) {
+  if (a.num_items > 0) {
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((a.num_items + 7) / 8, 148 * 16));
+    RGNN_LAUNCH((k_hgt_bwd_walk<TM, N>), grid, 256, 0, s, a);
+  }
+  if (a.num_split_rows > 0)
+    RGNN_LAUNCH((k_hgt_dq_merge<N>), (unsigned)std::min<int64_t>(a.num_split_rows, 148 * 8), 256, 0, s, a);
+  return RGNN_OK;
+}
+
+rgnn_status launch_hgt_bwd_walk(int prec, int N, const HgtBwdArgs& a, cudaStream_t s) {
+  const bool bf = prec == RGNN_BF16;
+  switch (N) {
+    case 32: return bf ? hgt_bwd_walk<__nv_bfloat16, 32>(a, s) : hgt_bwd_walk<float, 32>(a, s);
+    case 64: return bf ? hgt_bwd_walk<__nv_bfloat16, 64>(a, s) : hgt_bwd_walk<float, 64>(a, s);
+    case 128: return bf ? hgt_bwd_walk<__nv_bfloat16, 128>(a, s) : hgt_bwd_walk<float, 128>(a, s);
     default: return set_error(RGNN_E_UNSUPPORTED, "d_out=%d not in {32,64,128}", N);
   }
 }

@@ -128,6 +128,7 @@ struct DxArgs {
   float* part;                                // [num_parts, K] partial rows of split sources
   const int32_t *srow, *spos, *srun, *srel;  // source-major CSR over the positions
   const float* sinvc;                         // RGCN: 1/c per source slot
+  const float* wpos;                          // non-RGAT walk: weight per position (HGT), else sinvc
   const float2* ad;                           // RGAT: (alpha, dpre) per position
   const void* H;                              // [J, K] fp32: G_v W_r^T per (etype, dst) run
   const float* U0;                            // RGAT: [R, K] W_r A[r,0]
@@ -158,7 +159,33 @@ struct HgtAggArgs {
   float* lse;
   float* part;
 };
-rgnn_status launch_map_gather(int64_t n, const int32_t* idx, const int32_t* ninv, int32_t* out, cudaStream_t s);
+// HGT backward destination walk: per position alpha_e and da_e = alpha_e (G_t . m_e - G_t . Y_t),
+// per owned destination dq_t = sum_e da_e kw_e (split rows: partial rows, merged in slot order)
+struct HgtBwdArgs {
+  const Item* items;
+  int64_t num_items;
+  const int32_t* pos;     // slot -> position p
+  const int32_t* zrow;    // slot -> row of KW / M (compact: zrow_slot), null = pos
+  const void* KW;         // [zrows, N] fp32
+  const void* M;          // [zrows, N] T
+  const void* Q;          // [V, N] fp32, node-type order rows
+  const int32_t* ninv;
+  int64_t v0;
+  const float* Y;         // [V_own, N]
+  const float* dY;        // [V_own, N]
+  const float* lse;       // [V_own]
+  float* alpha;           // [E_own] by position
+  float* da;              // [E_own] by position
+  float* dQ;              // [V, N] node-id order (owned rows written)
+  float* part;            // [num_parts, N]
+  const SplitRow* split_rows;
+  int64_t num_split_rows;
+};
+rgnn_status launch_hgt_bwd_walk(int prec, int N, const HgtBwdArgs& a, cudaStream_t s);
+rgnn_status launch_f32_to_bf16(int64_t n, const float* a, void* b, cudaStream_t s);
+// out[i] = ninv[idx[i] + ofs]
+rgnn_status launch_map_gather(int64_t n, const int32_t* idx, const int32_t* ninv, int32_t* out, cudaStream_t s,
+                              int64_t ofs = 0);
 rgnn_status launch_bf16_to_f32(int64_t n, const void* a, float* b, cudaStream_t s);
 rgnn_status launch_round_bf16(int64_t n, const float* a, float* b, cudaStream_t s);
 rgnn_status launch_aggregate_hgt(int prec, int N, const HgtAggArgs& a, cudaStream_t s);

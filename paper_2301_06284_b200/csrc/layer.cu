@@ -38,7 +38,11 @@ struct WsLayout {
 struct SavedLayout {
   void* Z;         // RGAT: [E_own, N] T
   float* s_src;    // RGAT: [E_own]
-  float* lse;      // RGAT: [V_own]
+  float* lse;      // RGAT, HGT: [V_own]
+  // HGT: the forward's typed-linear outputs, read by the backward
+  float *Kf, *Qf;  // [V, N] fp32 (node-type order rows)
+  float* KWf;      // [zrows, N] fp32
+  void *Vn, *M;    // [V, N], [zrows, N] T
   size_t bytes;
 };
 
@@ -57,33 +61,62 @@ static int64_t dw0_chunks(const rgnn_graph* g) {
 }
 
 struct HgtWs {
-  float *Kf, *Qf, *KWf;   // score path, fp32 on both paths
-  void *Vn, *M, *wt;      // message path, T
+  void* wt;               // bf16 transposed weights of the tcgen05 typed GEMM
   float *Xf, *Wr;         // bf16 path: X as fp32, RNE-rounded WK | WQ | Wa
   float* Wtr;             // tf32 GEMM weights: (rounded) WK^T | WQ^T | Wa^T
   int32_t* gather;
   float* part;
+  // backward (training)
+  float *alpha, *da;      // [E_own] by position
+  int32_t *vrow, *qrow;   // [E_own] node-type rows of src / dst of position p
+  int32_t* qrun;          // [J] node-type row of the destination of run j
+  float *dQ, *dK, *dV;    // [V, N] node-id order
+  float* H;               // [J, N] fp32: G_t Wm_r^T, then q_t Wa_r^T
+  void* Bb;               // [max(E_own, V), N] bf16 B operand of the tcgen05 dW GEMMs
+  void* Kb;               // [V, N] bf16 copy of k (tcgen05 dWa)
+  float* dwpart;          // dW split-K partials
+  float *qpart, *xpart;   // split-row partial rows (dq; dk / dv)
+  float *WmT, *WaT, *Wmr, *War;  // [R, N, N]: W^T (SIMT GEMM) and W (tf32 GEMM), rounded on bf16
   size_t bytes;
 };
-static HgtWs hgt_ws_layout(const rgnn_graph* g, int K, int N, int prec, void* base) {
+static HgtWs hgt_ws_layout(const rgnn_graph* g, int K, int N, int prec, void* base, bool training = false) {
   HgtWs w{};
   Carver c(base);
-  const size_t e = prec == RGNN_BF16 ? 2 : 4;
   const int64_t V = std::max<int64_t>(g->V, 1);
   const int64_t zr = std::max<int64_t>(use_compact(g, RGNN_HGT) ? g->num_compact : g->E_own, 1);
   const int64_t T = std::max<int64_t>(g->num_ntypes, 1);
-  w.Kf = c.take<float>((size_t)V * N);
-  w.Qf = c.take<float>((size_t)V * N);
-  w.KWf = c.take<float>((size_t)zr * N);
-  w.Vn = c.take<char>((size_t)V * N * e);
-  w.M = c.take<char>((size_t)zr * N * e);
+  const bool bf = prec == RGNN_BF16;
   w.gather = c.take<int32_t>((size_t)zr);
   w.part = c.take<float>((size_t)std::max<int64_t>(g->num_parts, 1) * (N + 4));
   const int64_t nw = std::max<int64_t>(T * K * N, (int64_t)g->R * N * N);
-  w.wt = c.take<char>(prec == RGNN_BF16 ? (size_t)nw * 2 : 1);
-  w.Xf = c.take<float>(prec == RGNN_BF16 ? (size_t)V * K : 1);
-  w.Wr = c.take<float>(prec == RGNN_BF16 ? (size_t)(2 * T * K * N + (int64_t)g->R * N * N) : 1);
+  w.wt = c.take<char>(bf ? (size_t)nw * 2 : 1);
+  w.Xf = c.take<float>(bf ? (size_t)V * K : 1);
+  w.Wr = c.take<float>(bf ? (size_t)(2 * T * K * N + (int64_t)g->R * N * N) : 1);
   w.Wtr = c.take<float>((size_t)(2 * T * K * N + (int64_t)g->R * N * N));
+  if (training) {
+    const int64_t E = std::max<int64_t>(g->E_own, 1), J = std::max<int64_t>(g->J, 1);
+    w.alpha = c.take<float>(E);
+    w.da = c.take<float>(E);
+    w.vrow = c.take<int32_t>(E);
+    w.qrow = c.take<int32_t>(E);
+    w.qrun = c.take<int32_t>(J);
+    w.dQ = c.take<float>((size_t)V * N);
+    w.dK = c.take<float>((size_t)V * N);
+    w.dV = c.take<float>((size_t)V * N);
+    w.H = c.take<float>((size_t)J * N);
+    w.Bb = c.take<char>(bf ? (size_t)std::max(E, V) * N * 2 : 1);
+    w.Kb = c.take<char>(bf ? (size_t)V * N * 2 : 1);
+    const int64_t dwp = std::max<int64_t>(std::max<int64_t>(g->num_chunks, 1) * (N * N + N),
+                                          std::max<int64_t>(g->num_nchunks, 1) * (K * N + K));
+    w.dwpart = c.take<float>((size_t)dwp);
+    w.qpart = c.take<float>((size_t)std::max<int64_t>(g->num_parts, 1) * N);
+    w.xpart = c.take<float>((size_t)std::max<int64_t>(g->num_sparts, 1) * N);
+    const size_t rnn = (size_t)g->R * N * N;
+    w.WmT = c.take<float>(rnn);
+    w.WaT = c.take<float>(rnn);
+    w.Wmr = c.take<float>(rnn);
+    w.War = c.take<float>(rnn);
+  }
   w.bytes = c.off;
   return w;
 }
@@ -130,7 +163,13 @@ static SavedLayout saved_layout(const rgnn_graph* g, int model, int N, int prec,
     s.s_src = c.take<float>((size_t)zrows(g, model));
     s.lse = c.take<float>((size_t)std::max<int64_t>(g->V_own, 1));
   } else if (model == RGNN_HGT) {
+    const int64_t V = std::max<int64_t>(g->V, 1);
     s.lse = c.take<float>((size_t)std::max<int64_t>(g->V_own, 1));
+    s.Kf = c.take<float>((size_t)V * N);
+    s.Qf = c.take<float>((size_t)V * N);
+    s.KWf = c.take<float>((size_t)zrows(g, model) * N);
+    s.Vn = c.take<char>((size_t)V * N * elt(prec));
+    s.M = c.take<char>((size_t)zrows(g, model) * N * elt(prec));
   }
   s.bytes = c.off;
   return s;
@@ -231,7 +270,7 @@ rgnn_status rgnn_workspace_bytes(const rgnn_graph* g, rgnn_model model, int d_in
   if (!g) return set_error(RGNN_E_INVALID_ARG, "graph is NULL");
   if (!width_ok(d_in) || !width_ok(d_out)) return set_error(RGNN_E_UNSUPPORTED, "widths not in {32,64,128}");
   if (ws_bytes)
-    *ws_bytes = model == RGNN_HGT ? hgt_ws_layout(g, d_in, d_out, prec, nullptr).bytes
+    *ws_bytes = model == RGNN_HGT ? hgt_ws_layout(g, d_in, d_out, prec, nullptr, training != 0).bytes
                                   : ws_layout(g, model, d_in, d_out, prec, nullptr, training == RGNN_WS_DX).bytes;
   if (saved_bytes) *saved_bytes = saved_layout(g, model, d_out, prec, nullptr).bytes;
   return RGNN_OK;
@@ -297,9 +336,9 @@ rgnn_status hgt_forward(const rgnn_graph* g, int K, int N, rgnn_prec prec, const
       ga.Z = out; ga.wt_bf16 = w.wt; ga.num_w = (int)T; ga.x_rows = g->V; ga.z_rows = g->V;
       return p == RGNN_F32 ? f32_gemm(prec, K, N, ga, Wt32, s) : typed_gemm(p, K, N, ga, s);
     };
-    RGNN_TRY(node_gemm(RGNN_F32, Xs, WKs, w.Wtr, w.Kf));
-    RGNN_TRY(node_gemm(RGNN_F32, Xs, WQs, w.Wtr + T * K * N, w.Qf));
-    RGNN_TRY(node_gemm(prec, X, WV, nullptr, w.Vn));
+    RGNN_TRY(node_gemm(RGNN_F32, Xs, WKs, w.Wtr, sv.Kf));
+    RGNN_TRY(node_gemm(RGNN_F32, Xs, WQs, w.Wtr + T * K * N, sv.Qf));
+    RGNN_TRY(node_gemm(prec, X, WV, nullptr, sv.Vn));
   }
   const bool cm = use_compact(g, RGNN_HGT);
   const int64_t zr = cm ? g->num_compact : g->E_own;
@@ -314,15 +353,15 @@ rgnn_status hgt_forward(const rgnn_graph* g, int K, int N, rgnn_prec prec, const
       return p == RGNN_F32 ? f32_gemm(prec, N, N, ga, Wt32, s) : typed_gemm(p, N, N, ga, s);
     };
     if (nt) {
-      RGNN_TRY(rel_gemm(RGNN_F32, w.Kf, Was, w.Wtr + 2 * T * K * N, w.KWf));
-      RGNN_TRY(rel_gemm(prec, w.Vn, Wm, nullptr, w.M));
+      RGNN_TRY(rel_gemm(RGNN_F32, sv.Kf, Was, w.Wtr + 2 * T * K * N, sv.KWf));
+      RGNN_TRY(rel_gemm(prec, sv.Vn, Wm, nullptr, sv.M));
     }
   }
   {
     Phase ph("aggregate", s);
     HgtAggArgs ha{};
-    ha.items = g->items; ha.num_items = g->num_items; ha.pos = cm ? g->zrow_slot : g->pos; ha.KW = w.KWf;
-    ha.M = w.M; ha.Q = w.Qf; ha.ninv = g->ninv; ha.v0 = g->v0; ha.Y = Y; ha.lse = sv.lse; ha.part = w.part;
+    ha.items = g->items; ha.num_items = g->num_items; ha.pos = cm ? g->zrow_slot : g->pos; ha.KW = sv.KWf;
+    ha.M = sv.M; ha.Q = sv.Qf; ha.ninv = g->ninv; ha.v0 = g->v0; ha.Y = Y; ha.lse = sv.lse; ha.part = w.part;
     RGNN_TRY(launch_aggregate_hgt(prec, N, ha, s));
     // zero rows and split-row merges of the shared walk infrastructure (online-softmax states)
     AggArgs aa{};
@@ -331,6 +370,142 @@ rgnn_status hgt_forward(const rgnn_graph* g, int K, int N, rgnn_prec prec, const
     RGNN_TRY(launch_aggregate(prec, N, N, true, aa, s));
   }
   if (comm && Y_full) { Phase ph("comm", s); RGNN_TRY(comm_gather_rows(comm, Y, N, Y_full, s)); }
+  return RGNN_OK;
+}
+
+// HGT backward (chain rule of hgt_forward; the formulas of oracle_hgt_backward):
+//   walk     : alpha_e, da_e by position; dq_t = sum_e da_e kw_e            (owned rows)
+//   runs     : Hm_j = G_t Wm_r^T, Ha_j = q_t Wa_r^T per (etype, dst) run j  (fp32 GEMMs, J << E)
+//   sources  : dv_s = sum_{e: src=s} alpha_e Hm_j(e),  dk_s = sum_e da_e Ha_j(e)   (source walk)
+//   dW       : dWm_r = sum_p v_src^T (alpha_p G_t),  dWa_r = sum_p k_src^T (da_p q_t)   (position chunks)
+//              dWK / dWV / dWQ [tau] = sum_{nodes of type tau} x^T dk / dv / dq    (node-type chunks)
+// On the bf16 layer the dW GEMMs run on the tcgen05 segmented dW kernel with the B rows
+// materialised in bf16 (like the RGAT dZ); on the fp32 layer on the SIMT dW kernel.
+rgnn_status hgt_backward(const rgnn_graph* g, int K, int N, rgnn_prec prec, const void* X, const float* WK,
+                         const float* WQ, const float* WV, const float* Wa, const float* Wm, const float* Y,
+                         const float* dY, const void* saved, float* dWK, float* dWQ, float* dWV, float* dWa,
+                         float* dWm, void* ws, size_t ws_bytes, rgnn_comm* comm, void* stream) {
+  (void)WK; (void)WQ; (void)WV;
+  if (!g) return set_error(RGNN_E_INVALID_ARG, "graph is NULL");
+  if (!g->has_ntype) return set_error(RGNN_E_UNSUPPORTED, "HGT needs node types (rgnn_graph_desc.ntype)");
+  if (!g->has_dx) return set_error(RGNN_E_UNSUPPORTED, "HGT backward needs a graph built with RGNN_GRAPH_DX");
+  if (!width_ok(K) || !width_ok(N)) return set_error(RGNN_E_UNSUPPORTED, "d_in=%d d_out=%d not in {32,64,128}", K, N);
+  if (prec != RGNN_F32 && prec != RGNN_BF16) return set_error(RGNN_E_INVALID_ARG, "bad precision %d", prec);
+  const HgtWs need = hgt_ws_layout(g, K, N, prec, nullptr, true);
+  if (!ws || (uintptr_t)ws % kAlign) return set_error(RGNN_E_INVALID_ARG, "workspace NULL or not 256B aligned");
+  if (ws_bytes < need.bytes)
+    return set_error(RGNN_E_WORKSPACE, "workspace %zu < required %zu (size it with training=1)", ws_bytes, need.bytes);
+  if (!X || !Wa || !Wm || !Y || !dY || !saved || !dWK || !dWQ || !dWV || !dWa || !dWm)
+    return set_error(RGNN_E_INVALID_ARG, "X, Wa, Wm, Y, dY, saved and the five gradients must not be NULL");
+  if (comm) RGNN_TRY(comm_check_range(comm, g->v0, g->v0 + g->V_own));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HgtWs w = hgt_ws_layout(g, K, N, prec, ws, true);
+  SavedLayout sv = saved_layout(g, RGNN_HGT, N, prec, const_cast<void*>(saved));
+  const bool bf = prec == RGNN_BF16;
+  const bool cm = use_compact(g, RGNN_HGT);
+  const int64_t T = g->num_ntypes, V = g->V, E = g->E_own, J = g->J;
+  const size_t rnn = (size_t)g->R * N * N;
+  {
+    Phase ph("hgt_bwd_prep", s);
+    RGNN_TRY(launch_transpose_w(prec, g->R, N, N, Wm, w.WmT, s));
+    RGNN_TRY(launch_transpose_w(prec, g->R, N, N, Wa, w.WaT, s));
+    if (bf) {
+      RGNN_TRY(launch_round_bf16((int64_t)rnn, Wm, w.Wmr, s));
+      RGNN_TRY(launch_round_bf16((int64_t)rnn, Wa, w.War, s));
+    } else {
+      RGNN_CUDA_TRY(cudaMemcpyAsync(w.Wmr, Wm, sizeof(float) * rnn, cudaMemcpyDeviceToDevice, s));
+      RGNN_CUDA_TRY(cudaMemcpyAsync(w.War, Wa, sizeof(float) * rnn, cudaMemcpyDeviceToDevice, s));
+    }
+    RGNN_TRY(launch_map_gather(E, g->src_s, g->ninv, w.vrow, s));
+    RGNN_TRY(launch_map_gather(E, g->dst_s, g->ninv, w.qrow, s, g->v0));
+    RGNN_TRY(launch_map_gather(J, g->run_dst, g->ninv, w.qrun, s, g->v0));
+    RGNN_CUDA_TRY(cudaMemsetAsync(w.dQ, 0, sizeof(float) * (size_t)V * N, s));
+    RGNN_CUDA_TRY(cudaMemsetAsync(w.dK, 0, sizeof(float) * (size_t)V * N, s));
+    RGNN_CUDA_TRY(cudaMemsetAsync(w.dV, 0, sizeof(float) * (size_t)V * N, s));
+  }
+  {
+    Phase ph("hgt_bwd_walk", s);
+    HgtBwdArgs hb{};
+    hb.items = g->items; hb.num_items = g->num_items; hb.pos = g->pos; hb.zrow = cm ? g->zrow_slot : nullptr;
+    hb.KW = sv.KWf; hb.M = sv.M; hb.Q = sv.Qf; hb.ninv = g->ninv; hb.v0 = g->v0; hb.Y = Y; hb.dY = dY;
+    hb.lse = sv.lse; hb.alpha = w.alpha; hb.da = w.da; hb.dQ = w.dQ; hb.part = w.qpart;
+    hb.split_rows = g->split_rows; hb.num_split_rows = g->num_split_rows;
+    RGNN_TRY(launch_hgt_bwd_walk(prec, N, hb, s));
+  }
+  // source sums: dv = sum alpha Hm, dk = sum da Ha over each source's out-edges
+  auto src_sum = [&](const float* G, const int32_t* gidx, int64_t grows, const float* Wt, const float* Wrr,
+                     const float* wpos, float* out) -> rgnn_status {
+    if (g->num_rtiles) {
+      Phase ph("hgt_bwd_runs", s);
+      GemmFwdArgs gh{};
+      gh.tiles = g->rtiles; gh.num_tiles = g->num_rtiles; gh.X = G; gh.gather = gidx; gh.W = Wt; gh.Z = w.H;
+      gh.wt_bf16 = w.wt; gh.num_w = g->R; gh.x_rows = std::max<int64_t>(grows, 1); gh.z_rows = J;
+      RGNN_TRY(f32_gemm(prec, N, N, gh, Wrr, s));
+    }
+    Phase ph("hgt_bwd_src", s);
+    DxArgs xa{};
+    xa.V = V; xa.V_own = g->V_own; xa.v0 = g->v0;
+    xa.items = g->sitems; xa.num_items = g->num_sitems; xa.split = g->ssplit; xa.num_split = g->num_ssplit;
+    xa.part = w.xpart; xa.srow = g->srow; xa.spos = g->spos; xa.srun = g->srun; xa.srel = g->srel;
+    xa.sinvc = g->sinvc; xa.wpos = wpos; xa.H = w.H; xa.dX = out;
+    return launch_dx_walk(N, false, xa, s);
+  };
+  RGNN_TRY(src_sum(dY, g->run_dst, g->V_own, w.WmT, w.Wmr, w.alpha, w.dV));
+  RGNN_TRY(src_sum(sv.Qf, w.qrun, V, w.WaT, w.War, w.da, w.dK));
+  // dW GEMMs: part = sum_p Xin[gather p]^T (scale_p Gm[gidx p]), reduced per segment in chunk order
+  auto dw = [&](int xprec, int Kd, const void* Xin, const int32_t* gather, int64_t xrows, const Tile* chunks,
+                int64_t nch, const int32_t* cseg, int nseg, int64_t rows, const float* Gm, const int32_t* gidx,
+                const float* scale, float* out) -> rgnn_status {
+    if (nch == 0) {
+      RGNN_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)nseg * Kd * N, s));
+      return RGNN_OK;
+    }
+    GemmDwArgs a{};
+    a.chunks = chunks; a.num_chunks = nch; a.rows = rows; a.X = Xin; a.gather = gather; a.x_rows = xrows;
+    a.part = w.dwpart;
+    rgnn_status st = RGNN_E_UNSUPPORTED;
+    if (bf && xprec == RGNN_BF16 && (Kd == 64 || Kd == 128)) {
+      RGNN_TRY(launch_expand_dz(rows, N, gidx, scale, Gm, w.Bb, s));
+      a.Bz = w.Bb;
+      st = launch_gemm_dw_tc(Kd, N, a, s);
+      if (st != RGNN_OK && st != RGNN_E_UNSUPPORTED) return st;
+    }
+    if (st != RGNN_OK) {
+      a.Bz = nullptr; a.Bg = Gm; a.bgather = gidx; a.bscale = scale;
+      RGNN_TRY(launch_gemm_dw(xprec, Kd, N, a, s));
+    }
+    return launch_dw_reduce(xprec, Kd, N, nseg, nch, cseg, w.dwpart, nullptr, nullptr, nullptr, nullptr, out,
+                            nullptr, nullptr, s);
+  };
+  {
+    Phase ph("hgt_bwd_dw_rel", s);
+    RGNN_TRY(dw(prec, N, sv.Vn, w.vrow, V, g->chunks, g->num_chunks, g->chunk_seg, g->R, E, dY, g->dst_s, w.alpha,
+                dWm));
+    const void* Kin = sv.Kf;
+    int kp = RGNN_F32;
+    if (bf) {
+      RGNN_TRY(launch_f32_to_bf16((int64_t)V * N, sv.Kf, w.Kb, s));
+      Kin = w.Kb;
+      kp = RGNN_BF16;
+    }
+    RGNN_TRY(dw(kp, N, Kin, w.vrow, V, g->chunks, g->num_chunks, g->chunk_seg, g->R, E, sv.Qf, w.qrow, w.da, dWa));
+  }
+  {
+    Phase ph("hgt_bwd_dw_node", s);
+    RGNN_TRY(dw(prec, K, X, g->nperm, V, g->nchunks, g->num_nchunks, g->nchunk_seg, (int)T, V, w.dK, g->nperm,
+                nullptr, dWK));
+    RGNN_TRY(dw(prec, K, X, g->nperm, V, g->nchunks, g->num_nchunks, g->nchunk_seg, (int)T, V, w.dV, g->nperm,
+                nullptr, dWV));
+    RGNN_TRY(dw(prec, K, X, g->nperm, V, g->nchunks, g->num_nchunks, g->nchunk_seg, (int)T, V, w.dQ, g->nperm,
+                nullptr, dWQ));
+  }
+  if (comm) {
+    float* bufs[5] = {dWK, dWQ, dWV, dWa, dWm};
+    const size_t tkn = (size_t)T * K * N;
+    size_t counts[5] = {tkn, tkn, tkn, rnn, rnn};
+    Phase ph("comm", s);
+    RGNN_TRY(comm_allreduce_sum(comm, bufs, counts, 5, s));
+  }
   return RGNN_OK;
 }
 

@@ -228,6 +228,24 @@ def hgt_forward(g: Graph, X: torch.Tensor, WK: torch.Tensor, WQ: torch.Tensor, W
     return Y, ws
 
 
+def hgt_backward(g: Graph, X: torch.Tensor, WK: torch.Tensor, WQ: torch.Tensor, WV: torch.Tensor, Wa: torch.Tensor,
+                 Wm: torch.Tensor, Y: torch.Tensor, dY: torch.Tensor, ws: Workspace, *, prec="bf16",
+                 comm: Optional[Comm] = None, stream=None):
+    """hgt_backward (NEXT-3): returns (dWK, dWQ, dWV, dWa, dWm).  ws must come from the forward
+    (Workspace(..., training=True)); the graph must be built with build_dx=True and node types."""
+    p = _prec(prec)
+    _check_x(X, p)
+    T, K, N = WK.shape
+    R = Wa.shape[0]
+    dev = g.device
+    outs = [torch.empty(T, K, N, dtype=torch.float32, device=dev) for _ in range(3)] + \
+           [torch.empty(R, N, N, dtype=torch.float32, device=dev) for _ in range(2)]
+    B.call("hgt_backward", g.handle, K, N, p, _ptr(X), _ptr(WK), _ptr(WQ), _ptr(WV), _ptr(Wa), _ptr(Wm), _ptr(Y),
+           _ptr(dY), _ptr(ws.saved), *[_ptr(o) for o in outs], _ptr(ws.ws), ws.ws.numel(),
+           comm.handle if comm else None, _stream(stream))
+    return tuple(outs)
+
+
 def rgnn_backward(g: Graph, model, X: torch.Tensor, W: torch.Tensor, dY: torch.Tensor, ws: Workspace, *,
                   A: Optional[torch.Tensor] = None, slope: float = 0.2, Y: Optional[torch.Tensor] = None,
                   with_w0: bool = False, W0: Optional[torch.Tensor] = None, want_dx: bool = False, prec="bf16",

@@ -75,3 +75,81 @@ def test_hgt_needs_node_types(rgnn):
     with pytest.raises(rgnn.RgnnError) as ei:
         rgnn.hgt_forward(G, torch.from_numpy(t.X).cuda(), *Ws, prec="f32")
     assert ei.value.status == 3
+
+
+# ---------------------------------------------------------------- backward (NEXT-3)
+GRAD_NAMES = ("dWK", "dWQ", "dWV", "dWa", "dWm")
+
+
+def _run_bwd(rgnn, g, t, prec, materialization="auto", dst_range=None, split_cap=0):
+    import torch
+    v0, v1 = dst_range or (0, g.V)
+    G = rgnn.Graph(g.V, g.src, g.dst, g.etype, g.R, ntype=g.ntype, num_ntypes=g.T, dst_begin=v0, dst_end=v1,
+                   materialization=materialization, row_split_cap=split_cap, build_dx=True)
+    X = torch.from_numpy(t.X).cuda()
+    X = X.to(torch.bfloat16) if prec == "bf16" else X
+    Ws = [torch.from_numpy(a).cuda() for a in (t.WK, t.WQ, t.WV, t.Wa, t.Wm)]
+    T, K, N = t.WK.shape
+    ws = rgnn.Workspace(G, "hgt", K, N, prec, training=True)
+    Y, ws = rgnn.hgt_forward(G, X, *Ws, prec=prec, ws=ws)
+    dY = torch.from_numpy(t.dY[v0:v1]).cuda().contiguous()
+    grads = rgnn.hgt_backward(G, X, *Ws, Y, dY, ws, prec=prec)
+    torch.cuda.synchronize()
+    return [x.cpu().numpy() for x in grads]
+
+
+def _ref_bwd(g, t, prec, dst_range=None):
+    v0, v1 = dst_range or (0, g.V)
+    r = bf16_round if prec == "bf16" else (lambda a: a)
+    return oracle.hgt_backward(g.V, g.R, g.src, g.dst, g.etype, g.ntype, r(t.X), r(t.WK), r(t.WQ), r(t.WV),
+                               r(t.Wa), r(t.Wm), t.dY, v0=v0, v1=v1)
+
+
+def _check_grads(got, ref, prec, what):
+    for name, a, b in zip(GRAD_NAMES, got, ref):
+        assert_close(a, b, prec, f"{what} {name}", per_slice=True)
+
+
+@pytest.mark.parametrize("prec", ["f32", "bf16"])
+@pytest.mark.parametrize("mat", ["compact", "vanilla"])
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_hgt_backward_parity(rgnn, case, mat, prec):
+    g, K, N = case[1]()
+    t = synth.make_hgt_tensors(g.V, g.R, g.T, K, N)
+    _check_grads(_run_bwd(rgnn, g, t, prec, materialization=mat), _ref_bwd(g, t, prec), prec, f"hgt bwd {mat}/{prec}")
+
+
+def test_hgt_backward_split_rows_shards_and_determinism(rgnn):
+    g = synth.make_graph(synth.get_config("bgs").scaled(10))
+    t = synth.make_hgt_tensors(g.V, g.R, g.T, 64, 64)
+    got = _run_bwd(rgnn, g, t, "f32", split_cap=8)
+    _check_grads(got, _ref_bwd(g, t, "f32"), "f32", "hgt bwd split")
+    got2 = _run_bwd(rgnn, g, t, "f32", split_cap=8)
+    for a, b in zip(got, got2):
+        np.testing.assert_array_equal(a, b)
+    # dst-range shards: each shard's gradients match the oracle restricted to its rows, and
+    # they sum to the full gradients (what the all-reduce computes across ranks)
+    indeg = np.r_[0, np.cumsum(np.bincount(g.dst, minlength=g.V))]
+    b = rgnn.partition_dst(indeg, 3)
+    full = _ref_bwd(g, t, "bf16")
+    acc = None
+    for k in range(3):
+        rng = (int(b[k]), int(b[k + 1]))
+        gs = _run_bwd(rgnn, g, t, "bf16", dst_range=rng)
+        _check_grads(gs, _ref_bwd(g, t, "bf16", rng), "bf16", f"hgt bwd shard {k}")
+        acc = gs if acc is None else [x + y for x, y in zip(acc, gs)]
+    _check_grads(acc, full, "bf16", "hgt bwd shard sum")
+
+
+def test_hgt_backward_needs_dx_tables(rgnn):
+    import torch
+    g = synth.random_graph(60, 300, 3, seed=4, T=2)
+    t = synth.make_hgt_tensors(g.V, g.R, g.T, 32, 32)
+    G = rgnn.Graph(g.V, g.src, g.dst, g.etype, g.R, ntype=g.ntype, num_ntypes=g.T)
+    X = torch.from_numpy(t.X).cuda()
+    Ws = [torch.from_numpy(a).cuda() for a in (t.WK, t.WQ, t.WV, t.Wa, t.Wm)]
+    ws = rgnn.Workspace(G, "hgt", 32, 32, "f32", training=True)
+    Y, ws = rgnn.hgt_forward(G, X, *Ws, prec="f32", ws=ws)
+    with pytest.raises(rgnn.RgnnError) as ei:
+        rgnn.hgt_backward(G, X, *Ws, Y, torch.from_numpy(t.dY).cuda(), ws, prec="f32")
+    assert ei.value.status == 3
