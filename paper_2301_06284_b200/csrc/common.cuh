@@ -59,6 +59,7 @@ struct Carver {
 };
 
 constexpr int kTileRows = 128;       // GEMM M tile (rows of Z per tile)
+constexpr int kPieceRows = 64;       // HGT backward: run pieces hold <= 64 positions
 constexpr int kDefaultSplitCap = 256; // max in-edges per traversal work item
 
 // Work item of the destination walk: one CSR row, or one chunk of a long row.
@@ -108,6 +109,13 @@ struct rgnn_graph {
   rgnn::Tile* nchunks;   // dW split-K chunks over the node-type segments (HGT backward)
   int32_t* nchunk_seg;   // [T+1]
   int64_t num_nchunks;
+  // run pieces (HGT backward; node types + RGNN_GRAPH_DX): runs cut at multiples of kPieceRows
+  bool has_pieces;
+  int32_t* piece_ptr;    // [num_pieces + 1] first position of each piece
+  int32_t* prseg;        // [R+1] first piece of relation r
+  rgnn::Tile* pchunks;   // dW split-K chunks over the pieces
+  int32_t* pchunk_seg;   // [R+1] first piece chunk of relation r
+  int64_t num_pieces, num_pchunks;
   bool has_compact;  // compact tables built (COMPACT or AUTO)
   int mat_mode;      // rgnn_materialization requested
   int64_t num_compact, num_ctiles;

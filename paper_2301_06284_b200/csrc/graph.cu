@@ -20,12 +20,39 @@ namespace rgnn {
 struct Counters {
   int32_t bad_edge, bad_node, E_own, J, num_items, num_parts, num_split_rows, num_empty, num_compact;
   int32_t num_sitems, num_sparts, num_ssplit;  // dX source work list
+  int32_t num_pieces;                          // HGT backward run pieces
 };
 
 __global__ void k_init_counters(Counters* c, int32_t big) {
   c->bad_edge = big; c->bad_node = big; c->E_own = 0; c->J = 0;
   c->num_items = 0; c->num_parts = 0; c->num_split_rows = 0; c->num_empty = 0; c->num_compact = 0;
-  c->num_sitems = 0; c->num_sparts = 0; c->num_ssplit = 0;
+  c->num_sitems = 0; c->num_sparts = 0; c->num_ssplit = 0; c->num_pieces = 0;
+}
+
+// Run pieces (HGT backward): every (etype, dst) run cut at the multiples of kPieceRows,
+// so a piece holds <= kPieceRows consecutive positions of one run.  Pieces are numbered in
+// position order; piece_ptr[i] is the first position of piece i.
+__global__ void k_piece_counts(int64_t J, const int32_t* __restrict__ run_ptr, int32_t* __restrict__ cnt) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < J; j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = run_ptr[j], e = run_ptr[j + 1];
+    cnt[j] = (e - 1) / kPieceRows - s / kPieceRows + 1;
+  }
+}
+__global__ void k_piece_fill(int64_t J, const int32_t* __restrict__ run_ptr, const int32_t* __restrict__ pofs,
+                             int32_t* __restrict__ piece_ptr) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < J; j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = run_ptr[j], e = run_ptr[j + 1];
+    int32_t id = pofs[j];
+    piece_ptr[id++] = s;
+    for (int32_t b = (s / kPieceRows + 1) * kPieceRows; b < e; b += kPieceRows) piece_ptr[id++] = b;
+  }
+}
+__global__ void k_piece_seg(int32_t R, int64_t J, const int32_t* __restrict__ rseg, const int32_t* __restrict__ pofs,
+                            const Counters* c, int32_t* __restrict__ prseg, int32_t* __restrict__ piece_ptr,
+                            int32_t E_own) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r <= R; r += gridDim.x * blockDim.x)
+    prseg[r] = rseg[r] < J ? pofs[rseg[r]] : c->num_pieces;
+  if (blockIdx.x == 0 && threadIdx.x == 0) piece_ptr[c->num_pieces] = E_own;
 }
 
 // CSR-by-dst input: dst of every edge from row_ptr (one warp per row).
@@ -316,6 +343,8 @@ struct GraphLayout {
   int32_t *nperm, *ninv, *nseg;
   Tile *ntiles, *nchunks;
   int32_t* nchunk_seg;
+  int32_t *piece_ptr, *prseg, *pchunk_seg;
+  Tile* pchunks;
   size_t dev_bytes;
   // scratch
   Counters* ctr;
@@ -378,6 +407,11 @@ static GraphLayout layout(const rgnn_graph_desc* d, void* dev, void* scr) {
   L.ntiles = c.take<Tile>(nt ? Vn / kTileRows + d->num_ntypes + 1 : 1);
   L.nchunks = c.take<Tile>(nt ? Vn / kTileRows + d->num_ntypes + 1 : 1);  // chunks >= 128 rows: <= #ntiles
   L.nchunk_seg = c.take<int32_t>(nt ? d->num_ntypes + 1 : 1);
+  const bool pc = nt && dx;  // HGT backward run pieces
+  L.piece_ptr = c.take<int32_t>(pc ? Ec + Ec / kPieceRows + 2 : 1);
+  L.prseg = c.take<int32_t>(pc ? R + 1 : 1);
+  L.pchunks = c.take<Tile>(pc ? max_chunks(E, R) : 1);
+  L.pchunk_seg = c.take<int32_t>(pc ? R + 1 : 1);
   L.dev_bytes = c.off;
   Carver s(scr);
   L.ctr = s.take<Counters>(1);
@@ -573,7 +607,7 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
     RGNN_LAUNCH(k_bounds<uint32_t>, grid_for(NT + 1), T, 0, s, V, alt ? L.k1 : L.k0, (int64_t)NT, L.nseg);
     RGNN_CUDA_TRY(cudaMemcpyAsync(nseg_h.data(), L.nseg, sizeof(int32_t) * (NT + 1), cudaMemcpyDeviceToHost, s));
   }
-  std::vector<int32_t> rseg_h(R + 1, 0);
+  std::vector<int32_t> rseg_h(R + 1, 0), prseg_h;
   if (dx) {
     // source-major CSR over the positions (stable: ascending position within a source)
     if (n > 0) {
@@ -594,10 +628,22 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
                   L.ssplit);
     }
     RGNN_CUDA_TRY(cudaMemcpyAsync(rseg_h.data(), L.rseg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
+    if (d->ntype) {  // run pieces for the HGT backward's relation dW GEMMs
+      if (h.J > 0) {
+        RGNN_LAUNCH(k_piece_counts, grid_for(h.J), T, 0, s, (int64_t)h.J, L.run_ptr, L.flags);
+        RGNN_TRY(scan_exclusive(L.flags, L.flags, h.J, &L.ctr->num_pieces, L.prim, L.prim_bytes, s));
+        RGNN_LAUNCH(k_piece_fill, grid_for(h.J), T, 0, s, (int64_t)h.J, L.run_ptr, L.flags, L.piece_ptr);
+      }
+      RGNN_LAUNCH(k_piece_seg, (unsigned)((R + 256) / 256), 256, 0, s, R, (int64_t)h.J, L.rseg, L.flags, L.ctr,
+                  L.prseg, L.piece_ptr, (int32_t)n);
+      prseg_h.assign(R + 1, 0);
+      RGNN_CUDA_TRY(cudaMemcpyAsync(prseg_h.data(), L.prseg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
+    }
     Counters h2{};
     RGNN_CUDA_TRY(cudaMemcpyAsync(&h2, L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
     RGNN_CUDA_TRY(cudaStreamSynchronize(s));
     h.num_sitems = h2.num_sitems; h.num_sparts = h2.num_sparts; h.num_ssplit = h2.num_ssplit;
+    h.num_pieces = h2.num_pieces;
   }
   RGNN_CUDA_TRY(cudaStreamSynchronize(s));
   int dev_id = 0, sms = 148;
@@ -654,6 +700,22 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
         rtiles.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + kTileRows, rseg_h[r + 1]), 0});
   if (!rtiles.empty())
     RGNN_CUDA_TRY(cudaMemcpyAsync(L.rtiles, rtiles.data(), sizeof(Tile) * rtiles.size(), cudaMemcpyHostToDevice, s));
+  std::vector<Tile> pchunks;  // dW split-K chunks over the run pieces, never straddling relations
+  std::vector<int32_t> pchunk_seg(R + 1, 0);
+  if (!prseg_h.empty()) {
+    const int64_t np = h.num_pieces;
+    const int64_t pcr = std::max<int64_t>(kTileRows, ((np / (2 * sms) + 1) + kTileRows - 1) / kTileRows * kTileRows);
+    for (int32_t r = 0; r < R; ++r) {
+      pchunk_seg[r] = (int32_t)pchunks.size();
+      for (int64_t a = prseg_h[r]; a < prseg_h[r + 1]; a += pcr)
+        pchunks.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + pcr, prseg_h[r + 1]), 0});
+    }
+    pchunk_seg[R] = (int32_t)pchunks.size();
+    RGNN_CUDA_TRY(cudaMemcpyAsync(L.pchunk_seg, pchunk_seg.data(), sizeof(int32_t) * (R + 1), cudaMemcpyHostToDevice, s));
+    if ((int64_t)pchunks.size() > max_chunks(E, R)) return set_error(RGNN_E_CUDA, "internal: piece chunk overflow");
+    if (!pchunks.empty())
+      RGNN_CUDA_TRY(cudaMemcpyAsync(L.pchunks, pchunks.data(), sizeof(Tile) * pchunks.size(), cudaMemcpyHostToDevice, s));
+  }
   if ((int64_t)chunks.size() > max_chunks(E, R))
     return set_error(RGNN_E_CUDA, "internal: chunk table overflow");
   if (!tiles.empty())
@@ -684,6 +746,8 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   g->has_ntype = d->ntype != nullptr && V > 0; g->num_ntypes = d->ntype ? d->num_ntypes : 0;
   g->nperm = L.nperm; g->ninv = L.ninv; g->ntiles = L.ntiles; g->num_ntiles = (int64_t)ntiles.size();
   g->nchunks = L.nchunks; g->nchunk_seg = L.nchunk_seg; g->num_nchunks = (int64_t)nchunks.size();
+  g->has_pieces = !prseg_h.empty(); g->piece_ptr = L.piece_ptr; g->prseg = L.prseg; g->pchunks = L.pchunks; g->pchunk_seg = L.pchunk_seg;
+  g->num_pieces = g->has_pieces ? h.num_pieces : 0; g->num_pchunks = (int64_t)pchunks.size();
   g->seg_host = seg_h;
   g->chunk_seg_host = chunk_seg;
   RGNN_CUDA_TRY(cudaGetDevice(&g->device));

@@ -308,6 +308,93 @@ static rgnn_status hgt_bwd_walk(const HgtBwdArgs& a, cudaStream_t s) {
   return RGNN_OK;
 }
 
+// One warp per run piece (<= kPieceRows consecutive positions of one (etype, dst) run): lane
+// groups of L = N*sizeof(T)/16 lanes gather the v and k rows of interleaved positions, fp32 sums
+// merged in a fixed xor tree.  Positions are read in order (alpha, da, vrow contiguous).
+template <typename TO, int N>
+__global__ void __launch_bounds__(256) k_hgt_piece_agg(HgtPieceArgs a) {
+  using T = float;  // v and k rows are fp32
+  constexpr int EPL = 4;
+  constexpr int L = N / EPL;
+  constexpr int G = 32 / L;
+  static_assert(L >= 1 && L <= 32, "piece agg shape");
+  const T* Vn = static_cast<const T*>(a.Vn);
+  const T* Kn = static_cast<const T*>(a.Kn);
+  const int lane = threadIdx.x & 31, g = lane / L, l = lane % L;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = warp0; w < a.num_pieces; w += nwarps) {
+    const int32_t p0 = a.piece_ptr[w], p1 = a.piece_ptr[w + 1];
+    float va[EPL], ka[EPL];
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) va[i] = ka[i] = 0.f;
+    int32_t p = p0 + g;
+    for (; p + G < p1; p += 2 * G) {  // two positions per group in flight
+      const int32_t r0 = a.vrow[p], r1 = a.vrow[p + G];
+      const float al0 = a.alpha[p], al1 = a.alpha[p + G], d0 = a.da[p], d1 = a.da[p + G];
+      const uint4 v0 = ldg16(Vn + (size_t)r0 * N + l * EPL), v1 = ldg16(Vn + (size_t)r1 * N + l * EPL);
+      const uint4 k0 = ldg16(Kn + (size_t)r0 * N + l * EPL), k1 = ldg16(Kn + (size_t)r1 * N + l * EPL);
+      float f[EPL];
+      Vec16<T>{v0}.to_float(f);
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) va[i] = fmaf(al0, f[i], va[i]);
+      Vec16<T>{v1}.to_float(f);
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) va[i] = fmaf(al1, f[i], va[i]);
+      Vec16<T>{k0}.to_float(f);
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) ka[i] = fmaf(d0, f[i], ka[i]);
+      Vec16<T>{k1}.to_float(f);
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) ka[i] = fmaf(d1, f[i], ka[i]);
+    }
+    if (p < p1) {
+      const int32_t r0 = a.vrow[p];
+      const float al0 = a.alpha[p], d0 = a.da[p];
+      float f[EPL];
+      Vec16<T>{ldg16(Vn + (size_t)r0 * N + l * EPL)}.to_float(f);
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) va[i] = fmaf(al0, f[i], va[i]);
+      Vec16<T>{ldg16(Kn + (size_t)r0 * N + l * EPL)}.to_float(f);
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) ka[i] = fmaf(d0, f[i], ka[i]);
+    }
+#pragma unroll
+    for (int o = L; o < 32; o <<= 1)
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        va[i] += __shfl_xor_sync(0xffffffffu, va[i], o);
+        ka[i] += __shfl_xor_sync(0xffffffffu, ka[i], o);
+      }
+    if (g == 0) {
+      TO* vo = static_cast<TO*>(a.vagg) + (size_t)w * N + l * EPL;
+      TO* ko = static_cast<TO*>(a.kagg) + (size_t)w * N + l * EPL;
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        vo[i] = from_f<TO>(va[i]);
+        ko[i] = from_f<TO>(ka[i]);
+      }
+      if (l == 0) {
+        const int32_t d = a.dst_s[p0];
+        a.pdst[w] = d;
+        a.pq[w] = a.ninv[a.v0 + d];
+      }
+    }
+  }
+}
+
+rgnn_status launch_hgt_piece_agg(int prec, int N, const HgtPieceArgs& a, cudaStream_t s) {
+  if (a.num_pieces == 0) return RGNN_OK;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((a.num_pieces + 7) / 8, 148 * 16));
+  const bool bf = prec == RGNN_BF16;
+#define RGNN_PIECE(T, n) \
+  if (N == n) { RGNN_LAUNCH((k_hgt_piece_agg<T, n>), grid, 256, 0, s, a); return RGNN_OK; }
+  if (bf) { RGNN_PIECE(__nv_bfloat16, 32) RGNN_PIECE(__nv_bfloat16, 64) RGNN_PIECE(__nv_bfloat16, 128) }
+  else { RGNN_PIECE(float, 32) RGNN_PIECE(float, 64) RGNN_PIECE(float, 128) }
+#undef RGNN_PIECE
+  return set_error(RGNN_E_UNSUPPORTED, "d_out=%d not in {32,64,128}", N);
+}
+
 rgnn_status launch_hgt_bwd_walk(int prec, int N, const HgtBwdArgs& a, cudaStream_t s) {
   const bool bf = prec == RGNN_BF16;
   switch (N) {

@@ -151,7 +151,7 @@ struct HgtAggArgs {
   int64_t num_items;
   const int32_t* pos;     // slot -> row of KW / M (compact: zrow_slot)
   const void* KW;         // [zrows, N] fp32: k W_{a,r}
-  const void* M;          // [zrows, N] T: v W_{m,r}
+  const void* M;          // [zrows, N] fp32: v W_{m,r}
   const void* Q;          // [V, N] fp32: q rows in node-type order
   const int32_t* ninv;    // node -> its row in Q
   int64_t v0;
@@ -182,6 +182,22 @@ struct HgtBwdArgs {
   int64_t num_split_rows;
 };
 rgnn_status launch_hgt_bwd_walk(int prec, int N, const HgtBwdArgs& a, cudaStream_t s);
+// Run-piece sums of the HGT relation gradients (pieces: rgnn_graph.piece_ptr):
+//   vagg_i = sum_{p in piece i} alpha_p v_src(p),  kagg_i = sum_p da_p k_src(p)
+// so that dWm_r = sum_i vagg_i^T G_t(i) and dWa_r = sum_i kagg_i^T q_t(i) are GEMMs over the pieces.
+struct HgtPieceArgs {
+  int64_t num_pieces;
+  const int32_t* piece_ptr;
+  const int32_t* vrow;    // position -> node-type row of the source
+  const float *alpha, *da;
+  const void *Vn, *Kn;    // [V, N] fp32 (type-order rows)
+  const int32_t* dst_s;   // position -> local dst
+  const int32_t* ninv;
+  int64_t v0;
+  void *vagg, *kagg;      // [num_pieces, N] T (the layer's operand type: bf16 feeds the tcgen05 dW)
+  int32_t *pdst, *pq;     // [num_pieces] local dst / node-type row of the dst
+};
+rgnn_status launch_hgt_piece_agg(int prec, int N, const HgtPieceArgs& a, cudaStream_t s);
 rgnn_status launch_f32_to_bf16(int64_t n, const float* a, void* b, cudaStream_t s);
 // out[i] = ninv[idx[i] + ofs]
 rgnn_status launch_map_gather(int64_t n, const int32_t* idx, const int32_t* ninv, int32_t* out, cudaStream_t s,

@@ -40,9 +40,8 @@ struct SavedLayout {
   float* s_src;    // RGAT: [E_own]
   float* lse;      // RGAT, HGT: [V_own]
   // HGT: the forward's typed-linear outputs, read by the backward
-  float *Kf, *Qf;  // [V, N] fp32 (node-type order rows)
-  float* KWf;      // [zrows, N] fp32
-  void *Vn, *M;    // [V, N], [zrows, N] T
+  float *Kf, *Qf, *Vn;  // [V, N] fp32 (node-type order rows)
+  float *KWf, *M;       // [zrows, N] fp32
   size_t bytes;
 };
 
@@ -61,22 +60,22 @@ static int64_t dw0_chunks(const rgnn_graph* g) {
 }
 
 struct HgtWs {
-  void* wt;               // bf16 transposed weights of the tcgen05 typed GEMM
-  float *Xf, *Wr;         // bf16 path: X as fp32, RNE-rounded WK | WQ | Wa
-  float* Wtr;             // tf32 GEMM weights: (rounded) WK^T | WQ^T | Wa^T
+  float *Xf, *Wr;         // bf16 path: X as fp32, RNE-rounded WK | WQ | WV | Wa | Wm
+  float* Wtr;             // tf32 GEMM weights: (rounded) WK^T | WQ^T | WV^T | Wa^T | Wm^T
   int32_t* gather;
   float* part;
   // backward (training)
   float *alpha, *da;      // [E_own] by position
-  int32_t *vrow, *qrow;   // [E_own] node-type rows of src / dst of position p
+  int32_t* vrow;          // [E_own] node-type row of the source of position p
   int32_t* qrun;          // [J] node-type row of the destination of run j
   float *dQ, *dK, *dV;    // [V, N] node-id order
   float* H;               // [J, N] fp32: G_t Wm_r^T, then q_t Wa_r^T
   void* Bb;               // [max(E_own, V), N] bf16 B operand of the tcgen05 dW GEMMs
-  void* Kb;               // [V, N] bf16 copy of k (tcgen05 dWa)
   float* dwpart;          // dW split-K partials
   float *qpart, *xpart;   // split-row partial rows (dq; dk / dv)
   float *WmT, *WaT, *Wmr, *War;  // [R, N, N]: W^T (SIMT GEMM) and W (tf32 GEMM), rounded on bf16
+  void *vagg, *kagg;      // [num_pieces, N] T: run-piece sums (relation dW GEMM operand A)
+  int32_t *pdst, *pq;     // [num_pieces]
   size_t bytes;
 };
 static HgtWs hgt_ws_layout(const rgnn_graph* g, int K, int N, int prec, void* base, bool training = false) {
@@ -88,25 +87,22 @@ static HgtWs hgt_ws_layout(const rgnn_graph* g, int K, int N, int prec, void* ba
   const bool bf = prec == RGNN_BF16;
   w.gather = c.take<int32_t>((size_t)zr);
   w.part = c.take<float>((size_t)std::max<int64_t>(g->num_parts, 1) * (N + 4));
-  const int64_t nw = std::max<int64_t>(T * K * N, (int64_t)g->R * N * N);
-  w.wt = c.take<char>(bf ? (size_t)nw * 2 : 1);
   w.Xf = c.take<float>(bf ? (size_t)V * K : 1);
-  w.Wr = c.take<float>(bf ? (size_t)(2 * T * K * N + (int64_t)g->R * N * N) : 1);
-  w.Wtr = c.take<float>((size_t)(2 * T * K * N + (int64_t)g->R * N * N));
+  w.Wr = c.take<float>(bf ? (size_t)(3 * T * K * N + 2 * (int64_t)g->R * N * N) : 1);
+  w.Wtr = c.take<float>((size_t)(3 * T * K * N + 2 * (int64_t)g->R * N * N));
   if (training) {
     const int64_t E = std::max<int64_t>(g->E_own, 1), J = std::max<int64_t>(g->J, 1);
     w.alpha = c.take<float>(E);
     w.da = c.take<float>(E);
     w.vrow = c.take<int32_t>(E);
-    w.qrow = c.take<int32_t>(E);
     w.qrun = c.take<int32_t>(J);
     w.dQ = c.take<float>((size_t)V * N);
     w.dK = c.take<float>((size_t)V * N);
     w.dV = c.take<float>((size_t)V * N);
     w.H = c.take<float>((size_t)J * N);
-    w.Bb = c.take<char>(bf ? (size_t)std::max(E, V) * N * 2 : 1);
-    w.Kb = c.take<char>(bf ? (size_t)V * N * 2 : 1);
-    const int64_t dwp = std::max<int64_t>(std::max<int64_t>(g->num_chunks, 1) * (N * N + N),
+    const int64_t NP = std::max<int64_t>(g->num_pieces, 1);
+    w.Bb = c.take<char>(bf ? (size_t)std::max(std::max(E, V), NP) * N * 2 : 1);
+    const int64_t dwp = std::max<int64_t>(std::max<int64_t>(g->num_pchunks, 1) * (N * N + N),
                                           std::max<int64_t>(g->num_nchunks, 1) * (K * N + K));
     w.dwpart = c.take<float>((size_t)dwp);
     w.qpart = c.take<float>((size_t)std::max<int64_t>(g->num_parts, 1) * N);
@@ -116,6 +112,11 @@ static HgtWs hgt_ws_layout(const rgnn_graph* g, int K, int N, int prec, void* ba
     w.WaT = c.take<float>(rnn);
     w.Wmr = c.take<float>(rnn);
     w.War = c.take<float>(rnn);
+    const size_t e = bf ? 2 : 4;
+    w.vagg = c.take<char>((size_t)NP * N * e);
+    w.kagg = c.take<char>((size_t)NP * N * e);
+    w.pdst = c.take<int32_t>(NP);
+    w.pq = c.take<int32_t>(NP);
   }
   w.bytes = c.off;
   return w;
@@ -168,8 +169,8 @@ static SavedLayout saved_layout(const rgnn_graph* g, int model, int N, int prec,
     s.Kf = c.take<float>((size_t)V * N);
     s.Qf = c.take<float>((size_t)V * N);
     s.KWf = c.take<float>((size_t)zrows(g, model) * N);
-    s.Vn = c.take<char>((size_t)V * N * elt(prec));
-    s.M = c.take<char>((size_t)zrows(g, model) * N * elt(prec));
+    s.Vn = c.take<float>((size_t)V * N);
+    s.M = c.take<float>((size_t)zrows(g, model) * N);
   }
   s.bytes = c.off;
   return s;
@@ -306,39 +307,47 @@ rgnn_status hgt_forward(const rgnn_graph* g, int K, int N, rgnn_prec prec, const
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   HgtWs w = hgt_ws_layout(g, K, N, prec, ws);
   SavedLayout sv = saved_layout(g, RGNN_HGT, N, prec, saved);
-  // Score path (k, q, k W_{a,r}) in fp32 on both paths -- bf16 logits lose too much through the
-  // exponent (O23); the message path (v, v W_{m,r}) on the typed GEMM of the layer's
-  // precision (tcgen05 on the bf16 path).  Node-typed linears run over the node-type segments
-  // (rows in type order), relation-typed ones per (etype, src) pair (or per edge).
+  // Every per-node and per-edge intermediate (k, q, v, k W_{a,r}, v W_{m,r}) is fp32 on both
+  // paths; the bf16 layer takes X and the weights in bf16 (RNE-rounded weights), so its GEMMs run
+  // on the tcgen05 kind::tf32 kernel with bf16-exact operands (and a tf32 truncation of the fp32
+  // k / v in the relation GEMMs).  bf16 logits lose too much through the exponent, and bf16 v / m
+  // rows put the backward's dWa at ~0.9 of the bf16 bound (numpy model; O23).
+  // Node-typed linears run over the node-type segments (rows in type order), relation-typed ones
+  // per (etype, src) pair (or per edge).
   const bool bf = prec == RGNN_BF16;
   const int64_t T = g->num_ntypes;
-  const float *WKs = WK, *WQs = WQ, *Was = Wa;
+  const int64_t tkn = T * K * N, rnn = (int64_t)g->R * N * N;
+  const float *WKs = WK, *WQs = WQ, *WVs = WV, *Was = Wa, *Wms = Wm;
   const void* Xs = X;
   if (bf) {
     Phase ph("hgt_prep", s);
     RGNN_TRY(launch_bf16_to_f32(g->V * K, X, w.Xf, s));
-    RGNN_TRY(launch_round_bf16(T * K * N, WK, w.Wr, s));
-    RGNN_TRY(launch_round_bf16(T * K * N, WQ, w.Wr + T * K * N, s));
-    RGNN_TRY(launch_round_bf16((int64_t)g->R * N * N, Wa, w.Wr + 2 * T * K * N, s));
-    Xs = w.Xf; WKs = w.Wr; WQs = w.Wr + T * K * N; Was = w.Wr + 2 * T * K * N;
+    RGNN_TRY(launch_round_bf16(tkn, WK, w.Wr, s));
+    RGNN_TRY(launch_round_bf16(tkn, WQ, w.Wr + tkn, s));
+    RGNN_TRY(launch_round_bf16(tkn, WV, w.Wr + 2 * tkn, s));
+    RGNN_TRY(launch_round_bf16(rnn, Wa, w.Wr + 3 * tkn, s));
+    RGNN_TRY(launch_round_bf16(rnn, Wm, w.Wr + 3 * tkn + rnn, s));
+    Xs = w.Xf; WKs = w.Wr; WQs = w.Wr + tkn; WVs = w.Wr + 2 * tkn; Was = w.Wr + 3 * tkn; Wms = Was + rnn;
   }
   {
     Phase ph("hgt_prep", s);
     RGNN_TRY(launch_transpose_w(prec, (int)T, K, N, WK, w.Wtr, s));
-    RGNN_TRY(launch_transpose_w(prec, (int)T, K, N, WQ, w.Wtr + T * K * N, s));
-    RGNN_TRY(launch_transpose_w(prec, g->R, N, N, Wa, w.Wtr + 2 * T * K * N, s));
+    RGNN_TRY(launch_transpose_w(prec, (int)T, K, N, WQ, w.Wtr + tkn, s));
+    RGNN_TRY(launch_transpose_w(prec, (int)T, K, N, WV, w.Wtr + 2 * tkn, s));
+    RGNN_TRY(launch_transpose_w(prec, g->R, N, N, Wa, w.Wtr + 3 * tkn, s));
+    RGNN_TRY(launch_transpose_w(prec, g->R, N, N, Wm, w.Wtr + 3 * tkn + rnn, s));
   }
   if (g->num_ntiles) {
     Phase ph("hgt_node_gemm", s);
-    auto node_gemm = [&](int p, const void* Xin, const float* Win, const float* Wt32, void* out) -> rgnn_status {
+    auto node_gemm = [&](const float* Win, const float* Wt32, float* out) -> rgnn_status {
       GemmFwdArgs ga{};
-      ga.tiles = g->ntiles; ga.num_tiles = g->num_ntiles; ga.X = Xin; ga.gather = g->nperm; ga.W = Win;
-      ga.Z = out; ga.wt_bf16 = w.wt; ga.num_w = (int)T; ga.x_rows = g->V; ga.z_rows = g->V;
-      return p == RGNN_F32 ? f32_gemm(prec, K, N, ga, Wt32, s) : typed_gemm(p, K, N, ga, s);
+      ga.tiles = g->ntiles; ga.num_tiles = g->num_ntiles; ga.X = Xs; ga.gather = g->nperm; ga.W = Win;
+      ga.Z = out; ga.num_w = (int)T; ga.x_rows = g->V; ga.z_rows = g->V;
+      return f32_gemm(prec, K, N, ga, Wt32, s);
     };
-    RGNN_TRY(node_gemm(RGNN_F32, Xs, WKs, w.Wtr, sv.Kf));
-    RGNN_TRY(node_gemm(RGNN_F32, Xs, WQs, w.Wtr + T * K * N, sv.Qf));
-    RGNN_TRY(node_gemm(prec, X, WV, nullptr, sv.Vn));
+    RGNN_TRY(node_gemm(WKs, w.Wtr, sv.Kf));
+    RGNN_TRY(node_gemm(WQs, w.Wtr + tkn, sv.Qf));
+    RGNN_TRY(node_gemm(WVs, w.Wtr + 2 * tkn, sv.Vn));
   }
   const bool cm = use_compact(g, RGNN_HGT);
   const int64_t zr = cm ? g->num_compact : g->E_own;
@@ -346,15 +355,15 @@ rgnn_status hgt_forward(const rgnn_graph* g, int K, int N, rgnn_prec prec, const
   {
     Phase ph("hgt_rel_gemm", s);
     RGNN_TRY(launch_map_gather(zr, cm ? g->csrc : g->src_s, g->ninv, w.gather, s));
-    auto rel_gemm = [&](int p, const void* Xin, const float* Win, const float* Wt32, void* out) -> rgnn_status {
+    auto rel_gemm = [&](const float* Xin, const float* Win, const float* Wt32, float* out) -> rgnn_status {
       GemmFwdArgs ga{};
       ga.tiles = cm ? g->ctiles : g->tiles; ga.num_tiles = nt; ga.X = Xin; ga.gather = w.gather; ga.W = Win;
-      ga.Z = out; ga.wt_bf16 = w.wt; ga.num_w = g->R; ga.x_rows = g->V; ga.z_rows = zr;
-      return p == RGNN_F32 ? f32_gemm(prec, N, N, ga, Wt32, s) : typed_gemm(p, N, N, ga, s);
+      ga.Z = out; ga.num_w = g->R; ga.x_rows = g->V; ga.z_rows = zr;
+      return f32_gemm(prec, N, N, ga, Wt32, s);
     };
     if (nt) {
-      RGNN_TRY(rel_gemm(RGNN_F32, sv.Kf, Was, w.Wtr + 2 * T * K * N, sv.KWf));
-      RGNN_TRY(rel_gemm(prec, sv.Vn, Wm, nullptr, sv.M));
+      RGNN_TRY(rel_gemm(sv.Kf, Was, w.Wtr + 3 * tkn, sv.KWf));
+      RGNN_TRY(rel_gemm(sv.Vn, Wms, w.Wtr + 3 * tkn + rnn, sv.M));
     }
   }
   {
@@ -362,7 +371,7 @@ rgnn_status hgt_forward(const rgnn_graph* g, int K, int N, rgnn_prec prec, const
     HgtAggArgs ha{};
     ha.items = g->items; ha.num_items = g->num_items; ha.pos = cm ? g->zrow_slot : g->pos; ha.KW = sv.KWf;
     ha.M = sv.M; ha.Q = sv.Qf; ha.ninv = g->ninv; ha.v0 = g->v0; ha.Y = Y; ha.lse = sv.lse; ha.part = w.part;
-    RGNN_TRY(launch_aggregate_hgt(prec, N, ha, s));
+    RGNN_TRY(launch_aggregate_hgt(RGNN_F32, N, ha, s));
     // zero rows and split-row merges of the shared walk infrastructure (online-softmax states)
     AggArgs aa{};
     aa.num_items = 0; aa.Y = Y; aa.lse = sv.lse; aa.part = w.part; aa.split_rows = g->split_rows;
@@ -377,7 +386,8 @@ rgnn_status hgt_forward(const rgnn_graph* g, int K, int N, rgnn_prec prec, const
 //   walk     : alpha_e, da_e by position; dq_t = sum_e da_e kw_e            (owned rows)
 //   runs     : Hm_j = G_t Wm_r^T, Ha_j = q_t Wa_r^T per (etype, dst) run j  (fp32 GEMMs, J << E)
 //   sources  : dv_s = sum_{e: src=s} alpha_e Hm_j(e),  dk_s = sum_e da_e Ha_j(e)   (source walk)
-//   dW       : dWm_r = sum_p v_src^T (alpha_p G_t),  dWa_r = sum_p k_src^T (da_p q_t)   (position chunks)
+//   dW       : dWm_r = sum_i vagg_i^T G_t(i), dWa_r = sum_i kagg_i^T q_t(i) over run pieces i (<= 64
+//              positions of one (etype, dst) run): vagg_i = sum_p alpha_p v_src(p), kagg_i = sum_p da_p k_src(p)
 //              dWK / dWV / dWQ [tau] = sum_{nodes of type tau} x^T dk / dv / dq    (node-type chunks)
 // On the bf16 layer the dW GEMMs run on the tcgen05 segmented dW kernel with the B rows
 // materialised in bf16 (like the RGAT dZ); on the fp32 layer on the SIMT dW kernel.
@@ -388,7 +398,8 @@ rgnn_status hgt_backward(const rgnn_graph* g, int K, int N, rgnn_prec prec, cons
   (void)WK; (void)WQ; (void)WV;
   if (!g) return set_error(RGNN_E_INVALID_ARG, "graph is NULL");
   if (!g->has_ntype) return set_error(RGNN_E_UNSUPPORTED, "HGT needs node types (rgnn_graph_desc.ntype)");
-  if (!g->has_dx) return set_error(RGNN_E_UNSUPPORTED, "HGT backward needs a graph built with RGNN_GRAPH_DX");
+  if (!g->has_dx || !g->has_pieces)
+    return set_error(RGNN_E_UNSUPPORTED, "HGT backward needs a graph built with RGNN_GRAPH_DX");
   if (!width_ok(K) || !width_ok(N)) return set_error(RGNN_E_UNSUPPORTED, "d_in=%d d_out=%d not in {32,64,128}", K, N);
   if (prec != RGNN_F32 && prec != RGNN_BF16) return set_error(RGNN_E_INVALID_ARG, "bad precision %d", prec);
   const HgtWs need = hgt_ws_layout(g, K, N, prec, nullptr, true);
@@ -417,7 +428,6 @@ rgnn_status hgt_backward(const rgnn_graph* g, int K, int N, rgnn_prec prec, cons
       RGNN_CUDA_TRY(cudaMemcpyAsync(w.War, Wa, sizeof(float) * rnn, cudaMemcpyDeviceToDevice, s));
     }
     RGNN_TRY(launch_map_gather(E, g->src_s, g->ninv, w.vrow, s));
-    RGNN_TRY(launch_map_gather(E, g->dst_s, g->ninv, w.qrow, s, g->v0));
     RGNN_TRY(launch_map_gather(J, g->run_dst, g->ninv, w.qrun, s, g->v0));
     RGNN_CUDA_TRY(cudaMemsetAsync(w.dQ, 0, sizeof(float) * (size_t)V * N, s));
     RGNN_CUDA_TRY(cudaMemsetAsync(w.dK, 0, sizeof(float) * (size_t)V * N, s));
@@ -430,7 +440,7 @@ rgnn_status hgt_backward(const rgnn_graph* g, int K, int N, rgnn_prec prec, cons
     hb.KW = sv.KWf; hb.M = sv.M; hb.Q = sv.Qf; hb.ninv = g->ninv; hb.v0 = g->v0; hb.Y = Y; hb.dY = dY;
     hb.lse = sv.lse; hb.alpha = w.alpha; hb.da = w.da; hb.dQ = w.dQ; hb.part = w.qpart;
     hb.split_rows = g->split_rows; hb.num_split_rows = g->num_split_rows;
-    RGNN_TRY(launch_hgt_bwd_walk(prec, N, hb, s));
+    RGNN_TRY(launch_hgt_bwd_walk(RGNN_F32, N, hb, s));
   }
   // source sums: dv = sum alpha Hm, dk = sum da Ha over each source's out-edges
   auto src_sum = [&](const float* G, const int32_t* gidx, int64_t grows, const float* Wt, const float* Wrr,
@@ -439,7 +449,7 @@ rgnn_status hgt_backward(const rgnn_graph* g, int K, int N, rgnn_prec prec, cons
       Phase ph("hgt_bwd_runs", s);
       GemmFwdArgs gh{};
       gh.tiles = g->rtiles; gh.num_tiles = g->num_rtiles; gh.X = G; gh.gather = gidx; gh.W = Wt; gh.Z = w.H;
-      gh.wt_bf16 = w.wt; gh.num_w = g->R; gh.x_rows = std::max<int64_t>(grows, 1); gh.z_rows = J;
+      gh.num_w = g->R; gh.x_rows = std::max<int64_t>(grows, 1); gh.z_rows = J;
       RGNN_TRY(f32_gemm(prec, N, N, gh, Wrr, s));
     }
     Phase ph("hgt_bwd_src", s);
@@ -478,17 +488,19 @@ rgnn_status hgt_backward(const rgnn_graph* g, int K, int N, rgnn_prec prec, cons
                             nullptr, nullptr, s);
   };
   {
+    // relation gradients over the run pieces: the piece sums collapse each piece's positions
+    // (same relation and destination) into one GEMM row
     Phase ph("hgt_bwd_dw_rel", s);
-    RGNN_TRY(dw(prec, N, sv.Vn, w.vrow, V, g->chunks, g->num_chunks, g->chunk_seg, g->R, E, dY, g->dst_s, w.alpha,
-                dWm));
-    const void* Kin = sv.Kf;
-    int kp = RGNN_F32;
-    if (bf) {
-      RGNN_TRY(launch_f32_to_bf16((int64_t)V * N, sv.Kf, w.Kb, s));
-      Kin = w.Kb;
-      kp = RGNN_BF16;
-    }
-    RGNN_TRY(dw(kp, N, Kin, w.vrow, V, g->chunks, g->num_chunks, g->chunk_seg, g->R, E, sv.Qf, w.qrow, w.da, dWa));
+    HgtPieceArgs pa{};
+    pa.num_pieces = g->num_pieces; pa.piece_ptr = g->piece_ptr; pa.vrow = w.vrow; pa.alpha = w.alpha; pa.da = w.da;
+    pa.Vn = sv.Vn; pa.Kn = sv.Kf; pa.dst_s = g->dst_s; pa.ninv = g->ninv; pa.v0 = g->v0; pa.vagg = w.vagg;
+    pa.kagg = w.kagg; pa.pdst = w.pdst; pa.pq = w.pq;
+    RGNN_TRY(launch_hgt_piece_agg(prec, N, pa, s));
+    const int64_t NP = g->num_pieces;
+    RGNN_TRY(dw(prec, N, w.vagg, nullptr, std::max<int64_t>(NP, 1), g->pchunks, g->num_pchunks, g->pchunk_seg, g->R, NP,
+                dY, w.pdst, nullptr, dWm));
+    RGNN_TRY(dw(prec, N, w.kagg, nullptr, std::max<int64_t>(NP, 1), g->pchunks, g->num_pchunks, g->pchunk_seg, g->R, NP,
+                sv.Qf, w.pq, nullptr, dWa));
   }
   {
     Phase ph("hgt_bwd_dw_node", s);

@@ -153,3 +153,23 @@ def test_hgt_backward_needs_dx_tables(rgnn):
     with pytest.raises(rgnn.RgnnError) as ei:
         rgnn.hgt_backward(G, X, *Ws, Y, torch.from_numpy(t.dY).cuda(), ws, prec="f32")
     assert ei.value.status == 3
+
+
+def _hub_graph():
+    """Random graph plus hub runs: 700 edges of relation 1 into node 3 and 130 of relation 0 into
+    node 5 (runs longer than one 64-position piece, cut mid-run), and an isolated node type."""
+    base = synth.random_graph(200, 1500, 3, seed=11, T=3)
+    rng = np.random.Generator(np.random.PCG64(12))
+    src = np.r_[base.src, rng.integers(0, 200, 700), rng.integers(0, 200, 130)].astype(np.int32)
+    dst = np.r_[base.dst, np.full(700, 3), np.full(130, 5)].astype(np.int32)
+    et = np.r_[base.etype, np.full(700, 1), np.zeros(130)].astype(np.int32)
+    perm = rng.permutation(src.shape[0])
+    return synth.HeteroGraph(V=200, R=3, T=3, src=src[perm], dst=dst[perm], etype=et[perm], ntype=base.ntype,
+                             name="hub")
+
+
+@pytest.mark.parametrize("prec", ["f32", "bf16"])
+def test_hgt_backward_long_runs(rgnn, prec):
+    g = _hub_graph()
+    t = synth.make_hgt_tensors(g.V, g.R, g.T, 64, 64)
+    _check_grads(_run_bwd(rgnn, g, t, prec, materialization="vanilla"), _ref_bwd(g, t, prec), prec, "hgt bwd hub")
