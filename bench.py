@@ -98,10 +98,10 @@ def algorithmic_bytes(phase, model, prec, K, N, E, V_own, J, num_items, U=None):
     b = 2 if prec == "bf16" else 4
     if phase == "gemm_fwd":  # gather X rows, write Z, read src index (+ s_src write for RGAT, + 1/c read for RGCN)
         return (E if U is None else U) * (K * b + N * b + 4 + 4)
-    if phase == "aggregate" and model == "hgt":  # per edge: slot row, kw row (fp32), m row; per row q, Y, lse, item
-        return E * (4 + N * 4 + N * b) + num_items * (N * 4 + N * 4 + 4 + 16)
-    if phase == "hgt_bwd_walk":  # per edge: slot pos (+ row), kw row (fp32), m row, alpha/da writes; per row q, G, Y, dq
-        return E * (4 + (4 if U is not None else 0) + N * 4 + N * b + 8) + num_items * (4 * N * 4 + 4 + 16)
+    if phase == "aggregate" and model == "hgt":  # per edge: slot row, kw and m rows (fp32); per row q, Y, lse, item
+        return E * (4 + 2 * N * 4) + num_items * (N * 4 + N * 4 + 4 + 16)
+    if phase == "hgt_bwd_walk":  # per edge: slot pos (+ row), kw and m rows (fp32), alpha/da writes; per row q, G, Y, dq
+        return E * (4 + (4 if U is not None else 0) + 2 * N * 4 + 8) + num_items * (4 * N * 4 + 4 + 16)
     if phase == "aggregate":  # read pos, et, Z row (+ s_src) per edge; X_dst, Y, lse, item per row
         per_e = N * b + 8 + (4 if model == "rgat" or U is not None else 0)
         per_v = (K * b + N * 4 + 4 + 16) if model == "rgat" else (N * 4 + 16)

@@ -26,6 +26,10 @@ FULL_METRICS = {
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_pct_peak",
     "l1tex__throughput.avg.pct_of_peak_sustained_active": "l1_pct_peak",
     "lts__throughput.avg.pct_of_peak_sustained_elapsed": "l2_pct_peak",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed": "tensor_pipe_pct_peak",
+    "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed": "tc_pipe_pct_peak",
+    "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed": "tensor_hmma_pct_peak",
+    "sm__inst_executed_pipe_tc.sum": "tc_pipe_inst",
 }
 
 
