@@ -43,7 +43,14 @@ def _worker(rank, world, port, model, out_q):
         v0, v1 = int(bounds[rank]), int(bounds[rank + 1])
         G = np.zeros((g.V, 16)); G[v0:v1] = t.dY[v0:v1]
         rows = np.arange(v0, v1)
-        if model == "rgat":
+        if model == "hgt":  # NEXT-3: same partition; dWK, dWQ, dWV, dWa, dWm all-reduced
+            h = synth.make_hgt_tensors(g.V, g.R, g.T, 16, 16)
+            hw = (h.X, h.WK, h.WQ, h.WV, h.Wa, h.Wm)
+            G = np.zeros((g.V, 16)); G[v0:v1] = h.dY[v0:v1]
+            Y, _ = oracle.hgt_forward(g.V, g.R, g.src, g.dst, g.etype, g.ntype, *hw, rows=rows)
+            grads = oracle.hgt_backward(g.V, g.R, g.src, g.dst, g.etype, g.ntype, *hw, G, v0=v0, v1=v1)
+            dW, dA = np.concatenate([x.ravel() for x in grads]), np.zeros(1)
+        elif model == "rgat":
             Y, _, _ = oracle.rgat_forward(g.V, g.R, g.src, g.dst, g.etype, t.X, t.W, t.A, rows=rows)
             dW, dA = oracle.rgat_backward(g.V, g.R, g.src, g.dst, g.etype, t.X, t.W, t.A, G, v0=v0, v1=v1)
         else:
@@ -61,7 +68,11 @@ def _worker(rank, world, port, model, out_q):
         dist.all_reduce(dWt)
         dist.all_reduce(dAt)
         if rank == 0:
-            if model == "rgat":
+            if model == "hgt":
+                Yr, _ = oracle.hgt_forward(g.V, g.R, g.src, g.dst, g.etype, g.ntype, *hw)
+                gr = oracle.hgt_backward(g.V, g.R, g.src, g.dst, g.etype, g.ntype, *hw, h.dY)
+                dWr, dAr = np.concatenate([x.ravel() for x in gr]), np.zeros(1)
+            elif model == "rgat":
                 Yr, _, _ = oracle.rgat_forward(g.V, g.R, g.src, g.dst, g.etype, t.X, t.W, t.A)
                 dWr, dAr = oracle.rgat_backward(g.V, g.R, g.src, g.dst, g.etype, t.X, t.W, t.A, t.dY[:, :16])
             else:
@@ -80,7 +91,7 @@ def _worker(rank, world, port, model, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("model", ["rgat", "rgcn"])
+@pytest.mark.parametrize("model", ["rgat", "rgcn", "hgt"])
 def test_two_rank_dst_partition_gloo(model):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
