@@ -40,6 +40,31 @@ def test_single_rank_nccl_matches_no_comm(rgnn, model):
         assert torch.equal(dA0, dA1)
 
 
+def test_single_rank_nccl_matches_no_comm_hgt(rgnn):
+    import torch
+    g = synth.make_graph(synth.get_config("bgs").scaled(10))
+    t = synth.make_hgt_tensors(g.V, g.R, g.T, 64, 64)
+    G = rgnn.Graph(g.V, g.src, g.dst, g.etype, g.R, ntype=g.ntype, num_ntypes=g.T, build_dx=True)
+    X = torch.from_numpy(t.X).cuda().to(torch.bfloat16)
+    Ws = [torch.from_numpy(a).cuda() for a in (t.WK, t.WQ, t.WV, t.Wa, t.Wm)]
+    dY = torch.from_numpy(t.dY).cuda()
+    comm = rgnn.Comm([0, g.V], 0, 1)
+
+    def run(c):
+        Y_full = torch.full((g.V, 64), float("nan"), device="cuda") if c else None
+        ws = rgnn.Workspace(G, "hgt", 64, 64, "bf16", training=True)
+        Y, ws = rgnn.hgt_forward(G, X, *Ws, prec="bf16", ws=ws, comm=c, Y_full=Y_full)
+        grads = rgnn.hgt_backward(G, X, *Ws, Y, dY, ws, prec="bf16", comm=c)
+        torch.cuda.synchronize()
+        return Y, Y_full, grads
+
+    Y0, _, g0 = run(None)
+    Y1, Yf, g1 = run(comm)
+    assert torch.equal(Y0, Y1) and torch.equal(Yf, Y1)
+    for a, b in zip(g0, g1):
+        assert torch.equal(a, b)
+
+
 def test_comm_rejects_mismatched_range(rgnn):
     import torch
     g = synth.random_graph(100, 500, 3, seed=2)
