@@ -400,6 +400,26 @@ def run_ours(args):
     barrier()
     phases = m._binding.profile_read()
     m._binding.profile_enable(False)
+    # per-step distribution: fwd, bwd and fwd+bwd of each eager step by CUDA events
+    ev = []
+    barrier()
+    for _ in range(args.steps):
+        if flush:
+            fbuf.fill_(1)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(stream)
+        fwd()
+        e[1].record(stream)
+        bwd()
+        e[2].record(stream)
+        ev.append(e)
+    barrier()
+
+    def pct(xs):
+        return {"p10": round(float(np.percentile(xs, 10)), 4), "p50": round(float(np.percentile(xs, 50)), 4),
+                "p90": round(float(np.percentile(xs, 90)), 4)}
+    step_pct = {"fwd": pct([e[0].elapsed_time(e[1]) for e in ev]), "bwd": pct([e[1].elapsed_time(e[2]) for e in ev]),
+                "fwd+bwd": pct([e[0].elapsed_time(e[2]) for e in ev]), "launch": "eager", "steps": len(ev)}
     if world > 1:  # max over ranks
         tm = torch.tensor([ms], device=dev)
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
@@ -530,6 +550,7 @@ def run_ours(args):
                "clocks": clocks, "e2e": e2e,
                "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu,
                "phases_ms_per_step": {k: round(x[0], 4) for k, x in sorted(step_phase.items())},
+               "step_ms_percentiles": step_pct,
                "preprocess_ms": prep_ms, "generate_s": round(t_gen, 1)}
         print(json.dumps(out), flush=True)
     if world > 1:
