@@ -209,13 +209,21 @@ rgnn_status launch_aggregate_hgt(int prec, int N, const HgtAggArgs& a, cudaStrea
 // alpha_e and da_e are stored by position: the source sums (dk, dv) and the relation dW GEMMs
 // read them.  One warp per work item as the forward walk; a lane group of L = N*sizeof(TM)/16
 // lanes handles one edge, its lanes each holding EPL features of kw, m, q, G and dq.
+#ifndef RGNN_HGTB_UNR
+#define RGNN_HGTB_UNR 4
+#endif
+#ifndef RGNN_HGTB_MINB
+#define RGNN_HGTB_MINB 4
+#endif
 template <typename TM, int N>
-__global__ void __launch_bounds__(256) k_hgt_bwd_walk(HgtBwdArgs a) {
+__global__ void __launch_bounds__(256, RGNN_HGTB_MINB) k_hgt_bwd_walk(HgtBwdArgs a) {
   constexpr int EPL = 16 / sizeof(TM);
   constexpr int SV = EPL * 4 / 16;  // fp32 16-byte vectors per lane slice (kw, q, G, Y)
   constexpr int L = N / EPL;
   constexpr int G = 32 / L;
-  static_assert(L >= 1 && L <= 32, "hgt bwd walk shape");
+  constexpr int UNR = G >= 4 ? 1 : RGNN_HGTB_UNR;  // edges per lane group per step (rows in flight)
+  constexpr int B = G * UNR;
+  static_assert(L >= 1 && L <= 32 && B <= 32, "hgt bwd walk shape");
   const float* KW = static_cast<const float*>(a.KW);
   const TM* M = static_cast<const TM*>(a.M);
   const float* Q = static_cast<const float*>(a.Q);
@@ -224,56 +232,65 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_walk(HgtBwdArgs a) {
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t w = warp0; w < a.num_items; w += nwarps) {
     const Item it = a.items[w];
-    float qf[EPL], gf[EPL], yf[EPL];
+    float qf[EPL], gf[EPL];
+    float S = 0.f;
     {
       const float* qp = Q + (size_t)a.ninv[a.v0 + it.row] * N + l * EPL;
       const float* gp = a.dY + (size_t)it.row * N + l * EPL;
       const float* yp = a.Y + (size_t)it.row * N + l * EPL;
 #pragma unroll
       for (int v = 0; v < SV; ++v) {
+        float yf[4];
         Vec16<float>{ldg16(qp + 4 * v)}.to_float(qf + 4 * v);
         Vec16<float>{ldg16(gp + 4 * v)}.to_float(gf + 4 * v);
-        Vec16<float>{ldg16(yp + 4 * v)}.to_float(yf + 4 * v);
+        Vec16<float>{ldg16(yp + 4 * v)}.to_float(yf);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) S = fmaf(gf[4 * v + i], yf[i], S);
       }
     }
-    float S = 0.f;
-#pragma unroll
-    for (int i = 0; i < EPL; ++i) S = fmaf(gf[i], yf[i], S);
     S = group_sum<L>(S);
     const float lse = a.lse[it.row];
     float dq[EPL];
 #pragma unroll
     for (int i = 0; i < EPL; ++i) dq[i] = 0.f;
-    for (int32_t base = it.q0; base < it.q1; base += G) {
-      const int32_t q = base + g;
-      const bool ok = q < it.q1;
-      const int32_t p = ok ? a.pos[q] : 0;
-      const int32_t z = ok ? (a.zrow ? a.zrow[q] : p) : 0;
-      float kf[EPL], mf[EPL];
-      if (ok) {
+    for (int32_t base = it.q0; base < it.q1; base += B) {
+      uint4 kr[UNR][SV], mr[UNR];
+      int32_t pp[UNR];
+      bool ok[UNR];
 #pragma unroll
-        for (int v = 0; v < SV; ++v) Vec16<float>{ldg16(KW + (size_t)z * N + l * EPL + 4 * v)}.to_float(kf + 4 * v);
-        Vec16<TM>{ldg16(M + (size_t)z * N + l * EPL)}.to_float(mf);
-      } else {
+      for (int u = 0; u < UNR; ++u) {
+        const int32_t q = base + u * G + g;
+        ok[u] = q < it.q1;
+        pp[u] = ok[u] ? a.pos[q] : 0;
+        const int32_t z = ok[u] ? (a.zrow ? a.zrow[q] : pp[u]) : 0;
 #pragma unroll
-        for (int i = 0; i < EPL; ++i) kf[i] = mf[i] = 0.f;
-      }
-      float sa = 0.f, sd = 0.f;
-#pragma unroll
-      for (int i = 0; i < EPL; ++i) {
-        sa = fmaf(kf[i], qf[i], sa);
-        sd = fmaf(gf[i], mf[i], sd);
-      }
-      sa = group_sum<L>(sa);
-      sd = group_sum<L>(sd);
-      const float al = ok ? __expf(sa - lse) : 0.f;
-      const float dae = al * (sd - S);
-      if (ok && l == 0) {
-        a.alpha[p] = al;
-        a.da[p] = dae;
+        for (int v = 0; v < SV; ++v)
+          kr[u][v] = ok[u] ? ldg16(KW + (size_t)z * N + l * EPL + 4 * v) : make_uint4(0, 0, 0, 0);
+        mr[u] = ok[u] ? ldg16(M + (size_t)z * N + l * EPL) : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
-      for (int i = 0; i < EPL; ++i) dq[i] = fmaf(dae, kf[i], dq[i]);
+      for (int u = 0; u < UNR; ++u) {
+        float kf[EPL], mf[EPL];
+#pragma unroll
+        for (int v = 0; v < SV; ++v) Vec16<float>{kr[u][v]}.to_float(kf + 4 * v);
+        Vec16<TM>{mr[u]}.to_float(mf);
+        float sa = 0.f, sd = 0.f;
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) {
+          sa = fmaf(kf[i], qf[i], sa);
+          sd = fmaf(gf[i], mf[i], sd);
+        }
+        sa = group_sum<L>(sa);
+        sd = group_sum<L>(sd);
+        const float al = ok[u] ? __expf(sa - lse) : 0.f;
+        const float dae = al * (sd - S);
+        if (ok[u] && l == 0) {
+          a.alpha[pp[u]] = al;
+          a.da[pp[u]] = dae;
+        }
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) dq[i] = fmaf(dae, kf[i], dq[i]);
+      }
     }
 #pragma unroll
     for (int o = L; o < 32; o <<= 1)
