@@ -30,17 +30,27 @@ struct BfCfg {
 #ifndef RGNN_BWD_MT
 #define RGNN_BWD_MT 64
 #endif
-  static constexpr int MT = RGNN_BWD_MT;                     // positions per stage
+#ifndef RGNN_BWD_MT128
+#define RGNN_BWD_MT128 RGNN_BWD_MT
+#endif
+  static constexpr int MT = N == 128 ? RGNN_BWD_MT128 : RGNN_BWD_MT;  // positions per stage
   static constexpr int A_BYTES = MT * K * 2;
   static constexpr int B_BYTES = MT * N * 2;
   static constexpr int B2_BYTES = MT * 16 * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES + B2_BYTES;  // multiple of 1024 (SW128 bases)
   static constexpr int SC_STAGE = MT * 8;                     // per position: local dst (int), s_src or 1/c (float)
-  static constexpr int STAGES = (200 * 1024) / (STAGE + SC_STAGE) > 6 ? 6 : (200 * 1024) / (STAGE + SC_STAGE);
+#ifndef RGNN_BWD_SMAX
+#define RGNN_BWD_SMAX 6
+#endif
+  static constexpr int STAGES = (200 * 1024) / (STAGE + SC_STAGE) > RGNN_BWD_SMAX ? RGNN_BWD_SMAX
+                                                                                  : (200 * 1024) / (STAGE + SC_STAGE);
 #ifndef RGNN_BWD_CW
 #define RGNN_BWD_CW 16
 #endif
-  static constexpr int CW = RGNN_BWD_CW;                     // compute warps
+#ifndef RGNN_BWD_CW128
+#define RGNN_BWD_CW128 RGNN_BWD_CW
+#endif
+  static constexpr int CW = N == 128 ? RGNN_BWD_CW128 : RGNN_BWD_CW;  // compute warps
   static constexpr int PW = 4;                               // cp.async producer warps
   static constexpr int THREADS = 32 + PW * 32 + CW * 32;     // MMA warp, producers, compute warps
   static constexpr int DEPTH = STAGES - 1;                   // cp.async groups in flight per producer thread
@@ -375,9 +385,8 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
     const int row = K == 128 ? q * 32 + lane : q * 16 + lane;
     const bool rvalid = K == 128 || lane < 16;
     float* out = pr.part + (size_t)blockIdx.x * (K * N + K);
-    constexpr int HALF = N / (C::CW / 4);
-#pragma unroll
-    for (int c0 = half * HALF; c0 < (half + 1) * HALF; c0 += 16) {
+    // the CW / 4 warps of a lane quarter take interleaved 16-column chunks
+    for (int c0 = half * 16; c0 < N; c0 += (C::CW / 4) * 16) {
       uint32_t v[16];
       tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
       tc::tmem_ld_wait();

@@ -50,17 +50,6 @@ rgnn_status launch_map_gather(int64_t n, const int32_t* idx, const int32_t* ninv
   return RGNN_OK;
 }
 
-__global__ void k_f32_to_bf16(int64_t n, const float* __restrict__ a, __nv_bfloat16* __restrict__ b) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    b[i] = __float2bfloat16_rn(a[i]);
-}
-rgnn_status launch_f32_to_bf16(int64_t n, const float* a, void* b, cudaStream_t s) {
-  if (n == 0) return RGNN_OK;
-  RGNN_LAUNCH(k_f32_to_bf16, (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, s, n, a,
-              static_cast<__nv_bfloat16*>(b));
-  return RGNN_OK;
-}
-
 // One warp per work item (a destination row or a chunk of a hub row), as k_aggregate:
 // L = N*sizeof(T)/16 lanes read a 16-byte slice of the kw row and of the m row of an
 // edge; the warp's 32/L lane groups take interleaved edges with their own online

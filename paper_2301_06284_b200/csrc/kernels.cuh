@@ -198,7 +198,6 @@ struct HgtPieceArgs {
   int32_t *pdst, *pq;     // [num_pieces] local dst / node-type row of the dst
 };
 rgnn_status launch_hgt_piece_agg(int prec, int N, const HgtPieceArgs& a, cudaStream_t s);
-rgnn_status launch_f32_to_bf16(int64_t n, const float* a, void* b, cudaStream_t s);
 // out[i] = ninv[idx[i] + ofs]
 rgnn_status launch_map_gather(int64_t n, const int32_t* idx, const int32_t* ninv, int32_t* out, cudaStream_t s,
                               int64_t ofs = 0);
