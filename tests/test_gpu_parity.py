@@ -110,6 +110,9 @@ SMALL = [
     ("rand-kn", lambda: (synth.random_graph(400, 3000, 5, seed=8), 64, 128)),
     ("mutag/8", lambda: (synth.make_graph(synth.get_config("mutag").scaled(8)), 64, 64)),
     ("aifb", lambda: (synth.make_graph(synth.get_config("aifb")), 32, 32)),
+    # AM-shaped short rows (mean 4.3 in-edges per row, hub rows split)
+    ("am/60", lambda: (synth.make_graph(synth.get_config("am").scaled(60)), 64, 64)),
+    ("am/60-d32", lambda: (synth.make_graph(synth.get_config("am").scaled(60)), 32, 32)),
 ]
 
 
@@ -196,3 +199,4 @@ def test_determinism_and_simulated_shards(rgnn):
     np.testing.assert_array_equal(np.concatenate(ys), a["Y"])
     ref = run_oracle(oracle, g, t, "rgat", prec="bf16")
     assert_close(sum(dws), ref["dW"], "bf16", "sharded dW sum", per_slice=True)
+
