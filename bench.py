@@ -486,21 +486,75 @@ def run_ours(args):
             main.synchronize()  # the host reads the results every step
             s_out.synchronize()
 
-        e2e_step()
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(n_e2e):
-            e2e_step()
-        barrier()
-        ems = 1e3 * (time.perf_counter() - t0) / n_e2e
-        if world > 1:
-            tm = torch.tensor([ems], device=dev)
-            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-            ems = float(tm.item())
-        e2e = {"value": g.E / (ems * 1e-3), "unit": UNIT, "ms_per_step": ems, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "steps": n_e2e,
-               "pipelining": "X, W in then forward; dY copied in on a side stream during the forward, Y copied "
-                             "out on a side stream during the backward; gradients out after it"}
+        def timed(fn):
+            fn()
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(n_e2e):
+                fn()
+            barrier()
+            ems = 1e3 * (time.perf_counter() - t0) / n_e2e
+            if world > 1:
+                tm = torch.tensor([ems], device=dev)
+                dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+                ems = float(tm.item())
+            return ems
+
+        ems = timed(e2e_step)
+        e2e_io = {"value": g.E / (ems * 1e-3), "unit": UNIT, "ms_per_step": ems, "h2d_bytes_per_step": int(h2d),
+                  "d2h_bytes_per_step": int(d2h), "steps": n_e2e,
+                  "protocol": "layer I/O: X, W (A) and dY in, Y and the gradients out every step",
+                  "pipelining": "X, W in then forward; dY copied in on a side stream during the forward, Y copied "
+                                "out on a side stream during the backward; gradients out after it"}
+
+        # Training step of the paper's protocol (NLL loss on random labels): X, the weights and
+        # the labels in; forward; loss = NLL(log_softmax(Y)) and dY = d loss / dY on the device (torch,
+        # the caller's loss -- not part of the layer); backward; the loss and the gradients out.
+        lab = np.random.Generator(np.random.PCG64(5)).integers(0, N, size=g.V)  # label_seed = 5
+        hlab = torch.from_numpy(np.ascontiguousarray(lab[v0:v1])).pin_memory()
+        dlab = torch.empty_like(hlab, device=dev)
+        oloss = torch.empty(1, dtype=torch.float32).pin_memory()
+        nll_scale = 1.0 / g.V  # mean over all V rows (every rank owns a slice)
+
+        def train_step():
+            main = torch.cuda.current_stream(dev)
+            dX_.copy_(hX, non_blocking=True)
+            dlab.copy_(hlab, non_blocking=True)
+            if model == "hgt":
+                for a, b in zip(dHW, hHW):
+                    a.copy_(b, non_blocking=True)
+            else:
+                dW_.copy_(hW, non_blocking=True)
+                dA_.copy_(hA, non_blocking=True)
+            fwd(dX_, dW_, dA_, HWs=dHW if model == "hgt" else None)
+            lp = torch.log_softmax(Y, dim=1)
+            loss = -lp.gather(1, dlab.view(-1, 1)).sum() * nll_scale
+            dyy = lp.exp_()
+            dyy[torch.arange(dyy.shape[0], device=dev), dlab] -= 1.0
+            dyy.mul_(nll_scale)
+            bwd(dX_, dW_, dA_, dyy, HWs=dHW if model == "hgt" else None)
+            oloss.copy_(loss.view(1), non_blocking=True)
+            if model == "hgt":
+                for o, gr in zip(ohg, hgrads):
+                    o.copy_(gr, non_blocking=True)
+            else:
+                odW.copy_(dW, non_blocking=True)
+                if odA is not None:
+                    odA.copy_(dA, non_blocking=True)
+            main.synchronize()
+
+        tms = timed(train_step)
+        h2d_t = hX.numel() * hX.element_size() + hlab.numel() * 8 + (
+            sum(a.numel() * 4 for a in hHW) if model == "hgt" else hW.numel() * 4 + hA.numel() * 4)
+        d2h_t = 4 + (sum(a.numel() * 4 for a in ohg) if model == "hgt" else
+                     odW.numel() * 4 + (odA.numel() * 4 if odA is not None else 0))
+        e2e = {"value": g.E / (tms * 1e-3), "unit": UNIT, "ms_per_step": tms, "h2d_bytes_per_step": int(h2d_t),
+               "d2h_bytes_per_step": int(d2h_t), "steps": n_e2e,
+               "protocol": "training step (P:843): X, weights and random labels in; forward; NLL(log_softmax(Y)) "
+                           "loss and dY on the device (torch, the caller's loss); backward; loss and weight "
+                           "gradients out"
+                           + ("; dX not computed" if not args.dx else "; dX computed, not copied out"),
+               "layer_io": e2e_io}
 
     # ---- roofline of the dominant kernel phase (live CUDA-event durations from the timed region)
     hbm, tflops, peak_src = peaks()
