@@ -112,6 +112,9 @@ __device__ __forceinline__ void dst_scores(const float* xv, const float* U, int 
 #ifndef RGNN_AGG_MINB
 #define RGNN_AGG_MINB 4
 #endif
+#ifndef RGNN_AGG_PREFETCH
+#define RGNN_AGG_PREFETCH 1
+#endif
 template <typename T, int K, int N, bool RGAT, bool CACHE>
 __global__ void __launch_bounds__(256, RGNN_AGG_MINB) k_aggregate(AggArgs a) {
   using S = WalkShape<T, K, N>;
@@ -164,6 +167,25 @@ __global__ void __launch_bounds__(256, RGNN_AGG_MINB) k_aggregate(AggArgs a) {
         val[u] = base + j < it.q1;
         zr[u] = val[u] ? ldg16(Z + (size_t)p * N + l * EPL) : make_uint4(0, 0, 0, 0);
       }
+#if RGNN_AGG_PREFETCH
+      // L2 prefetch of the Z rows (and s_src) RGNN_AGG_PREFETCH steps ahead: no registers are
+      // held for them (one 128-byte line per instruction)
+      {
+        int pq = np;
+        bool pok = nok;
+        if constexpr (RGNN_AGG_PREFETCH > 1) {
+          const int q2 = base + RGNN_AGG_PREFETCH * B + lane;
+          pok = lane < B && q2 < it.q1;
+          pq = pok ? a.pos[q2] : 0;
+        }
+        if (pok) {
+          const char* zp = reinterpret_cast<const char*>(Z + (size_t)pq * N);
+#pragma unroll
+          for (int o = 0; o < N * (int)sizeof(T); o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(zp + o));
+          if constexpr (RGAT) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.s_src + pq));
+        }
+      }
+#endif
       if constexpr (RGAT) dst_scores<K, L, KPL, UNR, CACHE>(xv, a.U, l, rr, ssv, cr, cd, sc);
       else {
 #pragma unroll
