@@ -1,3 +1,7 @@
+"""Worst ratio of |GPU - oracle| to reading O19's bf16 bound (0.02 rms(slice) + 0.02 |ref|) for each
+HGT gradient on three dst-range shards of a BGS-shaped graph (run on the GPU box):
+    python tools/hgt_precision.py            (RGNN_DISABLE_TCGEN05=1 for the SIMT kernels)
+Used to choose the HGT precision layout (O23)."""
 import sys, os; sys.path.insert(0,'tests'); sys.path.insert(0,'.')
 import numpy as np, synth
 import paper_2301_06284_b200 as rgnn
