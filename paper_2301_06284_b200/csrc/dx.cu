@@ -35,19 +35,21 @@ __global__ void k_transpose_w(int R, int K, int N, const float* __restrict__ W, 
 // 16-byte loads, the warp's 32/L lane groups take interleaved slots, group
 // states merge in a fixed xor tree.  Chunks of split sources write partial
 // rows, summed in order by k_dx_merge.
-template <int K, bool RGAT>
+template <int K, bool RGAT, typename TH>
 __global__ void __launch_bounds__(256) k_dx_walk(DxArgs a) {
-  constexpr int EPL = 4;
+  constexpr int EPL = 16 / sizeof(TH);
   constexpr int L = K / EPL;
   constexpr int G = 32 / L;
   static_assert(L >= 1 && L <= 32, "dx walk shape");
-  const float* H = static_cast<const float*>(a.H);
+  const TH* H = static_cast<const TH*>(a.H);
   const int lane = threadIdx.x & 31, g = lane / L, l = lane % L;
   const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t w = warp0; w < a.num_items; w += nwarps) {
     const Item it = a.items[w];
-    float acc[EPL] = {0.f, 0.f, 0.f, 0.f};
+    float acc[EPL];
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
     for (int32_t q = it.q0 + g; q < it.q1; q += G) {
       const int32_t j = a.srun[q];
       float c, d = 0.f;
@@ -60,13 +62,17 @@ __global__ void __launch_bounds__(256) k_dx_walk(DxArgs a) {
       } else {
         c = a.wpos ? a.wpos[a.spos[q]] : a.sinvc[q];
       }
-      const float4 h = __ldg(reinterpret_cast<const float4*>(H + (size_t)j * K + l * EPL));
-      acc[0] = fmaf(c, h.x, acc[0]); acc[1] = fmaf(c, h.y, acc[1]);
-      acc[2] = fmaf(c, h.z, acc[2]); acc[3] = fmaf(c, h.w, acc[3]);
+      float hf[EPL];
+      Vec16<TH>{ldg16(H + (size_t)j * K + l * EPL)}.to_float(hf);
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) acc[i] = fmaf(c, hf[i], acc[i]);
       if constexpr (RGAT) {
-        const float4 u0 = __ldg(reinterpret_cast<const float4*>(a.U0 + (size_t)r * K + l * EPL));
-        acc[0] = fmaf(d, u0.x, acc[0]); acc[1] = fmaf(d, u0.y, acc[1]);
-        acc[2] = fmaf(d, u0.z, acc[2]); acc[3] = fmaf(d, u0.w, acc[3]);
+#pragma unroll
+        for (int i = 0; i < EPL; i += 4) {
+          const float4 u0 = __ldg(reinterpret_cast<const float4*>(a.U0 + (size_t)r * K + l * EPL + i));
+          acc[i] = fmaf(d, u0.x, acc[i]); acc[i + 1] = fmaf(d, u0.y, acc[i + 1]);
+          acc[i + 2] = fmaf(d, u0.z, acc[i + 2]); acc[i + 3] = fmaf(d, u0.w, acc[i + 3]);
+        }
       }
     }
 #pragma unroll
@@ -75,8 +81,10 @@ __global__ void __launch_bounds__(256) k_dx_walk(DxArgs a) {
       for (int i = 0; i < EPL; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
     if (g == 0) {
       float* out = it.part < 0 ? a.dX + (size_t)it.row * K : a.part + (size_t)it.part * K;
-      stg16(out + l * EPL, make_uint4(__float_as_uint(acc[0]), __float_as_uint(acc[1]), __float_as_uint(acc[2]),
-                                      __float_as_uint(acc[3])));
+#pragma unroll
+      for (int i = 0; i < EPL; i += 4)
+        stg16(out + l * EPL + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]),
+                                            __float_as_uint(acc[i + 2]), __float_as_uint(acc[i + 3])));
     }
   }
 }
@@ -175,8 +183,13 @@ static rgnn_status dx_walk(bool rgat, const DxArgs& a, cudaStream_t s) {
   {
     Phase ph("dx_src", s);
     if (a.num_items > 0) {
-      if (rgat) RGNN_LAUNCH((k_dx_walk<K, true>), warp_grid(a.num_items), 256, 0, s, a);
-      else RGNN_LAUNCH((k_dx_walk<K, false>), warp_grid(a.num_items), 256, 0, s, a);
+      if (a.h_bf16) {
+        if (rgat) RGNN_LAUNCH((k_dx_walk<K, true, __nv_bfloat16>), warp_grid(a.num_items), 256, 0, s, a);
+        else RGNN_LAUNCH((k_dx_walk<K, false, __nv_bfloat16>), warp_grid(a.num_items), 256, 0, s, a);
+      } else {
+        if (rgat) RGNN_LAUNCH((k_dx_walk<K, true, float>), warp_grid(a.num_items), 256, 0, s, a);
+        else RGNN_LAUNCH((k_dx_walk<K, false, float>), warp_grid(a.num_items), 256, 0, s, a);
+      }
     }
     if (a.num_split > 0)
       RGNN_LAUNCH((k_dx_merge<K>), (unsigned)std::min<int64_t>(a.num_split, 148 * 8), 256, 0, s, a);

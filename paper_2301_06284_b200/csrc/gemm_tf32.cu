@@ -49,6 +49,7 @@ struct Tf32Params {
   const int32_t* gather;
   const float* X;
   float* Z;
+  int z_bf16;  // store the rows as bf16 (RNE) instead of fp32
 };
 
 template <int K, int N>
@@ -216,14 +217,23 @@ __global__ void __launch_bounds__(288, 1)
       tc::mbar_wait(&acc_full[acc], (uint32_t)(it >> 1) & 1);
       tc::tc_fence_after();
       float* zrow = pr.Z + (size_t)p * N;
+      __nv_bfloat16* zrow_b = reinterpret_cast<__nv_bfloat16*>(pr.Z) + (size_t)p * N;
 #pragma unroll
       for (int c0 = 0; c0 < N; c0 += 16) {
         uint32_t v[16];
         tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * N + c0, v);
         tc::tmem_ld_wait();
         if (valid) {
+          if (pr.z_bf16) {
+            uint32_t b[8];
 #pragma unroll
-          for (int j = 0; j < 16; j += 4) stg16(zrow + c0 + j, make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+            for (int j = 0; j < 8; ++j) b[j] = tc::pack_bf16(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+            stg16(zrow_b + c0, make_uint4(b[0], b[1], b[2], b[3]));
+            stg16(zrow_b + c0 + 8, make_uint4(b[4], b[5], b[6], b[7]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) stg16(zrow + c0 + j, make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+          }
         }
       }
       tc::tc_fence_before();
@@ -256,7 +266,7 @@ static rgnn_status gemm_fwd_tf32(const GemmFwdArgs& a, const float* wt_f32, cuda
   RGNN_CUDA_TRY(cudaGetDevice(&dev));
   RGNN_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   Tf32Params pr{a.tiles, a.num_tiles, a.rows, a.gofs, a.gather, static_cast<const float*>(a.X),
-                static_cast<float*>(a.Z)};
+                static_cast<float*>(a.Z), a.z_bf16};
   const unsigned grid = (unsigned)std::min<int64_t>(ntiles, sms);
   RGNN_LAUNCH(kern, grid, C::THREADS, C::SMEM, s, wmap, pr);
   return RGNN_OK;

@@ -24,6 +24,7 @@ struct GemmFwdArgs {
   int num_w;                // number of weight matrices in W (R, or 1 for the self-loop W0)
   int64_t x_rows;           // rows of X (V)
   int64_t z_rows;           // rows of Z (E_own) when tiles != null
+  int z_bf16;               // tf32 kernel only: store Z as bf16
 };
 
 // dW split-K GEMM over chunks (DESIGN.md Sec. 6 "a5"):
@@ -130,7 +131,8 @@ struct DxArgs {
   const float* sinvc;                         // RGCN: 1/c per source slot
   const float* wpos;                          // non-RGAT walk: weight per position (HGT), else sinvc
   const float2* ad;                           // RGAT: (alpha, dpre) per position
-  const void* H;                              // [J, K] fp32: G_v W_r^T per (etype, dst) run
+  const void* H;                              // [J, K] fp32 (or bf16 with h_bf16): G_v W_r^T per (etype, dst) run
+  int h_bf16;
   const float* U0;                            // RGAT: [R, K] W_r A[r,0]
   const float* U1;                            // RGAT: [R, K] W_r A[r,1]
   const Item* ditems;                         // RGAT destination terms: the dst work list

@@ -8,6 +8,7 @@
 #include "kernels.cuh"
 
 namespace rgnn {
+bool tc_disabled();
 rgnn_status comm_check_range(const rgnn_comm* c, int64_t v0, int64_t v1);
 rgnn_status comm_gather_rows(rgnn_comm* c, const float* Y_own, int64_t N, float* Y_full, cudaStream_t s);
 rgnn_status comm_allreduce_sum(rgnn_comm* c, float* const* bufs, const size_t* counts, int n, cudaStream_t s);
@@ -442,14 +443,17 @@ rgnn_status hgt_backward(const rgnn_graph* g, int K, int N, rgnn_prec prec, cons
     hb.split_rows = g->split_rows; hb.num_split_rows = g->num_split_rows;
     RGNN_TRY(launch_hgt_bwd_walk(RGNN_F32, N, hb, s));
   }
-  // source sums: dv = sum alpha Hm, dk = sum da Ha over each source's out-edges
+  // source sums: dv = sum alpha Hm, dk = sum da Ha over each source's out-edges.  On the bf16 layer
+  // the run products H are stored in bf16 by the tf32 GEMM (dk / dv only feed the weight
+  // gradients dWK / dWV, sums over nodes; O23), halving the walks' gathered bytes.
+  const int h_bf16 = (bf && !tc_disabled() && !getenv("RGNN_HGT_H_F32")) ? 1 : 0;
   auto src_sum = [&](const float* G, const int32_t* gidx, int64_t grows, const float* Wt, const float* Wrr,
                      const float* wpos, float* out) -> rgnn_status {
     if (g->num_rtiles) {
       Phase ph("hgt_bwd_runs", s);
       GemmFwdArgs gh{};
       gh.tiles = g->rtiles; gh.num_tiles = g->num_rtiles; gh.X = G; gh.gather = gidx; gh.W = Wt; gh.Z = w.H;
-      gh.num_w = g->R; gh.x_rows = std::max<int64_t>(grows, 1); gh.z_rows = J;
+      gh.num_w = g->R; gh.x_rows = std::max<int64_t>(grows, 1); gh.z_rows = J; gh.z_bf16 = h_bf16;
       RGNN_TRY(f32_gemm(prec, N, N, gh, Wrr, s));
     }
     Phase ph("hgt_bwd_src", s);
@@ -457,7 +461,7 @@ rgnn_status hgt_backward(const rgnn_graph* g, int K, int N, rgnn_prec prec, cons
     xa.V = V; xa.V_own = g->V_own; xa.v0 = g->v0;
     xa.items = g->sitems; xa.num_items = g->num_sitems; xa.split = g->ssplit; xa.num_split = g->num_ssplit;
     xa.part = w.xpart; xa.srow = g->srow; xa.spos = g->spos; xa.srun = g->srun; xa.srel = g->srel;
-    xa.sinvc = g->sinvc; xa.wpos = wpos; xa.H = w.H; xa.dX = out;
+    xa.sinvc = g->sinvc; xa.wpos = wpos; xa.H = w.H; xa.h_bf16 = h_bf16; xa.dX = out;
     return launch_dx_walk(N, false, xa, s);
   };
   RGNN_TRY(src_sum(dY, g->run_dst, g->V_own, w.WmT, w.Wmr, w.alpha, w.dV));
