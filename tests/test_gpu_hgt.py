@@ -173,3 +173,15 @@ def test_hgt_backward_long_runs(rgnn, prec):
     g = _hub_graph()
     t = synth.make_hgt_tensors(g.V, g.R, g.T, 64, 64)
     _check_grads(_run_bwd(rgnn, g, t, prec, materialization="vanilla"), _ref_bwd(g, t, prec), prec, "hgt bwd hub")
+
+
+@pytest.mark.parametrize("prec", ["f32", "bf16"])
+def test_hgt_degenerate_graphs(rgnn, prec):
+    """E = 0 (Y = 0, all gradients 0), one node with self edges, one edge, a node type without nodes."""
+    cases = [synth.random_graph(50, 0, 3, seed=4, T=2), synth.random_graph(1, 20, 2, seed=5, T=1),
+             synth.random_graph(30, 1, 2, seed=6, T=3)]
+    for g in cases:
+        t = synth.make_hgt_tensors(g.V, g.R, g.T, 32, 32)
+        Y, _, _ = _run(rgnn, g, t, prec)
+        assert_close(Y, _ref(g, t, prec), prec, f"hgt degenerate {g.name} Y")
+        _check_grads(_run_bwd(rgnn, g, t, prec), _ref_bwd(g, t, prec), prec, f"hgt degenerate {g.name}")
