@@ -42,6 +42,17 @@ rgnn_status launch_round_bf16(int64_t n, const float* a, float* b, cudaStream_t 
   return RGNN_OK;
 }
 
+__global__ void k_f32_to_bf16(int64_t n, const float* __restrict__ a, __nv_bfloat16* __restrict__ b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = __float2bfloat16_rn(a[i]);
+}
+rgnn_status launch_f32_to_bf16(int64_t n, const float* a, void* b, cudaStream_t s) {
+  if (n == 0) return RGNN_OK;
+  RGNN_LAUNCH(k_f32_to_bf16, (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, s, n, a,
+              static_cast<__nv_bfloat16*>(b));
+  return RGNN_OK;
+}
+
 rgnn_status launch_map_gather(int64_t n, const int32_t* idx, const int32_t* ninv, int32_t* out, cudaStream_t s,
                               int64_t ofs) {
   if (n == 0) return RGNN_OK;
@@ -317,10 +328,9 @@ static rgnn_status hgt_bwd_walk(const HgtBwdArgs& a, cudaStream_t s) {
 // One warp per run piece (<= kPieceRows consecutive positions of one (etype, dst) run): lane
 // groups of L = N*sizeof(T)/16 lanes gather the v and k rows of interleaved positions, fp32 sums
 // merged in a fixed xor tree.  Positions are read in order (alpha, da, vrow contiguous).
-template <typename TO, int N>
+template <typename TO, typename T, int N>
 __global__ void __launch_bounds__(256) k_hgt_piece_agg(HgtPieceArgs a) {
-  using T = float;  // v and k rows are fp32
-  constexpr int EPL = 4;
+  constexpr int EPL = 16 / sizeof(T);  // v and k rows: fp32, or their bf16 copies
   constexpr int L = N / EPL;
   constexpr int G = 32 / L;
   static_assert(L >= 1 && L <= 32, "piece agg shape");
@@ -393,10 +403,14 @@ rgnn_status launch_hgt_piece_agg(int prec, int N, const HgtPieceArgs& a, cudaStr
   if (a.num_pieces == 0) return RGNN_OK;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((a.num_pieces + 7) / 8, 148 * 16));
   const bool bf = prec == RGNN_BF16;
-#define RGNN_PIECE(T, n) \
-  if (N == n) { RGNN_LAUNCH((k_hgt_piece_agg<T, n>), grid, 256, 0, s, a); return RGNN_OK; }
-  if (bf) { RGNN_PIECE(__nv_bfloat16, 32) RGNN_PIECE(__nv_bfloat16, 64) RGNN_PIECE(__nv_bfloat16, 128) }
-  else { RGNN_PIECE(float, 32) RGNN_PIECE(float, 64) RGNN_PIECE(float, 128) }
+#define RGNN_PIECE(TO, TI, n) \
+  if (N == n) { RGNN_LAUNCH((k_hgt_piece_agg<TO, TI, n>), grid, 256, 0, s, a); return RGNN_OK; }
+  if (bf && a.in_bf16) {
+    RGNN_PIECE(__nv_bfloat16, __nv_bfloat16, 32) RGNN_PIECE(__nv_bfloat16, __nv_bfloat16, 64)
+    RGNN_PIECE(__nv_bfloat16, __nv_bfloat16, 128)
+  } else if (bf) {
+    RGNN_PIECE(__nv_bfloat16, float, 32) RGNN_PIECE(__nv_bfloat16, float, 64) RGNN_PIECE(__nv_bfloat16, float, 128)
+  } else { RGNN_PIECE(float, float, 32) RGNN_PIECE(float, float, 64) RGNN_PIECE(float, float, 128) }
 #undef RGNN_PIECE
   return set_error(RGNN_E_UNSUPPORTED, "d_out=%d not in {32,64,128}", N);
 }

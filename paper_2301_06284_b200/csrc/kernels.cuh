@@ -192,7 +192,8 @@ struct HgtPieceArgs {
   const int32_t* piece_ptr;
   const int32_t* vrow;    // position -> node-type row of the source
   const float *alpha, *da;
-  const void *Vn, *Kn;    // [V, N] fp32 (type-order rows)
+  const void *Vn, *Kn;    // [V, N] fp32 (type-order rows), or bf16 copies (in_bf16)
+  int in_bf16;
   const int32_t* dst_s;   // position -> local dst
   const int32_t* ninv;
   int64_t v0;
@@ -200,6 +201,7 @@ struct HgtPieceArgs {
   int32_t *pdst, *pq;     // [num_pieces] local dst / node-type row of the dst
 };
 rgnn_status launch_hgt_piece_agg(int prec, int N, const HgtPieceArgs& a, cudaStream_t s);
+rgnn_status launch_f32_to_bf16(int64_t n, const float* a, void* b, cudaStream_t s);
 // out[i] = ninv[idx[i] + ofs]
 rgnn_status launch_map_gather(int64_t n, const int32_t* idx, const int32_t* ninv, int32_t* out, cudaStream_t s,
                               int64_t ofs = 0);

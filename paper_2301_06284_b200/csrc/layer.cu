@@ -102,7 +102,7 @@ static HgtWs hgt_ws_layout(const rgnn_graph* g, int K, int N, int prec, void* ba
     w.dV = c.take<float>((size_t)V * N);
     w.H = c.take<float>((size_t)J * N);
     const int64_t NP = std::max<int64_t>(g->num_pieces, 1);
-    w.Bb = c.take<char>(bf ? (size_t)std::max(std::max(E, V), NP) * N * 2 : 1);
+    w.Bb = c.take<char>(bf ? (size_t)std::max(std::max(E, 2 * V), NP) * N * 2 : 1);  // also the bf16 v, k copies
     const int64_t dwp = std::max<int64_t>(std::max<int64_t>(g->num_pchunks, 1) * (N * N + N),
                                           std::max<int64_t>(g->num_nchunks, 1) * (K * N + K));
     w.dwpart = c.take<float>((size_t)dwp);
@@ -497,7 +497,12 @@ rgnn_status hgt_backward(const rgnn_graph* g, int K, int N, rgnn_prec prec, cons
     Phase ph("hgt_bwd_dw_rel", s);
     HgtPieceArgs pa{};
     pa.num_pieces = g->num_pieces; pa.piece_ptr = g->piece_ptr; pa.vrow = w.vrow; pa.alpha = w.alpha; pa.da = w.da;
-    pa.Vn = sv.Vn; pa.Kn = sv.Kf; pa.dst_s = g->dst_s; pa.ninv = g->ninv; pa.v0 = g->v0; pa.vagg = w.vagg;
+    pa.Vn = sv.Vn; pa.Kn = sv.Kf;
+    if (bf && getenv("RGNN_HGT_PIECE_BF16")) {  // bf16 copies of v and k: half the gathered bytes
+      RGNN_TRY(launch_f32_to_bf16((int64_t)V * N, sv.Vn, w.Bb, s));
+      RGNN_TRY(launch_f32_to_bf16((int64_t)V * N, sv.Kf, static_cast<char*>(w.Bb) + (size_t)V * N * 2, s));
+      pa.Vn = w.Bb; pa.Kn = static_cast<char*>(w.Bb) + (size_t)V * N * 2; pa.in_bf16 = 1;
+    } pa.dst_s = g->dst_s; pa.ninv = g->ninv; pa.v0 = g->v0; pa.vagg = w.vagg;
     pa.kagg = w.kagg; pa.pdst = w.pdst; pa.pq = w.pq;
     RGNN_TRY(launch_hgt_piece_agg(prec, N, pa, s));
     const int64_t NP = g->num_pieces;
