@@ -121,7 +121,7 @@ struct TcFwdParams {
   int tcap;  // tile descriptors cached in shared memory (<= FwdCfg::TCAP; the launch sizes the smem)
 };
 
-template <int K, int N>
+template <int K, int N, bool F32OUT>
 __global__ void __launch_bounds__(288, 1)
     k_gemm_fwd_tc(const __grid_constant__ CUtensorMap wmap, TcFwdParams pr) {
   using C = FwdCfg<K, N>;
@@ -317,6 +317,16 @@ __global__ void __launch_bounds__(288, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) sdot = fmaf(f[j], sA0[c0 + j], sdot);
         }
+        if constexpr (F32OUT) {  // fp32 rows straight from the accumulator (no staging)
+          if (valid) {
+            float* zf = reinterpret_cast<float*>(pr.Z) + (size_t)p * N + c0;
+#pragma unroll
+            for (int j = 0; j < 16; j += 4)
+              stg16(zf + j, make_uint4(__float_as_uint(f[j] * scale), __float_as_uint(f[j + 1] * scale),
+                                       __float_as_uint(f[j + 2] * scale), __float_as_uint(f[j + 3] * scale)));
+          }
+          continue;
+        }
         uint4 w0, w1;
         w0.x = tc::pack_bf16(f[0] * scale, f[1] * scale); w0.y = tc::pack_bf16(f[2] * scale, f[3] * scale);
         w0.z = tc::pack_bf16(f[4] * scale, f[5] * scale); w0.w = tc::pack_bf16(f[6] * scale, f[7] * scale);
@@ -332,6 +342,7 @@ __global__ void __launch_bounds__(288, 1)
       if (lane == 0) tc::mbar_arrive(&acc_empty[acc]);
       if (pr.s_src && valid) pr.s_src[p] = sdot;
       tc::named_bar(1, 128);
+      if constexpr (F32OUT) continue;
       // coalesced copy-out of the valid rows (never past row1: the next segment's rows)
       const int nvalid = row1 - row0;
       for (int i = et; i < nvalid * NCH; i += 128) {
@@ -349,7 +360,7 @@ __global__ void __launch_bounds__(288, 1)
   }
 }
 
-template <int K, int N>
+template <int K, int N, bool F32OUT>
 static rgnn_status gemm_fwd_tc(const GemmFwdArgs& a, cudaStream_t s) {
   using C = FwdCfg<K, N>;
   const int64_t ntiles = a.tiles ? a.num_tiles : (a.rows + C::M - 1) / C::M;
@@ -360,7 +371,7 @@ static rgnn_status gemm_fwd_tc(const GemmFwdArgs& a, cudaStream_t s) {
               a.num_w, K, N, a.W, wt);
   CUtensorMap wmap;
   RGNN_TRY(make_tmap_2d_bf16(&wmap, wt, K, (uint64_t)a.num_w * N, K * 2, C::RB / 2, N, C::SWZ));
-  auto kern = k_gemm_fwd_tc<K, N>;
+  auto kern = k_gemm_fwd_tc<K, N, F32OUT>;
   RGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   int dev, sms;
   RGNN_CUDA_TRY(cudaGetDevice(&dev));
@@ -385,7 +396,13 @@ bool tc_disabled() {
 
 rgnn_status launch_gemm_fwd_tc(int K, int N, const GemmFwdArgs& a, cudaStream_t s) {
   if (tc_disabled()) return RGNN_E_UNSUPPORTED;
-  return RGNN_DISPATCH_KN(K, N, [&] { return gemm_fwd_tc<kK, kN>(a, s); });
+  return RGNN_DISPATCH_KN(K, N, [&] { return gemm_fwd_tc<kK, kN, false>(a, s); });
+}
+
+// bf16 operands, fp32 output rows (HGT node-typed linears on the bf16 layer)
+rgnn_status launch_gemm_fwd_tc_f32out(int K, int N, const GemmFwdArgs& a, cudaStream_t s) {
+  if (tc_disabled()) return RGNN_E_UNSUPPORTED;
+  return RGNN_DISPATCH_KN(K, N, [&] { return gemm_fwd_tc<kK, kN, true>(a, s); });
 }
 
 }  // namespace rgnn

@@ -107,6 +107,7 @@ rgnn_status launch_bwd_traverse(int prec, int K, int N, const BwdArgs& a, cudaSt
 
 // tcgen05 path (gemm_tc.cu): returns RGNN_E_UNSUPPORTED if the shape is not covered.
 rgnn_status launch_gemm_fwd_tc(int K, int N, const GemmFwdArgs& a, cudaStream_t s);
+rgnn_status launch_gemm_fwd_tc_f32out(int K, int N, const GemmFwdArgs& a, cudaStream_t s);
 rgnn_status launch_gemm_dw_tc(int K, int N, const GemmDwArgs& a, cudaStream_t s);
 // fp32 operands on the tensor cores (tcgen05 kind::tf32), fp32 output (gemm_tf32.cu).  wt_f32 =
 // the GEMM weight transposed, [num_w, N, K] fp32 (K-major B operand); a.W is not read.

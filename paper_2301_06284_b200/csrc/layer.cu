@@ -61,7 +61,8 @@ static int64_t dw0_chunks(const rgnn_graph* g) {
 }
 
 struct HgtWs {
-  float *Xf, *Wr;         // bf16 path: X as fp32, RNE-rounded WK | WQ | WV | Wa | Wm
+  void* wt;               // bf16 W^T of the tcgen05 node GEMMs (bf16 layer)
+  float *Xf, *Wr;         // bf16 path: X as fp32 (SIMT fallback only), RNE-rounded WK | WQ | WV | Wa | Wm
   float* Wtr;             // tf32 GEMM weights: (rounded) WK^T | WQ^T | WV^T | Wa^T | Wm^T
   int32_t* gather;
   float* part;
@@ -88,6 +89,7 @@ static HgtWs hgt_ws_layout(const rgnn_graph* g, int K, int N, int prec, void* ba
   const bool bf = prec == RGNN_BF16;
   w.gather = c.take<int32_t>((size_t)zr);
   w.part = c.take<float>((size_t)std::max<int64_t>(g->num_parts, 1) * (N + 4));
+  w.wt = c.take<char>(bf ? (size_t)T * K * N * 2 : 1);
   w.Xf = c.take<float>(bf ? (size_t)V * K : 1);
   w.Wr = c.take<float>(bf ? (size_t)(3 * T * K * N + 2 * (int64_t)g->R * N * N) : 1);
   w.Wtr = c.take<float>((size_t)(3 * T * K * N + 2 * (int64_t)g->R * N * N));
@@ -320,9 +322,13 @@ rgnn_status hgt_forward(const rgnn_graph* g, int K, int N, rgnn_prec prec, const
   const int64_t tkn = T * K * N, rnn = (int64_t)g->R * N * N;
   const float *WKs = WK, *WQs = WQ, *WVs = WV, *Was = Wa, *Wms = Wm;
   const void* Xs = X;
+  // bf16 layer: the node-typed linears read X in bf16 on the bf16 tcgen05 GEMM with fp32 output
+  // rows (bf16 x bf16 products are exact, fp32 accumulation: the same values the tf32 GEMM gives on
+  // the bf16-valued operands); the fp32 copy of X is made only for the SIMT fallback.
+  const bool node_tc = bf && !tc_disabled();
   if (bf) {
     Phase ph("hgt_prep", s);
-    RGNN_TRY(launch_bf16_to_f32(g->V * K, X, w.Xf, s));
+    if (!node_tc) RGNN_TRY(launch_bf16_to_f32(g->V * K, X, w.Xf, s));
     RGNN_TRY(launch_round_bf16(tkn, WK, w.Wr, s));
     RGNN_TRY(launch_round_bf16(tkn, WQ, w.Wr + tkn, s));
     RGNN_TRY(launch_round_bf16(tkn, WV, w.Wr + 2 * tkn, s));
@@ -340,15 +346,22 @@ rgnn_status hgt_forward(const rgnn_graph* g, int K, int N, rgnn_prec prec, const
   }
   if (g->num_ntiles) {
     Phase ph("hgt_node_gemm", s);
-    auto node_gemm = [&](const float* Win, const float* Wt32, float* out) -> rgnn_status {
+    auto node_gemm = [&](const float* Wmaster, const float* Win, const float* Wt32, float* out) -> rgnn_status {
       GemmFwdArgs ga{};
-      ga.tiles = g->ntiles; ga.num_tiles = g->num_ntiles; ga.X = Xs; ga.gather = g->nperm; ga.W = Win;
-      ga.Z = out; ga.num_w = (int)T; ga.x_rows = g->V; ga.z_rows = g->V;
+      ga.tiles = g->ntiles; ga.num_tiles = g->num_ntiles; ga.gather = g->nperm; ga.Z = out; ga.num_w = (int)T;
+      ga.x_rows = g->V; ga.z_rows = g->V;
+      if (node_tc) {
+        ga.X = X; ga.W = Wmaster; ga.wt_bf16 = w.wt;  // W rounded to bf16 (RNE) inside
+        rgnn_status st = launch_gemm_fwd_tc_f32out(K, N, ga, s);
+        if (st != RGNN_E_UNSUPPORTED) return st;
+        return set_error(RGNN_E_CUDA, "internal: tcgen05 node GEMM unavailable");
+      }
+      ga.X = Xs; ga.W = Win;
       return f32_gemm(prec, K, N, ga, Wt32, s);
     };
-    RGNN_TRY(node_gemm(WKs, w.Wtr, sv.Kf));
-    RGNN_TRY(node_gemm(WQs, w.Wtr + tkn, sv.Qf));
-    RGNN_TRY(node_gemm(WVs, w.Wtr + 2 * tkn, sv.Vn));
+    RGNN_TRY(node_gemm(WK, WKs, w.Wtr, sv.Kf));
+    RGNN_TRY(node_gemm(WQ, WQs, w.Wtr + tkn, sv.Qf));
+    RGNN_TRY(node_gemm(WV, WVs, w.Wtr + 2 * tkn, sv.Vn));
   }
   const bool cm = use_compact(g, RGNN_HGT);
   const int64_t zr = cm ? g->num_compact : g->E_own;
