@@ -53,6 +53,36 @@ rgnn_status launch_f32_to_bf16(int64_t n, const float* a, void* b, cudaStream_t 
   return RGNN_OK;
 }
 
+// Zero the gradient rows the walks do not write (instead of clearing whole [V, N] buffers):
+// dk / dv rows of nodes without out-edges (srow[u] == srow[u+1]), dq rows of the owned
+// destinations without in-edges (empty_rows) and of the rows outside the owned range [v0, v1).
+// Also used for dX (NEXT-2): dK = dV = dX, [v0, v1) = [0, V), no empty list.
+__global__ void k_hgt_zero_rows(int64_t V, int N, const int32_t* __restrict__ srow, float* __restrict__ dK,
+                                float* __restrict__ dV, int64_t v0, int64_t v1, const int32_t* __restrict__ empty_rows,
+                                int64_t num_empty, float* __restrict__ dQ) {
+  const int nch = N / 4;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < V; u += (int64_t)gridDim.x * blockDim.x) {
+    if (srow[u] == srow[u + 1]) {  // one thread per node: only the rows to clear are written
+      for (int c = 0; c < nch; ++c) {
+        reinterpret_cast<float4*>(dK + (size_t)u * N)[c] = z;
+        reinterpret_cast<float4*>(dV + (size_t)u * N)[c] = z;
+      }
+    }
+    if (u < v0 || u >= v1)
+      for (int c = 0; c < nch; ++c) reinterpret_cast<float4*>(dQ + (size_t)u * N)[c] = z;
+    if (u < num_empty)
+      for (int c = 0; c < nch; ++c) reinterpret_cast<float4*>(dQ + (size_t)(v0 + empty_rows[u]) * N)[c] = z;
+  }
+}
+rgnn_status launch_hgt_zero_rows(int64_t V, int N, const int32_t* srow, float* dK, float* dV, int64_t v0, int64_t v1,
+                                 const int32_t* empty_rows, int64_t num_empty, float* dQ, cudaStream_t s) {
+  if (V == 0) return RGNN_OK;
+  RGNN_LAUNCH(k_hgt_zero_rows, (unsigned)std::min<int64_t>((V + 255) / 256, 148 * 32), 256, 0, s, V, N, srow, dK, dV,
+              v0, v1, empty_rows, num_empty, dQ);
+  return RGNN_OK;
+}
+
 rgnn_status launch_map_gather(int64_t n, const int32_t* idx, const int32_t* ninv, int32_t* out, cudaStream_t s,
                               int64_t ofs) {
   if (n == 0) return RGNN_OK;

@@ -203,6 +203,8 @@ struct HgtPieceArgs {
 };
 rgnn_status launch_hgt_piece_agg(int prec, int N, const HgtPieceArgs& a, cudaStream_t s);
 rgnn_status launch_f32_to_bf16(int64_t n, const float* a, void* b, cudaStream_t s);
+rgnn_status launch_hgt_zero_rows(int64_t V, int N, const int32_t* srow, float* dK, float* dV, int64_t v0, int64_t v1,
+                                 const int32_t* empty_rows, int64_t num_empty, float* dQ, cudaStream_t s);
 // out[i] = ninv[idx[i] + ofs]
 rgnn_status launch_map_gather(int64_t n, const int32_t* idx, const int32_t* ninv, int32_t* out, cudaStream_t s,
                               int64_t ofs = 0);

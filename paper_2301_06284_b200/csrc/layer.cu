@@ -443,9 +443,8 @@ rgnn_status hgt_backward(const rgnn_graph* g, int K, int N, rgnn_prec prec, cons
     }
     RGNN_TRY(launch_map_gather(E, g->src_s, g->ninv, w.vrow, s));
     RGNN_TRY(launch_map_gather(J, g->run_dst, g->ninv, w.qrun, s, g->v0));
-    RGNN_CUDA_TRY(cudaMemsetAsync(w.dQ, 0, sizeof(float) * (size_t)V * N, s));
-    RGNN_CUDA_TRY(cudaMemsetAsync(w.dK, 0, sizeof(float) * (size_t)V * N, s));
-    RGNN_CUDA_TRY(cudaMemsetAsync(w.dV, 0, sizeof(float) * (size_t)V * N, s));
+    RGNN_TRY(launch_hgt_zero_rows(V, N, g->srow, w.dK, w.dV, g->v0, g->v0 + g->V_own, g->empty_rows, g->num_empty,
+                                  w.dQ, s));
   }
   {
     Phase ph("hgt_bwd_walk", s);
@@ -666,7 +665,10 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
       g0.wt_bf16 = w.wt; g0.num_w = 1; g0.x_rows = g->V_own;
       RGNN_TRY(f32_gemm(prec, N, K, g0, w.Wr + (size_t)g->R * N * K, s));
     }
-    { Phase ph("dx_zero", s); RGNN_CUDA_TRY(cudaMemsetAsync(dX, 0, sizeof(float) * (size_t)g->V * K, s)); }
+    {  // rows of nodes with out-edges are written by the source walk: zero only the others
+      Phase ph("dx_zero", s);
+      RGNN_TRY(launch_hgt_zero_rows(g->V, K, g->srow, dX, dX, 0, g->V, nullptr, 0, dX, s));
+    }
     DxArgs xa{};
     xa.V = g->V; xa.V_own = g->V_own; xa.v0 = g->v0;
     xa.items = g->sitems; xa.num_items = g->num_sitems; xa.split = g->ssplit; xa.num_split = g->num_ssplit;
