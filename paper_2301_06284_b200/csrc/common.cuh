@@ -199,8 +199,8 @@ __device__ __forceinline__ float group_sum(float v) {
 
 // Sum of a split row's parts in a fixed order: one block per split row; warp w
 // sums parts w, w+8, ... then warp 0 adds the 8 warp sums in warp order.
-template <int K>
-__device__ __forceinline__ void merge_parts(const float* __restrict__ part, int32_t part0, int32_t nparts, float* out,
+template <int K, typename TO = float>
+__device__ __forceinline__ void merge_parts(const float* __restrict__ part, int32_t part0, int32_t nparts, TO* out,
                                             bool add) {
   constexpr int KL = K / 32;
   __shared__ float red[8][K];
@@ -222,8 +222,12 @@ __device__ __forceinline__ void merge_parts(const float* __restrict__ part, int3
       float s = 0.f;
 #pragma unroll
       for (int w = 0; w < 8; ++w) s += red[w][lane + 32 * i];
-      if (add) out[lane + 32 * i] += s;
-      else out[lane + 32 * i] = s;
+      if constexpr (sizeof(TO) == 4) {
+        if (add) out[lane + 32 * i] += s;
+        else out[lane + 32 * i] = s;
+      } else {
+        out[lane + 32 * i] = from_f<TO>(s);  // bf16 rows (no accumulation)
+      }
     }
   }
   __syncthreads();

@@ -18,6 +18,11 @@
 
 namespace rgnn {
 
+__device__ __forceinline__ uint32_t tc_pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
 // Wt[r] = W[r]^T : [R, K, N] -> [R, N, K]; on the bf16 path the RNE-rounded
 // weight (the values the forward multiplied, reading O16), kept in fp32
 __global__ void k_transpose_w(int R, int K, int N, const float* __restrict__ W, float* __restrict__ Wt,
@@ -80,11 +85,18 @@ __global__ void __launch_bounds__(256) k_dx_walk(DxArgs a) {
 #pragma unroll
       for (int i = 0; i < EPL; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
     if (g == 0) {
-      float* out = it.part < 0 ? a.dX + (size_t)it.row * K : a.part + (size_t)it.part * K;
+      if (!RGAT && a.outb && it.part < 0) {  // bf16 row in node-type order (HGT dk / dv)
+        uint32_t* ob = reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(a.outb) + (size_t)a.orow[it.row] * K +
+                                                   l * EPL);
 #pragma unroll
-      for (int i = 0; i < EPL; i += 4)
-        stg16(out + l * EPL + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]),
-                                            __float_as_uint(acc[i + 2]), __float_as_uint(acc[i + 3])));
+        for (int i = 0; i < EPL; i += 2) ob[i / 2] = tc_pack_bf16(acc[i], acc[i + 1]);
+      } else {
+        float* out = it.part < 0 ? a.dX + (size_t)it.row * K : a.part + (size_t)it.part * K;
+#pragma unroll
+        for (int i = 0; i < EPL; i += 4)
+          stg16(out + l * EPL + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]),
+                                              __float_as_uint(acc[i + 2]), __float_as_uint(acc[i + 3])));
+      }
     }
   }
 }
@@ -93,7 +105,11 @@ template <int K>
 __global__ void __launch_bounds__(256) k_dx_merge(DxArgs a) {
   for (int64_t w = blockIdx.x; w < a.num_split; w += gridDim.x) {
     const SplitRow sr = a.split[w];
-    merge_parts<K>(a.part, sr.part0, sr.nparts, a.dX + (size_t)sr.row * K, false);
+    if (a.outb)
+      merge_parts<K>(a.part, sr.part0, sr.nparts,
+                     static_cast<__nv_bfloat16*>(a.outb) + (size_t)a.orow[sr.row] * K, false);
+    else
+      merge_parts<K>(a.part, sr.part0, sr.nparts, a.dX + (size_t)sr.row * K, false);
   }
 }
 

@@ -83,6 +83,32 @@ rgnn_status launch_hgt_zero_rows(int64_t V, int N, const int32_t* srow, float* d
   return RGNN_OK;
 }
 
+__global__ void k_hgt_zero_rows_b(int64_t V, int N, const int32_t* __restrict__ srow, const int32_t* __restrict__ ninv,
+                                  uint4* __restrict__ dK, uint4* __restrict__ dV, int64_t v0, int64_t v1,
+                                  const int32_t* __restrict__ empty_rows, int64_t num_empty, uint4* __restrict__ dQ) {
+  const int nch = N / 8;  // 16-byte chunks of a bf16 row
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < V; u += (int64_t)gridDim.x * blockDim.x) {
+    const size_t ro = (size_t)ninv[u] * nch;
+    if (srow[u] == srow[u + 1])
+      for (int c = 0; c < nch; ++c) { dK[ro + c] = z; dV[ro + c] = z; }
+    if (u < v0 || u >= v1)
+      for (int c = 0; c < nch; ++c) dQ[ro + c] = z;
+    if (u < num_empty) {
+      const size_t re = (size_t)ninv[v0 + empty_rows[u]] * nch;
+      for (int c = 0; c < nch; ++c) dQ[re + c] = z;
+    }
+  }
+}
+rgnn_status launch_hgt_zero_rows_b(int64_t V, int N, const int32_t* srow, const int32_t* ninv, void* dK, void* dV,
+                                   int64_t v0, int64_t v1, const int32_t* empty_rows, int64_t num_empty, void* dQ,
+                                   cudaStream_t s) {
+  if (V == 0) return RGNN_OK;
+  RGNN_LAUNCH(k_hgt_zero_rows_b, (unsigned)std::min<int64_t>((V + 255) / 256, 148 * 32), 256, 0, s, V, N, srow, ninv,
+              static_cast<uint4*>(dK), static_cast<uint4*>(dV), v0, v1, empty_rows, num_empty, static_cast<uint4*>(dQ));
+  return RGNN_OK;
+}
+
 rgnn_status launch_map_gather(int64_t n, const int32_t* idx, const int32_t* ninv, int32_t* out, cudaStream_t s,
                               int64_t ofs) {
   if (n == 0) return RGNN_OK;
@@ -327,11 +353,18 @@ __global__ void __launch_bounds__(256, RGNN_HGTB_MINB) k_hgt_bwd_walk(HgtBwdArgs
 #pragma unroll
       for (int i = 0; i < EPL; ++i) dq[i] += __shfl_xor_sync(0xffffffffu, dq[i], o);
     if (g == 0) {
-      float* out = it.part < 0 ? a.dQ + (size_t)(a.v0 + it.row) * N : a.part + (size_t)it.part * N;
+      if (a.dQb && it.part < 0) {  // bf16 row in node-type order
+        __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(a.dQb) + (size_t)a.ninv[a.v0 + it.row] * N + l * EPL;
 #pragma unroll
-      for (int i = 0; i < EPL; i += 4)
-        stg16(out + l * EPL + i, make_uint4(__float_as_uint(dq[i]), __float_as_uint(dq[i + 1]),
-                                            __float_as_uint(dq[i + 2]), __float_as_uint(dq[i + 3])));
+        for (int i = 0; i < EPL; i += 2)
+          *reinterpret_cast<__nv_bfloat162*>(ob + i) = __floats2bfloat162_rn(dq[i], dq[i + 1]);
+      } else {
+        float* out = it.part < 0 ? a.dQ + (size_t)(a.v0 + it.row) * N : a.part + (size_t)it.part * N;
+#pragma unroll
+        for (int i = 0; i < EPL; i += 4)
+          stg16(out + l * EPL + i, make_uint4(__float_as_uint(dq[i]), __float_as_uint(dq[i + 1]),
+                                              __float_as_uint(dq[i + 2]), __float_as_uint(dq[i + 3])));
+      }
     }
   }
 }
@@ -340,7 +373,11 @@ template <int N>
 __global__ void __launch_bounds__(256) k_hgt_dq_merge(HgtBwdArgs a) {
   for (int64_t w = blockIdx.x; w < a.num_split_rows; w += gridDim.x) {
     const SplitRow sr = a.split_rows[w];
-    merge_parts<N>(a.part, sr.part0, sr.nparts, a.dQ + (size_t)(a.v0 + sr.row) * N, false);
+    if (a.dQb)
+      merge_parts<N>(a.part, sr.part0, sr.nparts,
+                     static_cast<__nv_bfloat16*>(a.dQb) + (size_t)a.ninv[a.v0 + sr.row] * N, false);
+    else
+      merge_parts<N>(a.part, sr.part0, sr.nparts, a.dQ + (size_t)(a.v0 + sr.row) * N, false);
   }
 }
 

@@ -134,6 +134,8 @@ struct DxArgs {
   const float2* ad;                           // RGAT: (alpha, dpre) per position
   const void* H;                              // [J, K] fp32 (or bf16 with h_bf16): G_v W_r^T per (etype, dst) run
   int h_bf16;
+  void* outb;                                 // non-RGAT walk: bf16 output rows at orow[row] instead of dX (HGT)
+  const int32_t* orow;
   const float* U0;                            // RGAT: [R, K] W_r A[r,0]
   const float* U1;                            // RGAT: [R, K] W_r A[r,1]
   const Item* ditems;                         // RGAT destination terms: the dst work list
@@ -180,6 +182,7 @@ struct HgtBwdArgs {
   float* alpha;           // [E_own] by position
   float* da;              // [E_own] by position
   float* dQ;              // [V, N] node-id order (owned rows written)
+  void* dQb;              // or: bf16 rows in node-type order (ninv), when non-null
   float* part;            // [num_parts, N]
   const SplitRow* split_rows;
   int64_t num_split_rows;
@@ -205,6 +208,10 @@ rgnn_status launch_hgt_piece_agg(int prec, int N, const HgtPieceArgs& a, cudaStr
 rgnn_status launch_f32_to_bf16(int64_t n, const float* a, void* b, cudaStream_t s);
 rgnn_status launch_hgt_zero_rows(int64_t V, int N, const int32_t* srow, float* dK, float* dV, int64_t v0, int64_t v1,
                                  const int32_t* empty_rows, int64_t num_empty, float* dQ, cudaStream_t s);
+// the same on bf16 rows in node-type order (row of node u = ninv[u])
+rgnn_status launch_hgt_zero_rows_b(int64_t V, int N, const int32_t* srow, const int32_t* ninv, void* dK, void* dV,
+                                   int64_t v0, int64_t v1, const int32_t* empty_rows, int64_t num_empty, void* dQ,
+                                   cudaStream_t s);
 // out[i] = ninv[idx[i] + ofs]
 rgnn_status launch_map_gather(int64_t n, const int32_t* idx, const int32_t* ninv, int32_t* out, cudaStream_t s,
                               int64_t ofs = 0);

@@ -70,7 +70,8 @@ struct HgtWs {
   float *alpha, *da;      // [E_own] by position
   int32_t* vrow;          // [E_own] node-type row of the source of position p
   int32_t* qrun;          // [J] node-type row of the destination of run j
-  float *dQ, *dK, *dV;    // [V, N] node-id order
+  float *dQ, *dK, *dV;    // [V, N] node-id order (fp32 layer)
+  void *dQb, *dKb, *dVb;  // bf16 layer: [V, N] bf16 rows in node-type order (the node dW GEMMs' B operand)
   float* H;               // [J, N] fp32: G_t Wm_r^T, then q_t Wa_r^T
   void* Bb;               // [max(E_own, V), N] bf16 B operand of the tcgen05 dW GEMMs
   float* dwpart;          // dW split-K partials
@@ -102,6 +103,9 @@ static HgtWs hgt_ws_layout(const rgnn_graph* g, int K, int N, int prec, void* ba
     w.dQ = c.take<float>((size_t)V * N);
     w.dK = c.take<float>((size_t)V * N);
     w.dV = c.take<float>((size_t)V * N);
+    w.dQb = c.take<char>(bf ? (size_t)V * N * 2 : 1);
+    w.dKb = c.take<char>(bf ? (size_t)V * N * 2 : 1);
+    w.dVb = c.take<char>(bf ? (size_t)V * N * 2 : 1);
     w.H = c.take<float>((size_t)J * N);
     const int64_t NP = std::max<int64_t>(g->num_pieces, 1);
     w.Bb = c.take<char>(bf ? (size_t)std::max(std::max(E, 2 * V), NP) * N * 2 : 1);  // also the bf16 v, k copies
@@ -443,15 +447,20 @@ rgnn_status hgt_backward(const rgnn_graph* g, int K, int N, rgnn_prec prec, cons
     }
     RGNN_TRY(launch_map_gather(E, g->src_s, g->ninv, w.vrow, s));
     RGNN_TRY(launch_map_gather(J, g->run_dst, g->ninv, w.qrun, s, g->v0));
-    RGNN_TRY(launch_hgt_zero_rows(V, N, g->srow, w.dK, w.dV, g->v0, g->v0 + g->V_own, g->empty_rows, g->num_empty,
-                                  w.dQ, s));
+    if (bf)
+      RGNN_TRY(launch_hgt_zero_rows_b(V, N, g->srow, g->ninv, w.dKb, w.dVb, g->v0, g->v0 + g->V_own, g->empty_rows,
+                                      g->num_empty, w.dQb, s));
+    else
+      RGNN_TRY(launch_hgt_zero_rows(V, N, g->srow, w.dK, w.dV, g->v0, g->v0 + g->V_own, g->empty_rows,
+                                    g->num_empty, w.dQ, s));
   }
   {
     Phase ph("hgt_bwd_walk", s);
     HgtBwdArgs hb{};
     hb.items = g->items; hb.num_items = g->num_items; hb.pos = g->pos; hb.zrow = cm ? g->zrow_slot : nullptr;
     hb.KW = sv.KWf; hb.M = sv.M; hb.Q = sv.Qf; hb.ninv = g->ninv; hb.v0 = g->v0; hb.Y = Y; hb.dY = dY;
-    hb.lse = sv.lse; hb.alpha = w.alpha; hb.da = w.da; hb.dQ = w.dQ; hb.part = w.qpart;
+    hb.lse = sv.lse; hb.alpha = w.alpha; hb.da = w.da; hb.dQ = w.dQ; hb.dQb = bf ? w.dQb : nullptr;
+    hb.part = w.qpart;
     hb.split_rows = g->split_rows; hb.num_split_rows = g->num_split_rows;
     RGNN_TRY(launch_hgt_bwd_walk(RGNN_F32, N, hb, s));
   }
@@ -460,7 +469,7 @@ rgnn_status hgt_backward(const rgnn_graph* g, int K, int N, rgnn_prec prec, cons
   // gradients dWK / dWV, sums over nodes; O23), halving the walks' gathered bytes.
   const int h_bf16 = (bf && !tc_disabled() && !getenv("RGNN_HGT_H_F32")) ? 1 : 0;
   auto src_sum = [&](const float* G, const int32_t* gidx, int64_t grows, const float* Wt, const float* Wrr,
-                     const float* wpos, float* out) -> rgnn_status {
+                     const float* wpos, float* out, void* outb) -> rgnn_status {
     if (g->num_rtiles) {
       Phase ph("hgt_bwd_runs", s);
       GemmFwdArgs gh{};
@@ -474,10 +483,11 @@ rgnn_status hgt_backward(const rgnn_graph* g, int K, int N, rgnn_prec prec, cons
     xa.items = g->sitems; xa.num_items = g->num_sitems; xa.split = g->ssplit; xa.num_split = g->num_ssplit;
     xa.part = w.xpart; xa.srow = g->srow; xa.spos = g->spos; xa.srun = g->srun; xa.srel = g->srel;
     xa.sinvc = g->sinvc; xa.wpos = wpos; xa.H = w.H; xa.h_bf16 = h_bf16; xa.dX = out;
+    xa.outb = outb; xa.orow = g->ninv;  // bf16 layer: rows straight into the node dW GEMM's B layout
     return launch_dx_walk(N, false, xa, s);
   };
-  RGNN_TRY(src_sum(dY, g->run_dst, g->V_own, w.WmT, w.Wmr, w.alpha, w.dV));
-  RGNN_TRY(src_sum(sv.Qf, w.qrun, V, w.WaT, w.War, w.da, w.dK));
+  RGNN_TRY(src_sum(dY, g->run_dst, g->V_own, w.WmT, w.Wmr, w.alpha, w.dV, bf ? w.dVb : nullptr));
+  RGNN_TRY(src_sum(sv.Qf, w.qrun, V, w.WaT, w.War, w.da, w.dK, bf ? w.dKb : nullptr));
   // dW GEMMs: part = sum_p Xin[gather p]^T (scale_p Gm[gidx p]), reduced per segment in chunk order
   auto dw = [&](int xprec, int Kd, const void* Xin, const int32_t* gather, int64_t xrows, const Tile* chunks,
                 int64_t nch, const int32_t* cseg, int nseg, int64_t rows, const float* Gm, const int32_t* gidx,
@@ -514,7 +524,8 @@ rgnn_status hgt_backward(const rgnn_graph* g, int K, int N, rgnn_prec prec, cons
       RGNN_TRY(launch_f32_to_bf16((int64_t)V * N, sv.Vn, w.Bb, s));
       RGNN_TRY(launch_f32_to_bf16((int64_t)V * N, sv.Kf, static_cast<char*>(w.Bb) + (size_t)V * N * 2, s));
       pa.Vn = w.Bb; pa.Kn = static_cast<char*>(w.Bb) + (size_t)V * N * 2; pa.in_bf16 = 1;
-    } pa.dst_s = g->dst_s; pa.ninv = g->ninv; pa.v0 = g->v0; pa.vagg = w.vagg;
+    }
+    pa.dst_s = g->dst_s; pa.ninv = g->ninv; pa.v0 = g->v0; pa.vagg = w.vagg;
     pa.kagg = w.kagg; pa.pdst = w.pdst; pa.pq = w.pq;
     RGNN_TRY(launch_hgt_piece_agg(prec, N, pa, s));
     const int64_t NP = g->num_pieces;
@@ -525,12 +536,32 @@ rgnn_status hgt_backward(const rgnn_graph* g, int K, int N, rgnn_prec prec, cons
   }
   {
     Phase ph("hgt_bwd_dw_node", s);
-    RGNN_TRY(dw(prec, K, X, g->nperm, V, g->nchunks, g->num_nchunks, g->nchunk_seg, (int)T, V, w.dK, g->nperm,
-                nullptr, dWK));
-    RGNN_TRY(dw(prec, K, X, g->nperm, V, g->nchunks, g->num_nchunks, g->nchunk_seg, (int)T, V, w.dV, g->nperm,
-                nullptr, dWV));
-    RGNN_TRY(dw(prec, K, X, g->nperm, V, g->nchunks, g->num_nchunks, g->nchunk_seg, (int)T, V, w.dQ, g->nperm,
-                nullptr, dWQ));
+    if (bf) {  // B rows already bf16 in node-type order (written by the walks): no expansion pass
+      auto dw_b = [&](const void* Bt, float* out) -> rgnn_status {
+        if (g->num_nchunks == 0) {
+          RGNN_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)T * K * N, s));
+          return RGNN_OK;
+        }
+        GemmDwArgs a{};
+        a.chunks = g->nchunks; a.num_chunks = g->num_nchunks; a.rows = V; a.X = X; a.gather = g->nperm;
+        a.x_rows = V; a.part = w.dwpart; a.Bz = Bt;
+        rgnn_status st = launch_gemm_dw_tc(K, N, a, s);
+        if (st == RGNN_E_UNSUPPORTED) st = launch_gemm_dw(prec, K, N, a, s);  // d_in = 32 / no tcgen05
+        RGNN_TRY(st);
+        return launch_dw_reduce(prec, K, N, (int)T, g->num_nchunks, g->nchunk_seg, w.dwpart, nullptr, nullptr,
+                                nullptr, nullptr, out, nullptr, nullptr, s);
+      };
+      RGNN_TRY(dw_b(w.dKb, dWK));
+      RGNN_TRY(dw_b(w.dVb, dWV));
+      RGNN_TRY(dw_b(w.dQb, dWQ));
+    } else {
+      RGNN_TRY(dw(prec, K, X, g->nperm, V, g->nchunks, g->num_nchunks, g->nchunk_seg, (int)T, V, w.dK, g->nperm,
+                  nullptr, dWK));
+      RGNN_TRY(dw(prec, K, X, g->nperm, V, g->nchunks, g->num_nchunks, g->nchunk_seg, (int)T, V, w.dV, g->nperm,
+                  nullptr, dWV));
+      RGNN_TRY(dw(prec, K, X, g->nperm, V, g->nchunks, g->num_nchunks, g->nchunk_seg, (int)T, V, w.dQ, g->nperm,
+                  nullptr, dWQ));
+    }
   }
   if (comm) {
     float* bufs[5] = {dWK, dWQ, dWV, dWa, dWm};
