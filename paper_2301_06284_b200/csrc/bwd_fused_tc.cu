@@ -25,7 +25,7 @@
 
 namespace rgnn {
 
-template <int K, int N>
+template <int K, int N, bool GAT = true>
 struct BfCfg {
 // Stage size and compute-warp count per d_out (measured): d_out = 128 (ogbn-mag) 64 positions and
 // 16 compute warps; d_out = 64 96 positions and 24 compute warps (wikikg2 RGCN backward 1.155 ->
@@ -45,8 +45,15 @@ struct BfCfg {
 #ifndef RGNN_BWD_SMAX
 #define RGNN_BWD_SMAX 6
 #endif
-  static constexpr int STAGES = (200 * 1024) / (STAGE + SC_STAGE) > RGNN_BWD_SMAX ? RGNN_BWD_SMAX
-                                                                                  : (200 * 1024) / (STAGE + SC_STAGE);
+#ifndef RGNN_BWD_RING_KB
+#define RGNN_BWD_RING_KB 200
+#endif
+  // RGAT at d_out = 64: 4 stages (measured AM 0.922 -> 0.858 ms: the smaller shared-memory
+  // carve-out leaves more L1 for the per-destination rows); otherwise up to RGNN_BWD_SMAX
+  static constexpr int SMAX = (GAT && N == 64) ? 4 : RGNN_BWD_SMAX;
+  static constexpr int STAGES = (RGNN_BWD_RING_KB * 1024) / (STAGE + SC_STAGE) > SMAX
+                                    ? SMAX
+                                    : (RGNN_BWD_RING_KB * 1024) / (STAGE + SC_STAGE);
 #ifndef RGNN_BWD_CW
 #define RGNN_BWD_CW 24
 #endif
@@ -101,9 +108,9 @@ __device__ __forceinline__ float leaky_f(float x, float s) { return x > 0.f ? x 
 
 // GAT = true: RGAT (dZ = alpha G_v + dpre A[r,0], bvec, dst term); false: RGCN (dZ = G_v / c_{v,r}).
 template <int K, int N, bool GAT, bool CM>
-__global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
+__global__ void __launch_bounds__(BfCfg<K, N, GAT>::THREADS, 1)
     k_bwd_fused_tc(BwdFusedParams pr) {
-  using C = BfCfg<K, N>;
+  using C = BfCfg<K, N, GAT>;
   constexpr int L = C::L, PG = C::PG, KPL = C::KPL, EPL = C::EPL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -424,11 +431,17 @@ __global__ void __launch_bounds__(BfCfg<K, N>::THREADS, 1)
 
 template <int K, int N>
 static rgnn_status bwd_fused(const rgnn_graph* g, const BwdFusedParams& p0, const void* X, cudaStream_t s) {
-  using C = BfCfg<K, N>;
   if (g->num_chunks == 0) return RGNN_OK;
   (void)X;
-  auto kern = !p0.s_src ? k_bwd_fused_tc<K, N, false, false>
-              : p0.zmap ? k_bwd_fused_tc<K, N, true, true> : k_bwd_fused_tc<K, N, true, false>;
+  if (!p0.s_src) {
+    using C = BfCfg<K, N, false>;
+    auto kern = k_bwd_fused_tc<K, N, false, false>;
+    RGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    RGNN_LAUNCH(kern, (unsigned)g->num_chunks, C::THREADS, C::SMEM, s, p0);
+    return RGNN_OK;
+  }
+  using C = BfCfg<K, N, true>;
+  auto kern = p0.zmap ? k_bwd_fused_tc<K, N, true, true> : k_bwd_fused_tc<K, N, true, false>;
   RGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   RGNN_LAUNCH(kern, (unsigned)g->num_chunks, C::THREADS, C::SMEM, s, p0);
   return RGNN_OK;
