@@ -115,6 +115,9 @@ __device__ __forceinline__ void dst_scores(const float* xv, const float* U, int 
 #ifndef RGNN_AGG_PREFETCH
 #define RGNN_AGG_PREFETCH 1
 #endif
+#ifndef RGNN_RING
+#define RGNN_RING 4  // cp.async ring depth of the RGCN walk (steps of Z rows in flight + 1)
+#endif
 template <typename T, int K, int N, bool RGAT, bool CACHE>
 __global__ void __launch_bounds__(256, RGNN_AGG_MINB) k_aggregate(AggArgs a) {
   using S = WalkShape<T, K, N>;
@@ -693,7 +696,7 @@ static rgnn_status aggregate(bool rgat, const AggArgs& a, cudaStream_t s) {
     // 0.805 vs 0.836 ms); the ring still wins for RGCN at d_out = 64 (wikikg2 1.00 vs 1.26 ms)
     const bool ring = !no_ring && ((N <= 64 && !rgat) || force_ring);
     if (ring) {
-      constexpr int RING = 4, UNR = WalkShape<T, K, N>::UNR;
+      constexpr int RING = RGNN_RING, UNR = WalkShape<T, K, N>::UNR;
       const size_t smem = 8 * (RING * UNR * 32 * sizeof(uint4) + RING * 32 * 2 * sizeof(float));
       auto kern = !rgat ? k_aggregate_ring<T, K, N, false, RING, false>
                   : a.cache_dst ? k_aggregate_ring<T, K, N, true, RING, true> : k_aggregate_ring<T, K, N, true, RING, false>;
