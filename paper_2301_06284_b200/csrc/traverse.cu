@@ -33,12 +33,15 @@ __device__ __forceinline__ float leaky(float x, float slope) { return x > 0.f ? 
 #ifndef RGNN_WALK_UNR
 #define RGNN_WALK_UNR 4
 #endif
+#ifndef RGNN_WALK_UNR_NARROW
+#define RGNN_WALK_UNR_NARROW 2  // rows narrower than 8 lanes' 16-byte slices (G >= 4 groups per warp)
+#endif
 template <typename T, int K, int N>
 struct WalkShape {
   static constexpr int EPL = 16 / sizeof(T);  // features per lane (one 16-byte load)
   static constexpr int L = N / EPL;           // lanes per Z row
   static constexpr int G = 32 / L;            // edge groups per warp
-  static constexpr int UNR = G >= 4 ? 2 : RGNN_WALK_UNR;  // edges per group per step
+  static constexpr int UNR = G >= 4 ? RGNN_WALK_UNR_NARROW : RGNN_WALK_UNR;  // edges per group per step
   static constexpr int B = G * UNR;           // edges per warp step (<= 32)
   static constexpr int KPL = K / L;           // x_dst features per lane
   static_assert(L >= 1 && L <= 32 && B <= 32, "shape");
