@@ -91,7 +91,10 @@ struct FwdCfg {
   static constexpr uint32_t LAYOUT = RB == 128 ? 2u : 4u;   // UMMA layout type
   static constexpr int A_BYTES = M * K * 2;
   static constexpr int B_BYTES = N * K * 2;
-  static constexpr int STAGES = (96 * 1024) / A_BYTES > 8 ? 8 : (96 * 1024) / A_BYTES;
+#ifndef RGNN_FWD_RING_KB
+#define RGNN_FWD_RING_KB 64  // measured: 64 KB of A stages beats 32, 48, 96, 128 (mag, AM, wikikg2)
+#endif
+  static constexpr int STAGES = (RGNN_FWD_RING_KB * 1024) / A_BYTES > 8 ? 8 : (RGNN_FWD_RING_KB * 1024) / A_BYTES;
   static constexpr int DEPTH = STAGES - 1;                  // cp.async groups kept in flight per producer thread
   static constexpr int STG_BYTES = M * N * 2;
   static constexpr int NCOLS = (2 * N) <= 32 ? 32 : (2 * N) <= 64 ? 64 : (2 * N) <= 128 ? 128 : 256;
