@@ -31,7 +31,10 @@ struct Tf32Cfg {
   static constexpr int B_BYTES = N * K * 4;
   static constexpr int NB = (B_BYTES <= 32 * 1024) ? 2 : 1; // W slots
   static constexpr int STAGES_MAX = (200 * 1024 - NB * B_BYTES) / A_BYTES;
-  static constexpr int STAGES = STAGES_MAX > 6 ? 6 : STAGES_MAX;
+#ifndef RGNN_TF32_SMAX
+#define RGNN_TF32_SMAX 6
+#endif
+  static constexpr int STAGES = STAGES_MAX > RGNN_TF32_SMAX ? RGNN_TF32_SMAX : STAGES_MAX;
   static constexpr int DEPTH = STAGES - 1;
   static constexpr int NCOLS = (2 * N) <= 32 ? 32 : (2 * N) <= 64 ? 64 : (2 * N) <= 128 ? 128 : 256;
   static constexpr int SMEM = 1024 + STAGES * A_BYTES + NB * B_BYTES + 256;
