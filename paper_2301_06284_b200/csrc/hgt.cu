@@ -123,8 +123,11 @@ rgnn_status launch_map_gather(int64_t n, const int32_t* idx, const int32_t* ninv
 // (max, sum, acc) state, merged in a fixed xor tree.  Deterministic, no atomics.
 // TS: type of the score factors kw and q (fp32 on both paths: bf16 logits lose ~2-4% of rms(Y)
 // at single elements through exp, measured against the oracle; O23); TM: message type.
+#ifndef RGNN_HGTF_MINB
+#define RGNN_HGTF_MINB 1
+#endif
 template <typename TS, typename TM, int N>
-__global__ void __launch_bounds__(256) k_aggregate_hgt(HgtAggArgs a) {
+__global__ void __launch_bounds__(256, RGNN_HGTF_MINB) k_aggregate_hgt(HgtAggArgs a) {
   constexpr int EPL = 16 / sizeof(TM);
   constexpr int SV = EPL * sizeof(TS) / 16;  // 16-byte vectors of a lane's kw / q slice
   constexpr int L = N / EPL;
