@@ -182,8 +182,20 @@ __global__ void k_dw_reduce(int K, int N, int R, int64_t num_chunks, const int32
     int kn = (int)(i - (int64_t)r * K * N);
     int k = kn / N, n = kn - k * N;
     int c0 = chunk_seg ? chunk_seg[r] : 0, c1 = chunk_seg ? chunk_seg[r + 1] : (int)num_chunks;
-    float s = 0.f;
-    for (int c = c0; c < c1; ++c) s += part[(size_t)c * stride + kn];
+    // four independent partial sums (chunk c goes to c % 4), combined in a fixed order: the
+    // loads of four chunks are in flight at once and the result stays deterministic
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int c = c0;
+    for (; c + 3 < c1; c += 4) {
+      s0 += part[(size_t)c * stride + kn];
+      s1 += part[(size_t)(c + 1) * stride + kn];
+      s2 += part[(size_t)(c + 2) * stride + kn];
+      s3 += part[(size_t)(c + 3) * stride + kn];
+    }
+    if (c < c1) s0 += part[(size_t)c * stride + kn];
+    if (c + 1 < c1) s1 += part[(size_t)(c + 1) * stride + kn];
+    if (c + 2 < c1) s2 += part[(size_t)(c + 2) * stride + kn];
+    float s = (s0 + s1) + (s2 + s3);
     if (A) {
       float cv = 0.f;
       for (int c = cseg[r]; c < cseg[r + 1]; ++c) cv += cpart[(size_t)c * K + k];
