@@ -51,6 +51,13 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time of the cpu_baseline sample")
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of a captured CUDA graph")
     ap.add_argument("--dx", action="store_true", help="also compute the input-feature gradient dX (NEXT-2)")
+    ap.add_argument("--aggregate-first", action="store_true",
+                    help="RGCN: aggregate-first forward (NEXT-4: run-piece sums of x_src, GEMM over the pieces)")
+    ap.add_argument("--gather-sync", action="store_true", help="N>1: gather Y on the caller's stream (no overlap)")
+    ap.add_argument("--gather-bf16", action="store_true", help="N>1: gather Y_full in bf16 (half the volume)")
+    ap.add_argument("--comm-variants", action="store_true",
+                    help="also time compute-only / synchronous / overlapped / bf16 gathers (always on for N>1; "
+                         "at N=1 a one-rank communicator exercises the same path)")
     ap.add_argument("--materialization", default="auto", choices=["vanilla", "compact", "auto"],
                     help="per-edge (vanilla) or per-(etype, src) (compact, PAPER.md P:513-531) Z / s_src rows; "
                          "auto = compact when U <= E/2")
@@ -86,8 +93,8 @@ def config_json(cfg, model, prec, g, world):
                         f"fwd+bwd, d={cfg.K}",
             "model": model, "prec": prec, "V": int(g.V), "E": int(g.E), "R": int(g.R), "d_in": cfg.K,
             "d_out": cfg.N, "seeds": "graph 0, X 1, W 2, A 3, dY 4 (synth/)", "l2": l2,
-            "parallelism": f"dst-range partition x{world} (NCCL Y gather + dW all-reduce)" if world > 1
-            else "1 GPU"}
+            "parallelism": f"dst-range partition x{world} (NCCL Y gather overlapped with the backward + dW "
+                           f"all-reduce)" if world > 1 else "1 GPU"}
 
 
 # --------------------------------------------------------------------- algorithmic bytes
@@ -275,14 +282,19 @@ def run_ours(args):
     bounds = m.partition_dst(indeg, world)
     v0, v1 = int(bounds[rank]), int(bounds[rank + 1])
 
-    # preprocessing (timed separately, not part of the step)
+    # preprocessing (timed separately, not part of the step).  A tiny graph is created first so the
+    # library's lazily loaded kernels (CUDA module loading) are not charged to the timed creation.
+    tiny = synth.random_graph(64, 256, g.R, seed=1)
+    m.Graph(tiny.V, tiny.src, tiny.dst, tiny.etype, tiny.R, materialization=args.materialization,
+            build_dx=args.dx or model == "hgt", ntype=tiny.ntype if model == "hgt" else None,
+            num_ntypes=1 if model == "hgt" else 0, device=dev)
     src = torch.from_numpy(g.src).to(dev); dst = torch.from_numpy(g.dst).to(dev)
     et = torch.from_numpy(g.etype).to(dev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     G = m.Graph(g.V, src, dst, et, g.R, dst_begin=v0, dst_end=v1, materialization=args.materialization,
                 build_dx=args.dx or model == "hgt", ntype=g.ntype if model == "hgt" else None,
-                num_ntypes=g.T if model == "hgt" else 0, device=dev)
+                num_ntypes=g.T if model == "hgt" else 0, aggregate_first=args.aggregate_first, device=dev)
     torch.cuda.synchronize()
     prep_ms = 1e3 * (time.perf_counter() - t0)
     del src, dst, et
@@ -294,11 +306,19 @@ def run_ours(args):
     dY = torch.from_numpy(np.ascontiguousarray(t.dY[v0:v1])).to(dev)
     ws = m.Workspace(G, model, K, N, prec, dx=args.dx)
     dX = torch.empty(g.V, K, dtype=torch.float32, device=dev) if args.dx else None
-    Y_full = torch.empty(g.V, N, dtype=torch.float32, device=dev) if world > 1 else None
-    Y = Y_full[v0:v1] if world > 1 else torch.empty(v1 - v0, N, dtype=torch.float32, device=dev)
+    use_comm = world > 1 or args.comm_variants
+    # multi-GPU default: the Y gather is asynchronous (overlapped with the backward, which reads only
+    # the owned rows) and joined at the end of the step; --gather-sync / --gather-bf16 for A/B
+    gather_bf16 = args.gather_bf16
+    Y_full = (torch.empty(g.V, N, dtype=torch.bfloat16 if gather_bf16 else torch.float32, device=dev)
+              if use_comm else None)
+    Y = (Y_full[v0:v1] if use_comm and not gather_bf16
+         else torch.empty(v1 - v0, N, dtype=torch.float32, device=dev))
     dW = torch.empty(g.R, K, N, dtype=torch.float32, device=dev)
     dA = torch.empty(g.R, 2, N, dtype=torch.float32, device=dev) if model == "rgat" else None
-    comm = m.Comm(bounds, rank, world) if world > 1 else None
+    comm = m.Comm(bounds, rank, world) if use_comm else None
+    if comm is not None:
+        comm.set_options(gather_async=not args.gather_sync, gather_bf16=gather_bf16)
     stream = torch.cuda.current_stream(dev)
 
     HW = None
@@ -327,6 +347,8 @@ def run_ours(args):
     def step(Xs=X, Ws=W, As=A, dYs=dY, HWs=None):
         fwd(Xs, Ws, As, HWs)
         bwd(Xs, Ws, As, dYs, HWs)
+        if comm is not None:
+            comm.join()  # Y_full complete before the step ends
 
     def barrier():
         torch.cuda.synchronize()
@@ -426,6 +448,52 @@ def run_ours(args):
         ms = float(tm.item())
     value = g.E / (ms * 1e-3)
 
+    # ---- multi-GPU reporting: compute-only (sharded Y, no gather) and the step with a
+    # synchronous, an overlapped (asynchronous, joined at step end) and a bf16 overlapped gather;
+    # eager steps timed by CUDA events, max over ranks
+    multi = None
+    if comm is not None:
+        def timed_events(fn, n):
+            fn()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(n):
+                fn()
+            e1.record(stream)
+            barrier()
+            t_ = torch.tensor([e0.elapsed_time(e1) / n], device=dev)
+            if world > 1:
+                dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+            return float(t_.item())
+
+        nvar = max(3, min(args.steps, 10))
+        saved_full = Y_full
+
+        def variant(flags_async, flags_bf16, with_gather=True):
+            nonlocal Y_full
+            comm.set_options(gather_async=flags_async, gather_bf16=flags_bf16)
+            if not with_gather:
+                Y_full = None
+            elif flags_bf16 != gather_bf16:
+                Y_full = torch.empty(g.V, N, dtype=torch.bfloat16 if flags_bf16 else torch.float32, device=dev)
+            else:
+                Y_full = saved_full
+            try:
+                return timed_events(step, nvar)
+            finally:
+                Y_full = saved_full
+                comm.set_options(gather_async=not args.gather_sync, gather_bf16=gather_bf16)
+
+        yb = (g.V * N * 4, g.V * N * 2)
+        multi = {"compute_only_ms": variant(True, gather_bf16, with_gather=False),
+                 "gather_sync_ms": variant(False, False), "gather_overlapped_ms": variant(True, False),
+                 "gather_overlapped_bf16_ms": variant(True, True),
+                 "y_gather_bytes_per_rank": {"fp32": int(yb[0] * (world - 1) / max(world, 1)),
+                                             "bf16": int(yb[1] * (world - 1) / max(world, 1))},
+                 "steps": nvar, "launch": "eager", "default": "overlapped" + (" bf16" if gather_bf16 else "")
+                 if not args.gather_sync else "sync"}
+
     # ---- end to end through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
@@ -516,9 +584,26 @@ def run_ours(args):
         oloss = torch.empty(1, dtype=torch.float32).pin_memory()
         nll_scale = 1.0 / g.V  # mean over all V rows (every rank owns a slice)
 
+        # X (the large input) is double-buffered: step i+1's X is copied in on a side stream while
+        # step i runs (both copies stay inside the timed region: one X upload per timed step)
+        xbufs = [dX_, torch.empty_like(dX_)]
+        s_up = torch.cuda.Stream(dev)
+        ev_up = [torch.cuda.Event(), torch.cuda.Event()]
+        tstate = {"i": 0}
+        with torch.cuda.stream(s_up):
+            xbufs[0].copy_(hX, non_blocking=True)
+            ev_up[0].record(s_up)
+
         def train_step():
             main = torch.cuda.current_stream(dev)
-            dX_.copy_(hX, non_blocking=True)
+            i = tstate["i"]
+            cur, nxt = xbufs[i % 2], xbufs[(i + 1) % 2]
+            main.wait_event(ev_up[i % 2])          # this step's X has landed
+            s_up.wait_stream(main)                 # (the previous step, which read nxt, is done)
+            with torch.cuda.stream(s_up):
+                nxt.copy_(hX, non_blocking=True)   # next step's X under this step's compute
+                ev_up[(i + 1) % 2].record(s_up)
+            tstate["i"] = i + 1
             dlab.copy_(hlab, non_blocking=True)
             if model == "hgt":
                 for a, b in zip(dHW, hHW):
@@ -526,13 +611,13 @@ def run_ours(args):
             else:
                 dW_.copy_(hW, non_blocking=True)
                 dA_.copy_(hA, non_blocking=True)
-            fwd(dX_, dW_, dA_, HWs=dHW if model == "hgt" else None)
+            fwd(cur, dW_, dA_, HWs=dHW if model == "hgt" else None)
             lp = torch.log_softmax(Y, dim=1)
             loss = -lp.gather(1, dlab.view(-1, 1)).sum() * nll_scale
             dyy = lp.exp_()
             dyy[torch.arange(dyy.shape[0], device=dev), dlab] -= 1.0
             dyy.mul_(nll_scale)
-            bwd(dX_, dW_, dA_, dyy, HWs=dHW if model == "hgt" else None)
+            bwd(cur, dW_, dA_, dyy, HWs=dHW if model == "hgt" else None)
             oloss.copy_(loss.view(1), non_blocking=True)
             if model == "hgt":
                 for o, gr in zip(ohg, hgrads):
@@ -552,7 +637,8 @@ def run_ours(args):
                "d2h_bytes_per_step": int(d2h_t), "steps": n_e2e,
                "protocol": "training step (P:843): X, weights and random labels in; forward; NLL(log_softmax(Y)) "
                            "loss and dY on the device (torch, the caller's loss); backward; loss and weight "
-                           "gradients out"
+                           "gradients out; X double-buffered (step i+1's X is copied in on a side stream during "
+                           "step i, one X upload per timed step)"
                            + ("; dX not computed" if not args.dx else "; dX computed, not copied out"),
                "layer_io": e2e_io}
 
@@ -582,7 +668,7 @@ def run_ours(args):
                 "peak_source": peak_src}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:  # rank 0 only (the other ranks wait at the final barrier)
         run, want, cores = oracle_sample(g, t, model, K, N, args.cpu_seconds, args.slope, prec)
         ne, dt, rng = run(want)
         cpu = {"value": ne / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
@@ -598,14 +684,16 @@ def run_ours(args):
                               backward=("dWK, dWQ, dWV, dWa, dWm" if model == "hgt" else
                                         "dW, dA" + (", dX (NEXT-2)" if args.dx else "") if model == "rgat" else
                                         "dW" + (", dX (NEXT-2)" if args.dx else "")),
-                              materialization=("compact" if G.zrows(model) != G.E_own else "vanilla") + (
-                                  " (auto)" if args.materialization == "auto" else ""),
+                              materialization=("aggregate-first (run pieces)" if args.aggregate_first
+                                               and model == "rgcn" else
+                                               ("compact" if G.zrows(model) != G.E_own else "vanilla") + (
+                                  " (auto)" if args.materialization == "auto" else "")),
                               z_rows=G.zrows(model), compact_rows=int(G.num_compact)),
                "clocks": clocks, "e2e": e2e,
-               "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu,
+               "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu, "multi_gpu": multi,
                "phases_ms_per_step": {k: round(x[0], 4) for k, x in sorted(step_phase.items())},
                "step_ms_percentiles": step_pct,
-               "preprocess_ms": prep_ms, "generate_s": round(t_gen, 1)}
+               "preprocess_ms": G.create_ms, "preprocess_with_alloc_ms": prep_ms, "generate_s": round(t_gen, 1)}
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()

@@ -82,6 +82,14 @@ typedef enum { RGNN_MAT_VANILLA = 0, RGNN_MAT_COMPACT = 1, RGNN_MAT_AUTO = 2 } r
  * run of each position and its destination / relation, and a source-major
  * CSR over the positions with a split work list (≈ 7 int32 per edge + V).  */
 #define RGNN_GRAPH_DX 1
+/* RGNN_GRAPH_AGGFIRST: build the run-piece tables of the
+ * aggregate-first RGCN forward -- Y_v = sum_r (1/c_{v,r}) (sum_{e in run(r,v)}
+ * x_src) W_r: each (etype, dst) run cut into pieces of <= 64 positions,
+ * A_i = sum (1/c) x_src per piece, one typed GEMM P_i = A_i W_r over the
+ * pieces, and the destination walk adds each row's piece products.
+ * rgcn_forward on such a graph uses that formulation (the per-edge Z is
+ * never formed); the backward is unchanged.  (≈ 3 int32 per edge.)        */
+#define RGNN_GRAPH_AGGFIRST 2
 
 typedef struct rgnn_graph rgnn_graph;
 typedef struct rgnn_comm rgnn_comm;
@@ -128,6 +136,10 @@ typedef struct {
   const int32_t* crow_of_pos; /* [E_own] compact row of position p          */
   const int32_t* csrc;     /* [num_compact] src node of compact row         */
   const int32_t* cseg;     /* [R+1] compact rows of relation r              */
+  int64_t num_pieces;      /* run pieces (<= 64 positions of one run; 0: not built) */
+  const int32_t* piece_ptr;  /* [num_pieces+1] first position of piece i    */
+  const int32_t* slot_piece; /* [E_own] piece of slot q's position (AGGFIRST) */
+  const float* slot_w;     /* [E_own] 1 for a piece's first slot in its row, else 0 (AGGFIRST) */
 } rgnn_graph_view;
 
 /* Sizes of the caller-owned graph storage (kept for the handle's life) and
@@ -138,9 +150,14 @@ rgnn_status rgnn_graph_bytes(const rgnn_graph_desc* desc, size_t* dev_bytes, siz
  * ids; keep edges whose dst is owned; stable sort by (etype, dst); relation
  * segments; CSR-by-dst; (etype,dst) runs and 1/c; GEMM tile table; degree-
  * aware work list (rows longer than row_split_cap are split into chunks).
- * SYNC: host synchronisations read the validation flag, the owned-edge
- * count and the final counts (tile / chunk tables are built on the host).
- * RGNN_E_RANGE names the SMALLEST offending edge id (atomicMin).         */
+ * SYNC: two host synchronisations -- the validation flags with the owned-
+ * edge count, then the counts and relation segments (a third one when node
+ * types, dX tables or run pieces are built); the 128-row tile and dW chunk
+ * tables are then built on the host from the segments.
+ * RGNN_E_RANGE names the SMALLEST offending edge id (atomicMin).  CSR
+ * input: row_ptr is checked on the device (row_ptr[0] = 0, non-decreasing,
+ * row_ptr[V] = E) before it is used; a bad one returns RGNN_E_INVALID_ARG
+ * naming the first bad index (the expansion never writes outside [0, E)). */
 rgnn_status rgnn_graph_create(const rgnn_graph_desc* desc, void* dev, size_t dev_bytes, void* scratch,
                               size_t scratch_bytes, void* stream, rgnn_graph** out);
 rgnn_status rgnn_graph_export(const rgnn_graph* g, rgnn_graph_view* view /* [host] */);
@@ -223,8 +240,11 @@ rgnn_status hgt_backward(const rgnn_graph* g, int d_in, int d_out, rgnn_prec pre
  *   edges.  Needs a graph built with RGNN_GRAPH_DX and a workspace sized
  *   with RGNN_WS_DX (else RGNN_E_UNSUPPORTED / RGNN_E_WORKSPACE); RGCN with a
  *   self loop also needs W0 [d_in, d_out] (NULL: no self-loop term).
- *   With comm != NULL, dW / dA / dW0 / dX are all-reduced (sum) in place
- *   across ranks.  Outputs are overwritten.                                */
+ *   With comm != NULL, dW / dA / dW0 are all-reduced (sum) in place across
+ *   ranks, and dX is reduce-scattered over the dst partition: rows
+ *   [bounds[k], bounds[k+1]) of rank k's dX hold the full sum (the rows the
+ *   previous layer's rank k owns); its other rows keep rank k's partial
+ *   sums.  Outputs are overwritten.                                        */
 rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int d_in, int d_out, rgnn_prec prec,
                           const void* X, const float* W, const float* W0, const float* A, float slope,
                           const float* Y, const float* dY, const void* saved, float* dW, float* dA, float* dW0,
@@ -239,6 +259,21 @@ rgnn_status rgnn_comm_unique_id(void* id /* [host] 128 B */);
 rgnn_status rgnn_comm_create(const void* id /* [host] 128 B */, int nranks, int rank,
                              const int64_t* bounds /* [host] nranks+1 dst-range cut */, rgnn_comm** out);
 void rgnn_comm_destroy(rgnn_comm* c);
+
+/* Gather options (SURVEY.md Sec. 8(e) mitigations; default 0 = synchronous fp32 gather):
+ *   RGNN_COMM_GATHER_ASYNC  the forward's Y gather runs on the communicator's
+ *     own stream (a second NCCL communicator split from the first) after an
+ *     event on the caller's stream, which continues at once -- e.g. with the
+ *     backward, which reads only owned rows.  rgnn_comm_join(c, stream) makes
+ *     `stream` wait for the pending gather: call it before Y_full is read
+ *     (and before the end of a CUDA-graph capture that issued the gather).
+ *   RGNN_COMM_GATHER_BF16   Y_full is bf16 [V, d_out]: the owned rows are
+ *     rounded (RNE) into Y_full's own slice and broadcast from there (half
+ *     the NVLink volume); Y stays the fp32 owned rows.                      */
+#define RGNN_COMM_GATHER_ASYNC 1
+#define RGNN_COMM_GATHER_BF16 2
+rgnn_status rgnn_comm_set_options(rgnn_comm* c, int flags);
+rgnn_status rgnn_comm_join(rgnn_comm* c, void* stream);
 
 /* Balanced dst-range cut from the global in-degree prefix (host helper):
  * bounds[k] = the v whose indeg_prefix[v] is closest to k*E/P (ties -> the

@@ -11,6 +11,7 @@ Pins: tests/test_oracle_pins.py (DESIGN.md §5 lists which pin covers what).
 """
 from __future__ import annotations
 
+import bisect
 import ctypes as C
 import os
 import subprocess
@@ -142,7 +143,10 @@ def compaction(R: int, pre: Preprocessed) -> Compaction:
     crow = np.array([number[k] for k in keys], dtype=np.int32)
     csrc = np.array([s for _, s in pairs], dtype=np.int32)
     crel = np.array([r for r, _ in pairs], dtype=np.int32)
-    cseg = np.array([sum(1 for r2, _ in pairs if r2 < r) for r in range(R + 1)], dtype=np.int32)
+    # cseg[r] = number of pairs whose relation is < r; the pairs are sorted, so that count is the
+    # bisection point of r in their relation list (same numbers as counting them one by one)
+    rel_sorted = [r2 for r2, _ in pairs]
+    cseg = np.array([bisect.bisect_left(rel_sorted, r) for r in range(R + 1)], dtype=np.int32)
     return Compaction(crow, csrc, crel, cseg)
 
 

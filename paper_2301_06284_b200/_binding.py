@@ -18,7 +18,10 @@ RGNN_NORM_REL_INDEG, RGNN_NORM_NONE, RGNN_NORM_EDGE = 0, 1, 2
 RGNN_RGCN, RGNN_RGAT, RGNN_HGT = 0, 1, 2
 RGNN_MAT_VANILLA, RGNN_MAT_COMPACT, RGNN_MAT_AUTO = 0, 1, 2
 RGNN_GRAPH_DX = 1
+RGNN_GRAPH_AGGFIRST = 2
 RGNN_WS_DX = 3
+RGNN_COMM_GATHER_ASYNC = 1
+RGNN_COMM_GATHER_BF16 = 2
 
 STATUS_NAMES = {0: "RGNN_OK", 1: "RGNN_E_INVALID_ARG", 2: "RGNN_E_RANGE", 3: "RGNN_E_UNSUPPORTED",
                 4: "RGNN_E_WORKSPACE", 5: "RGNN_E_CUDA", 6: "RGNN_E_NCCL"}
@@ -39,7 +42,9 @@ class rgnn_graph_view(C.Structure):
                 ("perm", C.c_void_p), ("src_s", C.c_void_p), ("dst_s", C.c_void_p), ("seg", C.c_void_p),
                 ("row_ptr", C.c_void_p), ("pos", C.c_void_p), ("et_slot", C.c_void_p), ("inv_c", C.c_void_p),
                 ("run_ptr", C.c_void_p), ("rseg", C.c_void_p), ("seg_host", C.POINTER(C.c_int32)),
-                ("num_compact", C.c_int64), ("crow_of_pos", C.c_void_p), ("csrc", C.c_void_p), ("cseg", C.c_void_p)]
+                ("num_compact", C.c_int64), ("crow_of_pos", C.c_void_p), ("csrc", C.c_void_p), ("cseg", C.c_void_p),
+                ("num_pieces", C.c_int64), ("piece_ptr", C.c_void_p),
+                ("slot_piece", C.c_void_p), ("slot_w", C.c_void_p)]
 
 
 class RgnnError(RuntimeError):
@@ -65,6 +70,8 @@ _SIGS = {
                       _vp, _vp, _vp, _sz, _vp, _vp],
     "rgnn_comm_unique_id": [_vp],
     "rgnn_comm_create": [_vp, C.c_int, C.c_int, C.POINTER(_i64), C.POINTER(_vp)],
+    "rgnn_comm_set_options": [_vp, C.c_int],
+    "rgnn_comm_join": [_vp, _vp],
     "rgnn_partition_dst": [_i64, C.POINTER(_i64), C.c_int, C.POINTER(_i64)],
     "rgnn_zrows": [_vp, C.c_int, C.POINTER(_i64)],
     "hgt_forward": [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp, _vp],

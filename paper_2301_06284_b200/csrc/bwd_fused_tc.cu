@@ -146,7 +146,10 @@ __global__ void __launch_bounds__(BfCfg<K, N, GAT>::THREADS, 1)
     for (int i = 0; i < C::STAGES; ++i) {
       tc::mbar_init(&a_full[i], C::PW * 32);
       tc::mbar_init(&b_full[i], C::CW);
-      tc::mbar_init(&empty[i], 1);
+      // two arrivals free a stage: the MMAs' completion (tcgen05.commit) and the MMA thread itself,
+      // which has waited for the compute warps' dZ writes (b_full) -- redundant for the hardware, but
+      // a thread-level happens-before edge from those generic-proxy writes to the producer's refill
+      tc::mbar_init(&empty[i], 2);
     }
     tc::mbar_init(acc_full, 1);
     tc::mbar_fence_init();
@@ -261,6 +264,7 @@ __global__ void __launch_bounds__(BfCfg<K, N, GAT>::THREADS, 1)
           }
         }
         tc::umma_commit(&empty[st]);
+        tc::mbar_arrive(&empty[st]);
         if (it == nsub - 1) tc::umma_commit(acc_full);
       }
       __syncwarp();
@@ -431,6 +435,7 @@ __global__ void __launch_bounds__(BfCfg<K, N, GAT>::THREADS, 1)
 
 template <int K, int N>
 static rgnn_status bwd_fused(const rgnn_graph* g, const BwdFusedParams& p0, const void* X, cudaStream_t s) {
+  tc::watchdog_init();
   if (g->num_chunks == 0) return RGNN_OK;
   (void)X;
   if (!p0.s_src) {

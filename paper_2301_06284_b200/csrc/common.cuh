@@ -61,6 +61,10 @@ struct Carver {
 constexpr int kTileRows = 128;       // GEMM M tile (rows of Z per tile)
 constexpr int kPieceRows = 64;       // HGT backward: run pieces hold <= 64 positions
 constexpr int kDefaultSplitCap = 256; // max in-edges per traversal work item
+#ifndef RGNN_NARROW_CAP
+#define RGNN_NARROW_CAP 8
+#endif
+constexpr int kNarrowCap = RGNN_NARROW_CAP;  // forward walk: rows with <= this many in-edges go one per lane group
 
 // Work item of the destination walk: one CSR row, or one chunk of a long row.
 struct Item {
@@ -90,6 +94,11 @@ struct rgnn_graph {
   rgnn::SplitRow* split_rows;
   int32_t* empty_rows;  // rows without in-edges (no work item)
   int64_t num_empty;
+  // forward walk: rows with deg <= narrow_cap are walked one lane group per row (row-id order,
+  // empty rows included); witems = the work items of the other rows (deg > narrow_cap)
+  int32_t narrow_cap;
+  rgnn::Item* witems;
+  int64_t num_witems;
   // compact materialisation (NEXT-1): Z rows per unique (etype, src)
   // dX tables (NEXT-2; RGNN_GRAPH_DX)
   bool has_dx;
@@ -116,6 +125,13 @@ struct rgnn_graph {
   rgnn::Tile* pchunks;   // dW split-K chunks over the pieces
   int32_t* pchunk_seg;   // [R+1] first piece chunk of relation r
   int64_t num_pieces, num_pchunks;
+  // aggregate-first RGCN forward (NEXT-4; RGNN_GRAPH_AGGFIRST): GEMM tiles over the pieces, and per
+  // CSR slot its piece and weight (1 for the first slot of a piece in its row, else 0)
+  bool has_aggfirst;
+  rgnn::Tile* ptiles;
+  int64_t num_ptiles;
+  int32_t* slot_piece;
+  float* slot_w;
   bool has_compact;  // compact tables built (COMPACT or AUTO)
   int mat_mode;      // rgnn_materialization requested
   int64_t num_compact, num_ctiles;
@@ -249,7 +265,9 @@ struct Phase {
 rgnn_status scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int32_t* total, void* scratch,
                            size_t scratch_bytes, cudaStream_t s);
 size_t scan_scratch_bytes(int64_t n);
+// n_dev (optional): the number of items is *n_dev (device; <= n), read by the kernels -- the grid
+// and scratch are sized for n, so no host synchronisation is needed to learn the count.
 rgnn_status radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
-                             int bits, void* scratch, size_t scratch_bytes, cudaStream_t s, bool* result_in_alt);
+                             int bits, void* scratch, size_t scratch_bytes, cudaStream_t s, bool* result_in_alt, const int32_t* n_dev = nullptr);
 size_t radix_scratch_bytes(int64_t n);
 }  // namespace rgnn

@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(192, 1)
 
 template <int K, int N>
 static rgnn_status gemm_dw_tc(const GemmDwArgs& a, cudaStream_t s) {
+  tc::watchdog_init();
   using C = DwCfg<K, N>;
   if (a.num_chunks == 0) return RGNN_OK;
   if (!a.Bz) return RGNN_E_UNSUPPORTED;  // B must be a materialised bf16 dZ

@@ -182,7 +182,7 @@ __global__ void k_dw_reduce(int K, int N, int R, int64_t num_chunks, const int32
     int kn = (int)(i - (int64_t)r * K * N);
     int k = kn / N, n = kn - k * N;
     int c0 = chunk_seg ? chunk_seg[r] : 0, c1 = chunk_seg ? chunk_seg[r + 1] : (int)num_chunks;
-    // four independent partial sums (chunk c goes to c % 4), combined in a fixed order: the
+    // four independent partial sums (chunk c goes to (c - c0) % 4), combined in a fixed order: the
     // loads of four chunks are in flight at once and the result stays deterministic
     float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
     int c = c0;

@@ -4,8 +4,8 @@
 //
 // Segment MM (Sec. 2.2): tiles never straddle relations, one
 // bf16 copy of W_r per relation (never replicated per edge), X rows
-// gathered on load (the GEMM template's gather list) with TMA
-// tile::gather4, accumulators in TMEM, epilogue fused: RGAT source score
+// gathered on load (the GEMM template's gather list) by 16-byte
+// cp.async, accumulators in TMEM, epilogue fused: RGAT source score
 // s_src[p] = A[r,0] . Z_fp32[p] and RGCN per-row 1/c ("per-row
 // scalar ... applied to A tiles"), bf16 Z written through an XOR-swizzled smem
 // stage with coalesced 16-byte stores (rows beyond row1 are never written).
@@ -365,6 +365,7 @@ __global__ void __launch_bounds__(288, 1)
 
 template <int K, int N, bool F32OUT>
 static rgnn_status gemm_fwd_tc(const GemmFwdArgs& a, cudaStream_t s) {
+  tc::watchdog_init();
   using C = FwdCfg<K, N>;
   const int64_t ntiles = a.tiles ? a.num_tiles : (a.rows + C::M - 1) / C::M;
   if (ntiles == 0) return RGNN_OK;

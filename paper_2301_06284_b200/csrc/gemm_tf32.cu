@@ -258,6 +258,7 @@ bool tc_disabled();
 // which the caller fills (launch_transpose_w: RNE-rounded to bf16 values when requested).
 template <int K, int N>
 static rgnn_status gemm_fwd_tf32(const GemmFwdArgs& a, const float* wt_f32, cudaStream_t s) {
+  tc::watchdog_init();
   using C = Tf32Cfg<K, N>;
   const int64_t ntiles = a.tiles ? a.num_tiles : (a.rows + C::M - 1) / C::M;
   if (ntiles == 0) return RGNN_OK;

@@ -21,21 +21,24 @@ struct Counters {
   int32_t bad_edge, bad_node, E_own, J, num_items, num_parts, num_split_rows, num_empty, num_compact;
   int32_t num_sitems, num_sparts, num_ssplit;  // dX source work list
   int32_t num_pieces;                          // HGT backward run pieces
+  int32_t bad_csr;                             // CSR input: smallest row v with a bad row_ptr entry
+  int32_t num_witems;                          // forward walk: items of rows with deg > narrow cap
 };
 
 __global__ void k_init_counters(Counters* c, int32_t big) {
   c->bad_edge = big; c->bad_node = big; c->E_own = 0; c->J = 0;
   c->num_items = 0; c->num_parts = 0; c->num_split_rows = 0; c->num_empty = 0; c->num_compact = 0;
-  c->num_sitems = 0; c->num_sparts = 0; c->num_ssplit = 0; c->num_pieces = 0;
+  c->num_sitems = 0; c->num_sparts = 0; c->num_ssplit = 0; c->num_pieces = 0; c->bad_csr = big; c->num_witems = 0;
 }
 
-// Run pieces (HGT backward): every (etype, dst) run cut at the multiples of kPieceRows,
-// so a piece holds <= kPieceRows consecutive positions of one run.  Pieces are numbered in
+// Run pieces (HGT backward, aggregate-first RGCN): every (etype, dst) run cut every kPieceRows
+// positions from its start, so a piece holds <= kPieceRows consecutive positions of one run and
+// depends only on the run (a dst-range shard cuts its runs the same way).  Pieces are numbered in
 // position order; piece_ptr[i] is the first position of piece i.
 __global__ void k_piece_counts(int64_t J, const int32_t* __restrict__ run_ptr, int32_t* __restrict__ cnt) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < J; j += (int64_t)gridDim.x * blockDim.x) {
     const int32_t s = run_ptr[j], e = run_ptr[j + 1];
-    cnt[j] = (e - 1) / kPieceRows - s / kPieceRows + 1;
+    cnt[j] = (e - s + kPieceRows - 1) / kPieceRows;
   }
 }
 __global__ void k_piece_fill(int64_t J, const int32_t* __restrict__ run_ptr, const int32_t* __restrict__ pofs,
@@ -43,8 +46,32 @@ __global__ void k_piece_fill(int64_t J, const int32_t* __restrict__ run_ptr, con
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < J; j += (int64_t)gridDim.x * blockDim.x) {
     const int32_t s = run_ptr[j], e = run_ptr[j + 1];
     int32_t id = pofs[j];
-    piece_ptr[id++] = s;
-    for (int32_t b = (s / kPieceRows + 1) * kPieceRows; b < e; b += kPieceRows) piece_ptr[id++] = b;
+    for (int32_t b = s; b < e; b += kPieceRows) piece_ptr[id++] = b;
+  }
+}
+// Aggregate-first RGCN (NEXT-4): piece of every position (pieces hold <= kPieceRows positions),
+// then per CSR slot q its piece and weight 1 for the first slot of each piece within the row (the
+// row's slots list each piece's positions in a block), 0 for the others -- the walk then adds every
+// piece product once.
+__global__ void k_piece_mark(int64_t np_max, const Counters* c, const int32_t* __restrict__ piece_ptr,
+                             int32_t* __restrict__ piece_of_pos) {
+  const int64_t np = c->num_pieces;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np && i < np_max;
+       i += (int64_t)gridDim.x * blockDim.x)
+    for (int32_t p = piece_ptr[i]; p < piece_ptr[i + 1]; ++p) piece_of_pos[p] = (int32_t)i;
+}
+__global__ void k_piece_slots(int64_t n, const int32_t* __restrict__ pos, const int32_t* __restrict__ piece_of_pos,
+                              const int32_t* __restrict__ dst_s, int32_t* __restrict__ slot_piece,
+                              float* __restrict__ slot_w) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = pos[q], pc = piece_of_pos[p];
+    bool first = q == 0;
+    if (!first) {
+      const int32_t pp = pos[q - 1];
+      first = dst_s[pp] != dst_s[p] || piece_of_pos[pp] != pc;
+    }
+    slot_piece[q] = pc;
+    slot_w[q] = first ? 1.f : 0.f;
   }
 }
 __global__ void k_piece_seg(int32_t R, int64_t J, const int32_t* __restrict__ rseg, const int32_t* __restrict__ pofs,
@@ -55,12 +82,24 @@ __global__ void k_piece_seg(int32_t R, int64_t J, const int32_t* __restrict__ rs
   if (blockIdx.x == 0 && threadIdx.x == 0) piece_ptr[c->num_pieces] = E_own;
 }
 
-// CSR-by-dst input: dst of every edge from row_ptr (one warp per row).
-__global__ void k_expand_csr(const int32_t* __restrict__ row_ptr, int64_t V, int32_t* __restrict__ dst) {
+// CSR-by-dst input: row_ptr must be 0 at v = 0, non-decreasing and E at v = V; the smallest
+// offending index (v, or V for row_ptr[V] != E) is reported, before the expansion is used.
+__global__ void k_validate_csr(const int32_t* __restrict__ row_ptr, int64_t V, int64_t E, Counters* c) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v <= V; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t a = row_ptr[v];
+    const bool bad = v == 0 ? a != 0 : (a < row_ptr[v - 1] || (v == V && a != E));
+    if (bad) atomicMin(&c->bad_csr, (int32_t)v);
+  }
+}
+// CSR-by-dst input: dst of every edge from row_ptr (one warp per row).  The loop is clamped to
+// [0, E) so a malformed row_ptr never writes outside dst; k_validate_csr rejects it afterwards.
+__global__ void k_expand_csr(const int32_t* __restrict__ row_ptr, int64_t V, int64_t E, int32_t* __restrict__ dst) {
   int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
-  for (int64_t v = w; v < V; v += ((int64_t)gridDim.x * blockDim.x) >> 5)
-    for (int64_t e = row_ptr[v] + lane; e < row_ptr[v + 1]; e += 32) dst[e] = (int32_t)v;
+  for (int64_t v = w; v < V; v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t lo = max((int64_t)row_ptr[v], (int64_t)0), hi = min((int64_t)row_ptr[v + 1], E);
+    for (int64_t e = lo + lane; e < hi; e += 32) dst[e] = (int32_t)v;
+  }
 }
 
 __global__ void k_validate(int64_t E, int64_t V, int32_t R, const int32_t* __restrict__ src,
@@ -118,7 +157,9 @@ __global__ void k_after_sort(int64_t n, const uint32_t* __restrict__ keys, const
 // for b in [0, nbins]: one binary search per bin (balanced even when long runs
 // of empty bins exist, e.g. node types that receive no edges).
 template <typename KeyT>
-__global__ void k_bounds(int64_t n, const KeyT* __restrict__ key, int64_t nbins, int32_t* __restrict__ out) {
+__global__ void k_bounds(int64_t n, const KeyT* __restrict__ key, int64_t nbins, int32_t* __restrict__ out,
+                         const int32_t* __restrict__ n_dev = nullptr) {
+  if (n_dev) n = *n_dev;
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= nbins; b += (int64_t)gridDim.x * blockDim.x) {
     int64_t lo = 0, hi = n;
     while (lo < hi) {
@@ -149,6 +190,58 @@ __global__ void k_slots(int64_t n, const uint32_t* __restrict__ sorted_pos, cons
     pos[q] = p;
     et_slot[q] = et_s[p];
   }
+}
+
+// CSR from the runs.  Keys: the local dst of each run (j < J, J on the device).
+__global__ void k_run_keys(int64_t n, const Counters* c, const int32_t* __restrict__ run_ptr,
+                           const int32_t* __restrict__ dst_s, uint32_t* __restrict__ k, uint32_t* __restrict__ v) {
+  const int64_t J = c->J;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < J && j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    k[j] = (uint32_t)dst_s[run_ptr[j]];
+    v[j] = (uint32_t)j;
+  }
+}
+// Length of the i-th run in dst order (0 past J: the scan then gives every sorted run its first
+// slot), and the inverse permutation run -> sorted index.
+__global__ void k_run_lens(int64_t n, const Counters* c, const uint32_t* __restrict__ sorted_run,
+                           const int32_t* __restrict__ run_ptr, int32_t* __restrict__ len, uint32_t* __restrict__ inv) {
+  const int64_t J = c->J;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < J) {
+      const uint32_t j = sorted_run[i];
+      len[i] = run_ptr[j + 1] - run_ptr[j];
+      inv[j] = (uint32_t)i;
+    } else {
+      len[i] = 0;
+    }
+  }
+}
+// row_ptr[v] = first slot of the first sorted run whose dst is >= v (E_own past the last run).
+__global__ void k_row_ptr_runs(int64_t V_own, const Counters* c, const uint32_t* __restrict__ sorted_dst,
+                               const int32_t* __restrict__ q0, int32_t* __restrict__ row_ptr) {
+  const int64_t J = c->J;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v <= V_own; v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = J;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)sorted_dst[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    row_ptr[v] = lo < J ? q0[lo] : c->E_own;
+  }
+}
+// pos[q] for every position p: its run j, the run's sorted index and first slot, plus the offset.
+__global__ void k_slots_runs(int64_t n, const int32_t* __restrict__ head, const int32_t* __restrict__ run_ex,
+                             const int32_t* __restrict__ run_ptr, const uint32_t* __restrict__ inv,
+                             const int32_t* __restrict__ q0, int32_t* __restrict__ pos) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t j = run_ex[p] + head[p] - 1;
+    pos[q0[inv[j]] + (int32_t)(p - run_ptr[j])] = (int32_t)p;
+  }
+}
+__global__ void k_slot_et(int64_t n, const int32_t* __restrict__ pos, const int32_t* __restrict__ et_s,
+                          int32_t* __restrict__ et_slot) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    et_slot[q] = et_s[pos[q]];
 }
 
 // Runs of equal (etype, dst): run_ptr[j] = first position of run j.
@@ -204,10 +297,10 @@ __global__ void k_dx_runs(int64_t n, const int32_t* __restrict__ head, const int
                           int32_t* __restrict__ run_of_pos, int32_t* __restrict__ run_dst, int32_t* __restrict__ run_rel) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
     const int32_t j = run_ex[p] + head[p] - 1;
-    run_of_pos[p] = j;
+    if (run_of_pos) run_of_pos[p] = j;
     if (head[p]) {
       run_dst[j] = dst_s[p];
-      run_rel[j] = et_s[p];
+      if (run_rel) run_rel[j] = et_s[p];
     }
   }
 }
@@ -235,9 +328,10 @@ __global__ void k_dx_slots(int64_t n, const uint32_t* __restrict__ sorted_pos, c
 
 // Work list: rows with more than cap in-edges are split into ceil(deg/cap) chunks;
 // rows without in-edges get no item and go to the empty-row list (Y = 0 / self term).
+// n_wide (optional): the items of rows with deg > narrow (the forward walk's wide list).
 __global__ void k_item_counts(int64_t V_own, const int32_t* __restrict__ row_ptr, int cap, int32_t* __restrict__ n_items,
                               int32_t* __restrict__ n_parts, int32_t* __restrict__ n_split,
-                              int32_t* __restrict__ n_empty) {
+                              int32_t* __restrict__ n_empty, int narrow = 0, int32_t* __restrict__ n_wide = nullptr) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < V_own; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t deg = row_ptr[i + 1] - row_ptr[i];
     int32_t c = deg > cap ? (deg + cap - 1) / cap : (deg > 0 ? 1 : 0);
@@ -245,6 +339,7 @@ __global__ void k_item_counts(int64_t V_own, const int32_t* __restrict__ row_ptr
     n_parts[i] = c > 1 ? c : 0;
     n_split[i] = c > 1 ? 1 : 0;
     n_empty[i] = deg == 0 ? 1 : 0;
+    if (n_wide) n_wide[i] = deg > narrow ? c : 0;
   }
 }
 
@@ -257,7 +352,8 @@ __global__ void k_fill_empty(int64_t V_own, const int32_t* __restrict__ row_ptr,
 __global__ void k_fill_items(int64_t V_own, const int32_t* __restrict__ row_ptr, int cap,
                              const int32_t* __restrict__ item_ex, const int32_t* __restrict__ part_ex,
                              const int32_t* __restrict__ split_ex, Item* __restrict__ items,
-                             SplitRow* __restrict__ split_rows) {
+                             SplitRow* __restrict__ split_rows, int narrow = 0,
+                             const int32_t* __restrict__ wide_ex = nullptr, Item* __restrict__ witems = nullptr) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < V_own; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t lo = row_ptr[i], hi = row_ptr[i + 1], deg = hi - lo;
     int32_t c = deg > cap ? (deg + cap - 1) / cap : (deg > 0 ? 1 : 0);
@@ -270,6 +366,7 @@ __global__ void k_fill_items(int64_t V_own, const int32_t* __restrict__ row_ptr,
       it.part = c > 1 ? part_ex[i] + k : -1;
       if (c == 1) { it.q0 = lo; it.q1 = hi; }
       items[b + k] = it;
+      if (witems && deg > narrow) witems[wide_ex[i] + k] = it;
     }
     if (c > 1) {
       SplitRow s;
@@ -327,7 +424,7 @@ struct GraphLayout {
   // device storage
   int32_t *perm, *src_s, *dst_s, *seg, *row_ptr, *pos, *et_slot, *run_ptr, *rseg;
   float* inv_c;
-  Item* items;
+  Item *items, *witems;
   SplitRow* split_rows;
   int32_t* empty_rows;
   int32_t *crow_of_pos, *zrow_slot, *csrc, *cseg;
@@ -343,16 +440,27 @@ struct GraphLayout {
   int32_t *nperm, *ninv, *nseg;
   Tile *ntiles, *nchunks;
   int32_t* nchunk_seg;
-  int32_t *piece_ptr, *prseg, *pchunk_seg;
+  int32_t *piece_ptr, *prseg, *pchunk_seg, *slot_piece;
+  float* slot_w;
+  Tile* ptiles;
   Tile* pchunks;
   size_t dev_bytes;
   // scratch
   Counters* ctr;
-  int32_t *dst_tmp, *flags, *head, *run_ex, *et_s, *n_items, *n_parts, *n_split, *n_empty, *rseg_cnt, *crel;
+  int32_t *dst_tmp, *flags, *head, *run_ex, *et_s, *n_items, *n_parts, *n_split, *n_empty, *n_wide, *rseg_cnt, *crel;
   uint32_t *k0, *v0, *k1, *v1;
   void* prim;
   size_t prim_bytes, scratch_bytes;
 };
+
+// Forward walk: rows with at most this many in-edges (and never split) are walked one lane
+// group per row; the choice depends only on the row's degree, so a dst-range shard walks every
+// row exactly like one GPU does (pin P14).  RGNN_NARROW_CAP (environment) overrides it for A/B.
+static int narrow_cap(const rgnn_graph_desc* d) {
+  static const int env = getenv("RGNN_NARROW_CAP") ? atoi(getenv("RGNN_NARROW_CAP")) : -1;
+  const int cap = d->row_split_cap > 0 ? d->row_split_cap : kDefaultSplitCap;
+  return std::min(env >= 0 ? env : kNarrowCap, cap);
+}
 
 static int64_t max_chunks(int64_t E, int32_t R) { (void)E; return 8 * 1024 + 2 * (int64_t)R; }
 
@@ -376,6 +484,7 @@ static GraphLayout layout(const rgnn_graph_desc* d, void* dev, void* scr) {
   L.items = c.take<Item>(V_own + Ec / cap + 1);
   L.split_rows = c.take<SplitRow>(Ec / cap + 1);
   L.empty_rows = c.take<int32_t>(V_own + 1);
+  L.witems = c.take<Item>(Ec / (narrow_cap(d) + 1) + Ec / cap + 1);
   const bool cm = d->materialization != RGNN_MAT_VANILLA;
   L.crow_of_pos = c.take<int32_t>(cm ? Ec : 1);
   L.zrow_slot = c.take<int32_t>(cm ? Ec : 1);
@@ -389,14 +498,14 @@ static GraphLayout layout(const rgnn_graph_desc* d, void* dev, void* scr) {
   const bool dx = (d->flags & RGNN_GRAPH_DX) != 0;
   const int64_t Ex = dx ? Ec : 1;
   L.run_of_pos = c.take<int32_t>(Ex);
-  L.run_dst = c.take<int32_t>(Ex);
+  L.run_dst = c.take<int32_t>(Ec);  // always: the RGAT backward's per-run GEMM gathers G rows by it
   L.run_rel = c.take<int32_t>(Ex);
   L.spos = c.take<int32_t>(Ex);
   L.srun = c.take<int32_t>(Ex);
   L.srel = c.take<int32_t>(Ex);
   L.sinvc = c.take<float>(Ex);
   L.srow = c.take<int32_t>(dx ? d->num_nodes + 1 : 1);
-  L.rtiles = c.take<Tile>(dx ? Ec / kTileRows + R + 1 : 1);
+  L.rtiles = c.take<Tile>(Ec / kTileRows + R + 1);  // always (see run_dst)
   L.sitems = c.take<Item>(dx ? d->num_nodes + Ec / cap + 1 : 1);
   L.ssplit = c.take<SplitRow>(dx ? Ec / cap + 1 : 1);
   const bool nt = d->ntype != nullptr;
@@ -407,11 +516,15 @@ static GraphLayout layout(const rgnn_graph_desc* d, void* dev, void* scr) {
   L.ntiles = c.take<Tile>(nt ? Vn / kTileRows + d->num_ntypes + 1 : 1);
   L.nchunks = c.take<Tile>(nt ? Vn / kTileRows + d->num_ntypes + 1 : 1);  // chunks >= 128 rows: <= #ntiles
   L.nchunk_seg = c.take<int32_t>(nt ? d->num_ntypes + 1 : 1);
-  const bool pc = nt && dx;  // HGT backward run pieces
+  const bool af = (d->flags & RGNN_GRAPH_AGGFIRST) != 0;
+  const bool pc = (nt && dx) || af;  // run pieces: HGT backward, aggregate-first RGCN
   L.piece_ptr = c.take<int32_t>(pc ? Ec + Ec / kPieceRows + 2 : 1);
   L.prseg = c.take<int32_t>(pc ? R + 1 : 1);
   L.pchunks = c.take<Tile>(pc ? max_chunks(E, R) : 1);
   L.pchunk_seg = c.take<int32_t>(pc ? R + 1 : 1);
+  L.ptiles = c.take<Tile>(af ? (Ec + Ec / kPieceRows + 1) / kTileRows + R + 1 : 1);
+  L.slot_piece = c.take<int32_t>(af ? Ec : 1);
+  L.slot_w = c.take<float>(af ? Ec : 1);
   L.dev_bytes = c.off;
   Carver s(scr);
   L.ctr = s.take<Counters>(1);
@@ -425,6 +538,7 @@ static GraphLayout layout(const rgnn_graph_desc* d, void* dev, void* scr) {
   L.n_parts = s.take<int32_t>(Vw + 1);
   L.n_split = s.take<int32_t>(Vw + 1);
   L.n_empty = s.take<int32_t>(Vw + 1);
+  L.n_wide = s.take<int32_t>(V_own + 1);
   L.rseg_cnt = s.take<int32_t>(R + 1);
   L.crel = s.take<int32_t>(d->materialization != RGNN_MAT_VANILLA ? Ec : 1);
   const int64_t Ek = std::max<int64_t>(Ec, d->ntype ? d->num_nodes : 0);  // sort keys: edges, or nodes (types)
@@ -461,7 +575,8 @@ static rgnn_status check_desc(const rgnn_graph_desc* d) {
   if (d->materialization != RGNN_MAT_VANILLA && d->materialization != RGNN_MAT_COMPACT &&
       d->materialization != RGNN_MAT_AUTO)
     return set_error(RGNN_E_INVALID_ARG, "bad materialization %d", d->materialization);
-  if (d->flags & ~RGNN_GRAPH_DX) return set_error(RGNN_E_INVALID_ARG, "unknown flags 0x%x", d->flags);
+  if (d->flags & ~(RGNN_GRAPH_DX | RGNN_GRAPH_AGGFIRST))
+    return set_error(RGNN_E_INVALID_ARG, "unknown flags 0x%x", d->flags);
   if (d->materialization != RGNN_MAT_VANILLA &&
       (uint64_t)d->num_etypes * (uint64_t)(d->num_nodes > 0 ? d->num_nodes : 1) > 0xffffffffull)
     return set_error(RGNN_E_UNSUPPORTED, "compact materialisation needs R * V < 2^32 (sort key)");
@@ -506,20 +621,15 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   RGNN_LAUNCH(k_init_counters, 1, 1, 0, s, L.ctr, INT32_MAX);
   const int32_t* dst = d->dst;
   if (d->row_ptr) {
-    RGNN_LAUNCH(k_expand_csr, grid_for(V * 32), T, 0, s, d->row_ptr, V, L.dst_tmp);
+    RGNN_LAUNCH(k_validate_csr, grid_for(V + 1), T, 0, s, d->row_ptr, V, E, L.ctr);
+    RGNN_LAUNCH(k_expand_csr, grid_for(V * 32), T, 0, s, d->row_ptr, V, E, L.dst_tmp);
     dst = L.dst_tmp;
   }
   if (E > 0) RGNN_LAUNCH(k_validate, grid_for(E), T, 0, s, E, V, R, d->src, dst, d->etype, L.ctr);
   if (d->ntype && V > 0) RGNN_LAUNCH(k_validate_ntype, grid_for(V), T, 0, s, V, d->num_ntypes, d->ntype, L.ctr);
-  // Owned edges, compacted in input order.
+  // Owned edges, compacted in input order.  (These kernels only compare and copy ids, so they are
+  // safe on invalid input; the validation flags are read with the owned-edge count -- host sync 1.)
   Counters h{};
-  RGNN_CUDA_TRY(cudaMemcpyAsync(&h, L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
-  RGNN_CUDA_TRY(cudaStreamSynchronize(s));
-  if (h.bad_edge != INT32_MAX)
-    return set_error(RGNN_E_RANGE, "edge %d has an id out of range (V=%lld, R=%d)", h.bad_edge, (long long)V, R);
-  if (h.bad_node != INT32_MAX)
-    return set_error(RGNN_E_RANGE, "node %d has a node type out of range (T=%d)", h.bad_node, d->num_ntypes);
-
   int32_t* E_own_d = &L.ctr->E_own;
   if (E > 0) {
     RGNN_LAUNCH(k_own_flags, grid_for(E), T, 0, s, E, dst, v0, v1, L.flags);
@@ -528,6 +638,13 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   }
   RGNN_CUDA_TRY(cudaMemcpyAsync(&h, L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
   RGNN_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h.bad_csr != INT32_MAX)
+    return set_error(RGNN_E_INVALID_ARG, "row_ptr is not a CSR offset array (0 at v=0, non-decreasing, E at v=V): "
+                     "first bad entry row_ptr[%d]", h.bad_csr);
+  if (h.bad_edge != INT32_MAX)
+    return set_error(RGNN_E_RANGE, "edge %d has an id out of range (V=%lld, R=%d)", h.bad_edge, (long long)V, R);
+  if (h.bad_node != INT32_MAX)
+    return set_error(RGNN_E_RANGE, "node %d has a node type out of range (T=%d)", h.bad_node, d->num_ntypes);
   const int64_t n = h.E_own;
 
   // Stable sort of owned edges by (etype, dst).
@@ -540,38 +657,53 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
     RGNN_LAUNCH(k_after_sort, grid_for(n), T, 0, s, n, keys, vals, d->src, V_own, L.perm, L.src_s, L.dst_s, L.et_s,
                 L.head);
   RGNN_LAUNCH(k_bounds<int32_t>, grid_for(R + 1), T, 0, s, n, L.et_s, (int64_t)R, L.seg);
-  // CSR-by-dst: stable sort of positions by local dst -> ascending p within a row.
   if (n > 0) {
-    RGNN_LAUNCH(k_iota_keys, grid_for(n), T, 0, s, n, L.dst_s, L.k0, L.v0);
-    RGNN_TRY(radix_sort_pairs(L.k0, L.v0, L.k1, L.v1, n, bits_for((uint64_t)(V_own > 0 ? V_own - 1 : 0)), L.prim,
-                              L.prim_bytes, s, &alt));
-    RGNN_LAUNCH(k_slots, grid_for(n), T, 0, s, n, alt ? L.v1 : L.v0, L.et_s, L.pos, L.et_slot);
-    RGNN_LAUNCH(k_bounds<uint32_t>, grid_for(V_own + 1), T, 0, s, n, alt ? L.k1 : L.k0, V_own, L.row_ptr);
     // (etype, dst) runs
     RGNN_TRY(scan_exclusive(L.head, L.run_ex, n, &L.ctr->J, L.prim, L.prim_bytes, s));
     RGNN_LAUNCH(k_runs, grid_for(n), T, 0, s, n, L.head, L.run_ex, L.run_ptr);
+    RGNN_LAUNCH(k_run_end, 1, 1, 0, s, L.ctr, L.run_ptr);
+    // CSR-by-dst from the runs (a stable sort of the J runs by dst instead of the E positions):
+    // the runs are in (etype, dst) order, so sorting them stably by dst lists each row's runs in
+    // relation order, and each run's positions are consecutive -- the row's positions come out
+    // ascending, exactly the order a stable sort of the positions by dst gives (reading O14).
+    uint32_t* rk = L.k0; uint32_t* rv = L.v0;
+    RGNN_LAUNCH(k_run_keys, grid_for(n), T, 0, s, n, L.ctr, L.run_ptr, L.dst_s, rk, rv);
+    RGNN_TRY(radix_sort_pairs(L.k0, L.v0, L.k1, L.v1, n, bits_for((uint64_t)(V_own > 0 ? V_own - 1 : 0)), L.prim,
+                              L.prim_bytes, s, &alt, &L.ctr->J));
+    uint32_t* sk = alt ? L.k1 : L.k0;  // sorted run dst
+    uint32_t* sv = alt ? L.v1 : L.v0;  // sorted run ids
+    uint32_t* inv = alt ? L.v0 : L.v1;  // free buffer: sorted index of each run
+    int32_t* q0 = L.et_slot;           // scratch until the slots are written: slot offset of each sorted run
+    RGNN_LAUNCH(k_run_lens, grid_for(n), T, 0, s, n, L.ctr, sv, L.run_ptr, q0, inv);
+    RGNN_TRY(scan_exclusive(q0, q0, n, nullptr, L.prim, L.prim_bytes, s));
+    RGNN_LAUNCH(k_row_ptr_runs, grid_for(V_own + 1), T, 0, s, V_own, L.ctr, sk, q0, L.row_ptr);
+    RGNN_LAUNCH(k_slots_runs, grid_for(n), T, 0, s, n, L.head, L.run_ex, L.run_ptr, inv, q0, L.pos);
+    RGNN_LAUNCH(k_slot_et, grid_for(n), T, 0, s, n, L.pos, L.et_s, L.et_slot);
   }
-  if (n == 0) RGNN_LAUNCH(k_bounds<int32_t>, grid_for(V_own + 1), T, 0, s, (int64_t)0, L.et_s, V_own, L.row_ptr);
-  RGNN_LAUNCH(k_run_end, 1, 1, 0, s, L.ctr, L.run_ptr);
+  if (n == 0) {
+    RGNN_LAUNCH(k_bounds<int32_t>, grid_for(V_own + 1), T, 0, s, (int64_t)0, L.et_s, V_own, L.row_ptr);
+    RGNN_LAUNCH(k_run_end, 1, 1, 0, s, L.ctr, L.run_ptr);
+  }
   RGNN_LAUNCH(k_rseg, (unsigned)((R + 256) / 256), 256, 0, s, R, n, L.seg, L.run_ex, L.ctr, L.rseg);
   if (n > 0)
     RGNN_LAUNCH(k_inv_c, grid_for(n), T, 0, s, n, d->norm, L.head, L.run_ex, L.run_ptr, L.perm, d->edge_norm,
                 L.inv_c);
   const bool dx = (d->flags & RGNN_GRAPH_DX) != 0;
-  if (dx && n > 0)
-    RGNN_LAUNCH(k_dx_runs, grid_for(n), T, 0, s, n, L.head, L.run_ex, L.dst_s, L.et_s, L.run_of_pos, L.run_dst,
-                L.run_rel);
+  if (n > 0)
+    RGNN_LAUNCH(k_dx_runs, grid_for(n), T, 0, s, n, L.head, L.run_ex, L.dst_s, L.et_s, dx ? L.run_of_pos : nullptr,
+                L.run_dst, dx ? L.run_rel : nullptr);
   // Destination-walk work list.
   if (V_own > 0) {
     RGNN_LAUNCH(k_item_counts, grid_for(V_own), T, 0, s, V_own, L.row_ptr, cap, L.n_items, L.n_parts, L.n_split,
-                L.n_empty);
+                L.n_empty, narrow_cap(d), L.n_wide);
+    RGNN_TRY(scan_exclusive(L.n_wide, L.n_wide, V_own, &L.ctr->num_witems, L.prim, L.prim_bytes, s));
     RGNN_TRY(scan_exclusive(L.n_empty, L.n_empty, V_own, &L.ctr->num_empty, L.prim, L.prim_bytes, s));
     RGNN_LAUNCH(k_fill_empty, grid_for(V_own), T, 0, s, V_own, L.row_ptr, L.n_empty, L.empty_rows);
     RGNN_TRY(scan_exclusive(L.n_items, L.n_items, V_own, &L.ctr->num_items, L.prim, L.prim_bytes, s));
     RGNN_TRY(scan_exclusive(L.n_parts, L.n_parts, V_own, &L.ctr->num_parts, L.prim, L.prim_bytes, s));
     RGNN_TRY(scan_exclusive(L.n_split, L.n_split, V_own, &L.ctr->num_split_rows, L.prim, L.prim_bytes, s));
     RGNN_LAUNCH(k_fill_items, grid_for(V_own), T, 0, s, V_own, L.row_ptr, cap, L.n_items, L.n_parts, L.n_split,
-                L.items, L.split_rows);
+                L.items, L.split_rows, narrow_cap(d), L.n_wide, L.witems);
   }
   // Compact materialisation: unique (etype, src) rows, lexicographic.
   const bool cm = d->materialization != RGNN_MAT_VANILLA;
@@ -586,15 +718,15 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
     RGNN_LAUNCH(k_crows, grid_for(n), T, 0, s, n, ck, cv, L.head, L.run_ex, V, L.crow_of_pos, L.csrc, L.crel);
     RGNN_LAUNCH(k_cslots, grid_for(n), T, 0, s, n, L.pos, L.crow_of_pos, L.inv_c, L.zrow_slot, L.invc_slot);
   }
-  // The single readback: counts + relation segments.
+  // Host sync 2: counts + relation (and compact) segments.
   std::vector<int32_t> seg_h(R + 1), cseg_h(R + 1, 0);
+  if (cm)  // compact segments: first compact row of each relation (U counted on the device)
+    RGNN_LAUNCH(k_bounds<int32_t>, grid_for(R + 1), T, 0, s, (int64_t)0, L.crel, (int64_t)R, L.cseg,
+                &L.ctr->num_compact);
   RGNN_CUDA_TRY(cudaMemcpyAsync(&h, L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
   RGNN_CUDA_TRY(cudaMemcpyAsync(seg_h.data(), L.seg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
+  if (cm) RGNN_CUDA_TRY(cudaMemcpyAsync(cseg_h.data(), L.cseg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
   RGNN_CUDA_TRY(cudaStreamSynchronize(s));
-  if (cm) {  // compact segments: first compact row of each relation
-    RGNN_LAUNCH(k_bounds<int32_t>, grid_for(R + 1), T, 0, s, (int64_t)h.num_compact, L.crel, (int64_t)R, L.cseg);
-    RGNN_CUDA_TRY(cudaMemcpyAsync(cseg_h.data(), L.cseg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
-  }
   // node-type segments (HGT's node-typed linears, D4): stable sort of node ids by type
   std::vector<int32_t> nseg_h;
   if (d->ntype && V > 0) {
@@ -608,6 +740,7 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
     RGNN_CUDA_TRY(cudaMemcpyAsync(nseg_h.data(), L.nseg, sizeof(int32_t) * (NT + 1), cudaMemcpyDeviceToHost, s));
   }
   std::vector<int32_t> rseg_h(R + 1, 0), prseg_h;
+  RGNN_CUDA_TRY(cudaMemcpyAsync(rseg_h.data(), L.rseg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
   if (dx) {
     // source-major CSR over the positions (stable: ascending position within a source)
     if (n > 0) {
@@ -627,34 +760,68 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
       RGNN_LAUNCH(k_fill_items, grid_for(V), T, 0, s, V, L.srow, cap, L.n_items, L.n_parts, L.n_split, L.sitems,
                   L.ssplit);
     }
-    RGNN_CUDA_TRY(cudaMemcpyAsync(rseg_h.data(), L.rseg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
-    if (d->ntype) {  // run pieces for the HGT backward's relation dW GEMMs
-      if (h.J > 0) {
-        RGNN_LAUNCH(k_piece_counts, grid_for(h.J), T, 0, s, (int64_t)h.J, L.run_ptr, L.flags);
-        RGNN_TRY(scan_exclusive(L.flags, L.flags, h.J, &L.ctr->num_pieces, L.prim, L.prim_bytes, s));
-        RGNN_LAUNCH(k_piece_fill, grid_for(h.J), T, 0, s, (int64_t)h.J, L.run_ptr, L.flags, L.piece_ptr);
-      }
-      RGNN_LAUNCH(k_piece_seg, (unsigned)((R + 256) / 256), 256, 0, s, R, (int64_t)h.J, L.rseg, L.flags, L.ctr,
-                  L.prseg, L.piece_ptr, (int32_t)n);
-      prseg_h.assign(R + 1, 0);
-      RGNN_CUDA_TRY(cudaMemcpyAsync(prseg_h.data(), L.prseg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
+  }
+  const bool af = (d->flags & RGNN_GRAPH_AGGFIRST) != 0;
+  if ((d->ntype && dx) || af) {
+    // run pieces: every (etype, dst) run cut at the multiples of kPieceRows (HGT backward's
+    // relation dW GEMMs; the aggregate-first RGCN forward's GEMM rows)
+    if (h.J > 0) {
+      RGNN_LAUNCH(k_piece_counts, grid_for(h.J), T, 0, s, (int64_t)h.J, L.run_ptr, L.flags);
+      RGNN_TRY(scan_exclusive(L.flags, L.flags, h.J, &L.ctr->num_pieces, L.prim, L.prim_bytes, s));
+      RGNN_LAUNCH(k_piece_fill, grid_for(h.J), T, 0, s, (int64_t)h.J, L.run_ptr, L.flags, L.piece_ptr);
     }
+    RGNN_LAUNCH(k_piece_seg, (unsigned)((R + 256) / 256), 256, 0, s, R, (int64_t)h.J, L.rseg, L.flags, L.ctr,
+                L.prseg, L.piece_ptr, (int32_t)n);
+    if (af && n > 0) {
+      const int64_t np_max = n + n / kPieceRows + 1;
+      int32_t* piece_of_pos = reinterpret_cast<int32_t*>(L.k0);  // sort scratch, free by now
+      RGNN_LAUNCH(k_piece_mark, grid_for(np_max), T, 0, s, np_max, L.ctr, L.piece_ptr, piece_of_pos);
+      RGNN_LAUNCH(k_piece_slots, grid_for(n), T, 0, s, n, L.pos, piece_of_pos, L.dst_s, L.slot_piece, L.slot_w);
+    }
+    prseg_h.assign(R + 1, 0);
+    RGNN_CUDA_TRY(cudaMemcpyAsync(prseg_h.data(), L.prseg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
+  }
+  if (d->ntype || dx || af) {  // host sync 3 (node types, dX tables, run pieces): their counts and segments
     Counters h2{};
     RGNN_CUDA_TRY(cudaMemcpyAsync(&h2, L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
     RGNN_CUDA_TRY(cudaStreamSynchronize(s));
     h.num_sitems = h2.num_sitems; h.num_sparts = h2.num_sparts; h.num_ssplit = h2.num_ssplit;
     h.num_pieces = h2.num_pieces;
   }
-  RGNN_CUDA_TRY(cudaStreamSynchronize(s));
   int dev_id = 0, sms = 148;
   RGNN_CUDA_TRY(cudaGetDevice(&dev_id));
   RGNN_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev_id));
 
   // Host: 128-row GEMM tiles and dW split-K chunks, never straddling relations.
-  // dW chunks: about two per SM (split-K), multiples of the 128-row tile.
+  // dW chunks (the fused backward runs one CTA per chunk, one CTA per SM): sized so that at most
+  // waves * SMs chunks result (sum_r ceil(E_r / rows) <= E / rows + R), i.e. exactly `waves` full
+  // waves with no partial wave left over (r01 sizing gave 298 chunks = 2 waves + 2 on ogbn-mag);
+  // multiples of the 128-row tile.  Chunks are in position order, so each wave's CTAs gather the
+  // X / Z rows of one 1/waves slice of the position space at a time.  (Measured r02: one
+  // persistent CTA per SM over equal position ranges -- every SM spanning the whole position space
+  // at once -- was slower, 3.54 -> 4.97 ms on ogbn-mag.)
   std::vector<Tile> tiles, chunks;
   std::vector<int32_t> chunk_seg(R + 1, 0);
+  // RGNN_BWD_WAVES (A/B): 0 = the r01 sizing only
+  static const int64_t waves = getenv("RGNN_BWD_WAVES") ? std::max(0, atoi(getenv("RGNN_BWD_WAVES"))) : 2;
+  auto count_chunks = [&](int64_t cr) {
+    int64_t c = 0;
+    for (int32_t r = 0; r < R; ++r) c += (seg_h[r + 1] - seg_h[r] + cr - 1) / cr;
+    return c;
+  };
+  // the smallest multiple of 128 rows giving <= waves * SMs chunks; with more non-empty relations
+  // than that (many small relations), the r01 sizing (about two chunks' worth of rows per SM)
   int64_t chunk_rows = std::max<int64_t>(kTileRows, ((n / (2 * sms) + 1) + kTileRows - 1) / kTileRows * kTileRows);
+  if (waves > 0 && n > 0 && count_chunks(((n + kTileRows - 1) / kTileRows) * kTileRows) <= waves * sms) {
+    int64_t lo = 1, hi = (n + kTileRows - 1) / kTileRows;  // in units of 128 rows
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (count_chunks(mid * kTileRows) <= waves * sms) hi = mid; else lo = mid + 1;
+    }
+    // only when the chunks stay near the balanced size (many small relations would otherwise
+    // stretch the large relations' chunks)
+    if (lo * kTileRows <= 2 * ((n + waves * sms - 1) / (waves * sms))) chunk_rows = lo * kTileRows;
+  }
   for (int32_t r = 0; r < R; ++r) {
     for (int64_t a = seg_h[r]; a < seg_h[r + 1]; a += kTileRows)
       tiles.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + kTileRows, seg_h[r + 1]), 0});
@@ -693,13 +860,19 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
     RGNN_CUDA_TRY(cudaMemcpyAsync(L.nchunk_seg, nchunk_seg.data(), sizeof(int32_t) * nchunk_seg.size(),
                                   cudaMemcpyHostToDevice, s));
   }
-  std::vector<Tile> rtiles;  // 128-run GEMM tiles per relation (dX: H = G_v W_r^T per run)
-  if (dx)
-    for (int32_t r = 0; r < R; ++r)
+  std::vector<Tile> rtiles;  // 128-run GEMM tiles per relation (H = G_v W_r^T per run: RGAT backward, dX)
+  for (int32_t r = 0; r < R; ++r)
       for (int64_t a = rseg_h[r]; a < rseg_h[r + 1]; a += kTileRows)
         rtiles.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + kTileRows, rseg_h[r + 1]), 0});
   if (!rtiles.empty())
     RGNN_CUDA_TRY(cudaMemcpyAsync(L.rtiles, rtiles.data(), sizeof(Tile) * rtiles.size(), cudaMemcpyHostToDevice, s));
+  std::vector<Tile> ptiles;  // aggregate-first RGCN: 128-piece GEMM tiles per relation
+  if (af)
+    for (int32_t r = 0; r < R; ++r)
+      for (int64_t a = prseg_h[r]; a < prseg_h[r + 1]; a += kTileRows)
+        ptiles.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + kTileRows, prseg_h[r + 1]), 0});
+  if (!ptiles.empty())
+    RGNN_CUDA_TRY(cudaMemcpyAsync(L.ptiles, ptiles.data(), sizeof(Tile) * ptiles.size(), cudaMemcpyHostToDevice, s));
   std::vector<Tile> pchunks;  // dW split-K chunks over the run pieces, never straddling relations
   std::vector<int32_t> pchunk_seg(R + 1, 0);
   if (!prseg_h.empty()) {
@@ -723,7 +896,8 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   if (!chunks.empty())
     RGNN_CUDA_TRY(cudaMemcpyAsync(L.chunks, chunks.data(), sizeof(Tile) * chunks.size(), cudaMemcpyHostToDevice, s));
   RGNN_CUDA_TRY(cudaMemcpyAsync(L.chunk_seg, chunk_seg.data(), sizeof(int32_t) * (R + 1), cudaMemcpyHostToDevice, s));
-  RGNN_CUDA_TRY(cudaStreamSynchronize(s));  // host vectors go out of scope
+  // No final synchronisation: copies from pageable host memory return once the data is staged, so the
+  // host vectors may go out of scope; the tables reach the device in stream order before any layer call.
 
   rgnn_graph* g = new rgnn_graph();
   g->V = V; g->V_own = V_own; g->v0 = v0; g->E_in = E; g->E_own = n; g->J = h.J;
@@ -734,6 +908,7 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   g->pos = L.pos; g->et_slot = L.et_slot; g->run_ptr = L.run_ptr; g->rseg = L.rseg; g->inv_c = L.inv_c;
   g->items = L.items; g->split_rows = L.split_rows; g->tiles = L.tiles; g->chunks = L.chunks;
   g->empty_rows = L.empty_rows; g->num_empty = h.num_empty;
+  g->narrow_cap = narrow_cap(d); g->witems = L.witems; g->num_witems = h.num_witems;
   g->has_compact = cm; g->mat_mode = d->materialization; g->num_compact = cm ? h.num_compact : 0; g->crow_of_pos = L.crow_of_pos; g->zrow_slot = L.zrow_slot;
   g->invc_slot = L.invc_slot; g->csrc = L.csrc; g->cseg = L.cseg; g->ctiles = L.ctiles;
   g->num_ctiles = (int64_t)ctiles.size();
@@ -747,7 +922,9 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   g->nperm = L.nperm; g->ninv = L.ninv; g->ntiles = L.ntiles; g->num_ntiles = (int64_t)ntiles.size();
   g->nchunks = L.nchunks; g->nchunk_seg = L.nchunk_seg; g->num_nchunks = (int64_t)nchunks.size();
   g->has_pieces = !prseg_h.empty(); g->piece_ptr = L.piece_ptr; g->prseg = L.prseg; g->pchunks = L.pchunks; g->pchunk_seg = L.pchunk_seg;
-  g->num_pieces = g->has_pieces ? h.num_pieces : 0; g->num_pchunks = (int64_t)pchunks.size();
+  g->num_pieces = !prseg_h.empty() ? h.num_pieces : 0; g->num_pchunks = (int64_t)pchunks.size();
+  g->has_aggfirst = af; g->ptiles = L.ptiles; g->num_ptiles = (int64_t)ptiles.size();
+  g->slot_piece = L.slot_piece; g->slot_w = L.slot_w;
   g->seg_host = seg_h;
   g->chunk_seg_host = chunk_seg;
   RGNN_CUDA_TRY(cudaGetDevice(&g->device));
@@ -764,6 +941,9 @@ rgnn_status rgnn_graph_export(const rgnn_graph* g, rgnn_graph_view* v) {
   v->pos = g->pos; v->et_slot = g->et_slot; v->inv_c = g->inv_c; v->run_ptr = g->run_ptr; v->rseg = g->rseg;
   v->seg_host = g->seg_host.data();
   v->num_compact = g->num_compact; v->crow_of_pos = g->crow_of_pos; v->csrc = g->csrc; v->cseg = g->cseg;
+  v->num_pieces = g->num_pieces; v->piece_ptr = g->num_pieces ? g->piece_ptr : nullptr;
+  v->slot_piece = g->has_aggfirst ? g->slot_piece : nullptr;
+  v->slot_w = g->has_aggfirst ? g->slot_w : nullptr;
   return RGNN_OK;
 }
 

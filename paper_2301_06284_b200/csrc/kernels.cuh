@@ -80,8 +80,19 @@ struct AggArgs {
   int64_t num_split_rows;
   const int32_t* empty_rows;
   int64_t num_empty;
+  // narrow pass (forward walk): rows with deg <= narrow walked one lane group per row in row-id
+  // order (empty rows included); witems = the items of the other rows.  row_ptr null: no narrow
+  // pass (items cover every row with in-edges, empty_rows the rest).
+  const int32_t* row_ptr;
+  int64_t V_own;
+  int narrow;
+  const Item* witems;
+  int64_t num_witems;
 };
 rgnn_status launch_aggregate(int prec, int K, int N, bool rgat, const AggArgs& a, cudaStream_t s);
+// Aggregate-first RGCN (NEXT-4, aggfirst.cu): A_i = sum_{p in piece i} inv_c[p] X[src_s[p]], fp32 rows.
+rgnn_status launch_piece_agg(int prec, int K, int64_t np, const int32_t* piece_ptr, const float* inv_c,
+                             const int32_t* src_s, const void* X, void* A, cudaStream_t s);
 
 struct BwdArgs {
   const Item* items;

@@ -10,7 +10,8 @@
 namespace rgnn {
 bool tc_disabled();
 rgnn_status comm_check_range(const rgnn_comm* c, int64_t v0, int64_t v1);
-rgnn_status comm_gather_rows(rgnn_comm* c, const float* Y_own, int64_t N, float* Y_full, cudaStream_t s);
+rgnn_status comm_gather_rows(rgnn_comm* c, const float* Y_own, int64_t N, void* Y_full, cudaStream_t s);
+rgnn_status comm_reduce_rows(rgnn_comm* c, float* buf, int64_t K, cudaStream_t s);
 rgnn_status comm_allreduce_sum(rgnn_comm* c, float* const* bufs, const size_t* counts, int n, cudaStream_t s);
 
 struct WsLayout {
@@ -25,6 +26,8 @@ struct WsLayout {
   float* cpart;    // RGAT dst term: [num_chunks, K]
   float* vsum;     // RGAT dA vectors: [R, 2, K]
   void* wt;        // tcgen05: bf16 W^T [R, N, K]
+  float *PA, *PZ;  // aggregate-first RGCN: piece sums A [num_pieces, K] and products P [num_pieces, N], fp32
+  float *PWt, *PZ0;  // ... W^T [R, N, K] (tf32 GEMM operand) and the fp32 self term [V_own, N]
   // dX (with_dx)
   float2* ad;      // RGAT: (alpha, dpre) per position [E_own]
   float* dpart;    // RGAT: [num_parts, K] split-row partial destination terms
@@ -137,6 +140,13 @@ static WsLayout ws_layout(const rgnn_graph* g, int model, int K, int N, int prec
   w.U = c.take<float>((size_t)g->R * K);
   w.part = c.take<float>((size_t)std::max<int64_t>(g->num_parts, 1) * (N + 4));
   w.wt = c.take<char>(prec == RGNN_BF16 ? (size_t)g->R * K * N * 2 : 1);
+  if (model == RGNN_RGCN && g->has_aggfirst) {
+    const int64_t NP = std::max<int64_t>(g->num_pieces, 1);
+    w.PA = c.take<float>((size_t)NP * K);
+    w.PZ = c.take<float>((size_t)NP * N);
+    w.PWt = c.take<float>((size_t)g->R * N * K);
+    w.PZ0 = c.take<float>((size_t)std::max<int64_t>(g->V_own, 1) * N);
+  }
   if (model == RGNN_RGCN) {
     w.Z = c.take<char>((size_t)std::max(zrows(g, model), E) * N * e);  // also the bf16 dZ of the unfused dW path
     w.Z0 = c.take<char>((size_t)std::max<int64_t>(g->V_own, 1) * N * e);
@@ -148,13 +158,15 @@ static WsLayout ws_layout(const rgnn_graph* g, int model, int K, int N, int prec
   w.dw0part = c.take<float>(model == RGNN_RGCN ? (size_t)std::max<int64_t>(dw0_chunks(g), 1) * (K * N + K) : 1);
   w.cpart = c.take<float>((size_t)std::max<int64_t>(g->num_chunks, 1) * K);
   w.vsum = c.take<float>((size_t)g->R * 2 * K);
-  if (with_dx) {
+  if (with_dx) {  // run products H = G_v W_r^T (dX)
     const int64_t J = std::max<int64_t>(g->J, 1);
-    w.ad = c.take<float2>(model == RGNN_RGAT ? (size_t)E : 1);
-    w.dpart = c.take<float>(model == RGNN_RGAT ? (size_t)std::max<int64_t>(g->num_parts, 1) * K : 1);
     w.Wt = c.take<float>((size_t)g->R * N * K + (size_t)N * K);
     w.Wr = c.take<float>((size_t)g->R * N * K + (size_t)N * K);
     w.H = c.take<char>((size_t)J * K * 4);
+  }
+  if (with_dx) {
+    w.ad = c.take<float2>(model == RGNN_RGAT ? (size_t)E : 1);
+    w.dpart = c.take<float>(model == RGNN_RGAT ? (size_t)std::max<int64_t>(g->num_parts, 1) * K : 1);
     w.H0 = c.take<char>(model == RGNN_RGCN ? (size_t)std::max<int64_t>(g->V_own, 1) * K * 4 : 1);
     w.U0 = c.take<float>((size_t)g->R * K);
     w.xpart = c.take<float>((size_t)std::max<int64_t>(g->num_sparts, 1) * K);
@@ -219,6 +231,7 @@ static rgnn_status typed_gemm(int prec, int K, int N, const GemmFwdArgs& a, cuda
 static rgnn_status forward(const rgnn_graph* g, int model, int K, int N, int prec, const void* X, const float* W,
                            const float* W0, const float* A, float slope, float* Y, void* saved, void* ws,
                            size_t ws_bytes, rgnn_comm* comm, float* Y_full, void* stream) {
+  if (!g) return set_error(RGNN_E_INVALID_ARG, "graph is NULL");  // before any layout reads g
   const WsLayout need = ws_layout(g, model, K, N, prec, nullptr);
   RGNN_TRY(check_common(g, K, N, prec, ws, ws_bytes, need));
   if (!X || !W || !Y || (model == RGNN_RGAT && (!A || !saved)))
@@ -241,6 +254,8 @@ static rgnn_status forward(const rgnn_graph* g, int model, int K, int N, int pre
   }
   aa.v0 = g->v0; aa.slope = slope; aa.Y = Y; aa.part = w.part; aa.split_rows = g->split_rows;
   aa.num_split_rows = g->num_split_rows; aa.empty_rows = g->empty_rows; aa.num_empty = g->num_empty;
+  aa.row_ptr = g->row_ptr; aa.V_own = g->V_own; aa.narrow = g->narrow_cap; aa.witems = g->witems;
+  aa.num_witems = g->num_witems;
   static const int cache_env = getenv("RGNN_DST_CACHE") ? atoi(getenv("RGNN_DST_CACHE")) : -1;
   aa.cache_dst = cache_env >= 0 ? cache_env != 0 : g->E_own >= 4 * std::max<int64_t>(g->J, 1);  // mean run >= 4
   if (model == RGNN_RGAT) {
@@ -249,6 +264,36 @@ static rgnn_status forward(const rgnn_graph* g, int model, int K, int N, int pre
     if (ga.num_tiles) { Phase ph("gemm_fwd", s); RGNN_TRY(typed_gemm(prec, K, N, ga, s)); }
     aa.Z = sv.Z; aa.s_src = sv.s_src; aa.U = w.U; aa.lse = sv.lse;
     { Phase ph("aggregate", s); RGNN_TRY(launch_aggregate(prec, K, N, true, aa, s)); }
+  } else if (g->has_aggfirst && !getenv("RGNN_AGGFIRST_OFF")) {
+    // aggregate-first (NEXT-4, aggfirst.cu): piece sums of x_src, one typed GEMM over the pieces,
+    // and the walk adds each row's piece products once (slot weights 1 / 0)
+    { Phase ph("piece_agg", s);
+      RGNN_TRY(launch_piece_agg(prec, K, g->num_pieces, g->piece_ptr, g->inv_c, g->src_s, X, w.PA, s)); }
+    // A and P fp32 on both layers (aggfirst.cu): the piece GEMM on the tf32 tensor cores (bf16 layer:
+    // W^T rounded to bf16, exact in tf32) or the SIMT fp32 kernel, the walk in fp32
+    GemmFwdArgs gp{};
+    gp.tiles = g->ptiles; gp.num_tiles = g->num_ptiles; gp.X = w.PA; gp.gather = nullptr; gp.gofs = 0; gp.W = W;
+    gp.Z = w.PZ; gp.num_w = g->R; gp.x_rows = std::max<int64_t>(g->num_pieces, 1); gp.z_rows = g->num_pieces;
+    if (gp.num_tiles) {
+      Phase ph("gemm_fwd", s);
+      RGNN_TRY(launch_transpose_w(prec, g->R, K, N, W, w.PWt, s));
+      RGNN_TRY(f32_gemm(prec, K, N, gp, w.PWt, s));
+    }
+    if (W0 && g->V_own > 0) {  // the self term as fp32 rows (bf16 layer: bf16 tcgen05 GEMM, fp32 epilogue)
+      GemmFwdArgs g0{};
+      g0.rows = g->V_own; g0.X = X; g0.gofs = g->v0; g0.W = W0; g0.Z = w.PZ0; g0.wt_bf16 = w.wt;
+      g0.num_w = 1; g0.x_rows = g->V;
+      Phase ph("gemm_self", s);
+      rgnn_status st = prec == RGNN_BF16 ? launch_gemm_fwd_tc_f32out(K, N, g0, s) : RGNN_E_UNSUPPORTED;
+      if (st == RGNN_E_UNSUPPORTED) {
+        if (prec == RGNN_BF16) return set_error(RGNN_E_CUDA, "internal: tcgen05 self-loop GEMM unavailable");
+        st = typed_gemm(prec, K, N, g0, s);
+      }
+      RGNN_TRY(st);
+      aa.Z0 = w.PZ0;
+    }
+    aa.Z = w.PZ; aa.pos = g->slot_piece; aa.slot_scale = g->slot_w;
+    { Phase ph("aggregate", s); RGNN_TRY(launch_aggregate(RGNN_F32, K, N, false, aa, s)); }
   } else {
     ga.Z = w.Z; ga.row_scale = cm ? nullptr : g->inv_c;
     if (ga.num_tiles) { Phase ph("gemm_fwd", s); RGNN_TRY(typed_gemm(prec, K, N, ga, s)); }
@@ -274,8 +319,10 @@ extern "C" {
 
 rgnn_status rgnn_workspace_bytes(const rgnn_graph* g, rgnn_model model, int d_in, int d_out, rgnn_prec prec,
                                  int training, size_t* ws_bytes, size_t* saved_bytes) {
-  (void)training;
   if (!g) return set_error(RGNN_E_INVALID_ARG, "graph is NULL");
+  if (model != RGNN_RGCN && model != RGNN_RGAT && model != RGNN_HGT)
+    return set_error(RGNN_E_INVALID_ARG, "bad model %d", (int)model);
+  if (prec != RGNN_F32 && prec != RGNN_BF16) return set_error(RGNN_E_INVALID_ARG, "bad precision %d", (int)prec);
   if (!width_ok(d_in) || !width_ok(d_out)) return set_error(RGNN_E_UNSUPPORTED, "widths not in {32,64,128}");
   if (ws_bytes)
     *ws_bytes = model == RGNN_HGT ? hgt_ws_layout(g, d_in, d_out, prec, nullptr, training != 0).bytes
@@ -577,9 +624,11 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
                           const float* W, const float* W0, const float* A, float slope, const float* Y,
                           const float* dY, const void* saved, float* dW, float* dA, float* dW0, float* dX, void* ws,
                           size_t ws_bytes, rgnn_comm* comm, void* stream) {
-  if (model == RGNN_HGT) return set_error(RGNN_E_UNSUPPORTED, "HGT backward is not implemented (forward only)");
+  if (model == RGNN_HGT) return set_error(RGNN_E_UNSUPPORTED, "use hgt_backward for RGNN_HGT");
+  if (model != RGNN_RGCN && model != RGNN_RGAT) return set_error(RGNN_E_INVALID_ARG, "bad model %d", (int)model);
+  if (!g) return set_error(RGNN_E_INVALID_ARG, "graph is NULL");  // before any layout reads g
   const bool want_dx = dX != nullptr;
-  if (want_dx && g && !g->has_dx)
+  if (want_dx && !g->has_dx)
     return set_error(RGNN_E_UNSUPPORTED, "dX needs a graph built with RGNN_GRAPH_DX");
   const WsLayout need = ws_layout(g, model, K, N, prec, nullptr, want_dx);
   RGNN_TRY(check_common(g, K, N, prec, ws, ws_bytes, need));
@@ -603,12 +652,46 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     }
     return launch_gemm_dw(prec, K, N, args, s);
   };
+  // H_j = G_{v_j} W_{r_j}^T per (etype, dst) run j: one typed GEMM over the J runs (tf32 tensor
+  // cores on the bf16 layer, W rounded as in the forward; SIMT fp32 otherwise), read by dX (NEXT-2).
+  bool h_done = false;
+  auto run_products = [&]() -> rgnn_status {
+    { Phase ph("dx_prep", s);
+      RGNN_TRY(launch_transpose_w(prec, g->R, K, N, W, w.Wt, s));
+      if (model == RGNN_RGCN && W0) RGNN_TRY(launch_transpose_w(prec, 1, K, N, W0, w.Wt + (size_t)g->R * N * K, s));
+      // the tf32 GEMM reads its weight transposed: (W^T)^T = W, rounded like the SIMT copy
+      if (prec == RGNN_BF16) {
+        RGNN_TRY(launch_round_bf16((int64_t)g->R * K * N, W, w.Wr, s));
+        if (model == RGNN_RGCN && W0) RGNN_TRY(launch_round_bf16((int64_t)K * N, W0, w.Wr + (size_t)g->R * N * K, s));
+      } else {
+        RGNN_CUDA_TRY(cudaMemcpyAsync(w.Wr, W, sizeof(float) * g->R * K * N, cudaMemcpyDeviceToDevice, s));
+        if (model == RGNN_RGCN && W0)
+          RGNN_CUDA_TRY(cudaMemcpyAsync(w.Wr + (size_t)g->R * N * K, W0, sizeof(float) * K * N,
+                                        cudaMemcpyDeviceToDevice, s));
+      }
+    }
+    if (g->num_rtiles) {
+      Phase ph("run_gemm", s);
+      GemmFwdArgs gh{};
+      gh.tiles = g->rtiles; gh.num_tiles = g->num_rtiles; gh.X = dY; gh.gather = g->run_dst; gh.W = w.Wt;
+      gh.Z = w.H; gh.wt_bf16 = w.wt; gh.num_w = g->R; gh.x_rows = std::max<int64_t>(g->V_own, 1); gh.z_rows = g->J;
+      RGNN_TRY(f32_gemm(prec, N, K, gh, w.Wr, s));  // GEMM K = d_out, N = d_in
+    }
+    h_done = true;
+    return RGNN_OK;
+  };
   if (model == RGNN_RGAT) {
     { Phase ph("fold_u", s); RGNN_TRY(launch_fold_u(prec, g->R, K, N, W, A, w.U, s)); }
     rgnn_status fst = RGNN_E_UNSUPPORTED;
     if (tc_ok) {  // fused position-order backward: dZ built in smem, dW MMA + dst term in one kernel
+      // (Measured r02 and rejected: dalpha_e = H_j . x_src with the run products H_j = G_v W_r^T, so the
+      // kernel reads no Z rows -- ogbn-mag 3.64 -> 4.39 ms + 0.35 ms for the run GEMM, AM 0.85 -> 1.07
+      // + 0.31 ms: the H row becomes one more dependent load at every destination change of the
+      // compute warps, which are latency-bound there, while the Z rows it saves were prefetched by
+      // the producers.)
       Phase ph("bwd_fused", s);
-      fst = launch_bwd_fused_tc(K, N, g, X, sv.Z, use_compact(g, model) ? g->crow_of_pos : nullptr, sv.s_src, sv.lse, Y, dY, w.U, A, slope, w.dwpart, w.cpart, want_dx ? w.ad : nullptr, s);
+      fst = launch_bwd_fused_tc(K, N, g, X, sv.Z, use_compact(g, model) ? g->crow_of_pos : nullptr, sv.s_src, sv.lse,
+                                Y, dY, w.U, A, slope, w.dwpart, w.cpart, want_dx ? w.ad : nullptr, s);
       if (fst != RGNN_OK && fst != RGNN_E_UNSUPPORTED) return fst;
     }
     if (fst == RGNN_OK) {
@@ -662,31 +745,11 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
   }
   if (want_dx) {
     // dX (dx.cu): H = G_v W_r^T per (etype, dst) run by one typed GEMM, then the source walk
-    const int64_t J = g->J;
-    { Phase ph("dx_prep", s);
-      RGNN_TRY(launch_transpose_w(prec, g->R, K, N, W, w.Wt, s));
-      if (model == RGNN_RGCN && W0) RGNN_TRY(launch_transpose_w(prec, 1, K, N, W0, w.Wt + (size_t)g->R * N * K, s));
-      // the tf32 GEMM reads its weight transposed: (W^T)^T = W, rounded like the SIMT copy
-      if (prec == RGNN_BF16) {
-        RGNN_TRY(launch_round_bf16((int64_t)g->R * K * N, W, w.Wr, s));
-        if (model == RGNN_RGCN && W0) RGNN_TRY(launch_round_bf16((int64_t)K * N, W0, w.Wr + (size_t)g->R * N * K, s));
-      } else {
-        RGNN_CUDA_TRY(cudaMemcpyAsync(w.Wr, W, sizeof(float) * g->R * K * N, cudaMemcpyDeviceToDevice, s));
-        if (model == RGNN_RGCN && W0)
-          RGNN_CUDA_TRY(cudaMemcpyAsync(w.Wr + (size_t)g->R * N * K, W0, sizeof(float) * K * N,
-                                        cudaMemcpyDeviceToDevice, s));
-      }
-      if (model == RGNN_RGAT) {
-        RGNN_TRY(launch_fold_u(prec, g->R, K, N, W, A, w.U0, s, 0));
-      }
-    }
-    // fp32 GEMMs (SIMT): G is fp32, and rounding G or H to bf16 is too lossy for dX (dx.cu)
-    if (g->num_rtiles) {
-      Phase ph("dx_gemm", s);
-      GemmFwdArgs gh{};
-      gh.tiles = g->rtiles; gh.num_tiles = g->num_rtiles; gh.X = dY; gh.gather = g->run_dst; gh.W = w.Wt;
-      gh.Z = w.H; gh.wt_bf16 = w.wt; gh.num_w = g->R; gh.x_rows = std::max<int64_t>(g->V_own, 1); gh.z_rows = J;
-      RGNN_TRY(f32_gemm(prec, N, K, gh, w.Wr, s));  // GEMM K = d_out, N = d_in
+    // H = G_v W_r^T per run (fp32: rounding G or H to bf16 is too lossy for dX, dx.cu)
+    if (!h_done) RGNN_TRY(run_products());
+    if (model == RGNN_RGAT) {
+      Phase ph("dx_prep", s);
+      RGNN_TRY(launch_fold_u(prec, g->R, K, N, W, A, w.U0, s, 0));
     }
     const bool self = model == RGNN_RGCN && W0 && g->V_own > 0;
     if (self) {
@@ -711,10 +774,11 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     RGNN_TRY(launch_dx_walk(K, model == RGNN_RGAT, xa, s));
   }
   if (comm) {
-    float* bufs[4] = {dW, model == RGNN_RGAT ? dA : nullptr, model == RGNN_RGCN ? dW0 : nullptr, dX};
-    size_t counts[4] = {(size_t)g->R * K * N, (size_t)g->R * 2 * N, (size_t)K * N, (size_t)g->V * K};
+    float* bufs[3] = {dW, model == RGNN_RGAT ? dA : nullptr, model == RGNN_RGCN ? dW0 : nullptr};
+    size_t counts[3] = {(size_t)g->R * K * N, (size_t)g->R * 2 * N, (size_t)K * N};
     Phase ph("comm", s);
-    RGNN_TRY(comm_allreduce_sum(comm, bufs, counts, 4, s));
+    RGNN_TRY(comm_allreduce_sum(comm, bufs, counts, 3, s));
+    if (dX) RGNN_TRY(comm_reduce_rows(comm, dX, K, s));  // dX reduce-scattered over the dst ranges
   }
   return RGNN_OK;
 }

@@ -134,7 +134,9 @@ rgnn_status scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int32_t* 
 constexpr int kRsThreads = 256, kRsRounds = 8, kRsTile = kRsThreads * kRsRounds, kRsWarps = kRsThreads / 32;
 
 __global__ void __launch_bounds__(kRsThreads) k_rs_hist(const uint32_t* __restrict__ keys, int64_t n, int shift,
-                                                        int64_t nb, int32_t* __restrict__ counts) {
+                                                        int64_t nb, int32_t* __restrict__ counts,
+                                                        const int32_t* __restrict__ n_dev) {
+  if (n_dev) n = min(n, (int64_t)*n_dev);
   __shared__ int32_t h[256];
   h[threadIdx.x] = 0;
   __syncthreads();
@@ -152,7 +154,10 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const uint32_t* __res
                                                            const uint32_t* __restrict__ vals, int64_t n, int shift,
                                                            int64_t nb, const int32_t* __restrict__ offsets,
                                                            uint32_t* __restrict__ keys_out,
-                                                           uint32_t* __restrict__ vals_out) {
+                                                           uint32_t* __restrict__ vals_out,
+                                                           const int32_t* __restrict__ n_dev) {
+  if (n_dev) n = min(n, (int64_t)*n_dev);
+  if ((int64_t)blockIdx.x * kRsTile >= n) return;  // an empty tile (its histogram is zero)
   __shared__ int32_t s_run[256];
   __shared__ int32_t s_w[kRsWarps][256];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -199,7 +204,8 @@ size_t radix_scratch_bytes(int64_t n) {
 }
 
 rgnn_status radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
-                             int bits, void* scratch, size_t scratch_bytes, cudaStream_t s, bool* result_in_alt) {
+                             int bits, void* scratch, size_t scratch_bytes, cudaStream_t s, bool* result_in_alt,
+                             const int32_t* n_dev) {
   *result_in_alt = false;
   if (n <= 1 || bits <= 0) return RGNN_OK;
   if (scratch_bytes < radix_scratch_bytes(n)) return set_error(RGNN_E_WORKSPACE, "radix scratch too small");
@@ -209,9 +215,9 @@ rgnn_status radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt,
   size_t scan_bytes = scratch_bytes - align_up(sizeof(int32_t) * 256 * (size_t)nb);
   uint32_t *ki = keys, *vi = vals, *ko = keys_alt, *vo = vals_alt;
   for (int shift = 0; shift < bits; shift += 8) {
-    RGNN_LAUNCH(k_rs_hist, (unsigned)nb, kRsThreads, 0, s, ki, n, shift, nb, counts);
+    RGNN_LAUNCH(k_rs_hist, (unsigned)nb, kRsThreads, 0, s, ki, n, shift, nb, counts, n_dev);
     RGNN_TRY(scan_exclusive(counts, counts, 256 * nb, nullptr, scan_scr, scan_bytes, s));
-    RGNN_LAUNCH(k_rs_scatter, (unsigned)nb, kRsThreads, 0, s, ki, vi, n, shift, nb, counts, ko, vo);
+    RGNN_LAUNCH(k_rs_scatter, (unsigned)nb, kRsThreads, 0, s, ki, vi, n, shift, nb, counts, ko, vo, n_dev);
     uint32_t* t;
     t = ki; ki = ko; ko = t;
     t = vi; vi = vo; vo = t;

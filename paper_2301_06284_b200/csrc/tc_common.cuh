@@ -4,6 +4,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace rgnn {
@@ -49,12 +51,24 @@ __device__ __forceinline__ bool mbar_try_sleep(uint64_t* b, uint32_t parity) {
   return ok != 0;
 }
 // Wait for an mbarrier phase.  Watchdog: a wait longer than 10 s means a pipeline
-// bug (deadlock); trap so the launch fails instead of hanging the device.
+// bug (deadlock); trap so the launch fails instead of hanging the device.  The limit is
+// per translation unit and can be raised with RGNN_WATCHDOG_S (compute-sanitizer runs the
+// kernels orders of magnitude slower); watchdog_init() applies it before the first launch.
+static __device__ uint64_t g_watchdog_ns = 10000000000ull;
+static inline void watchdog_init() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  if (const char* e = getenv("RGNN_WATCHDOG_S")) {
+    const uint64_t ns = (uint64_t)strtoull(e, nullptr, 10) * 1000000000ull;
+    cudaMemcpyToSymbol(g_watchdog_ns, &ns, sizeof(ns));
+  }
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   if (mbar_try(b, parity)) return;
   const uint64_t t0 = global_ns();
   while (!mbar_try_sleep(b, parity)) {
-    if (global_ns() - t0 > 10000000000ull) {
+    if (global_ns() - t0 > g_watchdog_ns) {
       printf("rgnn watchdog: block %d thread %d stuck on mbarrier smem+0x%x parity %u\n", blockIdx.x, threadIdx.x,
              smem_u32(b), parity);
       __trap();

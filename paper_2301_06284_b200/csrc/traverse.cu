@@ -110,6 +110,312 @@ __device__ __forceinline__ void dst_scores(const float* xv, const float* U, int 
   }
 }
 
+// Packed fp32x2 FMA / MUL (Blackwell FFMA2 / FMUL2): the same per-element rounding as fmaf / *,
+// so results are bit-identical to the scalar loops, at half the instructions.
+#ifndef RGNN_WALK_FFMA2
+#define RGNN_WALK_FFMA2 0  // measured r02: FFMA2 on, ogbn-mag walk 1.82 -> 2.13 ms (register pressure); AM / wikikg2 unchanged
+#endif
+template <int EPL>
+__device__ __forceinline__ void fma_acc(float* acc, float e, const float* z) {
+  if constexpr (EPL % 2 == 0 && RGNN_WALK_FFMA2) {
+#pragma unroll
+    for (int i = 0; i < EPL; i += 2) {
+      uint64_t a, b, c, d;
+      asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(e), "f"(e));
+      asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(z[i]), "f"(z[i + 1]));
+      asm("mov.b64 %0, {%1, %2};" : "=l"(c) : "f"(acc[i]), "f"(acc[i + 1]));
+      asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[i]), "=f"(acc[i + 1]) : "l"(d));
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) acc[i] = fmaf(e, z[i], acc[i]);
+  }
+}
+template <int EPL>
+__device__ __forceinline__ void mul_acc(float* acc, float f) {
+  if constexpr (EPL % 2 == 0 && RGNN_WALK_FFMA2) {
+#pragma unroll
+    for (int i = 0; i < EPL; i += 2) {
+      uint64_t a, c, d;
+      asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(f), "f"(f));
+      asm("mov.b64 %0, {%1, %2};" : "=l"(c) : "f"(acc[i]), "f"(acc[i + 1]));
+      asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(c), "l"(a));
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[i]), "=f"(acc[i + 1]) : "l"(d));
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) acc[i] *= f;
+  }
+}
+
+// Narrow rows (deg <= a.narrow, never split): one lane group (L lanes, one 16-byte slice of a
+// Z row each) per row, G consecutive row ids per warp step, UN edges per group step and one
+// online state per row -- no cross-group merge, so short rows cost a quarter (d = 64 bf16) or
+// half (d = 128) of a warp instead of a whole warp plus a shuffle tree.  Rows are visited in id
+// order, so empty rows (Y = 0, or the RGCN self term, lse = -inf) are written here too, with
+// coalesced stores.  Which walk a row takes depends only on its degree: a dst-range shard walks
+// every row exactly as one GPU does (pin P14).
+// The three dependent loads of a row (row_ptr -> slot indices -> Z rows / s_src) are software
+// pipelined across the warp's row groups: while row group i is reduced, the slot indices of
+// group i+1 and the row bounds of group i+2 are already in flight.
+template <typename T, int K, int N, bool RGAT>
+__device__ __forceinline__ void narrow_rows_pipe(const AggArgs& a, int64_t warp0, int64_t nwarps, int lane) {
+  using S = WalkShape<T, K, N>;
+  constexpr int EPL = S::EPL, L = S::L, G = S::G, KPL = S::KPL;
+  constexpr int UN = L < 4 ? L : 4;  // edges per group step
+  const T* Z = static_cast<const T*>(a.Z);
+  const T* X = static_cast<const T*>(a.X);
+  const int g = lane / L, l = lane % L;
+  const unsigned gmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (g * L));
+  const int64_t ngroups = (a.V_own + G - 1) / G;
+  // row bounds of this group's row in row group rg (q1 < q0 marks "no narrow row here")
+  auto bounds = [&](int64_t rg, int& q0, int& q1) {
+    const int64_t row = rg * G + g;
+    q0 = 0; q1 = -1;
+    if (rg < ngroups && row < a.V_own) {
+      q0 = a.row_ptr[row]; q1 = a.row_ptr[row + 1];
+      if (q1 - q0 > a.narrow) q1 = -1;  // a wide row: walked from the item list
+    }
+  };
+  // slot indices of the first step (lanes l < UN): position / Z row, relation (RGAT) or 1/c (RGCN)
+  auto slots = [&](int q0, int q1, int& p, int& r, float& sc) {
+    const int q = q0 + l;
+    const bool ok = l < UN && q < q1;
+    p = ok ? a.pos[q] : 0;
+    r = (RGAT && ok) ? a.et_slot[q] : 0;
+    sc = RGAT ? 0.f : ((ok && a.slot_scale) ? a.slot_scale[q] : 1.f);
+  };
+  int q0c, q1c, q0n, q1n;  // current / next row group bounds
+  bounds(warp0, q0c, q1c);
+  bounds(warp0 + nwarps, q0n, q1n);
+  int pc, rc;
+  float sc_c;
+  slots(q0c, q1c, pc, rc, sc_c);
+  for (int64_t rg = warp0; rg < ngroups; rg += nwarps) {
+    const int64_t row = rg * G + g;
+    const int q0 = q0c, q1 = q1c;
+    int myp = pc, myr = rc;
+    float mys = sc_c;
+    // stage C of this group: its first step's Z rows and source scores ...
+    uint4 zr[UN];
+    float sc[UN];
+    int rr[UN];
+    bool val[UN];
+    float ssrc = 0.f;
+    if constexpr (RGAT) ssrc = (l < UN && q0 + l < q1) ? a.s_src[myp] : 0.f;
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int p = __shfl_sync(gmask, myp, u, L);
+      rr[u] = __shfl_sync(gmask, myr, u, L);
+      val[u] = q0 + u < q1;
+      zr[u] = val[u] ? ldg16(Z + (size_t)p * N + l * EPL) : make_uint4(0, 0, 0, 0);
+    }
+    // ... stage B of the next group (its slot indices) and stage A of the one after (its bounds)
+    slots(q0n, q1n, pc, rc, sc_c);
+    q0c = q0n; q1c = q1n;
+    bounds(rg + 2 * nwarps, q0n, q1n);
+    if (row >= a.V_own || q1 < q0) continue;  // no row, or a wide row (the whole group together)
+    if constexpr (RGAT) mys = ssrc;
+    float acc[EPL];
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
+    float m = -CUDART_INF_F, lsum = 0.f;
+    float xv[KPL];
+    if constexpr (RGAT) {
+      if (q1 > q0) load_slice<KPL>(X + (a.v0 + row) * (int64_t)K + l * KPL, xv);
+    }
+    for (int base = q0; base < q1; base += UN) {
+      if (base > q0) {  // later steps of a row longer than UN: loads issued here
+        const int q = base + l;
+        const bool ok = l < UN && q < q1;
+        myp = ok ? a.pos[q] : 0;
+        if constexpr (RGAT) {
+          myr = ok ? a.et_slot[q] : 0;
+          mys = ok ? a.s_src[myp] : 0.f;
+        } else {
+          mys = (ok && a.slot_scale) ? a.slot_scale[q] : 1.f;
+        }
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+          const int p = __shfl_sync(gmask, myp, u, L);
+          rr[u] = __shfl_sync(gmask, myr, u, L);
+          val[u] = base + u < q1;
+          zr[u] = val[u] ? ldg16(Z + (size_t)p * N + l * EPL) : make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UN; ++u) sc[u] = __shfl_sync(gmask, mys, u, L);
+      if constexpr (RGAT) {
+        float d[UN];
+#pragma unroll
+        for (int u = 0; u < UN; ++u) d[u] = dot_u<KPL>(xv, a.U + (size_t)rr[u] * K + l * KPL);
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+#pragma unroll
+          for (int o = L / 2; o > 0; o >>= 1) d[u] += __shfl_xor_sync(gmask, d[u], o);
+          sc[u] = val[u] ? leaky(sc[u] + d[u], a.slope) : -CUDART_INF_F;
+        }
+        float mnew = m;
+#pragma unroll
+        for (int u = 0; u < UN; ++u) mnew = fmaxf(mnew, sc[u]);
+        const float corr = __expf(m - mnew);  // m = -inf -> 0 (mnew is finite: edge base is valid)
+        lsum *= corr;
+        mul_acc<EPL>(acc, corr);
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+          const float e = val[u] ? __expf(sc[u] - mnew) : 0.f;
+          lsum += e;
+          float zf[EPL];
+          Vec16<T>{zr[u]}.to_float(zf);
+          fma_acc<EPL>(acc, e, zf);
+        }
+        m = mnew;
+      } else {
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+          float zf[EPL];
+          Vec16<T>{zr[u]}.to_float(zf);
+          fma_acc<EPL>(acc, sc[u], zf);  // invalid slots: z = 0
+        }
+      }
+    }
+    float* y = a.Y + (size_t)row * N + l * EPL;
+    if constexpr (RGAT) {
+      const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) acc[i] *= inv;
+      if (l == 0) a.lse[row] = lsum > 0.f ? m + __logf(lsum) : -CUDART_INF_F;
+    } else if (a.Z0) {
+      float z0[EPL];
+      Vec16<T>{ldg16(static_cast<const T*>(a.Z0) + (size_t)row * N + l * EPL)}.to_float(z0);
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) acc[i] += z0[i];
+    }
+#pragma unroll
+    for (int i = 0; i < EPL; i += 4)
+      stg16(y + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]), __float_as_uint(acc[i + 2]),
+                              __float_as_uint(acc[i + 3])));
+  }
+}
+
+// The same walk without the cross-row-group pipeline (measured faster for RGAT, whose per-row
+// x_dst slice and per-edge U dot make the pipelined version spill or lose a resident block:
+// AM 0.354 vs 0.402 ms; RGCN gains from the pipeline: wikikg2 walk 1.00 -> 0.77 ms).
+template <typename T, int K, int N, bool RGAT>
+__device__ __forceinline__ void narrow_rows(const AggArgs& a, int64_t warp0, int64_t nwarps, int lane) {
+  using S = WalkShape<T, K, N>;
+  constexpr int EPL = S::EPL, L = S::L, G = S::G, KPL = S::KPL;
+  constexpr int UN = L < 4 ? L : 4;  // edges per group step
+  const T* Z = static_cast<const T*>(a.Z);
+  const T* X = static_cast<const T*>(a.X);
+  const int g = lane / L, l = lane % L;
+  const unsigned gmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (g * L));
+  const int64_t ngroups = (a.V_own + G - 1) / G;
+  // the next row group's bounds are loaded one iteration ahead (one dependent load off the chain)
+  int nq0 = 0, nq1 = 0;
+  if (warp0 * G + g < a.V_own) { nq0 = a.row_ptr[warp0 * G + g]; nq1 = a.row_ptr[warp0 * G + g + 1]; }
+  for (int64_t rg = warp0; rg < ngroups; rg += nwarps) {
+    const int64_t row = rg * G + g;
+    const int q0 = nq0, q1 = nq1;
+    const int64_t nrow = (rg + nwarps) * G + g;
+    if (nrow < a.V_own) { nq0 = a.row_ptr[nrow]; nq1 = a.row_ptr[nrow + 1]; }
+    if (row >= a.V_own) continue;  // the whole group leaves together
+    if (q1 - q0 > a.narrow) continue;  // a wide row: walked from the item list
+    float acc[EPL];
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
+    float m = -CUDART_INF_F, lsum = 0.f;
+    float xv[KPL];
+    if constexpr (RGAT) {
+      if (q1 > q0) load_slice<KPL>(X + (a.v0 + row) * (int64_t)K + l * KPL, xv);
+    }
+    for (int base = q0; base < q1; base += UN) {
+      const int q = base + l;
+      const bool ok = l < UN && q < q1;
+      const int myp = ok ? a.pos[q] : 0;
+      int myr = 0;
+      float mys;
+      if constexpr (RGAT) {
+        myr = ok ? a.et_slot[q] : 0;
+        mys = ok ? a.s_src[myp] : 0.f;
+      } else {
+        mys = (ok && a.slot_scale) ? a.slot_scale[q] : 1.f;
+      }
+      uint4 zr[UN];
+      float sc[UN];
+      int rr[UN];
+      bool val[UN];
+#pragma unroll
+      for (int u = 0; u < UN; ++u) {  // all Z-row loads of the step first
+        const int p = __shfl_sync(gmask, myp, u, L);
+        rr[u] = __shfl_sync(gmask, myr, u, L);
+        sc[u] = __shfl_sync(gmask, mys, u, L);
+        val[u] = base + u < q1;
+        zr[u] = val[u] ? ldg16(Z + (size_t)p * N + l * EPL) : make_uint4(0, 0, 0, 0);
+      }
+      if constexpr (RGAT) {
+        float d[UN];
+#pragma unroll
+        for (int u = 0; u < UN; ++u) d[u] = dot_u<KPL>(xv, a.U + (size_t)rr[u] * K + l * KPL);
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+#pragma unroll
+          for (int o = L / 2; o > 0; o >>= 1) d[u] += __shfl_xor_sync(gmask, d[u], o);
+          sc[u] = val[u] ? leaky(sc[u] + d[u], a.slope) : -CUDART_INF_F;
+        }
+        float mnew = m;
+#pragma unroll
+        for (int u = 0; u < UN; ++u) mnew = fmaxf(mnew, sc[u]);
+        const float corr = __expf(m - mnew);
+        lsum *= corr;
+        mul_acc<EPL>(acc, corr);
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+          const float e = val[u] ? __expf(sc[u] - mnew) : 0.f;
+          lsum += e;
+          float zf[EPL];
+          Vec16<T>{zr[u]}.to_float(zf);
+          fma_acc<EPL>(acc, e, zf);
+        }
+        m = mnew;
+      } else {
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+          float zf[EPL];
+          Vec16<T>{zr[u]}.to_float(zf);
+          fma_acc<EPL>(acc, sc[u], zf);
+        }
+      }
+    }
+    float* y = a.Y + (size_t)row * N + l * EPL;
+    if constexpr (RGAT) {
+      const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) acc[i] *= inv;
+      if (l == 0) a.lse[row] = lsum > 0.f ? m + __logf(lsum) : -CUDART_INF_F;
+    } else if (a.Z0) {
+      float z0[EPL];
+      Vec16<T>{ldg16(static_cast<const T*>(a.Z0) + (size_t)row * N + l * EPL)}.to_float(z0);
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) acc[i] += z0[i];
+    }
+#pragma unroll
+    for (int i = 0; i < EPL; i += 4)
+      stg16(y + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]), __float_as_uint(acc[i + 2]),
+                              __float_as_uint(acc[i + 3])));
+  }
+}
+
+// resident blocks: RGAT 4 (64 registers, simple walk), RGCN 3 (80 registers, pipelined walk; 4
+// spilled ~150 B at d = 64)
+template <typename T, int K, int N, bool RGAT>
+__global__ void __launch_bounds__(256, RGAT ? 4 : 3) k_aggregate_narrow(AggArgs a) {
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  if constexpr (RGAT) narrow_rows<T, K, N, RGAT>(a, w0, nw, threadIdx.x & 31);
+  else narrow_rows_pipe<T, K, N, RGAT>(a, w0, nw, threadIdx.x & 31);
+}
+
 // 4 resident blocks (64 registers): measured r01 on ogbn-mag d=128, the walk is
 // latency bound and 32 warps / SM beat 24 warps with fewer spills (1.85 vs 2.43 ms)
 #ifndef RGNN_AGG_MINB
@@ -206,16 +512,14 @@ __global__ void __launch_bounds__(256, RGNN_AGG_MINB) k_aggregate(AggArgs a) {
         if (mnew != -CUDART_INF_F) {
           const float corr = __expf(m - mnew);  // m = -inf -> 0
           lsum *= corr;
-#pragma unroll
-          for (int i = 0; i < EPL; ++i) acc[i] *= corr;
+          mul_acc<EPL>(acc, corr);
 #pragma unroll
           for (int u = 0; u < UNR; ++u) {
             const float e = val[u] ? __expf(sc[u] - mnew) : 0.f;
             lsum += e;
             float zf[EPL];
             Vec16<T>{zr[u]}.to_float(zf);
-#pragma unroll
-            for (int i = 0; i < EPL; ++i) acc[i] = fmaf(e, zf[i], acc[i]);
+            fma_acc<EPL>(acc, e, zf);
           }
           m = mnew;
         }
@@ -224,8 +528,7 @@ __global__ void __launch_bounds__(256, RGNN_AGG_MINB) k_aggregate(AggArgs a) {
         for (int u = 0; u < UNR; ++u) {
           float zf[EPL];
           Vec16<T>{zr[u]}.to_float(zf);
-#pragma unroll
-          for (int i = 0; i < EPL; ++i) acc[i] = fmaf(sc[u], zf[i], acc[i]);  // fma(1, z, acc) == acc + z
+          fma_acc<EPL>(acc, sc[u], zf);  // fma(1, z, acc) == acc + z
         }
       }
     }
@@ -395,16 +698,14 @@ __global__ void __launch_bounds__(256) k_aggregate_ring(AggArgs a) {
         if (mnew != -CUDART_INF_F) {
           const float corr = __expf(m - mnew);
           lsum *= corr;
-#pragma unroll
-          for (int i = 0; i < EPL; ++i) acc[i] *= corr;
+          mul_acc<EPL>(acc, corr);
 #pragma unroll
           for (int u = 0; u < UNR; ++u) {
             const float e = val[u] ? __expf(sc[u] - mnew) : 0.f;
             lsum += e;
             float zf[EPL];
             Vec16<T>{zr[u]}.to_float(zf);
-#pragma unroll
-            for (int i = 0; i < EPL; ++i) acc[i] = fmaf(e, zf[i], acc[i]);
+            fma_acc<EPL>(acc, e, zf);
           }
           m = mnew;
         }
@@ -413,8 +714,7 @@ __global__ void __launch_bounds__(256) k_aggregate_ring(AggArgs a) {
         for (int u = 0; u < UNR; ++u) {
           float zf[EPL];
           Vec16<T>{zr[u]}.to_float(zf);
-#pragma unroll
-          for (int i = 0; i < EPL; ++i) acc[i] = fmaf(sc[u], zf[i], acc[i]);  // fma(1, z, acc) == acc + z
+          fma_acc<EPL>(acc, sc[u], zf);  // fma(1, z, acc) == acc + z
         }
       }
     }
@@ -687,12 +987,28 @@ static unsigned warps_grid(int64_t items) {
 }
 
 template <typename T, int K, int N>
-static rgnn_status aggregate(bool rgat, const AggArgs& a, cudaStream_t s) {
+static rgnn_status aggregate(bool rgat, const AggArgs& a_in, cudaStream_t s) {
+  AggArgs a = a_in;
+  // narrow pass: only when a row group is narrower than the warp (G >= 2); it also writes the
+  // empty rows, and the item walk then covers the wide rows only
+  static const bool no_narrow = getenv("RGNN_NO_NARROW") != nullptr;
+  const bool narrow = a.row_ptr && a.V_own > 0 && WalkShape<T, K, N>::G >= 2 && !no_narrow;
+  if (narrow) {
+    a.items = a.witems; a.num_items = a.num_witems; a.num_empty = 0;
+  } else {
+    a.row_ptr = nullptr;
+  }
+  constexpr int G = WalkShape<T, K, N>::G;
+  if (narrow) {  // the narrow rows (and the empty ones) first, one lane group per row
+    auto kn = rgat ? k_aggregate_narrow<T, K, N, true> : k_aggregate_narrow<T, K, N, false>;
+    RGNN_LAUNCH(kn, warps_grid((a.V_own + G - 1) / G), 256, 0, s, a);
+  }
+  const int64_t work = a.num_items;
   if (a.num_empty > 0) {
     const int64_t n = a.num_empty * (N / 4);
     RGNN_LAUNCH((k_empty_rows<T, N>), (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, s, a);
   }
-  if (a.num_items > 0) {
+  if (work > 0) {
     static const bool no_ring = getenv("RGNN_WALK_NO_RING") != nullptr;
     static const bool force_ring = getenv("RGNN_WALK_RING") != nullptr;
     // measured r01: with 4 resident blocks the plain walk wins for RGAT at every width (AM d=64
@@ -704,11 +1020,11 @@ static rgnn_status aggregate(bool rgat, const AggArgs& a, cudaStream_t s) {
       auto kern = !rgat ? k_aggregate_ring<T, K, N, false, RING, false>
                   : a.cache_dst ? k_aggregate_ring<T, K, N, true, RING, true> : k_aggregate_ring<T, K, N, true, RING, false>;
       RGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      RGNN_LAUNCH(kern, warps_grid(a.num_items), 256, smem, s, a);
+      RGNN_LAUNCH(kern, warps_grid(work), 256, smem, s, a);
     } else {
       auto kern = !rgat ? k_aggregate<T, K, N, false, false>
                   : a.cache_dst ? k_aggregate<T, K, N, true, true> : k_aggregate<T, K, N, true, false>;
-      RGNN_LAUNCH(kern, warps_grid(a.num_items), 256, 0, s, a);
+      RGNN_LAUNCH(kern, warps_grid(work), 256, 0, s, a);
     }
   }
   if (a.num_split_rows > 0) {

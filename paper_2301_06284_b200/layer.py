@@ -54,7 +54,7 @@ class Graph:
     def __init__(self, num_nodes: int, src, dst, etype, num_etypes: int, *, row_ptr=None, ntype=None,
                  num_ntypes: int = 0, norm: int = B.RGNN_NORM_REL_INDEG, edge_norm=None, row_split_cap: int = 0,
                  dst_begin: int = 0, dst_end: Optional[int] = None, materialization="vanilla", build_dx: bool = False,
-                 device="cuda", stream=None):
+                 aggregate_first: bool = False, device="cuda", stream=None):
         self.device = torch.device(device)
         self.V, self.R = int(num_nodes), int(num_etypes)
         self.src = _dev_i32(src, self.device)
@@ -72,7 +72,8 @@ class Graph:
                               row_ptr=_ptr(self.row_ptr_in), ntype=_ptr(self.ntype), edge_norm=_ptr(self.edge_norm),
                               norm=int(norm), row_split_cap=int(row_split_cap), dst_begin=self.dst_begin,
                               dst_end=self.dst_end, materialization=_mat(materialization),
-                              flags=B.RGNN_GRAPH_DX if build_dx else 0)
+                              flags=(B.RGNN_GRAPH_DX if build_dx else 0) |
+                              (B.RGNN_GRAPH_AGGFIRST if aggregate_first else 0))
         self._desc = d
         dev_b, scr_b = C.c_size_t(), C.c_size_t()
         B.call("rgnn_graph_bytes", C.byref(d), C.byref(dev_b), C.byref(scr_b))
@@ -80,8 +81,11 @@ class Graph:
         scratch = torch.empty(max(scr_b.value, 256), dtype=torch.uint8, device=self.device)
         h = C.c_void_p()
         self._handle = None
+        import time
+        t0 = time.perf_counter()
         B.call("rgnn_graph_create", C.byref(d), _ptr(self.storage), dev_b.value, _ptr(scratch), scr_b.value,
                _stream(stream), C.byref(h))  # SYNC
+        self.create_ms = 1e3 * (time.perf_counter() - t0)  # the library call alone (buffers preallocated)
         self._handle = h
         del scratch
         v = B.rgnn_graph_view()
@@ -121,6 +125,19 @@ class Graph:
         B.call("rgnn_zrows", self._handle, _model(model), C.byref(r))
         return int(r.value)
 
+    def num_pieces(self) -> int:
+        """Run pieces (HGT backward / aggregate-first RGCN tables), via the graph view."""
+        return int(self.view.num_pieces)
+
+    def piece_arrays(self) -> dict:
+        """Aggregate-first tables (graph created with aggregate_first=True), as NumPy arrays (tests)."""
+        v = self.view
+        E, NP = int(v.E_own), int(v.num_pieces)
+        i32, f32 = torch.int32, torch.float32
+        return {"piece_ptr": self._arr(v.piece_ptr, NP + 1, i32).cpu().numpy(),
+                "slot_piece": self._arr(v.slot_piece, E, i32).cpu().numpy(),
+                "slot_w": self._arr(v.slot_w, E, f32).cpu().numpy()}
+
     def compact_arrays(self) -> dict:
         """Compact materialisation tables (graph created with materialization="compact")."""
         v = self.view
@@ -147,6 +164,16 @@ class Comm:
         B.call("rgnn_comm_create", C.cast(idbuf, C.c_void_p), world, rank, b, C.byref(h))
         self._handle = h
         self.bounds = [int(x) for x in bounds]
+
+    def set_options(self, gather_async: bool = False, gather_bf16: bool = False):
+        """rgnn_comm_set_options: asynchronous Y gather (join before reading Y_full) / bf16 Y_full."""
+        flags = (B.RGNN_COMM_GATHER_ASYNC if gather_async else 0) | (B.RGNN_COMM_GATHER_BF16 if gather_bf16 else 0)
+        B.call("rgnn_comm_set_options", self._handle, flags)
+        return self
+
+    def join(self, stream=None):
+        """rgnn_comm_join: `stream` waits for the pending asynchronous Y gather."""
+        B.call("rgnn_comm_join", self._handle, _stream(stream))
 
     @property
     def handle(self):

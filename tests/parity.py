@@ -10,9 +10,51 @@ for fp32 and "2e-2 rel" for bf16):
 """
 from __future__ import annotations
 
+import json
+import os
+
 import numpy as np
 
 TOL = {"f32": (1e-4, 1e-5, True), "bf16": (2e-2, 2e-2, False)}
+
+
+def _atol(ref, prec: str, per_slice: bool):
+    """per_slice: one rms per leading index -- per relation for dW [R,K,N] / dA [R,2,N], per
+    destination row for Y [V,N] (O19: each slice is its own sum with its own scale)."""
+    rtol, ascale, floor1 = TOL[prec]
+    if per_slice and ref.ndim >= 2:
+        rms = np.sqrt(np.mean(ref * ref, axis=tuple(range(1, ref.ndim)), keepdims=True))
+    else:
+        rms = float(np.sqrt(np.mean(ref * ref)))
+    return ascale * (np.maximum(1.0, rms) if floor1 else rms)
+
+
+def error_ratio(got, ref, prec: str, per_slice: bool = False) -> float:
+    """Worst |got - ref| / (atol + rtol |ref|) over the elements (<= 1 passes the elementwise bound)."""
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    if ref.size == 0:
+        return 0.0
+    bound = _atol(ref, prec, per_slice) + TOL[prec][0] * np.abs(ref)
+    err = np.abs(got - ref)
+    # exact zeros of the reference (empty rows / relations) must be matched exactly: 0 / 0 -> 0
+    return float(np.max(np.where(bound > 0, err / np.where(bound > 0, bound, 1.0), np.where(err > 0, np.inf, 0.0))))
+
+
+def _log_ratio(got, ref, prec, what, per_slice):
+    """RGNN_PARITY_LOG=<file>: append the worst error / bound ratio of this assertion under both
+    atol scalings (global rms; per-relation rms) -- the evidence DESIGN.md O19 cites."""
+    path = os.environ.get("RGNN_PARITY_LOG")
+    if not path:
+        return
+    rec = {"what": what, "prec": prec, "shape": list(np.shape(ref)),
+           "ratio_global": error_ratio(got, ref, prec, False)}
+    if np.ndim(ref) >= 2:
+        rec["ratio_per_slice"] = error_ratio(got, ref, prec, True)
+    r = np.asarray(ref, dtype=np.float64)
+    rec["fro"] = float(np.linalg.norm(np.asarray(got, np.float64) - r) / max(np.linalg.norm(r), 1e-300))
+    with open(path, "a") as f:
+        f.write(json.dumps(rec) + "\n")
 
 
 def assert_close(got, ref, prec: str, what: str = "", per_slice: bool = False):
@@ -21,12 +63,9 @@ def assert_close(got, ref, prec: str, what: str = "", per_slice: bool = False):
     assert got.shape == ref.shape, (what, got.shape, ref.shape)
     if ref.size == 0:
         return
-    rtol, ascale, floor1 = TOL[prec]
-    if per_slice and ref.ndim == 3:  # one scale per relation (O19)
-        rms = np.sqrt(np.mean(ref * ref, axis=(1, 2), keepdims=True))
-    else:
-        rms = float(np.sqrt(np.mean(ref * ref)))
-    atol = ascale * (np.maximum(1.0, rms) if floor1 else rms)
+    _log_ratio(got, ref, prec, what, per_slice)
+    rtol = TOL[prec][0]
+    atol = _atol(ref, prec, per_slice)
     err = np.abs(got - ref)
     bad = err > atol + rtol * np.abs(ref)
     if bad.any():

@@ -2,7 +2,8 @@
 partition (rgnn_partition_dst from librgnn.so), per-rank shards computed by the
 fp64 oracle, an all-gather of the owned Y rows and an all-reduce (sum) of dW / dA
 must reproduce the unsharded layer exactly as the multi-GPU path composes it
-(Y gathered by grouped broadcasts, dW / dA all-reduced)."""
+(Y gathered by grouped broadcasts, dW / dA all-reduced, dX
+reduce-scattered over the dst ranges)."""
 import os
 import socket
 
@@ -67,6 +68,23 @@ def _worker(rank, world, port, model, out_q):
         dWt, dAt = torch.from_numpy(dW), torch.from_numpy(dA)
         dist.all_reduce(dWt)
         dist.all_reduce(dAt)
+        if model in ("rgat", "rgcn"):
+            # dX (NEXT-2) reduce-scattered over the dst ranges (comm_reduce_rows: one in-place reduce
+            # per slice, rooted at the slice's owner): rank k's rows [b_k, b_k+1) become the full dX rows
+            if model == "rgat":
+                dX = oracle.rgat_dx(g.V, g.R, g.src, g.dst, g.etype, t.X, t.W, t.A, G, v0=v0, v1=v1)
+                dXr = oracle.rgat_dx(g.V, g.R, g.src, g.dst, g.etype, t.X, t.W, t.A, t.dY[:, :16])
+            else:
+                dX = oracle.rgcn_dx(g.V, g.R, g.src, g.dst, g.etype, t.W, G, v0=v0, v1=v1)
+                dXr = oracle.rgcn_dx(g.V, g.R, g.src, g.dst, g.etype, t.W, t.dY[:, :16])
+            dXt = torch.from_numpy(dX)
+            for k in range(world):
+                a, b = int(bounds[k]), int(bounds[k + 1])
+                sl = dXt[a:b].contiguous()
+                dist.reduce(sl, dst=k)
+                if k == rank:
+                    dXt[a:b] = sl
+            np.testing.assert_allclose(dXt[v0:v1].numpy(), dXr[v0:v1], rtol=1e-12, atol=1e-12)
         if rank == 0:
             if model == "hgt":
                 Yr, _ = oracle.hgt_forward(g.V, g.R, g.src, g.dst, g.etype, g.ntype, *hw)
