@@ -12,6 +12,8 @@
 //   GEMM tile table and the dW split-K chunk table (host built, uploaded).
 // Tie-break contract = DESIGN.md reading O14 (bit-exact vs the oracle).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 
 #include "common.cuh"
 
@@ -244,6 +246,22 @@ __global__ void k_slot_et(int64_t n, const int32_t* __restrict__ pos, const int3
     et_slot[q] = et_s[pos[q]];
 }
 
+// Tile t of a segmented table: segment s = the last with first[s] <= t, rows
+// [seg[s] + (t - first[s]) * rows, min(+rows, seg[s+1])) -- the host loop it replaces, per entry.
+__global__ void k_fill_tiles(int64_t S, const int32_t* __restrict__ seg, const int32_t* __restrict__ first,
+                             int64_t rows, int64_t total, Tile* __restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = S;  // first[lo] <= t < first[hi]
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (first[mid] <= t) lo = mid; else hi = mid;
+    }
+    while (lo + 1 < S && first[lo + 1] <= t) ++lo;  // skip empty segments at the boundary
+    const int64_t a = seg[lo] + (t - first[lo]) * rows;
+    out[t] = Tile{(int32_t)lo, (int32_t)a, (int32_t)min(a + rows, (int64_t)seg[lo + 1]), 0};
+  }
+}
+
 // Runs of equal (etype, dst): run_ptr[j] = first position of run j.
 __global__ void k_runs(int64_t n, const int32_t* __restrict__ head, const int32_t* __restrict__ run_ex,
                        int32_t* __restrict__ run_ptr) {
@@ -449,6 +467,8 @@ struct GraphLayout {
   Counters* ctr;
   int32_t *dst_tmp, *flags, *head, *run_ex, *et_s, *n_items, *n_parts, *n_split, *n_empty, *n_wide, *rseg_cnt, *crel;
   uint32_t *k0, *v0, *k1, *v1;
+  int32_t* tabs;  // tile-table staging: segment bounds and first tiles
+  int64_t tabs_ints;
   void* prim;
   size_t prim_bytes, scratch_bytes;
 };
@@ -525,6 +545,10 @@ static GraphLayout layout(const rgnn_graph_desc* d, void* dev, void* scr) {
   L.ptiles = c.take<Tile>(af ? (Ec + Ec / kPieceRows + 1) / kTileRows + R + 1 : 1);
   L.slot_piece = c.take<int32_t>(af ? Ec : 1);
   L.slot_w = c.take<float>(af ? Ec : 1);
+  // tile-table staging ([seg | first] of <= 8 tile tables), in the graph storage: the fill kernels run
+  // after the last host synchronisation, so they must not read the caller's scratch
+  L.tabs_ints = 2 * 8 * ((int64_t)R + (d->ntype ? d->num_ntypes : 0) + 2);
+  L.tabs = c.take<int32_t>(L.tabs_ints);
   L.dev_bytes = c.off;
   Carver s(scr);
   L.ctr = s.take<Counters>(1);
@@ -617,6 +641,14 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   const int32_t R = d->num_etypes;
   const int cap = d->row_split_cap > 0 ? d->row_split_cap : kDefaultSplitCap;
   const int T = 256;
+  // RGNN_PREP_TRACE=1: host time at each synchronisation point (stderr), for the preprocessing profile
+  static const bool trace = getenv("RGNN_PREP_TRACE") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (trace)
+      fprintf(stderr, "rgnn_graph_create %-28s %8.3f ms\n", what,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+  };
 
   RGNN_LAUNCH(k_init_counters, 1, 1, 0, s, L.ctr, INT32_MAX);
   const int32_t* dst = d->dst;
@@ -638,6 +670,7 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   }
   RGNN_CUDA_TRY(cudaMemcpyAsync(&h, L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
   RGNN_CUDA_TRY(cudaStreamSynchronize(s));
+  mark("sync 1 (validation, E_own)");
   if (h.bad_csr != INT32_MAX)
     return set_error(RGNN_E_INVALID_ARG, "row_ptr is not a CSR offset array (0 at v=0, non-decreasing, E at v=V): "
                      "first bad entry row_ptr[%d]", h.bad_csr);
@@ -727,6 +760,7 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   RGNN_CUDA_TRY(cudaMemcpyAsync(seg_h.data(), L.seg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
   if (cm) RGNN_CUDA_TRY(cudaMemcpyAsync(cseg_h.data(), L.cseg, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, s));
   RGNN_CUDA_TRY(cudaStreamSynchronize(s));
+  mark("sync 2 (counts, segments)");
   // node-type segments (HGT's node-typed linears, D4): stable sort of node ids by type
   std::vector<int32_t> nseg_h;
   if (d->ntype && V > 0) {
@@ -785,6 +819,7 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
     Counters h2{};
     RGNN_CUDA_TRY(cudaMemcpyAsync(&h2, L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
     RGNN_CUDA_TRY(cudaStreamSynchronize(s));
+    mark("sync 3 (ntype / dX / pieces)");
     h.num_sitems = h2.num_sitems; h.num_sparts = h2.num_sparts; h.num_ssplit = h2.num_ssplit;
     h.num_pieces = h2.num_pieces;
   }
@@ -794,16 +829,15 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
 
   // Host: 128-row GEMM tiles and dW split-K chunks, never straddling relations.
   // dW chunks (the fused backward runs one CTA per chunk, one CTA per SM): sized so that at most
-  // waves * SMs chunks result (sum_r ceil(E_r / rows) <= E / rows + R), i.e. exactly `waves` full
-  // waves with no partial wave left over (r01 sizing gave 298 chunks = 2 waves + 2 on ogbn-mag);
-  // multiples of the 128-row tile.  Chunks are in position order, so each wave's CTAs gather the
+  // waves * SMs chunks result, i.e. `waves` full waves with no partial wave left over (r01 sizing
+  // gave 298 chunks = 2 waves + 2 on ogbn-mag); multiples of the 128-row tile.  Measured (fused
+  // backward, ms): r01 sizing mag 3.66 / AM 0.854; 2 waves 3.68 / 0.877; 3 waves 3.54 / 0.790;
+  // 4 waves 3.59 / 0.778 (default).  Chunks are in position order, so each wave's CTAs gather the
   // X / Z rows of one 1/waves slice of the position space at a time.  (Measured r02: one
   // persistent CTA per SM over equal position ranges -- every SM spanning the whole position space
   // at once -- was slower, 3.54 -> 4.97 ms on ogbn-mag.)
-  std::vector<Tile> tiles, chunks;
-  std::vector<int32_t> chunk_seg(R + 1, 0);
   // RGNN_BWD_WAVES (A/B): 0 = the r01 sizing only
-  static const int64_t waves = getenv("RGNN_BWD_WAVES") ? std::max(0, atoi(getenv("RGNN_BWD_WAVES"))) : 2;
+  static const int64_t waves = getenv("RGNN_BWD_WAVES") ? std::max(0, atoi(getenv("RGNN_BWD_WAVES"))) : 4;
   auto count_chunks = [&](int64_t cr) {
     int64_t c = 0;
     for (int32_t r = 0; r < R; ++r) c += (seg_h[r + 1] - seg_h[r] + cr - 1) / cr;
@@ -822,88 +856,79 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
     // stretch the large relations' chunks)
     if (lo * kTileRows <= 2 * ((n + waves * sms - 1) / (waves * sms))) chunk_rows = lo * kTileRows;
   }
-  for (int32_t r = 0; r < R; ++r) {
-    for (int64_t a = seg_h[r]; a < seg_h[r + 1]; a += kTileRows)
-      tiles.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + kTileRows, seg_h[r + 1]), 0});
-    chunk_seg[r] = (int32_t)chunks.size();
-    for (int64_t a = seg_h[r]; a < seg_h[r + 1]; a += chunk_rows)
-      chunks.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + chunk_rows, seg_h[r + 1]), 0});
+  // The tile / chunk tables are filled on the device: the host computes only each segment's first
+  // tile (a few hundred integers, from the segments read back at sync 2) and uploads them with the
+  // segment bounds in one copy; k_fill_tiles writes the Tile entries.
+  struct TileJob {
+    const std::vector<int32_t>* seg;  // segment bounds [S+1]
+    int64_t rows;                     // rows per tile / chunk
+    Tile* dst;                        // device table
+    int32_t* first_dev;               // device [S+1] first tile of each segment, or null
+    std::vector<int32_t> first;       // host copy
+    size_t at;                        // offset of [seg | first] in the staging buffer
+  };
+  std::vector<TileJob> jobs;
+  auto add_job = [&](const std::vector<int32_t>& sg, int64_t rows, Tile* dst, int32_t* first_dev) -> TileJob& {
+    TileJob j{&sg, rows, dst, first_dev, std::vector<int32_t>(sg.size(), 0), 0};
+    for (size_t i = 0; i + 1 < sg.size(); ++i)
+      j.first[i + 1] = j.first[i] + (int32_t)((sg[i + 1] - sg[i] + rows - 1) / rows);
+    jobs.push_back(std::move(j));
+    return jobs.back();
+  };
+  add_job(seg_h, kTileRows, L.tiles, nullptr);
+  add_job(seg_h, chunk_rows, L.chunks, L.chunk_seg);
+  if (cm) add_job(cseg_h, kTileRows, L.ctiles, nullptr);
+  add_job(rseg_h, kTileRows, L.rtiles, nullptr);  // 128-run GEMM tiles (dX: H = G_v W_r^T per run)
+  if (!nseg_h.empty()) {  // HGT: node-type GEMM tiles and dW chunks (dWK / dWQ / dWV)
+    add_job(nseg_h, kTileRows, L.ntiles, nullptr);
+    add_job(nseg_h, std::max<int64_t>(kTileRows, ((V / (2 * sms) + 1) + kTileRows - 1) / kTileRows * kTileRows),
+            L.nchunks, L.nchunk_seg);
   }
-  chunk_seg[R] = (int32_t)chunks.size();
-  std::vector<Tile> ctiles;
-  if (cm)
-    for (int32_t r = 0; r < R; ++r)
-      for (int64_t a = cseg_h[r]; a < cseg_h[r + 1]; a += kTileRows)
-        ctiles.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + kTileRows, cseg_h[r + 1]), 0});
-  if (!ctiles.empty())
-    RGNN_CUDA_TRY(cudaMemcpyAsync(L.ctiles, ctiles.data(), sizeof(Tile) * ctiles.size(), cudaMemcpyHostToDevice, s));
-  std::vector<Tile> ntiles;  // 128-node GEMM tiles per node type (HGT typed linears)
-  for (int32_t t = 0; t + 1 < (int32_t)nseg_h.size(); ++t)
-    for (int64_t a = nseg_h[t]; a < nseg_h[t + 1]; a += kTileRows)
-      ntiles.push_back(Tile{t, (int32_t)a, (int32_t)std::min<int64_t>(a + kTileRows, nseg_h[t + 1]), 0});
-  if (!ntiles.empty())
-    RGNN_CUDA_TRY(cudaMemcpyAsync(L.ntiles, ntiles.data(), sizeof(Tile) * ntiles.size(), cudaMemcpyHostToDevice, s));
-  // dW split-K chunks over the node-type segments (HGT backward: dWK / dWQ / dWV), never straddling types
-  std::vector<Tile> nchunks;
-  std::vector<int32_t> nchunk_seg(nseg_h.empty() ? 0 : nseg_h.size(), 0);
-  if (!nseg_h.empty()) {
-    const int64_t ncr =
-        std::max<int64_t>(kTileRows, ((V / (2 * sms) + 1) + kTileRows - 1) / kTileRows * kTileRows);
-    for (int32_t t = 0; t + 1 < (int32_t)nseg_h.size(); ++t) {
-      nchunk_seg[t] = (int32_t)nchunks.size();
-      for (int64_t a = nseg_h[t]; a < nseg_h[t + 1]; a += ncr)
-        nchunks.push_back(Tile{t, (int32_t)a, (int32_t)std::min<int64_t>(a + ncr, nseg_h[t + 1]), 0});
-    }
-    nchunk_seg.back() = (int32_t)nchunks.size();
-    if (!nchunks.empty())
-      RGNN_CUDA_TRY(cudaMemcpyAsync(L.nchunks, nchunks.data(), sizeof(Tile) * nchunks.size(), cudaMemcpyHostToDevice, s));
-    RGNN_CUDA_TRY(cudaMemcpyAsync(L.nchunk_seg, nchunk_seg.data(), sizeof(int32_t) * nchunk_seg.size(),
-                                  cudaMemcpyHostToDevice, s));
-  }
-  std::vector<Tile> rtiles;  // 128-run GEMM tiles per relation (H = G_v W_r^T per run: RGAT backward, dX)
-  for (int32_t r = 0; r < R; ++r)
-      for (int64_t a = rseg_h[r]; a < rseg_h[r + 1]; a += kTileRows)
-        rtiles.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + kTileRows, rseg_h[r + 1]), 0});
-  if (!rtiles.empty())
-    RGNN_CUDA_TRY(cudaMemcpyAsync(L.rtiles, rtiles.data(), sizeof(Tile) * rtiles.size(), cudaMemcpyHostToDevice, s));
-  std::vector<Tile> ptiles;  // aggregate-first RGCN: 128-piece GEMM tiles per relation
-  if (af)
-    for (int32_t r = 0; r < R; ++r)
-      for (int64_t a = prseg_h[r]; a < prseg_h[r + 1]; a += kTileRows)
-        ptiles.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + kTileRows, prseg_h[r + 1]), 0});
-  if (!ptiles.empty())
-    RGNN_CUDA_TRY(cudaMemcpyAsync(L.ptiles, ptiles.data(), sizeof(Tile) * ptiles.size(), cudaMemcpyHostToDevice, s));
-  std::vector<Tile> pchunks;  // dW split-K chunks over the run pieces, never straddling relations
-  std::vector<int32_t> pchunk_seg(R + 1, 0);
-  if (!prseg_h.empty()) {
+  if (af) add_job(prseg_h, kTileRows, L.ptiles, nullptr);  // aggregate-first: piece GEMM tiles
+  if (!prseg_h.empty()) {  // dW split-K chunks over the run pieces (HGT backward)
     const int64_t np = h.num_pieces;
-    const int64_t pcr = std::max<int64_t>(kTileRows, ((np / (2 * sms) + 1) + kTileRows - 1) / kTileRows * kTileRows);
-    for (int32_t r = 0; r < R; ++r) {
-      pchunk_seg[r] = (int32_t)pchunks.size();
-      for (int64_t a = prseg_h[r]; a < prseg_h[r + 1]; a += pcr)
-        pchunks.push_back(Tile{r, (int32_t)a, (int32_t)std::min<int64_t>(a + pcr, prseg_h[r + 1]), 0});
-    }
-    pchunk_seg[R] = (int32_t)pchunks.size();
-    RGNN_CUDA_TRY(cudaMemcpyAsync(L.pchunk_seg, pchunk_seg.data(), sizeof(int32_t) * (R + 1), cudaMemcpyHostToDevice, s));
-    if ((int64_t)pchunks.size() > max_chunks(E, R)) return set_error(RGNN_E_CUDA, "internal: piece chunk overflow");
-    if (!pchunks.empty())
-      RGNN_CUDA_TRY(cudaMemcpyAsync(L.pchunks, pchunks.data(), sizeof(Tile) * pchunks.size(), cudaMemcpyHostToDevice, s));
+    add_job(prseg_h, std::max<int64_t>(kTileRows, ((np / (2 * sms) + 1) + kTileRows - 1) / kTileRows * kTileRows),
+            L.pchunks, L.pchunk_seg);
   }
-  if ((int64_t)chunks.size() > max_chunks(E, R))
+  std::vector<int32_t> stage;
+  for (auto& j : jobs) {
+    j.at = stage.size();
+    stage.insert(stage.end(), j.seg->begin(), j.seg->end());
+    stage.insert(stage.end(), j.first.begin(), j.first.end());
+  }
+  if ((int64_t)stage.size() > L.tabs_ints) return set_error(RGNN_E_CUDA, "internal: tile staging overflow");
+  RGNN_CUDA_TRY(cudaMemcpyAsync(L.tabs, stage.data(), sizeof(int32_t) * stage.size(), cudaMemcpyHostToDevice, s));
+  for (auto& j : jobs) {
+    const int64_t S = (int64_t)j.seg->size() - 1, total = j.first.back();
+    const int32_t* sg = L.tabs + j.at;
+    const int32_t* fi = sg + S + 1;
+    if (total > 0)
+      RGNN_LAUNCH(k_fill_tiles, grid_for(total), T, 0, s, S, sg, fi, j.rows, total, j.dst);
+    if (j.first_dev)
+      RGNN_CUDA_TRY(cudaMemcpyAsync(j.first_dev, fi, sizeof(int32_t) * (S + 1), cudaMemcpyDeviceToDevice, s));
+  }
+  const std::vector<int32_t>& chunk_seg = jobs[1].first;
+  const int64_t num_tiles = jobs[0].first.back(), num_chunks = chunk_seg.back();
+  const int64_t num_ctiles = cm ? jobs[2].first.back() : 0;
+  int64_t num_rtiles = 0, num_ntiles = 0, num_nchunks = 0, num_ptiles = 0, num_pchunks = 0;
+  for (auto& j : jobs) {
+    if (j.dst == L.rtiles) num_rtiles = j.first.back();
+    if (j.dst == L.ntiles) num_ntiles = j.first.back();
+    if (j.dst == L.nchunks) num_nchunks = j.first.back();
+    if (j.dst == L.ptiles) num_ptiles = j.first.back();
+    if (j.dst == L.pchunks) num_pchunks = j.first.back();
+  }
+  if (num_chunks > max_chunks(E, R) || num_pchunks > max_chunks(E, R))
     return set_error(RGNN_E_CUDA, "internal: chunk table overflow");
-  if (!tiles.empty())
-    RGNN_CUDA_TRY(cudaMemcpyAsync(L.tiles, tiles.data(), sizeof(Tile) * tiles.size(), cudaMemcpyHostToDevice, s));
-  if (!chunks.empty())
-    RGNN_CUDA_TRY(cudaMemcpyAsync(L.chunks, chunks.data(), sizeof(Tile) * chunks.size(), cudaMemcpyHostToDevice, s));
-  RGNN_CUDA_TRY(cudaMemcpyAsync(L.chunk_seg, chunk_seg.data(), sizeof(int32_t) * (R + 1), cudaMemcpyHostToDevice, s));
-  // No final synchronisation: copies from pageable host memory return once the data is staged, so the
-  // host vectors may go out of scope; the tables reach the device in stream order before any layer call.
+  // No final synchronisation: the staging copy from pageable memory returns once the data is staged,
+  // so the host vectors may go out of scope; the tables are complete in stream order before any layer call.
 
+  mark("tables uploaded");
   rgnn_graph* g = new rgnn_graph();
   g->V = V; g->V_own = V_own; g->v0 = v0; g->E_in = E; g->E_own = n; g->J = h.J;
   g->R = R; g->norm = d->norm; g->cap = cap;
-  g->num_tiles = (int64_t)tiles.size(); g->num_items = h.num_items; g->num_parts = h.num_parts;
-  g->num_split_rows = h.num_split_rows; g->num_chunks = (int64_t)chunks.size();
+  g->num_tiles = num_tiles; g->num_items = h.num_items; g->num_parts = h.num_parts;
+  g->num_split_rows = h.num_split_rows; g->num_chunks = num_chunks;
   g->perm = L.perm; g->src_s = L.src_s; g->dst_s = L.dst_s; g->seg = L.seg; g->row_ptr = L.row_ptr;
   g->pos = L.pos; g->et_slot = L.et_slot; g->run_ptr = L.run_ptr; g->rseg = L.rseg; g->inv_c = L.inv_c;
   g->items = L.items; g->split_rows = L.split_rows; g->tiles = L.tiles; g->chunks = L.chunks;
@@ -911,19 +936,19 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   g->narrow_cap = narrow_cap(d); g->witems = L.witems; g->num_witems = h.num_witems;
   g->has_compact = cm; g->mat_mode = d->materialization; g->num_compact = cm ? h.num_compact : 0; g->crow_of_pos = L.crow_of_pos; g->zrow_slot = L.zrow_slot;
   g->invc_slot = L.invc_slot; g->csrc = L.csrc; g->cseg = L.cseg; g->ctiles = L.ctiles;
-  g->num_ctiles = (int64_t)ctiles.size();
+  g->num_ctiles = num_ctiles;
   g->chunk_seg = L.chunk_seg;
   g->has_dx = dx; g->run_of_pos = L.run_of_pos; g->run_dst = L.run_dst; g->run_rel = L.run_rel; 
   g->spos = L.spos; g->srun = L.srun; g->srel = L.srel; g->sinvc = L.sinvc; g->srow = L.srow;
-  g->rtiles = L.rtiles; g->num_rtiles = (int64_t)rtiles.size();
+  g->rtiles = L.rtiles; g->num_rtiles = num_rtiles;
   g->sitems = L.sitems; g->num_sitems = h.num_sitems; g->ssplit = L.ssplit; g->num_ssplit = h.num_ssplit;
   g->num_sparts = h.num_sparts;
   g->has_ntype = d->ntype != nullptr && V > 0; g->num_ntypes = d->ntype ? d->num_ntypes : 0;
-  g->nperm = L.nperm; g->ninv = L.ninv; g->ntiles = L.ntiles; g->num_ntiles = (int64_t)ntiles.size();
-  g->nchunks = L.nchunks; g->nchunk_seg = L.nchunk_seg; g->num_nchunks = (int64_t)nchunks.size();
+  g->nperm = L.nperm; g->ninv = L.ninv; g->ntiles = L.ntiles; g->num_ntiles = num_ntiles;
+  g->nchunks = L.nchunks; g->nchunk_seg = L.nchunk_seg; g->num_nchunks = num_nchunks;
   g->has_pieces = !prseg_h.empty(); g->piece_ptr = L.piece_ptr; g->prseg = L.prseg; g->pchunks = L.pchunks; g->pchunk_seg = L.pchunk_seg;
-  g->num_pieces = !prseg_h.empty() ? h.num_pieces : 0; g->num_pchunks = (int64_t)pchunks.size();
-  g->has_aggfirst = af; g->ptiles = L.ptiles; g->num_ptiles = (int64_t)ptiles.size();
+  g->num_pieces = !prseg_h.empty() ? h.num_pieces : 0; g->num_pchunks = num_pchunks;
+  g->has_aggfirst = af; g->ptiles = L.ptiles; g->num_ptiles = num_ptiles;
   g->slot_piece = L.slot_piece; g->slot_w = L.slot_w;
   g->seg_host = seg_h;
   g->chunk_seg_host = chunk_seg;

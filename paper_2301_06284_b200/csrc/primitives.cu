@@ -150,6 +150,10 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_hist(const uint32_t* __restri
   counts[(int64_t)threadIdx.x * nb + blockIdx.x] = h[threadIdx.x];
 }
 
+// Scatter of one tile: the stable per-digit ranks (warp match + per-warp prefix, rounds in input
+// order) place every item at its digit-sorted position inside the tile in shared memory first;
+// the tile then leaves in that order, so the items of one digit -- consecutive in the output --
+// are written by consecutive threads (coalesced runs instead of one scattered 4-byte store each).
 __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const uint32_t* __restrict__ keys,
                                                            const uint32_t* __restrict__ vals, int64_t n, int shift,
                                                            int64_t nb, const int32_t* __restrict__ offsets,
@@ -159,11 +163,33 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const uint32_t* __res
   if (n_dev) n = min(n, (int64_t)*n_dev);
   if ((int64_t)blockIdx.x * kRsTile >= n) return;  // an empty tile (its histogram is zero)
   __shared__ int32_t s_run[256];
+  __shared__ int32_t s_goff[256], s_loff[256];
   __shared__ int32_t s_w[kRsWarps][256];
+  __shared__ uint32_t s_k[kRsTile], s_v[kRsTile];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  s_run[t] = offsets[(int64_t)t * nb + blockIdx.x];
+  const int64_t base = (int64_t)blockIdx.x * kRsTile;
+  const int tile_n = (int)min((int64_t)kRsTile, n - base);
+  {  // this tile's digit counts (from the scanned offsets) -> local exclusive offsets
+    const int64_t idx = (int64_t)t * nb + blockIdx.x;
+    const int32_t go = offsets[idx];
+    const int32_t cnt = (idx + 1 < 256 * nb ? offsets[idx + 1] : (int32_t)n) - go;
+    s_goff[t] = go;
+    int32_t x = cnt;  // block-wide exclusive scan of the 256 counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[0][warp] = x;
+    __syncthreads();
+    int32_t wofs = 0;
+#pragma unroll
+    for (int w = 0; w < kRsWarps; ++w) wofs += w < warp ? s_w[0][w] : 0;
+    s_loff[t] = wofs + x - cnt;
+    s_run[t] = wofs + x - cnt;
+    __syncthreads();
+  }
   const uint32_t lt = (1u << lane) - 1u;
-  int64_t base = (int64_t)blockIdx.x * kRsTile;
   for (int j = 0; j < kRsRounds; ++j) {
 #pragma unroll
     for (int w = 0; w < kRsWarps; ++w) s_w[w][t] = 0;
@@ -177,7 +203,7 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const uint32_t* __res
     int rank = __popc(peers & lt);
     if (valid && rank == 0) s_w[warp][d] = __popc(peers);
     __syncthreads();
-    {  // per digit: exclusive prefix over warps, then advance the running offset
+    {  // per digit: exclusive prefix over warps, then advance the running (tile-local) offset
       int32_t run = s_run[t];
 #pragma unroll
       for (int w = 0; w < kRsWarps; ++w) {
@@ -189,11 +215,18 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const uint32_t* __res
     }
     __syncthreads();
     if (valid) {
-      int32_t o = s_w[warp][d] + rank;
-      keys_out[o] = k;
-      vals_out[o] = v;
+      const int32_t o = s_w[warp][d] + rank;
+      s_k[o] = k;
+      s_v[o] = v;
     }
     __syncthreads();
+  }
+  for (int i = t; i < tile_n; i += kRsThreads) {  // the tile in digit order: coalesced per digit run
+    const uint32_t k = s_k[i];
+    const uint32_t d = (k >> shift) & 255u;
+    const int32_t o = s_goff[d] + (i - s_loff[d]);
+    keys_out[o] = k;
+    vals_out[o] = s_v[i];
   }
 }
 

@@ -66,9 +66,14 @@ static inline void watchdog_init() {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   if (mbar_try(b, parity)) return;
-  const uint64_t t0 = global_ns();
-  while (!mbar_try_sleep(b, parity)) {
-    if (global_ns() - t0 > g_watchdog_ns) {
+  // the timer is read every 64 wake-ups only: r02 ncu showed the waits' loop instructions (timer
+  // read, address conversion) at ~17% of the fused backward's executed instructions
+  uint64_t t0 = 0;
+  for (uint32_t n = 1; !mbar_try_sleep(b, parity); ++n) {
+    if ((n & 63) != 0) continue;
+    const uint64_t t = global_ns();
+    if (t0 == 0) t0 = t;
+    if (t - t0 > g_watchdog_ns) {
       printf("rgnn watchdog: block %d thread %d stuck on mbarrier smem+0x%x parity %u\n", blockIdx.x, threadIdx.x,
              smem_u32(b), parity);
       __trap();
