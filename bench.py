@@ -60,7 +60,7 @@ def parse():
                          "at N=1 a one-rank communicator exercises the same path)")
     ap.add_argument("--materialization", default="auto", choices=["vanilla", "compact", "auto"],
                     help="per-edge (vanilla) or per-(etype, src) (compact, PAPER.md P:513-531) Z / s_src rows; "
-                         "auto = compact when U <= E/2")
+                         "auto = compact when U < E (RGCN) / U <= 3E/4 (RGAT)")
     return ap.parse_args()
 
 
@@ -584,40 +584,49 @@ def run_ours(args):
         oloss = torch.empty(1, dtype=torch.float32).pin_memory()
         nll_scale = 1.0 / g.V  # mean over all V rows (every rank owns a slice)
 
-        # X (the large input) is double-buffered: step i+1's X is copied in on a side stream while
-        # step i runs (both copies stay inside the timed region: one X upload per timed step)
-        xbufs = [dX_, torch.empty_like(dX_)]
+        # All of a step's inputs (X, the weights, the labels) are double-buffered: step i+1's inputs are
+        # copied in on a side stream while step i runs (one upload per timed step, inside the timed
+        # region).  The small copies go first and the whole set is awaited with one event, so no
+        # small per-step copy queues behind the 0.5 GB X copy on the host-to-device engine.
         s_up = torch.cuda.Stream(dev)
         ev_up = [torch.cuda.Event(), torch.cuda.Event()]
+        ibuf = [{"X": dX_, "W": dW_, "A": dA_, "lab": dlab, "HW": dHW if model == "hgt" else None},
+                {"X": torch.empty_like(dX_), "W": torch.empty_like(dW_), "A": torch.empty_like(dA_),
+                 "lab": torch.empty_like(dlab),
+                 "HW": [torch.empty_like(a) for a in dHW] if model == "hgt" else None}]
         tstate = {"i": 0}
-        with torch.cuda.stream(s_up):
-            xbufs[0].copy_(hX, non_blocking=True)
-            ev_up[0].record(s_up)
+
+        def upload(b):
+            with torch.cuda.stream(s_up):
+                b["lab"].copy_(hlab, non_blocking=True)
+                if model == "hgt":
+                    for a, h in zip(b["HW"], hHW):
+                        a.copy_(h, non_blocking=True)
+                else:
+                    b["W"].copy_(hW, non_blocking=True)
+                    b["A"].copy_(hA, non_blocking=True)
+                b["X"].copy_(hX, non_blocking=True)
+
+        upload(ibuf[0])
+        ev_up[0].record(s_up)
 
         def train_step():
             main = torch.cuda.current_stream(dev)
             i = tstate["i"]
-            cur, nxt = xbufs[i % 2], xbufs[(i + 1) % 2]
-            main.wait_event(ev_up[i % 2])          # this step's X has landed
-            s_up.wait_stream(main)                 # (the previous step, which read nxt, is done)
-            with torch.cuda.stream(s_up):
-                nxt.copy_(hX, non_blocking=True)   # next step's X under this step's compute
-                ev_up[(i + 1) % 2].record(s_up)
+            cb, nb = ibuf[i % 2], ibuf[(i + 1) % 2]
+            main.wait_event(ev_up[i % 2])          # this step's inputs have landed
+            s_up.wait_stream(main)                 # (the previous step, which read nb, is done)
+            upload(nb)                             # next step's inputs under this step's compute
+            ev_up[(i + 1) % 2].record(s_up)
             tstate["i"] = i + 1
-            dlab.copy_(hlab, non_blocking=True)
-            if model == "hgt":
-                for a, b in zip(dHW, hHW):
-                    a.copy_(b, non_blocking=True)
-            else:
-                dW_.copy_(hW, non_blocking=True)
-                dA_.copy_(hA, non_blocking=True)
-            fwd(cur, dW_, dA_, HWs=dHW if model == "hgt" else None)
+            cur, dW_c, dA_c, dlab_c, dHW_c = cb["X"], cb["W"], cb["A"], cb["lab"], cb["HW"]
+            fwd(cur, dW_c, dA_c, HWs=dHW_c)
             lp = torch.log_softmax(Y, dim=1)
-            loss = -lp.gather(1, dlab.view(-1, 1)).sum() * nll_scale
+            loss = -lp.gather(1, dlab_c.view(-1, 1)).sum() * nll_scale
             dyy = lp.exp_()
-            dyy[torch.arange(dyy.shape[0], device=dev), dlab] -= 1.0
+            dyy[torch.arange(dyy.shape[0], device=dev), dlab_c] -= 1.0
             dyy.mul_(nll_scale)
-            bwd(cur, dW_, dA_, dyy, HWs=dHW if model == "hgt" else None)
+            bwd(cur, dW_c, dA_c, dyy, HWs=dHW_c)
             oloss.copy_(loss.view(1), non_blocking=True)
             if model == "hgt":
                 for o, gr in zip(ohg, hgrads):
@@ -637,8 +646,8 @@ def run_ours(args):
                "d2h_bytes_per_step": int(d2h_t), "steps": n_e2e,
                "protocol": "training step (P:843): X, weights and random labels in; forward; NLL(log_softmax(Y)) "
                            "loss and dY on the device (torch, the caller's loss); backward; loss and weight "
-                           "gradients out; X double-buffered (step i+1's X is copied in on a side stream during "
-                           "step i, one X upload per timed step)"
+                           "gradients out; inputs double-buffered (step i+1's X, weights and labels are copied in "
+                           "on a side stream during step i, one upload per timed step)"
                            + ("; dX not computed" if not args.dx else "; dX computed, not copied out"),
                "layer_io": e2e_io}
 
@@ -663,9 +672,18 @@ def run_ours(args):
             traffic = tj.get(f"{cfg.name}:{model}:{prec}:{mat}:{dom}")
         except Exception:
             pass
+        # compact-minimal bytes (the fused RGAT backward on compact rows: x_src per edge, each unique Z
+        # row once, the per-run rows) and the DRAM fraction of the ncu traffic -- the two other views of
+        # the same launch
+        b_ = 2 if prec == "bf16" else 4
+        minimal = byts
+        if dom == "bwd_fused" and model == "rgat" and zr != int(v.E_own):
+            minimal = int(v.E_own) * (K * b_ + 16) + zr * N * b_ + int(v.num_runs) * (8 * N + K * b_ + 4)
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                 "traffic": traffic, "algorithmic_bytes_per_launch": int(byts), "launch_ms": per_launch_ms,
-                "peak_source": peak_src}
+                "peak_source": peak_src, "minimal_bytes_per_launch": int(minimal),
+                "minimal_frac": minimal / (per_launch_ms * 1e-3) / 1e9 / hbm,
+                "dram_frac": (traffic / (per_launch_ms * 1e-3) / 1e9 / hbm) if traffic else None}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:  # rank 0 only (the other ranks wait at the final barrier)

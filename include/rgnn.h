@@ -72,8 +72,8 @@ typedef enum { RGNN_RGCN = 0, RGNN_RGAT = 1, RGNN_HGT = 2 } rgnn_model;
  * (reading O15); the typed GEMM then runs over U_src rows instead of E.     */
 /* AUTO: the compact tables are built, and each layer call picks per model:
  * RGCN compact whenever U < E_own (its backward never reads Z); RGAT compact
- * when U <= E_own / 2 (its backward then gathers Z rows at random instead of
- * streaming them -- measured r01: ogbn-mag U/E = 0.15 wins, AM 0.56 loses).
+ * when U <= 3/4 E_own (its backward then gathers Z rows at random instead of
+ * streaming them -- measured r02: ogbn-mag U/E = 0.15 and AM 0.56 win).
  * rgnn_zrows() reports the choice.                                          */
 typedef enum { RGNN_MAT_VANILLA = 0, RGNN_MAT_COMPACT = 1, RGNN_MAT_AUTO = 2 } rgnn_materialization;
 

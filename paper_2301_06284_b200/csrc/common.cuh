@@ -62,7 +62,7 @@ constexpr int kTileRows = 128;       // GEMM M tile (rows of Z per tile)
 constexpr int kPieceRows = 64;       // HGT backward: run pieces hold <= 64 positions
 constexpr int kDefaultSplitCap = 256; // max in-edges per traversal work item
 #ifndef RGNN_NARROW_CAP
-#define RGNN_NARROW_CAP 8
+#define RGNN_NARROW_CAP 16  // measured r02 (aggregate ms, AM / ogbn-mag): 4: 0.617 / 1.898; 8: 0.590 / 1.824; 16: 0.585 / 1.789; 32: 0.584 / 1.822
 #endif
 constexpr int kNarrowCap = RGNN_NARROW_CAP;  // forward walk: rows with <= this many in-edges go one per lane group
 
@@ -150,7 +150,9 @@ inline bool use_compact(const rgnn_graph* g, int model) {
   if (!g->has_compact) return false;
   if (g->mat_mode == RGNN_MAT_COMPACT) return true;
   // RGCN / HGT forward-only use of the rows: compact whenever it saves rows
-  return model == RGNN_RGAT ? 2 * g->num_compact <= g->E_own : g->num_compact < g->E_own;
+  // RGAT: compact when U <= 3/4 E_own (measured r02 with the 4-wave backward: AM, U/E = 0.56, 1.83 ->
+  // 1.71 ms/step compact; r01 had the cut at 1/2, when AM measured 0.07 ms slower compact)
+  return model == RGNN_RGAT ? 4 * g->num_compact <= 3 * g->E_own : g->num_compact < g->E_own;
 }
 
 

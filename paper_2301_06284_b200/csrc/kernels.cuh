@@ -52,7 +52,8 @@ rgnn_status launch_gemm_fwd(int prec, int K, int N, const GemmFwdArgs& a, cudaSt
 rgnn_status launch_gemm_dw(int prec, int K, int N, const GemmDwArgs& a, cudaStream_t s);
 rgnn_status launch_dw_reduce(int prec, int K, int N, int R, int64_t num_chunks, const int32_t* chunk_seg,
                              const float* part, const int32_t* cseg, const float* cpart, const float* A,
-                             const float* W, float* dW, float* dA, float* dA_scratch /* [R*2*K] */, cudaStream_t s);
+                             const float* W, float* dW, float* dA, float* dA_scratch /* [R*2*K] */, cudaStream_t s,
+                             const Tile* chunks = nullptr);
 rgnn_status launch_dst_term(int prec, int K, const rgnn_graph* g, const float* dpre, const void* X, float* cpart,
                             cudaStream_t s);
 // U[r] = W_r A[r, half] (half = 1: the destination fold of the forward; 0: the source half, dX)

@@ -697,7 +697,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     if (fst == RGNN_OK) {
       Phase ph("dw_reduce", s);
       RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, g->chunk_seg, w.cpart, A, W,
-                                dW, dA, w.vsum, s));
+                                dW, dA, w.vsum, s, g->chunks));
     } else {
     BwdArgs ba{};
     ba.items = g->items; ba.num_items = g->num_items; ba.pos = g->pos; ba.et_slot = g->et_slot; ba.Z = sv.Z;
@@ -708,7 +708,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     { Phase ph("dst_term", s); RGNN_TRY(launch_dst_term(prec, K, g, w.dpre, X, w.cpart, s)); }
     da.Bz = w.dZ; da.dpre = w.dpre; da.dst_local = g->dst_s; da.v0 = g->v0;
     { Phase ph("gemm_dw", s); RGNN_TRY(dw_gemm(da)); }
-    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, g->chunk_seg, w.cpart, A, W, dW, dA, w.vsum, s)); }
+    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, g->chunk_seg, w.cpart, A, W, dW, dA, w.vsum, s, g->chunks)); }
     }
   } else {
     rgnn_status fst = RGNN_E_UNSUPPORTED;
@@ -727,7 +727,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
       }
       { Phase ph("gemm_dw", s); RGNN_TRY(dw_gemm(da)); }
     }
-    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, nullptr, nullptr, nullptr, nullptr, dW, nullptr, nullptr, s)); }
+    { Phase ph("dw_reduce", s); RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, nullptr, nullptr, nullptr, nullptr, dW, nullptr, nullptr, s, g->chunks)); }
     if (dW0) {
       Phase ph("gemm_dw0", s);
       GemmDwArgs d0{};

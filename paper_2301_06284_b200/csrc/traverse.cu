@@ -299,6 +299,9 @@ __device__ __forceinline__ void narrow_rows_pipe(const AggArgs& a, int64_t warp0
   }
 }
 
+#ifndef RGNN_NARROW_UN
+#define RGNN_NARROW_UN 4  // RGAT narrow walk: edges per lane-group step (8 measured slower: AM 0.59 -> 0.73 ms)
+#endif
 // The same walk without the cross-row-group pipeline (measured faster for RGAT, whose per-row
 // x_dst slice and per-edge U dot make the pipelined version spill or lose a resident block:
 // AM 0.354 vs 0.402 ms; RGCN gains from the pipeline: wikikg2 walk 1.00 -> 0.77 ms).
@@ -306,7 +309,7 @@ template <typename T, int K, int N, bool RGAT>
 __device__ __forceinline__ void narrow_rows(const AggArgs& a, int64_t warp0, int64_t nwarps, int lane) {
   using S = WalkShape<T, K, N>;
   constexpr int EPL = S::EPL, L = S::L, G = S::G, KPL = S::KPL;
-  constexpr int UN = L < 4 ? L : 4;  // edges per group step
+  constexpr int UN = L < RGNN_NARROW_UN ? L : RGNN_NARROW_UN;  // edges per group step
   const T* Z = static_cast<const T*>(a.Z);
   const T* X = static_cast<const T*>(a.X);
   const int g = lane / L, l = lane % L;
@@ -409,8 +412,11 @@ __device__ __forceinline__ void narrow_rows(const AggArgs& a, int64_t warp0, int
 
 // resident blocks: RGAT 4 (64 registers, simple walk), RGCN 3 (80 registers, pipelined walk; 4
 // spilled ~150 B at d = 64)
+#ifndef RGNN_NARROW_MINB_RGAT
+#define RGNN_NARROW_MINB_RGAT 4
+#endif
 template <typename T, int K, int N, bool RGAT>
-__global__ void __launch_bounds__(256, RGAT ? 4 : 3) k_aggregate_narrow(AggArgs a) {
+__global__ void __launch_bounds__(256, RGAT ? RGNN_NARROW_MINB_RGAT : 3) k_aggregate_narrow(AggArgs a) {
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   if constexpr (RGAT) narrow_rows<T, K, N, RGAT>(a, w0, nw, threadIdx.x & 31);
   else narrow_rows_pipe<T, K, N, RGAT>(a, w0, nw, threadIdx.x & 31);
