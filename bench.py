@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--dx", action="store_true", help="also compute the input-feature gradient dX (NEXT-2)")
     ap.add_argument("--aggregate-first", action="store_true",
                     help="RGCN: aggregate-first forward (NEXT-4: run-piece sums of x_src, GEMM over the pieces)")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
+                    help="N>1: NCCL collectives, or the peer-memory communicator (CUDA IPC; the walk stores Y rows "
+                         "into every rank's Y_full itself, device-side barrier)")
     ap.add_argument("--gather-sync", action="store_true", help="N>1: gather Y on the caller's stream (no overlap)")
     ap.add_argument("--gather-bf16", action="store_true", help="N>1: gather Y_full in bf16 (half the volume)")
     ap.add_argument("--comm-variants", action="store_true",
@@ -316,8 +319,13 @@ def run_ours(args):
          else torch.empty(v1 - v0, N, dtype=torch.float32, device=dev))
     dW = torch.empty(g.R, K, N, dtype=torch.float32, device=dev)
     dA = torch.empty(g.R, 2, N, dtype=torch.float32, device=dev) if model == "rgat" else None
-    comm = m.Comm(bounds, rank, world) if use_comm else None
-    if comm is not None:
+    comm = None
+    if use_comm and args.comm == "peer":
+        if gather_bf16:
+            raise SystemExit("--gather-bf16 does not apply to --comm peer (fp32 Y_full)")
+        comm = m.PeerComm(bounds, rank, world, Y_full, g.R * K * N + g.R * 2 * N + K * N)
+    elif use_comm:
+        comm = m.Comm(bounds, rank, world)
         comm.set_options(gather_async=not args.gather_sync, gather_bf16=gather_bf16)
     stream = torch.cuda.current_stream(dev)
 
@@ -486,6 +494,12 @@ def run_ours(args):
                 comm.set_options(gather_async=not args.gather_sync, gather_bf16=gather_bf16)
 
         yb = (g.V * N * 4, g.V * N * 2)
+        if args.comm == "peer":
+            multi = {"compute_only_ms": variant(False, False, with_gather=False),
+                     "peer_fused_gather_ms": variant(False, False),
+                     "y_gather_bytes_per_rank": {"fp32": int(yb[0] * (world - 1) / max(world, 1))},
+                     "steps": nvar, "launch": "eager", "default": "peer-memory (walk epilogue stores + barrier)"}
+    if comm is not None and args.comm != "peer":
         multi = {"compute_only_ms": variant(True, gather_bf16, with_gather=False),
                  "gather_sync_ms": variant(False, False), "gather_overlapped_ms": variant(True, False),
                  "gather_overlapped_bf16_ms": variant(True, True),

@@ -275,6 +275,30 @@ void rgnn_comm_destroy(rgnn_comm* c);
 rgnn_status rgnn_comm_set_options(rgnn_comm* c, int flags);
 rgnn_status rgnn_comm_join(rgnn_comm* c, void* stream);
 
+/* Peer-memory communicator ("P2P stores fused into the N-K2 epilogue"; no
+ * NCCL).  One process per GPU; the buffers of every rank are mapped into every process with CUDA
+ * IPC, so a forward's walk kernels store each finished Y row straight into every rank's Y_full (the
+ * transfer overlaps the rest of the walk; NVLink stores on a multi-GPU box) and a device-side
+ * barrier (signal words, release / acquire at system scope) ends the call: Y_full is complete on
+ * every rank in stream order, with no host synchronisation (CUDA-graph capturable).  An entry
+ * barrier before the first peer store orders it after everything each rank did with its Y_full
+ * earlier in its stream.  dW / dA / dW0
+ * are all-reduced through the staging buffers (each rank sums all ranks' partials in rank order:
+ * bit-identical on every rank).  Y_full is fp32 (the gather options above do not apply); dX is not
+ * supported (RGNN_E_UNSUPPORTED; use NCCL).  Ranks may share one GPU (tests).
+ *   rgnn_comm_create_local: the communicator without transport (nranks <= 8).  [host]
+ *   rgnn_ipc_export: the IPC handle [host, 64 B] of the allocation holding `ptr` and ptr's offset in it.
+ *   rgnn_comm_attach_peers: `handles` [host, nranks x 3 x 64 B] and `offsets` [host, nranks x 3]
+ *     are every rank's exports of (Y_full, sig, stage) in rank order (exchanged by the caller, e.g.
+ *     torch.distributed); Y_full [V, d_out] fp32, sig >= 9 uint32 zeroed before first use, stage
+ *     >= the gradient floats of one backward (R*d_in*d_out + R*2*d_out + d_in*d_out) -- all
+ *     caller-owned, alive for the communicator's life.  SYNC (opens the mappings).              */
+rgnn_status rgnn_comm_create_local(int nranks, int rank, const int64_t* bounds /* [host] nranks+1 */,
+                                   rgnn_comm** out);
+rgnn_status rgnn_ipc_export(const void* ptr, void* handle /* [host] 64 B */, int64_t* offset /* [host] */);
+rgnn_status rgnn_comm_attach_peers(rgnn_comm* c, const void* handles, const int64_t* offsets, float* Y_full,
+                                   uint32_t* sig, float* stage, size_t stage_floats);
+
 /* Balanced dst-range cut from the global in-degree prefix (host helper):
  * bounds[k] = the v whose indeg_prefix[v] is closest to k*E/P (ties -> the
  * smaller v), nondecreasing, bounds[0] = 0, bounds[P] = V.  Deterministic.

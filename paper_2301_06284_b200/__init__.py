@@ -7,5 +7,5 @@ missing; there is no CPU or eager-PyTorch fallback.
 from . import _binding  # noqa: F401  (loads librgnn.so or raises)
 from ._binding import (RGNN_BF16, RGNN_F32, RGNN_NORM_EDGE, RGNN_NORM_NONE,  # noqa: F401
                        RGNN_NORM_REL_INDEG, RGNN_RGAT, RGNN_RGCN, RgnnError, launch_count, version)
-from .layer import (Comm, Graph, Workspace, hgt_backward, hgt_forward, partition_dst, rgat_forward, rgcn_forward,  # noqa: F401
-                    rgnn_backward)
+from .layer import (Comm, Graph, PeerComm, Workspace, hgt_backward, hgt_forward, partition_dst, rgat_forward,  # noqa: F401, E501
+                    rgcn_forward, rgnn_backward)

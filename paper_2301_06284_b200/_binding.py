@@ -71,6 +71,9 @@ _SIGS = {
     "rgnn_comm_unique_id": [_vp],
     "rgnn_comm_create": [_vp, C.c_int, C.c_int, C.POINTER(_i64), C.POINTER(_vp)],
     "rgnn_comm_set_options": [_vp, C.c_int],
+    "rgnn_comm_create_local": [C.c_int, C.c_int, C.POINTER(_i64), C.POINTER(_vp)],
+    "rgnn_ipc_export": [_vp, _vp, C.POINTER(_i64)],
+    "rgnn_comm_attach_peers": [_vp, _vp, C.POINTER(_i64), _vp, _vp, _vp, _sz],
     "rgnn_comm_join": [_vp, _vp],
     "rgnn_partition_dst": [_i64, C.POINTER(_i64), C.c_int, C.POINTER(_i64)],
     "rgnn_zrows": [_vp, C.c_int, C.POINTER(_i64)],

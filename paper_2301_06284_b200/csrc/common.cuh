@@ -61,6 +61,8 @@ struct Carver {
 constexpr int kTileRows = 128;       // GEMM M tile (rows of Z per tile)
 constexpr int kPieceRows = 64;       // HGT backward: run pieces hold <= 64 positions
 constexpr int kDefaultSplitCap = 256; // max in-edges per traversal work item
+constexpr int kMaxRanks = 8;           // peer-memory communicator: ranks (one GPU each)
+constexpr int kMaxPeers = kMaxRanks - 1;
 #ifndef RGNN_NARROW_CAP
 #define RGNN_NARROW_CAP 16  // measured r02 (aggregate ms, AM / ogbn-mag): 4: 0.617 / 1.898; 8: 0.590 / 1.824; 16: 0.585 / 1.789; 32: 0.584 / 1.822
 #endif

@@ -89,6 +89,10 @@ struct AggArgs {
   int narrow;
   const Item* witems;
   int64_t num_witems;
+  // peer-memory gather (rgnn_comm_create_local + attach): every finished Y row is also stored into
+  // these ranks' Y_full (global row v0 + row), from the walk's own epilogue
+  float* peer_y[kMaxPeers];
+  int npeer;
 };
 rgnn_status launch_aggregate(int prec, int K, int N, bool rgat, const AggArgs& a, cudaStream_t s);
 // Aggregate-first RGCN (NEXT-4, aggfirst.cu): A_i = sum_{p in piece i} inv_c[p] X[src_s[p]], fp32 rows.

@@ -12,6 +12,10 @@ bool tc_disabled();
 rgnn_status comm_check_range(const rgnn_comm* c, int64_t v0, int64_t v1);
 rgnn_status comm_gather_rows(rgnn_comm* c, const float* Y_own, int64_t N, void* Y_full, cudaStream_t s);
 rgnn_status comm_reduce_rows(rgnn_comm* c, float* buf, int64_t K, cudaStream_t s);
+int comm_peer_rows(const rgnn_comm* c, float** out);
+bool comm_is_ipc(const rgnn_comm* c);
+rgnn_status comm_peer_gather(rgnn_comm* c, const float* Y_own, int64_t N, float* Y_full, bool fused, cudaStream_t s);
+rgnn_status comm_peer_barrier(rgnn_comm* c, cudaStream_t s);
 rgnn_status comm_allreduce_sum(rgnn_comm* c, float* const* bufs, const size_t* counts, int n, cudaStream_t s);
 
 struct WsLayout {
@@ -256,6 +260,15 @@ static rgnn_status forward(const rgnn_graph* g, int model, int K, int N, int pre
   aa.num_split_rows = g->num_split_rows; aa.empty_rows = g->empty_rows; aa.num_empty = g->num_empty;
   aa.row_ptr = g->row_ptr; aa.V_own = g->V_own; aa.narrow = g->narrow_cap; aa.witems = g->witems;
   aa.num_witems = g->num_witems;
+  // peer-memory communicator: the walk stores every finished Y row into the peers' Y_full itself
+  const bool peer_fused = comm && Y_full && comm_is_ipc(comm);
+  if (peer_fused) {
+    aa.npeer = comm_peer_rows(comm, aa.peer_y);
+    // entry barrier: every rank has reached this call, so whatever it did with its Y_full before
+    // (stream-ordered) is finished before any rank stores into it
+    Phase ph("comm", s);
+    RGNN_TRY(comm_peer_barrier(comm, s));
+  }
   static const int cache_env = getenv("RGNN_DST_CACHE") ? atoi(getenv("RGNN_DST_CACHE")) : -1;
   aa.cache_dst = cache_env >= 0 ? cache_env != 0 : g->E_own >= 4 * std::max<int64_t>(g->J, 1);  // mean run >= 4
   if (model == RGNN_RGAT) {
@@ -307,7 +320,13 @@ static rgnn_status forward(const rgnn_graph* g, int model, int K, int N, int pre
     aa.Z = w.Z;
     { Phase ph("aggregate", s); RGNN_TRY(launch_aggregate(prec, K, N, false, aa, s)); }
   }
-  if (comm && Y_full) { Phase ph("comm", s); RGNN_TRY(comm_gather_rows(comm, Y, N, Y_full, s)); }
+  if (peer_fused) {  // rows already in the peers' Y_full: own slice + device barrier
+    Phase ph("comm", s);
+    RGNN_TRY(comm_peer_gather(comm, Y, N, Y_full, true, s));
+  } else if (comm && Y_full) {
+    Phase ph("comm", s);
+    RGNN_TRY(comm_gather_rows(comm, Y, N, Y_full, s));
+  }
   return RGNN_OK;
 }
 

@@ -149,6 +149,24 @@ __device__ __forceinline__ void mul_acc(float* acc, float f) {
   }
 }
 
+// A finished 16-byte slice of Y row `row` (local): the owned rows, and -- peer-memory gather -- the
+// same slice of every peer's Y_full, stored from the walk's epilogue (the transfer overlaps the
+// rest of the walk; NVLink stores on a multi-GPU box).
+#ifndef RGNN_PEER_STORES
+#define RGNN_PEER_STORES 1  // 0: build without the fused peer stores (A/B of their cost on one GPU)
+#endif
+template <int N>
+__device__ __forceinline__ void put_y(const AggArgs& a, int64_t row, int col, uint4 v) {
+  stg16(a.Y + (size_t)row * N + col, v);
+  if (RGNN_PEER_STORES)
+    for (int p = 0; p < a.npeer; ++p) stg16(a.peer_y[p] + (size_t)(a.v0 + row) * N + col, v);
+}
+// writers into peer memory fence their stores before the kernel ends (the barrier that follows
+// releases them to the peers)
+__device__ __forceinline__ void peer_fence(const AggArgs& a) {
+  if (a.npeer) __threadfence_system();
+}
+
 // Narrow rows (deg <= a.narrow, never split): one lane group (L lanes, one 16-byte slice of a
 // Z row each) per row, G consecutive row ids per warp step, UN edges per group step and one
 // online state per row -- no cross-group merge, so short rows cost a quarter (d = 64 bf16) or
@@ -280,7 +298,6 @@ __device__ __forceinline__ void narrow_rows_pipe(const AggArgs& a, int64_t warp0
         }
       }
     }
-    float* y = a.Y + (size_t)row * N + l * EPL;
     if constexpr (RGAT) {
       const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
 #pragma unroll
@@ -294,7 +311,7 @@ __device__ __forceinline__ void narrow_rows_pipe(const AggArgs& a, int64_t warp0
     }
 #pragma unroll
     for (int i = 0; i < EPL; i += 4)
-      stg16(y + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]), __float_as_uint(acc[i + 2]),
+      put_y<N>(a, row, l * EPL + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]), __float_as_uint(acc[i + 2]),
                               __float_as_uint(acc[i + 3])));
   }
 }
@@ -391,7 +408,6 @@ __device__ __forceinline__ void narrow_rows(const AggArgs& a, int64_t warp0, int
         }
       }
     }
-    float* y = a.Y + (size_t)row * N + l * EPL;
     if constexpr (RGAT) {
       const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
 #pragma unroll
@@ -405,7 +421,7 @@ __device__ __forceinline__ void narrow_rows(const AggArgs& a, int64_t warp0, int
     }
 #pragma unroll
     for (int i = 0; i < EPL; i += 4)
-      stg16(y + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]), __float_as_uint(acc[i + 2]),
+      put_y<N>(a, row, l * EPL + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]), __float_as_uint(acc[i + 2]),
                               __float_as_uint(acc[i + 3])));
   }
 }
@@ -420,6 +436,7 @@ __global__ void __launch_bounds__(256, RGAT ? RGNN_NARROW_MINB_RGAT : 3) k_aggre
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   if constexpr (RGAT) narrow_rows<T, K, N, RGAT>(a, w0, nw, threadIdx.x & 31);
   else narrow_rows_pipe<T, K, N, RGAT>(a, w0, nw, threadIdx.x & 31);
+  peer_fence(a);
 }
 
 // 4 resident blocks (64 registers): measured r01 on ogbn-mag d=128, the walk is
@@ -561,8 +578,7 @@ __global__ void __launch_bounds__(256, RGNN_AGG_MINB) k_aggregate(AggArgs a) {
     }
     if (g == 0) {
       if (it.part < 0) {
-        float* y = a.Y + (size_t)it.row * N + l * EPL;
-        if constexpr (RGAT) {
+            if constexpr (RGAT) {
           const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
 #pragma unroll
           for (int i = 0; i < EPL; ++i) acc[i] *= inv;
@@ -574,7 +590,7 @@ __global__ void __launch_bounds__(256, RGNN_AGG_MINB) k_aggregate(AggArgs a) {
           for (int i = 0; i < EPL; ++i) acc[i] += z0[i];
         }
 #pragma unroll
-        for (int i = 0; i < EPL; i += 4) stg16(y + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]),
+        for (int i = 0; i < EPL; i += 4) put_y<N>(a, it.row, l * EPL + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]),
                                                                  __float_as_uint(acc[i + 2]), __float_as_uint(acc[i + 3])));
       } else {
         float* pp = a.part + (size_t)it.part * (N + 4);
@@ -585,6 +601,7 @@ __global__ void __launch_bounds__(256, RGNN_AGG_MINB) k_aggregate(AggArgs a) {
       }
     }
   }
+  peer_fence(a);
 }
 
 // Same computation as k_aggregate with a per-warp cp.async ring: the Z-row
@@ -746,8 +763,7 @@ __global__ void __launch_bounds__(256) k_aggregate_ring(AggArgs a) {
     }
     if (g == 0) {
       if (it.part < 0) {
-        float* y = a.Y + (size_t)it.row * N + l * EPL;
-        if constexpr (RGAT) {
+            if constexpr (RGAT) {
           const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
 #pragma unroll
           for (int i = 0; i < EPL; ++i) acc[i] *= inv;
@@ -759,7 +775,7 @@ __global__ void __launch_bounds__(256) k_aggregate_ring(AggArgs a) {
           for (int i = 0; i < EPL; ++i) acc[i] += z0[i];
         }
 #pragma unroll
-        for (int i = 0; i < EPL; i += 4) stg16(y + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]),
+        for (int i = 0; i < EPL; i += 4) put_y<N>(a, it.row, l * EPL + i, make_uint4(__float_as_uint(acc[i]), __float_as_uint(acc[i + 1]),
                                                                  __float_as_uint(acc[i + 2]), __float_as_uint(acc[i + 3])));
       } else {
         float* pp = a.part + (size_t)it.part * (N + 4);
@@ -771,6 +787,7 @@ __global__ void __launch_bounds__(256) k_aggregate_ring(AggArgs a) {
     }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
+  peer_fence(a);
 }
 
 // Combine the partial states of each split row: one block per split row, warp w
@@ -875,8 +892,12 @@ __global__ void __launch_bounds__(512) k_merge(AggArgs a) {
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     const int n = lane + 32 * i;
-    if (n < N) y[n] = acc[i];
+    if (n < N) {
+      y[n] = acc[i];
+      for (int p = 0; p < a.npeer; ++p) a.peer_y[p][(size_t)(a.v0 + sr.row) * N + n] = acc[i];
+    }
   }
+  peer_fence(a);
 }
 
 template <typename T, int K, int N>
@@ -983,8 +1004,10 @@ __global__ void __launch_bounds__(256) k_empty_rows(AggArgs a) {
       v = make_float4(to_f(z[0]), to_f(z[1]), to_f(z[2]), to_f(z[3]));
     }
     reinterpret_cast<float4*>(a.Y + (size_t)row * N)[c] = v;
+    for (int p = 0; p < a.npeer; ++p) reinterpret_cast<float4*>(a.peer_y[p] + (size_t)(a.v0 + row) * N)[c] = v;
     if (a.lse && c == 0) a.lse[row] = -CUDART_INF_F;
   }
+  peer_fence(a);
 }
 
 static unsigned warps_grid(int64_t items) {

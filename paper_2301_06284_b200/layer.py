@@ -185,6 +185,45 @@ class Comm:
             self._handle = None
 
 
+class PeerComm(Comm):
+    """Peer-memory communicator (rgnn_comm_create_local + rgnn_ipc_export + rgnn_comm_attach_peers):
+    every rank's Y_full, signal words and gradient staging buffer are mapped into every process with
+    CUDA IPC; the handles are exchanged over the torch.distributed group (any backend, e.g. gloo).
+    The forward's walk then stores each finished Y row into every rank's Y_full itself."""
+
+    def __init__(self, bounds, rank: int, world: int, Y_full: torch.Tensor, grad_floats: int, group=None):
+        import torch.distributed as dist
+        b = (C.c_int64 * (world + 1))(*[int(x) for x in bounds])
+        h = C.c_void_p()
+        B.call("rgnn_comm_create_local", world, rank, b, C.byref(h))
+        self._handle = h
+        self.bounds = [int(x) for x in bounds]
+        dev = Y_full.device
+        self.Y_full = Y_full
+        self.sig = torch.zeros(16, dtype=torch.int32, device=dev)       # signal words + epoch
+        self.stage = torch.empty(max(int(grad_floats), 1), dtype=torch.float32, device=dev)
+        torch.cuda.synchronize(dev)
+        mine = []
+        for t in (self.Y_full, self.sig, self.stage):
+            hb = (C.c_char * 64)()
+            off = C.c_int64()
+            B.call("rgnn_ipc_export", _ptr(t), C.cast(hb, C.c_void_p), C.byref(off))
+            mine.append((bytes(hb), int(off.value)))
+        allx = [None] * world
+        if world > 1:
+            dist.all_gather_object(allx, mine, group=group)
+        else:
+            allx = [mine]
+        handles = (C.c_char * (64 * 3 * world))()
+        offs = (C.c_int64 * (3 * world))()
+        for k in range(world):
+            for j in range(3):
+                C.memmove(C.addressof(handles) + (k * 3 + j) * 64, allx[k][j][0], 64)
+                offs[k * 3 + j] = allx[k][j][1]
+        B.call("rgnn_comm_attach_peers", self._handle, C.cast(handles, C.c_void_p), offs, _ptr(self.Y_full),
+               _ptr(self.sig), _ptr(self.stage), self.stage.numel())
+
+
 def partition_dst(indeg_prefix, nparts: int):
     """rgnn_partition_dst: balanced dst ranges from the in-degree prefix (host)."""
     p = np.ascontiguousarray(indeg_prefix, dtype=np.int64)
