@@ -832,12 +832,13 @@ rgnn_status rgnn_graph_create(const rgnn_graph_desc* d, void* dev, size_t dev_by
   // waves * SMs chunks result, i.e. `waves` full waves with no partial wave left over (r01 sizing
   // gave 298 chunks = 2 waves + 2 on ogbn-mag); multiples of the 128-row tile.  Measured (fused
   // backward, ms): r01 sizing mag 3.66 / AM 0.854; 2 waves 3.68 / 0.877; 3 waves 3.54 / 0.790;
-  // 4 waves 3.59 / 0.778 (default).  Chunks are in position order, so each wave's CTAs gather the
+  // 4 waves 3.59 / 0.778; then with compact AM rows: 4 waves 3.46 / 0.790, 5: 3.43 / 0.795,
+  // 6: 3.45 / 0.766, 8: 3.42 / 0.756 (default).  Chunks are in position order, so each wave's CTAs gather the
   // X / Z rows of one 1/waves slice of the position space at a time.  (Measured r02: one
   // persistent CTA per SM over equal position ranges -- every SM spanning the whole position space
   // at once -- was slower, 3.54 -> 4.97 ms on ogbn-mag.)
   // RGNN_BWD_WAVES (A/B): 0 = the r01 sizing only
-  static const int64_t waves = getenv("RGNN_BWD_WAVES") ? std::max(0, atoi(getenv("RGNN_BWD_WAVES"))) : 4;
+  static const int64_t waves = getenv("RGNN_BWD_WAVES") ? std::max(0, atoi(getenv("RGNN_BWD_WAVES"))) : 8;
   auto count_chunks = [&](int64_t cr) {
     int64_t c = 0;
     for (int32_t r = 0; r < R; ++r) c += (seg_h[r + 1] - seg_h[r] + cr - 1) / cr;
