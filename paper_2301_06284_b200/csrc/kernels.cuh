@@ -125,6 +125,10 @@ rgnn_status launch_bwd_traverse(int prec, int K, int N, const BwdArgs& a, cudaSt
 rgnn_status launch_gemm_fwd_tc(int K, int N, const GemmFwdArgs& a, cudaStream_t s);
 rgnn_status launch_gemm_fwd_tc_f32out(int K, int N, const GemmFwdArgs& a, cudaStream_t s);
 rgnn_status launch_gemm_dw_tc(int K, int N, const GemmDwArgs& a, cudaStream_t s);
+// fp32 operands (X fp32, Bz fp32 or Bg/bgather/bscale), 3xTF32 tcgen05 (gemm_dw_tf32.cu)
+rgnn_status launch_gemm_dw_tf32x3(int K, int N, const GemmDwArgs& a, cudaStream_t s);
+// fp32 typed GEMM, 3xTF32 tcgen05 (gemm_fwd_tf32x3.cu); a.wt_bf16 = [2, num_w, N, K] fp32 workspace
+rgnn_status launch_gemm_fwd_tf32x3(int K, int N, const GemmFwdArgs& a, cudaStream_t s);
 // fp32 operands on the tensor cores (tcgen05 kind::tf32), fp32 output (gemm_tf32.cu).  wt_f32 =
 // the GEMM weight transposed, [num_w, N, K] fp32 (K-major B operand); a.W is not read.
 rgnn_status launch_gemm_fwd_tf32(int K, int N, const GemmFwdArgs& a, const float* wt_f32, cudaStream_t s);

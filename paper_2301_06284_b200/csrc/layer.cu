@@ -143,7 +143,7 @@ static WsLayout ws_layout(const rgnn_graph* g, int model, int K, int N, int prec
   const int64_t E = std::max<int64_t>(g->E_own, 1);
   w.U = c.take<float>((size_t)g->R * K);
   w.part = c.take<float>((size_t)std::max<int64_t>(g->num_parts, 1) * (N + 4));
-  w.wt = c.take<char>(prec == RGNN_BF16 ? (size_t)g->R * K * N * 2 : 1);
+  w.wt = c.take<char>((size_t)g->R * K * N * (prec == RGNN_BF16 ? 2 : 8));  // bf16 W^T | fp32 W^T hi, lo
   if (model == RGNN_RGCN && g->has_aggfirst) {
     const int64_t NP = std::max<int64_t>(g->num_pieces, 1);
     w.PA = c.take<float>((size_t)NP * K);
@@ -224,9 +224,25 @@ static rgnn_status f32_gemm(int prec, int K, int N, const GemmFwdArgs& a, const 
   return launch_gemm_fwd(RGNN_F32, K, N, a, s);
 }
 
+// dW GEMM of fp32 operands: 3xTF32 on the tensor cores (gemm_dw_tf32.cu) unless d_in = 32 or
+// RGNN_DW_SIMT=1 (the SIMT fp32 kernel, kept for d_in = 32 and as the measured baseline).
+static rgnn_status gemm_dw_f32(int xprec, int K, int N, const GemmDwArgs& a, cudaStream_t s) {
+  static const bool simt = getenv("RGNN_DW_SIMT") && atoi(getenv("RGNN_DW_SIMT")) != 0;
+  if (xprec == RGNN_F32 && !simt) {
+    rgnn_status st = launch_gemm_dw_tf32x3(K, N, a, s);
+    if (st != RGNN_E_UNSUPPORTED) return st;
+  }
+  return launch_gemm_dw(xprec, K, N, a, s);
+}
+
 static rgnn_status typed_gemm(int prec, int K, int N, const GemmFwdArgs& a, cudaStream_t s) {
   if (prec == RGNN_BF16) {
     rgnn_status st = launch_gemm_fwd_tc(K, N, a, s);
+    if (st != RGNN_E_UNSUPPORTED) return st;
+  }
+  static const bool simt = getenv("RGNN_FWD_SIMT") && atoi(getenv("RGNN_FWD_SIMT")) != 0;
+  if (prec == RGNN_F32 && !simt) {  // 3xTF32 tensor cores (W^T hi / lo in a.wt_bf16)
+    rgnn_status st = launch_gemm_fwd_tf32x3(K, N, a, s);
     if (st != RGNN_E_UNSUPPORTED) return st;
   }
   return launch_gemm_fwd(prec, K, N, a, s);
@@ -574,7 +590,7 @@ rgnn_status hgt_backward(const rgnn_graph* g, int K, int N, rgnn_prec prec, cons
     }
     if (st != RGNN_OK) {
       a.Bz = nullptr; a.Bg = Gm; a.bgather = gidx; a.bscale = scale;
-      RGNN_TRY(launch_gemm_dw(xprec, Kd, N, a, s));
+      RGNN_TRY(gemm_dw_f32(xprec, Kd, N, a, s));
     }
     return launch_dw_reduce(xprec, Kd, N, nseg, nch, cseg, w.dwpart, nullptr, nullptr, nullptr, nullptr, out,
                             nullptr, nullptr, s);
@@ -669,7 +685,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
       rgnn_status st = launch_gemm_dw_tc(K, N, args, s);
       if (st != RGNN_E_UNSUPPORTED) return st;
     }
-    return launch_gemm_dw(prec, K, N, args, s);
+    return gemm_dw_f32(prec, K, N, args, s);
   };
   // H_j = G_{v_j} W_{r_j}^T per (etype, dst) run j: one typed GEMM over the J runs (tf32 tensor
   // cores on the bf16 layer, W rounded as in the forward; SIMT fp32 otherwise), read by dX (NEXT-2).
