@@ -3,7 +3,8 @@
 memcheck (out-of-bounds and misaligned accesses), racecheck (shared-memory hazards), synccheck
 (illegal barrier use) and initcheck (reads of uninitialised device memory) must report 0 errors
 on a tiny graph through every kernel family: tcgen05 typed GEMM, narrow / wide / ring walks,
-fused tcgen05 backward, tcgen05 dW GEMM (unfused backward), tf32 GEMM + dX source walk, HGT.
+fused tcgen05 backward, tcgen05 dW GEMM (unfused backward), tf32 GEMM + dX source walk, HGT,
+and the fp32 layer's 3xTF32 typed and dW GEMMs.
 The logs go to gpurun_out/sanitize/ when that directory exists (copied to profiles/ per round).
 """
 import os
@@ -19,7 +20,7 @@ SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitize
 
 
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
-@pytest.mark.parametrize("variant", ["fused", "unfused"])
+@pytest.mark.parametrize("variant", ["fused", "unfused", "f32"])
 def test_sanitizer_clean(tool, variant):
     if not os.path.exists(SAN):
         pytest.skip("compute-sanitizer not found")
