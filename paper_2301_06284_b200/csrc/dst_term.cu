@@ -7,7 +7,8 @@
 // that does not cut through a destination run may sum dpre per piece first:
 //   c_r = sum_pieces (sum_{p in piece} dpre[p]) x_{v(piece)}.
 // A warp takes 32 positions at a time, forms the pieces with a segmented
-// shuffle scan keyed by dst, and gathers one X row per piece (not per edge).
+// shuffle scan keyed by dst, and gathers one X row per piece (not per edge),
+// four pieces' rows in flight at a time (one vector load per lane and row).
 // Blocks follow the dW chunk table (never straddling relations), warps stride
 // over the chunk, warps are combined in a fixed order: deterministic.
 #include "kernels.cuh"
@@ -18,13 +19,14 @@ template <typename T, int K>
 __global__ void __launch_bounds__(512) k_dst_term(const Tile* __restrict__ chunks, const int32_t* __restrict__ dst_s,
                                                   const float* __restrict__ dpre, const T* __restrict__ X, int64_t v0,
                                                   float* __restrict__ cpart) {
-  constexpr int PER = (K + 31) / 32, NW = 16;
+  // lane l holds features l*FPL .. l*FPL+FPL-1 (one 4- or 8-byte load per X row); K = 32: one each
+  constexpr int FPL = K / 32 >= 1 ? K / 32 : 1, NW = 16, GRP = 4;
   __shared__ float s_acc[NW][K];
   const Tile ch = chunks[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float acc[PER];
+  float acc[FPL];
 #pragma unroll
-  for (int i = 0; i < PER; ++i) acc[i] = 0.f;
+  for (int i = 0; i < FPL; ++i) acc[i] = 0.f;
   for (int base = ch.row0 + warp * 32; base < ch.row1; base += NW * 32) {
     const int p = base + lane;
     const bool valid = p < ch.row1;
@@ -39,22 +41,47 @@ __global__ void __launch_bounds__(512) k_dst_term(const Tile* __restrict__ chunk
     const int knext = __shfl_down_sync(0xffffffffu, key, 1);
     const bool last = valid && (lane == 31 || knext != key);
     uint32_t mask = __ballot_sync(0xffffffffu, last);
+    // GRP pieces at a time: their X rows are loaded together (independent loads in flight), then
+    // accumulated in piece order
     while (mask) {
-      const int l = __ffs(mask) - 1;
-      mask &= mask - 1;
-      const float D = __shfl_sync(0xffffffffu, d, l);
-      const int v = __shfl_sync(0xffffffffu, key, l);
-      const T* xv = X + (v0 + v) * (int64_t)K;
+      float D[GRP], xf[GRP][FPL];
 #pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        const int k = lane + 32 * i;
-        if (k < K) acc[i] = fmaf(D, to_f(xv[k]), acc[i]);
+      for (int g = 0; g < GRP; ++g) {
+        D[g] = 0.f;
+#pragma unroll
+        for (int i = 0; i < FPL; ++i) xf[g][i] = 0.f;
+        if (mask) {
+          const int l = __ffs(mask) - 1;
+          mask &= mask - 1;
+          D[g] = __shfl_sync(0xffffffffu, d, l);
+          const int v = __shfl_sync(0xffffffffu, key, l);
+          const T* xv = X + (v0 + v) * (int64_t)K + lane * FPL;
+          if (lane * FPL < K) {
+            if constexpr (sizeof(T) == 2 && FPL == 4) {
+              const uint2 u = __ldg(reinterpret_cast<const uint2*>(xv));
+              const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+              const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+              xf[g][0] = a.x; xf[g][1] = a.y; xf[g][2] = b.x; xf[g][3] = b.y;
+            } else if constexpr (sizeof(T) == 2 && FPL == 2) {
+              const uint32_t u = __ldg(reinterpret_cast<const unsigned int*>(xv));
+              const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
+              xf[g][0] = a.x; xf[g][1] = a.y;
+            } else {
+#pragma unroll
+              for (int i = 0; i < FPL; ++i) xf[g][i] = to_f(xv[i]);
+            }
+          }
+        }
       }
+#pragma unroll
+      for (int g = 0; g < GRP; ++g)
+#pragma unroll
+        for (int i = 0; i < FPL; ++i) acc[i] = fmaf(D[g], xf[g][i], acc[i]);
     }
   }
 #pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    const int k = lane + 32 * i;
+  for (int i = 0; i < FPL; ++i) {
+    const int k = lane * FPL + i;
     if (k < K) s_acc[warp][k] = acc[i];
   }
   __syncthreads();

@@ -202,7 +202,7 @@ __global__ void k_dw_group(int K, int N, int64_t num_chunks, const Tile* __restr
 __global__ void k_dw_reduce(int K, int N, int R, int64_t num_chunks, const int32_t* __restrict__ chunk_seg,
                             const float* __restrict__ part, const int32_t* __restrict__ cseg,
                             const float* __restrict__ cpart, const float* __restrict__ A, float* __restrict__ dW,
-                            const float* __restrict__ vsum, int gstep) {
+                            const float* __restrict__ vsum, int gstep, int src_term) {
   const int64_t total = (int64_t)R * K * N;
   const int stride = K * N + K;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -233,6 +233,9 @@ __global__ void k_dw_reduce(int K, int N, int R, int64_t num_chunks, const int32
         for (int c = cseg[r]; c < cseg[r + 1]; c += gstep) cv += cpart[(size_t)c * K + k];
       }
       s = fmaf(cv, A[(size_t)r * 2 * N + N + n], s);
+      // the score's source term (sum_p dpre_p x_src(p)) (x) A[r,0], when the gradient rows dZ carried
+      // only alpha G_v (bwd_tm.cu)
+      if (src_term && vsum) s = fmaf(vsum[((size_t)r * 2) * K + k], A[(size_t)r * 2 * N + n], s);
     }
     dW[i] = s;
   }
@@ -344,7 +347,7 @@ rgnn_status launch_gemm_dw(int prec, int K, int N, const GemmDwArgs& a, cudaStre
 rgnn_status launch_dw_reduce(int prec, int K, int N, int R, int64_t num_chunks, const int32_t* chunk_seg,
                              const float* part, const int32_t* cseg, const float* cpart, const float* A,
                              const float* W, float* dW, float* dA, float* dA_scratch, cudaStream_t s,
-                             const Tile* chunks) {
+                             const Tile* chunks, bool src_term) {
   int64_t total = (int64_t)R * K * N;
   unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16));
   // two stages when the chunk table is known (the partials are summed in groups of kRedGroup chunks
@@ -362,7 +365,7 @@ rgnn_status launch_dw_reduce(int prec, int K, int N, int R, int64_t num_chunks, 
     RGNN_LAUNCH(k_da_vsum, g1, 128, 0, s, K, N, R, chunk_seg, part, cseg, cpart, vsum, gstep);
   }
   RGNN_LAUNCH(k_dw_reduce, grid, 256, 0, s, K, N, R, num_chunks, chunk_seg, part, cseg, cpart, A, dW,
-              (A && dA) ? vsum : nullptr, gstep);
+              (A && dA) ? vsum : nullptr, gstep, src_term ? 1 : 0);
   if (dA) {
     unsigned g2 = (unsigned)std::max<int64_t>(1, ((int64_t)R * 2 * N + 127) / 128);
     RGNN_LAUNCH(k_da, g2, 128, 0, s, K, N, R, vsum, W, dA, prec == RGNN_BF16 ? 1 : 0);

@@ -718,7 +718,23 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
   if (model == RGNN_RGAT) {
     { Phase ph("fold_u", s); RGNN_TRY(launch_fold_u(prec, g->R, K, N, W, A, w.U, s)); }
     rgnn_status fst = RGNN_E_UNSUPPORTED;
-    if (tc_ok) {  // fused position-order backward: dZ built in smem, dW MMA + dst term in one kernel
+    bool tm_done = false;
+    if (tc_ok && bwd_tm_enabled(K, N, prec)) {
+      // tensor-core backward (bwd_tm.cu): Z tiles recomputed by tcgen05 from the staged X_src rows, the
+      // destination rows read once per run, the destination term summed per run
+      { Phase ph("bwd_fused", s);
+        RGNN_TRY(launch_bwd_rgat_tm(K, N, g, X, W, w.wt, use_compact(g, model) ? g->crow_of_pos : nullptr, sv.s_src,
+                                    w.U, sv.lse, Y, dY, slope, w.dwpart, w.cpart, w.dpre, want_dx ? w.ad : nullptr,
+                                    s)); }
+      if (!bwd_tm_dst_in_kernel()) {
+        Phase ph("dst_term", s);
+        RGNN_TRY(launch_dst_term(prec, K, g, w.dpre, X, w.cpart, s));
+      }
+      Phase ph("dw_reduce", s);
+      RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, g->chunk_seg, w.cpart, A, W,
+                                dW, dA, w.vsum, s, g->chunks, true));
+      tm_done = true;
+    } else if (tc_ok) {  // fused position-order backward: dZ built in smem, dW MMA + dst term in one kernel
       // (Measured r02 and rejected: dalpha_e = H_j . x_src with the run products H_j = G_v W_r^T, so the
       // kernel reads no Z rows -- ogbn-mag 3.64 -> 4.39 ms + 0.35 ms for the run GEMM, AM 0.85 -> 1.07
       // + 0.31 ms: the H row becomes one more dependent load at every destination change of the
@@ -729,7 +745,9 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
                                 Y, dY, w.U, A, slope, w.dwpart, w.cpart, want_dx ? w.ad : nullptr, s);
       if (fst != RGNN_OK && fst != RGNN_E_UNSUPPORTED) return fst;
     }
-    if (fst == RGNN_OK) {
+    if (tm_done) {
+      // tensor-core backward above (dW, dA reduced)
+    } else if (fst == RGNN_OK) {
       Phase ph("dw_reduce", s);
       RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, g->chunk_seg, w.cpart, A, W,
                                 dW, dA, w.vsum, s, g->chunks));

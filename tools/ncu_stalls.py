@@ -10,8 +10,14 @@ top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kern}",
                       "--print-source", "sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
-hdr = rows[1]
-body = [r for r in rows[2:] if len(r) == len(hdr)]
+hi = next(i for i, r in enumerate(rows) if "Warp Stall Sampling (All Samples)" in r)
+hdr = rows[hi]
+body = []
+for r in rows[hi + 1:]:  # the first launch's block only (several captures repeat the header)
+    if r == hdr or (r and r[0] == hdr[0]):
+        break
+    if len(r) == len(hdr):
+        body.append(r)
 si = hdr.index("Warp Stall Sampling (All Samples)")
 stall_cols = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
 tot = {hdr[i]: sum(float(r[i] or 0) for r in body) for i in stall_cols}
@@ -19,7 +25,14 @@ alls = sum(float(r[si] or 0) for r in body)
 print(f"samples {alls:.0f}")
 for k, v in sorted(tot.items(), key=lambda x: -x[1])[:10]:
     print(f"  {k:24s} {100 * v / max(alls, 1):5.1f}%")
-print("hottest instructions:")
-for r in sorted(body, key=lambda r: -float(r[si] or 0))[:top]:
+base = int(body[0][0], 16) if body and body[0][0].startswith("0x") else 0
+pos = {id(r): i for i, r in enumerate(body)}
+print("hottest instructions (offset from the kernel start; with the 3 instructions before the top 8):")
+for n, r in enumerate(sorted(body, key=lambda r: -float(r[si] or 0))[:top]):
     st = sorted(((hdr[i], float(r[i] or 0)) for i in stall_cols), key=lambda x: -x[1])[:2]
-    print(f"  {r[0]:>6s} {100 * float(r[si] or 0) / max(alls, 1):5.1f}%  {r[1][:60]:60s} {st[0][0]}={st[0][1]:.0f} {st[1][0]}={st[1][1]:.0f}")
+    off = int(r[0], 16) - base if r[0].startswith("0x") else r[0]
+    print(f"  {off:>#7x} {100 * float(r[si] or 0) / max(alls, 1):5.1f}%  {r[1][:60]:60s} {st[0][0]}={st[0][1]:.0f} {st[1][0]}={st[1][1]:.0f}")
+    if n < 8:
+        i = pos[id(r)]
+        for b in body[max(0, i - 3):i]:
+            print(f"          {'':6s}  {b[1][:70]}")
