@@ -56,7 +56,8 @@ struct TmCfg {
                        // AM 0.82 -> 1.08 ms, against 0.21 / 0.22 ms for k_dst_term); 0: k_dst_term from dpre
 #endif
 #ifndef RGNN_TM_RPF
-#define RGNN_TM_RPF 1  // L2 prefetch of the run rows (dY, Y, x of each run head) when a stage is issued
+#define RGNN_TM_RPF 2  // run rows (dY, Y, x of each run head) of stage it + RPF prefetched to L2 when stage it is
+                       // issued (0: off)
 #endif
 #ifndef RGNN_TM_XPF
 #define RGNN_TM_XPF 2  // X rows of stage it + STAGES + XPF - 1 prefetched to L2 when stage it is issued (0: off)
@@ -273,19 +274,24 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&a_full[st])) : "memory");
       if (pw == 0) TMT(it, 2);
-      // L2 prefetch of the per-destination rows read for these positions (run heads)
-      const int vp = __shfl_up_sync(0xffffffffu, v, 1);
-      if (RGNN_TM_RPF && p < row1 && (lane == 0 || vp != v)) {
-        const char* gp = reinterpret_cast<const char*>(pr.dY + (size_t)v * N);
-        const char* yp = reinterpret_cast<const char*>(pr.Y + (size_t)v * N);
-        const char* xp = reinterpret_cast<const char*>(pr.X + (pr.v0 + v) * (int64_t)K);
+      // L2 prefetch of the per-destination rows (dY, Y, x of each run head) of stage it + RGNN_TM_RPF, so
+      // that they have arrived when a compute group reads them (it does so as soon as a stage is issued)
+      if (RGNN_TM_RPF > 0) {
+        const int pf = row0 + (it + RGNN_TM_RPF) * MT + lp;
+        const int vf = pf < row1 ? __ldg(pr.dst_s + pf) : -1;
+        const int vfp = __shfl_up_sync(0xffffffffu, vf, 1);
+        if (vf >= 0 && (lane == 0 || vfp != vf)) {
+          const char* gp = reinterpret_cast<const char*>(pr.dY + (size_t)vf * N);
+          const char* yp = reinterpret_cast<const char*>(pr.Y + (size_t)vf * N);
+          const char* xp = reinterpret_cast<const char*>(pr.X + (pr.v0 + vf) * (int64_t)K);
 #pragma unroll
-        for (int o = 0; o < N * 4; o += 128) {
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(gp + o));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(yp + o));
+          for (int o = 0; o < N * 4; o += 128) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(gp + o));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(yp + o));
+          }
+#pragma unroll
+          for (int o = 0; o < K * 2; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(xp + o));
         }
-#pragma unroll
-        for (int o = 0; o < K * 2; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(xp + o));
       }
       src = nsrc; v = nv; p = np; zr = nzr;
     }
@@ -485,8 +491,12 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
         }
         tc::tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) t = fmaf(g[i], bf16r(__uint_as_float(z[i])), t);  // Z as the forward stored it:
-        // for a destination with one in-edge Y_v = bf16(Z_p), so dalpha - S_v must vanish exactly
+        for (int i = 0; i < 16; i += 2) {  // Z rounded as the forward stored it (one cvt per pair):
+          const uint32_t zb = tc::pack_bf16(__uint_as_float(z[i]), __uint_as_float(z[i + 1]));
+          t = fmaf(g[i], __uint_as_float(zb << 16), t);
+          t = fmaf(g[i + 1], __uint_as_float(zb & 0xffff0000u), t);
+        }
+        // for a destination with one in-edge Y_v = bf16(Z_p), so dalpha - S_v must vanish exactly)
         uint4 o0 = make_uint4(0, 0, 0, 0), o1 = make_uint4(0, 0, 0, 0);
         if (valid) {
           o0 = make_uint4(tc::pack_bf16(alpha * g[0], alpha * g[1]), tc::pack_bf16(alpha * g[2], alpha * g[3]),

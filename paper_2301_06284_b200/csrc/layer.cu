@@ -719,7 +719,12 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     { Phase ph("fold_u", s); RGNN_TRY(launch_fold_u(prec, g->R, K, N, W, A, w.U, s)); }
     rgnn_status fst = RGNN_E_UNSUPPORTED;
     bool tm_done = false;
-    if (tc_ok && bwd_tm_enabled(K, N, prec)) {
+    // tensor-core backward where destination runs are long (ogbn-mag: mean run 14.5 positions); with short
+    // runs (AM: 2.3) the per-run reads buy little and the fused kernel below is faster (measured r02: AM
+    // 0.76 + 0.19 ms dst term vs 0.755 ms).  RGNN_BWD_TM=1 / 0 forces either.
+    const int tm_env = getenv("RGNN_BWD_TM") ? atoi(getenv("RGNN_BWD_TM")) : -1;  // read per call (tests)
+    const bool tm_pick = tm_env >= 0 ? tm_env != 0 : g->E_own >= 4 * std::max<int64_t>(g->J, 1);
+    if (tc_ok && tm_pick && bwd_tm_enabled(K, N, prec)) {
       // tensor-core backward (bwd_tm.cu): Z tiles recomputed by tcgen05 from the staged X_src rows, the
       // destination rows read once per run, the destination term summed per run
       { Phase ph("bwd_fused", s);

@@ -35,6 +35,9 @@ def _worker(rank, world, port, model, q):
     sys.path.insert(0, ROOT)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    # one backward kernel on every shard and on the unsharded graph (the default picks per owned graph
+    # by its mean (etype, dst) run length; the two kernels agree to the bf16 tolerance, not to 1e-5)
+    os.environ["RGNN_BWD_TM"] = "1"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2301_06284_b200 as m
