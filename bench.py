@@ -123,6 +123,11 @@ def algorithmic_bytes(phase, model, prec, K, N, E, V_own, J, num_items, U=None):
             return E * (K * b + 12) + J * 4 * N
         # read Z, s_src, dst, src (+ compact row) per edge, gather X_src; per run G_v, Y_v, X_v, lse
         return E * (N * b + K * b + 12 + (4 if U is not None else 0)) + J * (8 * N + K * b + 4)
+    if phase == "bwd_tm":  # RGAT, messages recomputed (bwd_tm.cu): per edge gather X_src, read src, dst, s_src
+        # (+ compact row), write dpre; per (etype, dst) run G_v, Y_v (fp32), x_v, lse
+        return E * (K * b + 16 + (4 if U is not None else 0)) + J * (8 * N + K * b + 4)
+    if phase == "dst_term":  # read dst, dpre per edge; x_v per run
+        return E * 8 + J * K * b
     if phase == "gemm_dw":  # gather X rows, read dZ (RGAT) or gather G rows (RGCN), indices; dst term per run
         if model == "rgat":
             return E * (K * b + N * b + 4 + 4 + 4) + J * K * b
@@ -670,7 +675,7 @@ def run_ours(args):
     v = G.view
     step_phase = {k: (tot / args.steps, n // max(args.steps, 1)) for k, (tot, n) in phases.items()}
     cand = {k: x for k, x in step_phase.items()
-            if k in ("gemm_fwd", "aggregate", "bwd_traverse", "gemm_dw", "bwd_fused", "hgt_bwd_walk")}
+            if k in ("gemm_fwd", "aggregate", "bwd_traverse", "gemm_dw", "bwd_fused", "bwd_tm", "hgt_bwd_walk")}
     roof = None
     if cand:
         dom = max(cand, key=lambda k: cand[k][0])

@@ -727,7 +727,7 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
     if (tc_ok && tm_pick && bwd_tm_enabled(K, N, prec)) {
       // tensor-core backward (bwd_tm.cu): Z tiles recomputed by tcgen05 from the staged X_src rows, the
       // destination rows read once per run, the destination term summed per run
-      { Phase ph("bwd_fused", s);
+      { Phase ph("bwd_tm", s);
         RGNN_TRY(launch_bwd_rgat_tm(K, N, g, X, W, w.wt, use_compact(g, model) ? g->crow_of_pos : nullptr, sv.s_src,
                                     w.U, sv.lse, Y, dY, slope, w.dwpart, w.cpart, w.dpre, want_dx ? w.ad : nullptr,
                                     s)); }

@@ -15,7 +15,7 @@ for c in "$@"; do
     --log-file $OUT/launches_$c.csv $B > $OUT/launches_$c.log 2>&1
   python tools/ncu_summarize.py launches $OUT/launches_$c.csv $OUT/launches_summary_$c.txt "$B"
   timeout 1200 ncu --set full --metrics $TP --clock-control none --import-source on \
-    -k regex:"$KRE" -c 4 -o $REP/full_$c $B > $OUT/full_$c.log 2>&1
+    -k regex:"$KRE" -c ${NCAP:-4} -o $REP/full_$c $B > $OUT/full_$c.log 2>&1
   python tools/ncu_summarize.py full $REP/full_$c.ncu-rep $OUT/full_summary_$c.json > /dev/null
   for k in $(ncu -i $REP/full_$c.ncu-rep --page raw --csv --metrics launch__grid_size 2>/dev/null | \
              python -c "import csv,sys; r=list(csv.reader(sys.stdin)); i=r[0].index('Kernel Name'); print(' '.join(sorted({x[i].split('(')[0].split('<')[0].replace('void ','').replace('rgnn::','').strip() for x in r[2:]})))"); do

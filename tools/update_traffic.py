@@ -11,7 +11,7 @@ import os
 import sys
 
 PHASES = {"gemm_fwd": ("k_gemm_fwd_tc",), "aggregate": ("k_aggregate_narrow", "k_aggregate<", "k_aggregate_ring"),
-          "bwd_fused": ("k_bwd_fused_tc",)}
+          "bwd_fused": ("k_bwd_fused_tc",), "bwd_tm": ("k_bwd_rgat_tm",), "dst_term": ("k_dst_term",)}
 
 
 def main(summary, key, note=None):
