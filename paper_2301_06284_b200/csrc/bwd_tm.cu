@@ -21,8 +21,9 @@
 //     (sum_p dpre_p x_src(p)) (x) A[r,0] = Db (x) A[r,0], is added by k_dw_reduce.
 // The message rows are never read from HBM: Z = X_src W_r is the MMA the forward's typed GEMM issued
 // (P:300-305), so the backward reads the X_src rows plus one G / Y / x row triple per run.  The
-// destination term c_r = sum_p dpre_p x_dst(p) is summed per run in the same kernel; part / cpart are
-// reduced in chunk order by k_dw_reduce (deterministic).
+// destination term c_r = sum_p dpre_p x_dst(p) is summed by k_dst_term from dpre (measured r02: summing it
+// per run inside this kernel, after each stage's per-position pass, made the backward 0.33 ms slower on
+// ogbn-mag against 0.20 ms for k_dst_term); part is reduced in chunk order by k_dw_reduce (deterministic).
 #include <math_constants.h>
 
 #include "kernels.cuh"
@@ -44,16 +45,11 @@ struct TmCfg {
 #endif
   static constexpr int DZB = RGNN_TM_DZB;
   static constexpr int W_BYTES = N * K * 2;      // W_r^T, K-major SW128
-  static constexpr int GSEL_BYTES = N == 64 ? 16384 : 6144;  // bf16 run rows per buffer (runs past CAP read dY directly)
+  static constexpr int GSEL_BYTES = N == 64 ? 16384 : 7168;  // bf16 run rows per buffer (runs past CAP read dY directly)
   static constexpr int CAP = GSEL_BYTES / (N * 2);
-  static constexpr int RUNTAB = MT * 4 * 6 + 16;  // per buffer: run and dpre of each position; S, dst score, dst,
-                                                  // first row per run
+  static constexpr int RUNTAB = MT * 4 * 4;      // per buffer: run of each position; S, dst score, dst per run
 #ifndef RGNN_TM_SMAX
 #define RGNN_TM_SMAX 6
-#endif
-#ifndef RGNN_TM_DST
-#define RGNN_TM_DST 0  // 1: destination term summed per run in this kernel (measured slower: mag 2.83 -> 3.16 ms,
-                       // AM 0.82 -> 1.08 ms, against 0.21 / 0.22 ms for k_dst_term); 0: k_dst_term from dpre
 #endif
 #ifndef RGNN_TM_RPF
 #define RGNN_TM_RPF 2  // run rows (dY, Y, x of each run head) of stage it + RPF prefetched to L2 when stage it is
@@ -97,7 +93,6 @@ struct BwdTmParams {
   const float* dY;
   float slope;
   float* part;
-  float* cpart;  // [chunks, K] destination term c_r per chunk
   float* dpre;
   float2* ad;
 };
@@ -181,8 +176,6 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
   auto sS = [&](int b) { return reinterpret_cast<float*>(sRt + b * C::RUNTAB + MT * 4); };
   auto sHv = [&](int b) { return reinterpret_cast<int*>(sRt + b * C::RUNTAB + MT * 8); };
   auto sDs = [&](int b) { return reinterpret_cast<float*>(sRt + b * C::RUNTAB + MT * 12); };
-  auto sDp = [&](int b) { return reinterpret_cast<float*>(sRt + b * C::RUNTAB + MT * 16); };
-  auto sHs = [&](int b) { return reinterpret_cast<int*>(sRt + b * C::RUNTAB + MT * 20); };  // [MT + 1]
   // 16-byte chunk c of line `row` in a 128B-swizzled tile of `rows` lines per 64-element block
   auto swz = [&](int c, int row, int rows) { return (c >> 3) * (rows * 128) + row * 128 + (((c & 7) ^ (row & 7)) << 4); };
 
@@ -360,9 +353,6 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     constexpr int LPR = C::LPR, RPIT = C::RUNS_PI, BATCH = 4, KPL = K / LPR;
     const int sub = lane / LPR, ln = lane % LPR;
-    float cacc[KPL];  // destination-term partial: features ln * KPL .. of the runs this lane's subgroup takes
-#pragma unroll
-    for (int i = 0; i < KPL; ++i) cacc[i] = 0.f;
     for (int it = grp; it < nsub; it += 2) {
       const int st = it % C::STAGES, buf = it & 1;
       const int p = row0 + it * MT + lp;
@@ -386,15 +376,11 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
         const int j = nruns + __popc(hb & (0xffffffffu >> (31 - lane))) - 1;
         if (gw == 0) {
           sRun(buf)[l2] = j;
-          if (head) {
-            sHv(buf)[j] = v;
-            sHs(buf)[j] = l2;
-          }
+          if (head) sHv(buf)[j] = v;
         }
         nruns += __popc(hb);
         lastv = __shfl_sync(0xffffffffu, v, 31);
       }
-      if (gw == 0 && lane == 0) sHs(buf)[nruns] = min(MT, row1 - (row0 + it * MT));  // end of the last run
       tc::named_bar(9 + grp, 256);
       if (gw == 0) TMT(it, 7);
       // (2) per run (warps of the group take interleaved runs, BATCH runs' loads in flight): G_v as a
@@ -523,7 +509,6 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
         // dpre as hi + lo bf16 (columns 0, 1 of the side operand): Db = X_src^T dpre to ~2^-16
         const float hi = __bfloat162float(__float2bfloat16_rn(dp));
         *reinterpret_cast<uint32_t*>(sB2(buf) + (lp >> 3) * 256 + (lp & 7) * 16) = tc::pack_bf16(hi, dp - hi);
-        sDp(buf)[lp] = dp;
         if (valid) {
           pr.dpre[p] = dp;
           if (pr.ad) pr.ad[p] = make_float2(alpha, dp);
@@ -533,25 +518,6 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&bfull[buf]);
       if (gw == 0) TMT(it, 13);
-      // (4) destination term c_r += (sum_{p in run} dpre_p) x_v, once per run (the x_v rows were just
-      // read for the score, so they come from L1); the run's dpre summed in a fixed order
-      if (RGNN_TM_DST) tc::named_bar(9 + grp, 256);
-      for (int j0 = gw * RPIT; RGNN_TM_DST && j0 < nruns; j0 += 8 * RPIT) {
-        const int jr = j0 + sub;
-        float dsum = 0.f;
-        if (jr < nruns) {
-          const int e = sHs(buf)[jr + 1];
-          for (int l2 = sHs(buf)[jr] + ln; l2 < e; l2 += LPR) dsum += sDp(buf)[l2];
-        }
-#pragma unroll
-        for (int o = LPR / 2; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
-        if (jr < nruns) {
-          float xv[KPL];
-          load_bf16<KPL>(pr.X + (pr.v0 + sHv(buf)[jr]) * (int64_t)K + ln * KPL, xv);
-#pragma unroll
-          for (int i = 0; i < KPL; ++i) cacc[i] = fmaf(dsum, xv[i], cacc[i]);
-        }
-      }
     }
     // epilogue: TMEM accumulators -> part[c]; the four warps of a lane quarter split the columns
     tc::mbar_wait(acc_full, 0);
@@ -576,19 +542,6 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
       tc::tmem_ld16(tl + N, vv);
       tc::tmem_ld_wait();
       if (rvalid) out[K * N + row] = __uint_as_float(vv[0]) + __uint_as_float(vv[1]);
-    }
-    // destination-term partials -> smem (the X stages are free now: every MMA has completed), then
-    // summed over warps and subgroups in a fixed order
-    float* sC = reinterpret_cast<float*>(sAst);
-    if (RGNN_TM_DST) {
-#pragma unroll
-    for (int i = 0; i < KPL; ++i) sC[(cw * RPIT + sub) * K + ln * KPL + i] = cacc[i];
-    tc::named_bar(11, C::CW * 32);
-    for (int k = cw * 32 + lane; k < K; k += C::CW * 32) {
-      float sum = 0.f;
-      for (int w = 0; w < C::CW * RPIT; ++w) sum += sC[w * K + k];
-      pr.cpart[(size_t)blockIdx.x * K + k] = sum;
-    }
     }
   }
   tc::tc_fence_before();
@@ -618,8 +571,6 @@ bool bwd_tm_enabled(int K, int N, int prec) {
   return prec == RGNN_BF16 && !off && !tc_disabled() && (K == 64 || K == 128) && (N == 64 || N == 128);
 }
 
-bool bwd_tm_dst_in_kernel() { return RGNN_TM_DST != 0; }
-
 template <int K, int N>
 static rgnn_status bwd_tm(const rgnn_graph* g, const BwdTmParams& p, cudaStream_t s) {
   using C = TmCfg<K, N>;
@@ -644,8 +595,8 @@ static rgnn_status bwd_tm(const rgnn_graph* g, const BwdTmParams& p, cudaStream_
 
 rgnn_status launch_bwd_rgat_tm(int K, int N, const rgnn_graph* g, const void* X, const float* W, void* Wt,
                                const int32_t* zmap, const float* s_src, const float* U, const float* lse,
-                               const float* Y, const float* dY, float slope, float* part, float* cpart, float* dpre,
-                               float2* ad, cudaStream_t s) {
+                               const float* Y, const float* dY, float slope, float* part, float* dpre, float2* ad,
+                               cudaStream_t s) {
   tc::watchdog_init();
   if (g->num_chunks == 0) return RGNN_OK;
   auto* wt = static_cast<__nv_bfloat16*>(Wt);
@@ -653,7 +604,7 @@ rgnn_status launch_bwd_rgat_tm(int K, int N, const rgnn_graph* g, const void* X,
   RGNN_LAUNCH(k_tm_wt, (unsigned)std::max<int64_t>(1, std::min<int64_t>((nw + 255) / 256, 4096)), 256, 0, s, g->R, K,
               N, W, wt);
   BwdTmParams p{g->chunks, g->src_s, g->dst_s, zmap, s_src, U, lse, static_cast<const __nv_bfloat16*>(X), g->v0, wt,
-                Y, dY, slope, part, cpart, dpre, ad};
+                Y, dY, slope, part, dpre, ad};
   if (K == 64 && N == 64) return bwd_tm<64, 64>(g, p, s);
   if (K == 64 && N == 128) return bwd_tm<64, 128>(g, p, s);
   if (K == 128 && N == 64) return bwd_tm<128, 64>(g, p, s);

@@ -178,22 +178,26 @@ __global__ void __launch_bounds__(256) k_gemm_dw_simt(GemmDwArgs a) {
 // sums the group leaders of a relation in order.  Deterministic; measured r02 on ogbn-mag with 592
 // chunks: the single-stage per-element loop over 148 chunks per relation took 0.08-0.17 ms.
 constexpr int kRedGroup = 8;
-__global__ void k_dw_group(int K, int N, int64_t num_chunks, const Tile* __restrict__ chunks,
-                           const int32_t* __restrict__ chunk_seg, float* __restrict__ part, float* __restrict__ cpart) {
+// grid = (element blocks, chunks): blockIdx.y = chunk c; blocks of non-leader chunks exit at once, a
+// leader's blocks sum its group's partials for a contiguous slice of elements (coalesced, in chunk order).
+// (r01 / early r02: one thread per (chunk, element) over the whole partial space, 7 of 8 threads idle and
+// a 64-bit division per element -- 67 us on ogbn-mag.)
+__global__ void __launch_bounds__(256) k_dw_group(int K, int N, const Tile* __restrict__ chunks,
+                                                  const int32_t* __restrict__ chunk_seg, float* __restrict__ part,
+                                                  float* __restrict__ cpart) {
+  const int c = blockIdx.y;
+  const int r = chunks[c].r, c0 = chunk_seg[r], c1 = chunk_seg[r + 1];
+  if ((c - c0) % kRedGroup != 0) return;  // not a group leader
+  const int cend = min(c1, c + kRedGroup);
   const int stride = K * N + K;
-  const int64_t total = num_chunks * (int64_t)(stride + (cpart ? K : 0));
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const bool is_c = t >= num_chunks * (int64_t)stride;  // the destination-term partials [num_chunks, K]
-    const int64_t u = is_c ? t - num_chunks * (int64_t)stride : t;
-    const int w = is_c ? K : stride;
-    const int64_t c = u / w;
-    const int e = (int)(u - c * w);
-    const int r = chunks[c].r, c0 = chunk_seg[r], c1 = chunk_seg[r + 1];
-    if ((c - c0) % kRedGroup != 0) continue;  // not a group leader
+  const int tot = stride + (cpart ? K : 0);
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += gridDim.x * blockDim.x) {
+    const bool is_c = e >= stride;  // the destination-term partials [num_chunks, K]
     float* base = is_c ? cpart : part;
-    float acc = base[(size_t)c * w + e];
-    for (int64_t d = c + 1; d < c1 && d < c + kRedGroup; ++d) acc += base[(size_t)d * w + e];
-    base[(size_t)c * w + e] = acc;
+    const int w = is_c ? K : stride, ee = is_c ? e - stride : e;
+    float acc = base[(size_t)c * w + ee];
+    for (int d = c + 1; d < cend; ++d) acc += base[(size_t)d * w + ee];
+    base[(size_t)c * w + ee] = acc;
   }
 }
 
@@ -266,20 +270,35 @@ __global__ void k_da_vsum(int K, int N, int R, const int32_t* __restrict__ chunk
   }
 }
 
-// dA[r,h,n] = vsum[r][h] . W_r[:,n]  (h = 0: sum dpre x_src, h = 1: sum dpre x_dst)
-__global__ void k_da(int K, int N, int R, const float* __restrict__ vsum, const float* __restrict__ W,
-                     float* __restrict__ dA, int round_bf16) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)R * 2 * N;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(i / (2 * N)), h = (int)((i / N) % 2), n = (int)(i % N);
-    const float* v = vsum + ((size_t)r * 2 + h) * K;
-    float s = 0.f;
-    for (int k = 0; k < K; ++k) {
+// dA[r,h,n] = vsum[r][h] . W_r[:,n]  (h = 0: sum dpre x_src, h = 1: sum dpre x_dst).  One block of 8
+// warps per (r, h, 32 columns): warp w sums k in its eighth of [0, K), lane = column; the eight partials
+// are added in warp order (deterministic).  (The r01 kernel ran one serial K-loop per output on 8 blocks:
+// 33 us on ogbn-mag.)
+__global__ void __launch_bounds__(256) k_da(int K, int N, int R, const float* __restrict__ vsum,
+                                            const float* __restrict__ W, float* __restrict__ dA, int round_bf16) {
+  __shared__ float s_p[8][32];
+  const int ncb = (N + 31) / 32;
+  const int rh = blockIdx.x / ncb, cb = blockIdx.x % ncb;
+  const int r = rh / 2, h = rh % 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = cb * 32 + lane;
+  const float* v = vsum + ((size_t)r * 2 + h) * K;
+  const int kper = (K + 7) / 8, k0 = warp * kper, k1 = min(K, k0 + kper);
+  float acc = 0.f;
+  if (n < N) {
+    for (int k = k0; k < k1; ++k) {
       float w = W[((size_t)r * K + k) * N + n];
       if (round_bf16) w = __bfloat162float(__float2bfloat16_rn(w));
-      s = fmaf(v[k], w, s);
+      acc = fmaf(v[k], w, acc);
     }
-    dA[i] = s;
+  }
+  s_p[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && n < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += s_p[i][lane];
+    dA[((size_t)r * 2 + h) * N + n] = t;
   }
 }
 
@@ -354,9 +373,10 @@ rgnn_status launch_dw_reduce(int prec, int K, int N, int R, int64_t num_chunks, 
   // in place first); the dst-term partials cpart are grouped along (they use the same chunks)
   int gstep = 1;
   if (chunks && chunk_seg && num_chunks > kRedGroup) {
-    const int64_t n1 = num_chunks * (int64_t)(K * N + K + (cpart ? K : 0));
-    RGNN_LAUNCH(k_dw_group, (unsigned)std::min<int64_t>((n1 + 255) / 256, 148 * 32), 256, 0, s, K, N, num_chunks,
-                chunks, chunk_seg, const_cast<float*>(part), const_cast<float*>(cpart));
+    const int tot = K * N + K + (cpart ? K : 0);
+    const dim3 grid_g((unsigned)std::min(8, (tot + 255) / 256), (unsigned)num_chunks);
+    RGNN_LAUNCH(k_dw_group, grid_g, 256, 0, s, K, N, chunks, chunk_seg, const_cast<float*>(part),
+                const_cast<float*>(cpart));
     gstep = kRedGroup;
   }
   float* vsum = dA ? dA_scratch : nullptr;
@@ -367,8 +387,8 @@ rgnn_status launch_dw_reduce(int prec, int K, int N, int R, int64_t num_chunks, 
   RGNN_LAUNCH(k_dw_reduce, grid, 256, 0, s, K, N, R, num_chunks, chunk_seg, part, cseg, cpart, A, dW,
               (A && dA) ? vsum : nullptr, gstep, src_term ? 1 : 0);
   if (dA) {
-    unsigned g2 = (unsigned)std::max<int64_t>(1, ((int64_t)R * 2 * N + 127) / 128);
-    RGNN_LAUNCH(k_da, g2, 128, 0, s, K, N, R, vsum, W, dA, prec == RGNN_BF16 ? 1 : 0);
+    const unsigned g2 = (unsigned)(R * 2 * ((N + 31) / 32));
+    RGNN_LAUNCH(k_da, g2, 256, 0, s, K, N, R, vsum, W, dA, prec == RGNN_BF16 ? 1 : 0);
   }
   return RGNN_OK;
 }

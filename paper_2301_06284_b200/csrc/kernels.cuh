@@ -139,14 +139,13 @@ rgnn_status launch_bwd_fused_tc(int K, int N, const rgnn_graph* g, const void* X
                                 float slope, float* part, float* cpart, float2* ad, cudaStream_t s);
 // RGAT backward with Z recomputed on the tensor cores (bwd_tm.cu): bf16 layer, d_in, d_out in {64, 128}.
 // zmap (compact): s_src row of position p, null = p; U = W_r A[r,1] (fold); Wt = bf16 workspace [R, N, K].
-// Writes part (dW with alpha G_v rows + sum dpre x_src, per chunk), cpart (sum dpre x_dst per chunk), dpre per
-// position and (dX) ad = (alpha, dpre) per position.
+// Writes part (dW with alpha G_v rows + sum dpre x_src, per chunk), dpre per position and (dX) ad = (alpha,
+// dpre) per position.
 bool bwd_tm_enabled(int K, int N, int prec);
-bool bwd_tm_dst_in_kernel();  // RGNN_TM_DST: cpart written by the kernel (else launch_dst_term from dpre)
 rgnn_status launch_bwd_rgat_tm(int K, int N, const rgnn_graph* g, const void* X, const float* W, void* Wt,
                                const int32_t* zmap, const float* s_src, const float* U, const float* lse,
-                               const float* Y, const float* dY, float slope, float* part, float* cpart, float* dpre,
-                               float2* ad, cudaStream_t s);
+                               const float* Y, const float* dY, float slope, float* part, float* dpre, float2* ad,
+                               cudaStream_t s);
 rgnn_status launch_expand_dz(int64_t E, int N, const int32_t* dst_s, const float* inv_c, const float* G, void* dZ,
                              cudaStream_t s);
 

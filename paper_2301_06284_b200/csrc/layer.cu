@@ -729,12 +729,8 @@ rgnn_status rgnn_backward(const rgnn_graph* g, rgnn_model model, int K, int N, r
       // destination rows read once per run, the destination term summed per run
       { Phase ph("bwd_tm", s);
         RGNN_TRY(launch_bwd_rgat_tm(K, N, g, X, W, w.wt, use_compact(g, model) ? g->crow_of_pos : nullptr, sv.s_src,
-                                    w.U, sv.lse, Y, dY, slope, w.dwpart, w.cpart, w.dpre, want_dx ? w.ad : nullptr,
-                                    s)); }
-      if (!bwd_tm_dst_in_kernel()) {
-        Phase ph("dst_term", s);
-        RGNN_TRY(launch_dst_term(prec, K, g, w.dpre, X, w.cpart, s));
-      }
+                                    w.U, sv.lse, Y, dY, slope, w.dwpart, w.dpre, want_dx ? w.ad : nullptr, s)); }
+      { Phase ph("dst_term", s); RGNN_TRY(launch_dst_term(prec, K, g, w.dpre, X, w.cpart, s)); }
       Phase ph("dw_reduce", s);
       RGNN_TRY(launch_dw_reduce(prec, K, N, g->R, g->num_chunks, g->chunk_seg, w.dwpart, g->chunk_seg, w.cpart, A, W,
                                 dW, dA, w.vsum, s, g->chunks, true));
