@@ -167,6 +167,10 @@ __device__ __forceinline__ void peer_fence(const AggArgs& a) {
   if (a.npeer) __threadfence_system();
 }
 
+#ifndef RGNN_NARROW_EMPTY
+#define RGNN_NARROW_EMPTY 1  // 1: the narrow pass writes the empty rows (Y = 0 / self term, lse = -inf); 0: k_empty_rows
+                             // (measured r02: mag walk 1.83 -> 1.90 ms, AM 0.62 -> 0.67 ms with 0)
+#endif
 // Narrow rows (deg <= a.narrow, never split): one lane group (L lanes, one 16-byte slice of a
 // Z row each) per row, G consecutive row ids per warp step, UN edges per group step and one
 // online state per row -- no cross-group merge, so short rows cost a quarter (d = 64 bf16) or
@@ -234,6 +238,7 @@ __device__ __forceinline__ void narrow_rows_pipe(const AggArgs& a, int64_t warp0
     q0c = q0n; q1c = q1n;
     bounds(rg + 2 * nwarps, q0n, q1n);
     if (row >= a.V_own || q1 < q0) continue;  // no row, or a wide row (the whole group together)
+    if (!RGNN_NARROW_EMPTY && q1 == q0) continue;  // empty rows: k_empty_rows
     if constexpr (RGAT) mys = ssrc;
     float acc[EPL];
 #pragma unroll
@@ -342,6 +347,7 @@ __device__ __forceinline__ void narrow_rows(const AggArgs& a, int64_t warp0, int
     if (nrow < a.V_own) { nq0 = a.row_ptr[nrow]; nq1 = a.row_ptr[nrow + 1]; }
     if (row >= a.V_own) continue;  // the whole group leaves together
     if (q1 - q0 > a.narrow) continue;  // a wide row: walked from the item list
+    if (!RGNN_NARROW_EMPTY && q1 == q0) continue;  // empty rows: k_empty_rows
     float acc[EPL];
 #pragma unroll
     for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
@@ -1023,7 +1029,8 @@ static rgnn_status aggregate(bool rgat, const AggArgs& a_in, cudaStream_t s) {
   static const bool no_narrow = getenv("RGNN_NO_NARROW") != nullptr;
   const bool narrow = a.row_ptr && a.V_own > 0 && WalkShape<T, K, N>::G >= 2 && !no_narrow;
   if (narrow) {
-    a.items = a.witems; a.num_items = a.num_witems; a.num_empty = 0;
+    a.items = a.witems; a.num_items = a.num_witems;
+    if (RGNN_NARROW_EMPTY) a.num_empty = 0;  // the narrow pass writes the empty rows too
   } else {
     a.row_ptr = nullptr;
   }
