@@ -1,4 +1,4 @@
 mkdir -p gpurun_out/c8
-timeout 1200 bash tools/variants.sh mag am wikikg2 > gpurun_out/c8/variants.txt 2>&1
-cp variants/EMPTY0.so paper_2301_06284_b200/librgnn.so
-timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_compact.py -x -q > gpurun_out/c8/pytest_empty0.log 2>&1; echo "rc $?" >> gpurun_out/c8/pytest_empty0.log
+for c in mag am; do timeout 300 python bench.py --config $c --steps 30 --warmup 5 --no-e2e --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(\"$c\", round(d[\"ms_per_step\"],3), d[\"phases_ms_per_step\"])" >> gpurun_out/c8/dst.txt; done
+RGNN_BWD_TM=1 timeout 300 python bench.py --config am --steps 30 --warmup 5 --no-e2e --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(\"am tm\", round(d[\"ms_per_step\"],3), d[\"phases_ms_per_step\"])" >> gpurun_out/c8/dst.txt
+timeout 600 python -m pytest tests/test_gpu_bwd_tm.py -x -q > gpurun_out/c8/pytest.log 2>&1; echo "rc $?" >> gpurun_out/c8/pytest.log
