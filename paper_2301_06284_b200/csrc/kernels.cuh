@@ -70,6 +70,7 @@ struct AggArgs {
   const void* X;
   int64_t v0;
   const float* U;
+  int R;                 // relations (rows of U)
   float slope;
   const void* Z0;        // RGCN self-loop rows [V_own, N] T or null
   const float* slot_scale;  // RGCN compact: 1/c of slot q (Z rows unscaled), or null

@@ -272,7 +272,7 @@ static rgnn_status forward(const rgnn_graph* g, int model, int K, int N, int pre
     aa.pos = g->zrow_slot;
     if (model == RGNN_RGCN) aa.slot_scale = g->invc_slot;  // 1/c applied per edge in the walk
   }
-  aa.v0 = g->v0; aa.slope = slope; aa.Y = Y; aa.part = w.part; aa.split_rows = g->split_rows;
+  aa.v0 = g->v0; aa.R = g->R; aa.slope = slope; aa.Y = Y; aa.part = w.part; aa.split_rows = g->split_rows;
   aa.num_split_rows = g->num_split_rows; aa.empty_rows = g->empty_rows; aa.num_empty = g->num_empty;
   aa.row_ptr = g->row_ptr; aa.V_own = g->V_own; aa.narrow = g->narrow_cap; aa.witems = g->witems;
   aa.num_witems = g->num_witems;

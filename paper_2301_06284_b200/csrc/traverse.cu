@@ -62,18 +62,18 @@ __device__ __forceinline__ void load_slice(const T* p, float* out) {
 }
 
 // x . U[r] over this lane's KPL features (U fp32, float4 loads when possible).
-template <int KPL>
+template <int KPL, bool SM = false>
 __device__ __forceinline__ float dot_u(const float* xv, const float* Ur) {
   float d = 0.f;
   if constexpr (KPL % 4 == 0) {
 #pragma unroll
     for (int i = 0; i < KPL; i += 4) {
-      const float4 u = __ldg(reinterpret_cast<const float4*>(Ur + i));
+      const float4 u = SM ? *reinterpret_cast<const float4*>(Ur + i) : __ldg(reinterpret_cast<const float4*>(Ur + i));
       d = fmaf(xv[i], u.x, d); d = fmaf(xv[i + 1], u.y, d); d = fmaf(xv[i + 2], u.z, d); d = fmaf(xv[i + 3], u.w, d);
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < KPL; ++i) d = fmaf(xv[i], __ldg(Ur + i), d);
+    for (int i = 0; i < KPL; ++i) d = fmaf(xv[i], SM ? Ur[i] : __ldg(Ur + i), d);
   }
   return d;
 }
@@ -327,8 +327,9 @@ __device__ __forceinline__ void narrow_rows_pipe(const AggArgs& a, int64_t warp0
 // The same walk without the cross-row-group pipeline (measured faster for RGAT, whose per-row
 // x_dst slice and per-edge U dot make the pipelined version spill or lose a resident block:
 // AM 0.354 vs 0.402 ms; RGCN gains from the pipeline: wikikg2 walk 1.00 -> 0.77 ms).
-template <typename T, int K, int N, bool RGAT>
-__device__ __forceinline__ void narrow_rows(const AggArgs& a, int64_t warp0, int64_t nwarps, int lane) {
+template <typename T, int K, int N, bool RGAT, bool USM = false>
+__device__ __forceinline__ void narrow_rows(const AggArgs& a, int64_t warp0, int64_t nwarps, int lane,
+                                            const float* Uw) {
   using S = WalkShape<T, K, N>;
   constexpr int EPL = S::EPL, L = S::L, G = S::G, KPL = S::KPL;
   constexpr int UN = L < RGNN_NARROW_UN ? L : RGNN_NARROW_UN;  // edges per group step
@@ -383,7 +384,7 @@ __device__ __forceinline__ void narrow_rows(const AggArgs& a, int64_t warp0, int
       if constexpr (RGAT) {
         float d[UN];
 #pragma unroll
-        for (int u = 0; u < UN; ++u) d[u] = dot_u<KPL>(xv, a.U + (size_t)rr[u] * K + l * KPL);
+        for (int u = 0; u < UN; ++u) d[u] = dot_u<KPL, USM>(xv, Uw + (size_t)rr[u] * K + l * KPL);
 #pragma unroll
         for (int u = 0; u < UN; ++u) {
 #pragma unroll
@@ -437,10 +438,22 @@ __device__ __forceinline__ void narrow_rows(const AggArgs& a, int64_t warp0, int
 #ifndef RGNN_NARROW_MINB_RGAT
 #define RGNN_NARROW_MINB_RGAT 4
 #endif
-template <typename T, int K, int N, bool RGAT>
+// USM: the fused attention vectors U[r] (R x K fp32) staged in shared memory (dynamic, sized R*K*4 at launch)
+#ifndef RGNN_WALK_USMEM
+#define RGNN_WALK_USMEM 1  // measured r02: AM walk 0.618 -> 0.595 ms, ogbn-mag 1.815 -> 1.792 ms
+#endif
+template <typename T, int K, int N, bool RGAT, bool USM = false>
 __global__ void __launch_bounds__(256, RGAT ? RGNN_NARROW_MINB_RGAT : 3) k_aggregate_narrow(AggArgs a) {
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  if constexpr (RGAT) narrow_rows<T, K, N, RGAT>(a, w0, nw, threadIdx.x & 31);
+  extern __shared__ float4 su4[];
+  const float* Uw = a.U;
+  if constexpr (RGAT && USM) {
+    float* su = reinterpret_cast<float*>(su4);
+    for (int i = threadIdx.x; i < a.R * K / 4; i += blockDim.x) su4[i] = __ldg(reinterpret_cast<const float4*>(a.U) + i);
+    __syncthreads();
+    Uw = su;
+  }
+  if constexpr (RGAT) narrow_rows<T, K, N, RGAT, USM>(a, w0, nw, threadIdx.x & 31, Uw);
   else narrow_rows_pipe<T, K, N, RGAT>(a, w0, nw, threadIdx.x & 31);
   peer_fence(a);
 }
@@ -1036,8 +1049,11 @@ static rgnn_status aggregate(bool rgat, const AggArgs& a_in, cudaStream_t s) {
   }
   constexpr int G = WalkShape<T, K, N>::G;
   if (narrow) {  // the narrow rows (and the empty ones) first, one lane group per row
-    auto kn = rgat ? k_aggregate_narrow<T, K, N, true> : k_aggregate_narrow<T, K, N, false>;
-    RGNN_LAUNCH(kn, warps_grid((a.V_own + G - 1) / G), 256, 0, s, a);
+    const size_t ub = (size_t)a.R * K * sizeof(float);
+    const bool usm = RGNN_WALK_USMEM && rgat && a.R > 0 && ub <= 48 * 1024;
+    auto kn = !rgat ? k_aggregate_narrow<T, K, N, false> : usm ? k_aggregate_narrow<T, K, N, true, true>
+                                                               : k_aggregate_narrow<T, K, N, true>;
+    RGNN_LAUNCH(kn, warps_grid((a.V_own + G - 1) / G), 256, usm ? ub : 0, s, a);
   }
   const int64_t work = a.num_items;
   if (a.num_empty > 0) {

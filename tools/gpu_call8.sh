@@ -1,4 +1,3 @@
 mkdir -p gpurun_out/c8
-for c in mag am; do timeout 300 python bench.py --config $c --steps 30 --warmup 5 --no-e2e --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(\"$c\", round(d[\"ms_per_step\"],3), d[\"phases_ms_per_step\"])" >> gpurun_out/c8/dst.txt; done
-RGNN_BWD_TM=1 timeout 300 python bench.py --config am --steps 30 --warmup 5 --no-e2e --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(\"am tm\", round(d[\"ms_per_step\"],3), d[\"phases_ms_per_step\"])" >> gpurun_out/c8/dst.txt
-timeout 600 python -m pytest tests/test_gpu_bwd_tm.py -x -q > gpurun_out/c8/pytest.log 2>&1; echo "rc $?" >> gpurun_out/c8/pytest.log
+timeout 1200 bash tools/variants.sh am mag > gpurun_out/c8/variants_usm.txt 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_compact.py tests/test_gpu_bwd_tm.py -x -q > gpurun_out/c8/pytest_usm.log 2>&1; echo "rc $?" >> gpurun_out/c8/pytest_usm.log
