@@ -101,7 +101,12 @@ struct FwdCfg {
   static constexpr int SMEM0 = 1024 + STAGES * A_BYTES + 2 * B_BYTES + STG_BYTES + N * 4 + 256;
   // tile descriptors of the CTA's range cached in shared memory (up to TCAP, in what is left of
   // 227 KB): every role reads its next tile without a dependent global load
-  static constexpr int TCAP_RAW = (227 * 1024 - SMEM0 - 64) / 16;
+#ifndef RGNN_FWD_MINB64
+#define RGNN_FWD_MINB64 2  // resident CTAs per SM at d_in, d_out <= 64 (registers capped at 112, smem halved; measured
+                           // r02: AM 0.228 -> 0.169 ms, wikikg2 0.602 -> 0.444 ms against one CTA per SM)
+#endif
+  static constexpr int MINB = (K <= 64 && N <= 64) ? RGNN_FWD_MINB64 : 1;
+  static constexpr int TCAP_RAW = (227 * 1024 / MINB - 1024 * (MINB - 1) - SMEM0 - 64) / 16;
   // (measured: AM / wikikg2 d = 64 typed GEMM -7%; at d_in = 128 the global descriptor loads are
   // hidden by the longer tiles and the cache costs 7% on ogbn-mag, so it is off there)
   static constexpr int TCAP = K > 64 ? 0 : (TCAP_RAW > 4096 ? 4096 : (TCAP_RAW < 0 ? 0 : TCAP_RAW));
@@ -125,7 +130,7 @@ struct TcFwdParams {
 };
 
 template <int K, int N, bool F32OUT>
-__global__ void __launch_bounds__(288, 1)
+__global__ void __launch_bounds__(288, FwdCfg<K, N>::MINB)
     k_gemm_fwd_tc(const __grid_constant__ CUtensorMap wmap, TcFwdParams pr) {
   using C = FwdCfg<K, N>;
   extern __shared__ uint8_t smem_raw[];
@@ -380,7 +385,7 @@ static rgnn_status gemm_fwd_tc(const GemmFwdArgs& a, cudaStream_t s) {
   int dev, sms;
   RGNN_CUDA_TRY(cudaGetDevice(&dev));
   RGNN_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, sms);
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * C::MINB);
   const int64_t per = (ntiles + grid - 1) / grid;
   const int tcap = a.tiles ? (int)std::min<int64_t>(per, C::TCAP) : 0;
   TcFwdParams pr{a.tiles, a.num_tiles, a.rows, a.gofs, a.gather, static_cast<const __nv_bfloat16*>(a.X),

@@ -83,14 +83,14 @@ __device__ __forceinline__ float dot_u(const float* xv, const float* Ur) {
 // in ascending order) and x_dst . U[r] depends only on (dst, r), so it is recomputed only when
 // some group's relation changes (warp-uniform vote: no divergence) -- chosen for graphs with
 // long (etype, dst) runs.  Otherwise one dot per edge, UNR independent chains.
-template <int K, int L, int KPL, int UNR, bool CACHE>
+template <int K, int L, int KPL, int UNR, bool CACHE, bool USM = false>
 __device__ __forceinline__ void dst_scores(const float* xv, const float* U, int l, const int* rr, const float* ssv,
                                            int& cr, float& cd, float* sc) {
   if constexpr (CACHE) {
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       if (__any_sync(0xffffffffu, rr[u] != cr)) {
-        float d = dot_u<KPL>(xv, U + (size_t)rr[u] * K + l * KPL);
+        float d = dot_u<KPL, USM>(xv, U + (size_t)rr[u] * K + l * KPL);
 #pragma unroll
         for (int o = L / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
         cd = d;
@@ -100,7 +100,7 @@ __device__ __forceinline__ void dst_scores(const float* xv, const float* U, int 
     }
   } else {
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) sc[u] = dot_u<KPL>(xv, U + (size_t)rr[u] * K + l * KPL);
+    for (int u = 0; u < UNR; ++u) sc[u] = dot_u<KPL, USM>(xv, U + (size_t)rr[u] * K + l * KPL);
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
 #pragma unroll
@@ -469,12 +469,19 @@ __global__ void __launch_bounds__(256, RGAT ? RGNN_NARROW_MINB_RGAT : 3) k_aggre
 #ifndef RGNN_RING
 #define RGNN_RING 4  // cp.async ring depth of the RGCN walk (steps of Z rows in flight + 1)
 #endif
-template <typename T, int K, int N, bool RGAT, bool CACHE>
+template <typename T, int K, int N, bool RGAT, bool CACHE, bool USM = false>
 __global__ void __launch_bounds__(256, RGNN_AGG_MINB) k_aggregate(AggArgs a) {
   using S = WalkShape<T, K, N>;
   constexpr int EPL = S::EPL, L = S::L, G = S::G, UNR = S::UNR, B = S::B, KPL = S::KPL;
   const T* Z = static_cast<const T*>(a.Z);
   const T* X = static_cast<const T*>(a.X);
+  extern __shared__ float4 su4[];
+  const float* Uw = a.U;
+  if constexpr (RGAT && USM) {  // U[r] staged in shared memory (per-edge dots when runs are short)
+    for (int i = threadIdx.x; i < a.R * K / 4; i += blockDim.x) su4[i] = __ldg(reinterpret_cast<const float4*>(a.U) + i);
+    __syncthreads();
+    Uw = reinterpret_cast<const float*>(su4);
+  }
   const int lane = threadIdx.x & 31, g = lane / L, l = lane % L;
   const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -540,7 +547,7 @@ __global__ void __launch_bounds__(256, RGNN_AGG_MINB) k_aggregate(AggArgs a) {
         }
       }
 #endif
-      if constexpr (RGAT) dst_scores<K, L, KPL, UNR, CACHE>(xv, a.U, l, rr, ssv, cr, cd, sc);
+      if constexpr (RGAT) dst_scores<K, L, KPL, UNR, CACHE, USM>(xv, Uw, l, rr, ssv, cr, cd, sc);
       else {
 #pragma unroll
         for (int u = 0; u < UNR; ++u) sc[u] = ssv[u];  // edge weight (1 when Z rows are pre-scaled)
@@ -1074,9 +1081,12 @@ static rgnn_status aggregate(bool rgat, const AggArgs& a_in, cudaStream_t s) {
       RGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       RGNN_LAUNCH(kern, warps_grid(work), 256, smem, s, a);
     } else {
+      const size_t ub = (size_t)a.R * K * sizeof(float);
+      const bool usm = RGNN_WALK_USMEM && rgat && !a.cache_dst && a.R > 0 && ub <= 48 * 1024;
       auto kern = !rgat ? k_aggregate<T, K, N, false, false>
-                  : a.cache_dst ? k_aggregate<T, K, N, true, true> : k_aggregate<T, K, N, true, false>;
-      RGNN_LAUNCH(kern, warps_grid(work), 256, 0, s, a);
+                  : a.cache_dst ? k_aggregate<T, K, N, true, true>
+                  : usm ? k_aggregate<T, K, N, true, false, true> : k_aggregate<T, K, N, true, false>;
+      RGNN_LAUNCH(kern, warps_grid(work), 256, usm ? ub : 0, s, a);
     }
   }
   if (a.num_split_rows > 0) {
