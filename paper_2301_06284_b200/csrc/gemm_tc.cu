@@ -94,18 +94,19 @@ struct FwdCfg {
 #ifndef RGNN_FWD_RING_KB
 #define RGNN_FWD_RING_KB 64  // measured: 64 KB of A stages beats 32, 48, 96, 128 (mag, AM, wikikg2)
 #endif
-  static constexpr int STAGES = (RGNN_FWD_RING_KB * 1024) / A_BYTES > 8 ? 8 : (RGNN_FWD_RING_KB * 1024) / A_BYTES;
+#ifndef RGNN_FWD_MINB64
+#define RGNN_FWD_MINB64 3  // resident CTAs per SM at d_in, d_out <= 64, with a 32 KB A ring each (measured r02: AM
+                           // 0.228 / 0.169 / 0.147 ms and wikikg2 0.602 / 0.444 / 0.375 ms with 1 / 2 / 3 CTAs per SM)
+#endif
+  static constexpr int MINB = (K <= 64 && N <= 64) ? RGNN_FWD_MINB64 : 1;
+  static constexpr int RING_KB = MINB >= 3 ? 32 : RGNN_FWD_RING_KB;
+  static constexpr int STAGES = (RING_KB * 1024) / A_BYTES > 8 ? 8 : (RING_KB * 1024) / A_BYTES;
   static constexpr int DEPTH = STAGES - 1;                  // cp.async groups kept in flight per producer thread
   static constexpr int STG_BYTES = M * N * 2;
   static constexpr int NCOLS = (2 * N) <= 32 ? 32 : (2 * N) <= 64 ? 64 : (2 * N) <= 128 ? 128 : 256;
   static constexpr int SMEM0 = 1024 + STAGES * A_BYTES + 2 * B_BYTES + STG_BYTES + N * 4 + 256;
   // tile descriptors of the CTA's range cached in shared memory (up to TCAP, in what is left of
-  // 227 KB): every role reads its next tile without a dependent global load
-#ifndef RGNN_FWD_MINB64
-#define RGNN_FWD_MINB64 2  // resident CTAs per SM at d_in, d_out <= 64 (registers capped at 112, smem halved; measured
-                           // r02: AM 0.228 -> 0.169 ms, wikikg2 0.602 -> 0.444 ms against one CTA per SM)
-#endif
-  static constexpr int MINB = (K <= 64 && N <= 64) ? RGNN_FWD_MINB64 : 1;
+  // 227 KB per SM): every role reads its next tile without a dependent global load
   static constexpr int TCAP_RAW = (227 * 1024 / MINB - 1024 * (MINB - 1) - SMEM0 - 64) / 16;
   // (measured: AM / wikikg2 d = 64 typed GEMM -7%; at d_in = 128 the global descriptor loads are
   // hidden by the longer tiles and the cache costs 7% on ogbn-mag, so it is off there)
