@@ -111,7 +111,11 @@ __device__ __forceinline__ float leaky_f(float x, float s) { return x > 0.f ? x 
 
 // GAT = true: RGAT (dZ = alpha G_v + dpre A[r,0], bvec, dst term); false: RGCN (dZ = G_v / c_{v,r}).
 template <int K, int N, bool GAT, bool CM>
-__global__ void __launch_bounds__(BfCfg<K, N, GAT>::THREADS, 1)
+#ifndef RGNN_BWD_MINB64
+#define RGNN_BWD_MINB64 1  // resident CTAs per SM at d_out = 64 (measured r02: 2 CTAs of 32-position stages and 8 compute
+                           // warps, AM 0.757 -> 0.856 ms, wikikg2 0.870 -> 1.19 ms)
+#endif
+__global__ void __launch_bounds__(BfCfg<K, N, GAT>::THREADS, N == 64 ? RGNN_BWD_MINB64 : 1)
     k_bwd_fused_tc(BwdFusedParams pr) {
   using C = BfCfg<K, N, GAT>;
   constexpr int L = C::L, PG = C::PG, KPL = C::KPL, EPL = C::EPL;
