@@ -469,19 +469,13 @@ __global__ void __launch_bounds__(256, RGAT ? RGNN_NARROW_MINB_RGAT : 3) k_aggre
 #ifndef RGNN_RING
 #define RGNN_RING 4  // cp.async ring depth of the RGCN walk (steps of Z rows in flight + 1)
 #endif
-template <typename T, int K, int N, bool RGAT, bool CACHE, bool USM = false>
+template <typename T, int K, int N, bool RGAT, bool CACHE>
 __global__ void __launch_bounds__(256, RGNN_AGG_MINB) k_aggregate(AggArgs a) {
   using S = WalkShape<T, K, N>;
   constexpr int EPL = S::EPL, L = S::L, G = S::G, UNR = S::UNR, B = S::B, KPL = S::KPL;
   const T* Z = static_cast<const T*>(a.Z);
   const T* X = static_cast<const T*>(a.X);
-  extern __shared__ float4 su4[];
-  const float* Uw = a.U;
-  if constexpr (RGAT && USM) {  // U[r] staged in shared memory (per-edge dots when runs are short)
-    for (int i = threadIdx.x; i < a.R * K / 4; i += blockDim.x) su4[i] = __ldg(reinterpret_cast<const float4*>(a.U) + i);
-    __syncthreads();
-    Uw = reinterpret_cast<const float*>(su4);
-  }
+
   const int lane = threadIdx.x & 31, g = lane / L, l = lane % L;
   const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -547,7 +541,7 @@ __global__ void __launch_bounds__(256, RGNN_AGG_MINB) k_aggregate(AggArgs a) {
         }
       }
 #endif
-      if constexpr (RGAT) dst_scores<K, L, KPL, UNR, CACHE, USM>(xv, Uw, l, rr, ssv, cr, cd, sc);
+      if constexpr (RGAT) dst_scores<K, L, KPL, UNR, CACHE>(xv, a.U, l, rr, ssv, cr, cd, sc);
       else {
 #pragma unroll
         for (int u = 0; u < UNR; ++u) sc[u] = ssv[u];  // edge weight (1 when Z rows are pre-scaled)
@@ -1081,12 +1075,10 @@ static rgnn_status aggregate(bool rgat, const AggArgs& a_in, cudaStream_t s) {
       RGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       RGNN_LAUNCH(kern, warps_grid(work), 256, smem, s, a);
     } else {
-      const size_t ub = (size_t)a.R * K * sizeof(float);
-      const bool usm = RGNN_WALK_USMEM && rgat && !a.cache_dst && a.R > 0 && ub <= 48 * 1024;
+      // (U in shared memory here as in the narrow walk measured slower: AM wide walk 0.173 -> 0.190 ms)
       auto kern = !rgat ? k_aggregate<T, K, N, false, false>
-                  : a.cache_dst ? k_aggregate<T, K, N, true, true>
-                  : usm ? k_aggregate<T, K, N, true, false, true> : k_aggregate<T, K, N, true, false>;
-      RGNN_LAUNCH(kern, warps_grid(work), 256, usm ? ub : 0, s, a);
+                  : a.cache_dst ? k_aggregate<T, K, N, true, true> : k_aggregate<T, K, N, true, false>;
+      RGNN_LAUNCH(kern, warps_grid(work), 256, 0, s, a);
     }
   }
   if (a.num_split_rows > 0) {
