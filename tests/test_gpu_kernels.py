@@ -14,7 +14,8 @@ def _align(x, a=256):
     return (x + a - 1) // a * a
 
 
-@pytest.mark.parametrize("K,N", [(32, 32), (64, 64), (128, 128), (64, 128), (128, 64), (32, 128), (128, 32)])
+@pytest.mark.parametrize("K,N", [(32, 32), (64, 64), (128, 128), (64, 128), (128, 64), (32, 128), (128, 32), (64, 32),
+                                 (32, 64)])
 def test_tc_gemm_matches_numpy(rgnn, K, N):
     import torch
     g = synth.random_graph(3000, 20000, 9, seed=K + N)
