@@ -16,7 +16,11 @@
 namespace rgnn {
 
 template <typename T, int K>
-__global__ void __launch_bounds__(512) k_dst_term(const Tile* __restrict__ chunks, const int32_t* __restrict__ dst_s,
+#ifndef RGNN_DST_MINB
+#define RGNN_DST_MINB 3  // minimum resident 512-thread blocks per SM (measured r02 on ogbn-mag: 1 -> 0.27 ms, 3 -> 0.20,
+                         // 4 -> 0.21)
+#endif
+__global__ void __launch_bounds__(512, RGNN_DST_MINB) k_dst_term(const Tile* __restrict__ chunks, const int32_t* __restrict__ dst_s,
                                                   const float* __restrict__ dpre, const T* __restrict__ X, int64_t v0,
                                                   float* __restrict__ cpart) {
   // lane l holds features l*FPL .. l*FPL+FPL-1 (one 4- or 8-byte load per X row); K = 32: one each
