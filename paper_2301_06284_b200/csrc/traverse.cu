@@ -631,11 +631,17 @@ __global__ void __launch_bounds__(256, RGNN_AGG_MINB) k_aggregate(AggArgs a) {
 // items form one continuous stream of B-edge steps, so short rows do not drain
 // the pipeline.  Results are bit-identical to k_aggregate (same per-group edge
 // assignment, same arithmetic order).
-template <typename T, int K, int N, bool RGAT, int RING, bool CACHE>
+// BULK: each Z row (N * sizeof(T) bytes, contiguous in the ring: lanes g*L .. g*L+L-1 of a (slot, u)
+// entry hold one row) arrives by one 1-D TMA bulk copy issued by the edge's lane, completing on the slot's
+// mbarrier (expect_tx = the step's row bytes), instead of L 16-byte cp.async per row: one instruction per
+// row (tools/bulk_gather_bench.cu: random 256-byte rows at 6.9 TB/s, as many as register-held loads).
+template <typename T, int K, int N, bool RGAT, int RING, bool CACHE, bool BULK = false>
 __global__ void __launch_bounds__(256) k_aggregate_ring(AggArgs a) {
   using S = WalkShape<T, K, N>;
   constexpr int EPL = S::EPL, L = S::L, G = S::G, UNR = S::UNR, B = S::B, KPL = S::KPL;
+  constexpr int ROWB = N * (int)sizeof(T);
   extern __shared__ uint4 ring_smem[];
+  __shared__ uint64_t zbar[8][RING];  // BULK: per warp and slot
   const T* Z = static_cast<const T*>(a.Z);
   const T* X = static_cast<const T*>(a.X);
   const int lane = threadIdx.x & 31, g = lane / L, l = lane % L, wib = threadIdx.x >> 5;
@@ -665,21 +671,44 @@ __global__ void __launch_bounds__(256) k_aggregate_ring(AggArgs a) {
       if (pw < a.num_items) { pit = a.items[pw]; pbase = pit.q0; }
     }
   };
+  if constexpr (BULK) {
+    if (lane < RING) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(
+                                      &zbar[wib][lane])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+  }
   int pslot = 0;
   auto produce = [&]() {  // issue the copies of the producer's current step into ring slot pslot
     if (pw < a.num_items) {
       const int myp = np, myr = nr;
       const int q = pbase + lane;
       const bool ok = lane < B && q < pit.q1;
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const int j = u * G + g;
-        const int p = __shfl_sync(0xffffffffu, myp, j);
-        if (pbase + j < pit.q1)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(
-                           zring + ((size_t)pslot * UNR + u) * 32 + lane)),
-                       "l"(Z + (size_t)p * N + l * EPL)
+      if constexpr (BULK) {
+        const int nvalid = min(B, pit.q1 - pbase);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the slot's generic reads before the refill
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(
+                           &zbar[wib][pslot])), "r"(nvalid * ROWB)
                        : "memory");
+        __syncwarp();
+        if (ok) {  // lane j = u * G + g copies the row of edge j to entry (pslot, u), lanes g*L ..
+          const int u = lane / G, gg = lane % G;
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(zring + ((size_t)pslot * UNR + u) * 32 + gg * L)),
+                       "l"(Z + (size_t)myp * N), "r"(ROWB), "r"((uint32_t)__cvta_generic_to_shared(&zbar[wib][pslot]))
+                       : "memory");
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const int j = u * G + g;
+          const int p = __shfl_sync(0xffffffffu, myp, j);
+          if (pbase + j < pit.q1)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(
+                             zring + ((size_t)pslot * UNR + u) * 32 + lane)),
+                         "l"(Z + (size_t)p * N + l * EPL)
+                         : "memory");
+        }
       }
       if (ok && (RGAT || a.slot_scale))  // RGAT: s_src of the Z row; compact RGCN: 1/c of the slot
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(
@@ -699,6 +728,7 @@ __global__ void __launch_bounds__(256) k_aggregate_ring(AggArgs a) {
   for (int i = 0; i < RING - 1; ++i) produce();
 
   int cslot = 0;
+  uint32_t cuse = 0;  // BULK: steps consumed (mbarrier phase of the slot = (cuse / RING) & 1)
   for (int64_t w = warp0; w < a.num_items; w += nwarps) {
     const Item it = a.items[w];
     float acc[EPL];
@@ -712,6 +742,16 @@ __global__ void __launch_bounds__(256) k_aggregate_ring(AggArgs a) {
     for (int base = it.q0; base < it.q1; base += B) {
       produce();  // keeps RING-1 steps in flight
       asm volatile("cp.async.wait_group %0;" ::"n"(RING - 1) : "memory");
+      if constexpr (BULK) {
+        uint32_t done = 0;
+        const uint32_t ph = (cuse / RING) & 1;
+        while (!done)
+          asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                       : "=r"(done)
+                       : "r"((uint32_t)__cvta_generic_to_shared(&zbar[wib][cslot])), "r"(ph)
+                       : "memory");
+        ++cuse;
+      }
       __syncwarp();
       uint4 zr[UNR];
       float sc[UNR], ssv[UNR];
@@ -1070,8 +1110,10 @@ static rgnn_status aggregate(bool rgat, const AggArgs& a_in, cudaStream_t s) {
     if (ring) {
       constexpr int RING = RGNN_RING, UNR = WalkShape<T, K, N>::UNR;
       const size_t smem = 8 * (RING * UNR * 32 * sizeof(uint4) + RING * 32 * 2 * sizeof(float));
-      auto kern = !rgat ? k_aggregate_ring<T, K, N, false, RING, false>
-                  : a.cache_dst ? k_aggregate_ring<T, K, N, true, RING, true> : k_aggregate_ring<T, K, N, true, RING, false>;
+      static const bool bulk = getenv("RGNN_WALK_BULK") && atoi(getenv("RGNN_WALK_BULK")) != 0;
+      auto kern = !rgat ? (bulk ? k_aggregate_ring<T, K, N, false, RING, false, true> : k_aggregate_ring<T, K, N, false, RING, false>)
+                  : a.cache_dst ? (bulk ? k_aggregate_ring<T, K, N, true, RING, true, true> : k_aggregate_ring<T, K, N, true, RING, true>)
+                                : (bulk ? k_aggregate_ring<T, K, N, true, RING, false, true> : k_aggregate_ring<T, K, N, true, RING, false>);
       RGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       RGNN_LAUNCH(kern, warps_grid(work), 256, smem, s, a);
     } else {
