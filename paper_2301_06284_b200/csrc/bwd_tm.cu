@@ -233,18 +233,24 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
     };
     int src = 0, v = 0, p = 0, zr = 0;
     if (nsub > 0) load_idx(0, src, v, p, zr);
+    // the indices the prefetches need are loaded one iteration before they are used (a prefetch that
+    // waits for its own index load costs the producer a memory latency per stage)
+    constexpr int XA = C::STAGES + RGNN_TM_XPF - 1;  // X rows prefetched XA stages ahead
+    auto pf_src = [&](int it) { const int q = row0 + it * MT + lp; return q < row1 ? __ldg(pr.src_s + q) : -1; };
+    auto pf_dst = [&](int it) { const int q = row0 + it * MT + lp; return q < row1 ? __ldg(pr.dst_s + q) : -1; };
+    int xs = RGNN_TM_XPF > 0 ? pf_src(XA) : -1;
+    int rv = RGNN_TM_RPF > 0 ? pf_dst(RGNN_TM_RPF) : -1;
     for (int it = 0; it < nsub; ++it) {
       const int st = it % C::STAGES;
       const uint32_t use = (uint32_t)(it / C::STAGES);
       int nsrc = 0, nv = 0, np = 0, nzr = 0;
       if (it + 1 < nsub) load_idx(it + 1, nsrc, nv, np, nzr);
-      if (RGNN_TM_XPF > 0) {  // L2 prefetch of a later stage's X rows (the ring is only STAGES deep)
-        const int pf = row0 + (it + C::STAGES + RGNN_TM_XPF - 1) * MT + lp;
-        if (pf < row1) {
-          const char* xp = reinterpret_cast<const char*>(pr.X + (size_t)__ldg(pr.src_s + pf) * K);
+      const int xs_n = RGNN_TM_XPF > 0 ? pf_src(it + 1 + XA) : -1;
+      const int rv_n = RGNN_TM_RPF > 0 ? pf_dst(it + 1 + RGNN_TM_RPF) : -1;
+      if (RGNN_TM_XPF > 0 && xs >= 0) {  // L2 prefetch of a later stage's X rows (the ring is only STAGES deep)
+        const char* xp = reinterpret_cast<const char*>(pr.X + (size_t)xs * K);
 #pragma unroll
-          for (int o = 0; o < K * 2; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(xp + o));
-        }
+        for (int o = 0; o < K * 2; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(xp + o));
       }
       if (pw == 0) TMT(it, 0);
       if (use > 0) tc::mbar_wait(&empty[st], (use - 1) & 1);
@@ -270,8 +276,7 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
       // L2 prefetch of the per-destination rows (dY, Y, x of each run head) of stage it + RGNN_TM_RPF, so
       // that they have arrived when a compute group reads them (it does so as soon as a stage is issued)
       if (RGNN_TM_RPF > 0) {
-        const int pf = row0 + (it + RGNN_TM_RPF) * MT + lp;
-        const int vf = pf < row1 ? __ldg(pr.dst_s + pf) : -1;
+        const int vf = rv;
         const int vfp = __shfl_up_sync(0xffffffffu, vf, 1);
         if (vf >= 0 && (lane == 0 || vfp != vf)) {
           const char* gp = reinterpret_cast<const char*>(pr.dY + (size_t)vf * N);
@@ -287,6 +292,7 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
         }
       }
       src = nsrc; v = nv; p = np; zr = nzr;
+      xs = xs_n; rv = rv_n;
     }
     tc::cp_async_wait<0>();
   } else if (warp == 0) {
