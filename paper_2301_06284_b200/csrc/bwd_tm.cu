@@ -255,14 +255,6 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
       if (pw == 0) TMT(it, 0);
       if (use > 0) tc::mbar_wait(&empty[st], (use - 1) & 1);
       if (pw == 0) TMT(it, 1);
-      uint8_t* a = sA(st);
-#pragma unroll 4
-      for (int i = 0; i < 32 / C::RPI; ++i) {
-        const int rr = i * C::RPI + lane / C::CPR;
-        const int c = lane % C::CPR;
-        const int xr = __shfl_sync(0xffffffffu, src, rr);
-        tc::cp_async16(a + swz(c, pw * 32 + rr, MT), pr.X + (size_t)xr * K + c * 8);
-      }
       // the stage's destinations go out first (plain stores + idx_full): the compute group finds the
       // stage's runs and reads their rows while the X rows are still in flight
       sDst(st)[lp] = p < row1 ? v : -1;
@@ -270,6 +262,14 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
       if (p < row1) {
         cp_async4(sSs(st) + lp, pr.s_src + zr);
         cp_async4(sLse(st) + lp, pr.lse + v);
+      }
+      uint8_t* a = sA(st);
+#pragma unroll
+      for (int i = 0; i < 32 / C::RPI; ++i) {  // all row indices first, then the copies back to back
+        const int rr = i * C::RPI + lane / C::CPR;
+        const int c = lane % C::CPR;
+        const int xr = __shfl_sync(0xffffffffu, src, rr);
+        tc::cp_async16(a + swz(c, pw * 32 + rr, MT), pr.X + (size_t)xr * K + c * 8);
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&a_full[st])) : "memory");
       if (pw == 0) TMT(it, 2);
