@@ -55,6 +55,9 @@ struct TmCfg {
 #define RGNN_TM_RPF 2  // run rows (dY, Y, x of each run head) of stage it + RPF prefetched to L2 when stage it is
                        // issued (0: off)
 #endif
+#ifndef RGNN_TM_L1PF
+#define RGNN_TM_L1PF 0  // 1: the next stage's run rows prefetched into L1 by the producers (measured r02: 2.44 -> 2.47 ms)
+#endif
 #ifndef RGNN_TM_XPF
 #define RGNN_TM_XPF 2  // X rows of stage it + STAGES + XPF - 1 prefetched to L2 when stage it is issued (0: off)
 #endif
@@ -289,6 +292,21 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
           }
 #pragma unroll
           for (int o = 0; o < K * 2; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(xp + o));
+        }
+      }
+      if (RGNN_TM_L1PF && it + 1 < nsub) {  // the next stage's run rows into this SM's L1 (its run pass reads them)
+        const int vp1 = __shfl_up_sync(0xffffffffu, nv, 1);
+        if (np < row1 && (lane == 0 || vp1 != nv)) {
+          const char* gp = reinterpret_cast<const char*>(pr.dY + (size_t)nv * N);
+          const char* yp = reinterpret_cast<const char*>(pr.Y + (size_t)nv * N);
+          const char* xp = reinterpret_cast<const char*>(pr.X + (pr.v0 + nv) * (int64_t)K);
+#pragma unroll
+          for (int o = 0; o < N * 4; o += 128) {
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(gp + o));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(yp + o));
+          }
+#pragma unroll
+          for (int o = 0; o < K * 2; o += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(xp + o));
         }
       }
       src = nsrc; v = nv; p = np; zr = nzr;
