@@ -55,6 +55,10 @@ struct TmCfg {
 #define RGNN_TM_RPF 2  // run rows (dY, Y, x of each run head) of stage it + RPF prefetched to L2 when stage it is
                        // issued (0: off)
 #endif
+#ifndef RGNN_TM_EARLY
+#define RGNN_TM_EARLY 0  // 1: build the group's next run table and request its first run rows before this stage's
+                        // per-position pass (measured r02: 2.49 -> 3.05 ms on ogbn-mag)
+#endif
 #ifndef RGNN_TM_L1PF
 #define RGNN_TM_L1PF 0  // 1: the next stage's run rows prefetched into L1 by the producers (measured r02: 2.44 -> 2.47 ms)
 #endif
@@ -377,16 +381,13 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     constexpr int LPR = C::LPR, RPIT = C::RUNS_PI, BATCH = 4, KPL = K / LPR;
     const int sub = lane / LPR, ln = lane % LPR;
-    for (int it = grp; it < nsub; it += 2) {
+    volatile int* sFlag = reinterpret_cast<volatile int*>(tmem_slot + 1);  // per group: next stage staged
+    // (1) the stage's destination runs: a run = maximal block of stage rows with one destination (rows of
+    // a relation are sorted by destination); every warp of the group derives the same table, warp 0
+    // stores it.  Returns the number of runs.
+    auto build_table = [&](int it) -> int {
       const int st = it % C::STAGES, buf = it & 1;
-      const int p = row0 + it * MT + lp;
-      const bool valid = p < row1;
       tc::mbar_wait(&idx_full[st], (uint32_t)(it / C::STAGES) & 1);
-      if (gw == 0) TMT(it, 6);
-      // (1) the stage's destination runs: a run = maximal block of stage rows with one destination
-      // (rows of a relation are sorted by destination); every warp of the group derives the same
-      // table, warp 0 stores it.  The group's previous stage is finished by all its warps first.
-      tc::named_bar(9 + grp, 256);
       int nruns = 0, lastv = -2;
 #pragma unroll
       for (int c = 0; c < MT / 32; ++c) {
@@ -405,58 +406,70 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
         nruns += __popc(hb);
         lastv = __shfl_sync(0xffffffffu, v, 31);
       }
-      tc::named_bar(9 + grp, 256);
-      if (gw == 0) TMT(it, 7);
-      // (2) per run (warps of the group take interleaved runs, BATCH runs' loads in flight): G_v as a
-      // bf16 row (if j < CAP), S_v = G_v . Y_v and the destination score x_v . U[r], read once per run
-      for (int j0 = gw * RPIT; j0 < nruns; j0 += 8 * RPIT * BATCH) {
+      return nruns;
+    };
+    // (2) per run (warps of the group take interleaved runs, NB runs' loads in flight per warp): G_v as a
+    // bf16 row (if j < CAP), S_v = G_v . Y_v and the destination score x_v . U[r], read once per run
+    auto load_run = [&](int buf, int nruns, int jj, float4& g, float4& y, float* xv) {
+      if (jj < nruns) {
+        const int v = sHv(buf)[jj];
+        g = __ldg(reinterpret_cast<const float4*>(pr.dY + (size_t)v * N) + ln);
+        y = __ldg(reinterpret_cast<const float4*>(pr.Y + (size_t)v * N) + ln);
+        load_bf16<KPL>(pr.X + (pr.v0 + v) * (int64_t)K + ln * KPL, xv);
+      } else {
+        g = y = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < KPL; ++i) xv[i] = 0.f;
+      }
+    };
+    auto store_run = [&](int buf, int nruns, int jj, float4 g, float4 y, const float* xv) {
+      // G_v as the per-position pass sees it (bf16), so that sum_p alpha_p dalpha_p = S_v holds for the
+      // rounded values as it does in exact arithmetic (Y_v = sum_p alpha_p bf16(Z_p))
+      g = make_float4(bf16r(g.x), bf16r(g.y), bf16r(g.z), bf16r(g.w));
+      float sv = g.x * y.x;
+      sv = fmaf(g.y, y.y, sv);
+      sv = fmaf(g.z, y.z, sv);
+      sv = fmaf(g.w, y.w, sv);
+      float dsc = 0.f;
+#pragma unroll
+      for (int i = 0; i < KPL; ++i) dsc = fmaf(xv[i], sU[ln * KPL + i], dsc);
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) {
+        sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        dsc += __shfl_xor_sync(0xffffffffu, dsc, o);
+      }
+      if (jj < nruns) {
+        if (ln == 0) {
+          sS(buf)[jj] = sv;
+          sDs(buf)[jj] = dsc;
+        }
+        if (jj < C::CAP)
+          *reinterpret_cast<uint2*>(sG(buf) + (size_t)jj * N + ln * 4) =
+              make_uint2(tc::pack_bf16(g.x, g.y), tc::pack_bf16(g.z, g.w));
+      }
+    };
+    auto runs_from = [&](int buf, int nruns, int j0) {  // runs j0, j0 + 8 RPIT, ... of this warp, BATCH at a time
+      for (; j0 < nruns; j0 += 8 * RPIT * BATCH) {
         float4 g[BATCH], y[BATCH];
         float xv[BATCH][KPL];
-        int jj[BATCH];
 #pragma unroll
-        for (int b = 0; b < BATCH; ++b) {
-          jj[b] = j0 + b * 8 * RPIT + sub;
-          if (jj[b] < nruns) {
-            const int v = sHv(buf)[jj[b]];
-            g[b] = __ldg(reinterpret_cast<const float4*>(pr.dY + (size_t)v * N) + ln);
-            y[b] = __ldg(reinterpret_cast<const float4*>(pr.Y + (size_t)v * N) + ln);
-            load_bf16<KPL>(pr.X + (pr.v0 + v) * (int64_t)K + ln * KPL, xv[b]);
-          } else {
-            g[b] = y[b] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int b = 0; b < BATCH; ++b) load_run(buf, nruns, j0 + b * 8 * RPIT + sub, g[b], y[b], xv[b]);
 #pragma unroll
-            for (int i = 0; i < KPL; ++i) xv[b][i] = 0.f;
-          }
-        }
-#pragma unroll
-        for (int b = 0; b < BATCH; ++b) {
-          // G_v as the per-position pass sees it (bf16), so that sum_p alpha_p dalpha_p = S_v holds for
-          // the rounded values as it does in exact arithmetic (Y_v = sum_p alpha_p bf16(Z_p))
-          g[b] = make_float4(bf16r(g[b].x), bf16r(g[b].y), bf16r(g[b].z), bf16r(g[b].w));
-          float sv = g[b].x * y[b].x;
-          sv = fmaf(g[b].y, y[b].y, sv);
-          sv = fmaf(g[b].z, y[b].z, sv);
-          sv = fmaf(g[b].w, y[b].w, sv);
-          float dsc = 0.f;
-#pragma unroll
-          for (int i = 0; i < KPL; ++i) dsc = fmaf(xv[b][i], sU[ln * KPL + i], dsc);
-#pragma unroll
-          for (int o = LPR / 2; o > 0; o >>= 1) {
-            sv += __shfl_xor_sync(0xffffffffu, sv, o);
-            dsc += __shfl_xor_sync(0xffffffffu, dsc, o);
-          }
-          if (jj[b] < nruns) {
-            if (ln == 0) {
-              sS(buf)[jj[b]] = sv;
-              sDs(buf)[jj[b]] = dsc;
-            }
-            if (jj[b] < C::CAP)
-              *reinterpret_cast<uint2*>(sG(buf) + (size_t)jj[b] * N + ln * 4) =
-                  make_uint2(tc::pack_bf16(g[b].x, g[b].y), tc::pack_bf16(g[b].z, g[b].w));
-          }
-        }
+        for (int b = 0; b < BATCH; ++b) store_run(buf, nruns, j0 + b * 8 * RPIT + sub, g[b], y[b], xv[b]);
       }
+    };
+    auto prep = [&](int it) {  // blocking: the group's previous stage is finished by all its warps first
+      tc::named_bar(9 + grp, 256);
+      const int nr = build_table(it);
+      tc::named_bar(9 + grp, 256);
+      runs_from(it & 1, nr, gw * RPIT);
       tc::named_bar(9 + grp, 256);  // run rows and scalars visible to the group
-      if (gw == 0) TMT(it, 8);
+    };
+    if (grp < nsub) prep(grp);
+    for (int it = grp; it < nsub; it += 2) {
+      const int st = it % C::STAGES, buf = it & 1;
+      const int p = row0 + it * MT + lp;
+      const bool valid = p < row1;
       // (3) per position
       tc::mbar_wait(&a_full[st], (uint32_t)(it / C::STAGES) & 1);  // s_src, lse of the stage
       tc::mbar_wait(&zfull[buf], (uint32_t)(it >> 1) & 1);
@@ -470,6 +483,25 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
       const __nv_bfloat16* grow = sG(buf) + (size_t)(in_smem ? j : 0) * N + h * C::NH;
       const float* gglob = pr.dY + (size_t)(valid && !in_smem ? sDst(st)[lp] : 0) * N + h * C::NH;
       const float alpha = valid ? __expf((pre > 0.f ? pre : pr.slope * pre) - lse) : 0.f;
+      // the group's next stage: if its indices are already staged, its run table is built and the first
+      // of its run rows are requested now (in flight during this stage's per-position pass)
+      const bool nxt = it + 2 < nsub;
+      bool early = false;
+      int nr2 = 0;
+      float4 eg[2], ey[2];
+      float ex[2][KPL];
+      if (RGNN_TM_EARLY && nxt) {
+        if (gw == 0 && lane == 0)
+          sFlag[grp] = tc::mbar_try(&idx_full[(it + 2) % C::STAGES], (uint32_t)((it + 2) / C::STAGES) & 1) ? 1 : 0;
+        tc::named_bar(9 + grp, 256);  // every warp has read this stage's run entries; the flag is visible
+        early = sFlag[grp] != 0;
+        if (early) {
+          nr2 = build_table(it + 2);
+          tc::named_bar(9 + grp, 256);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) load_run(buf, nr2, gw * RPIT + e * 8 * RPIT + sub, eg[e], ey[e], ex[e]);
+        }
+      }
       if (gw == 0) TMT(it, 10);
       if (C::DZB == 1) {  // one dZ buffer: the dW MMAs of the previous stage (other group) have read it
         if (it >= 1) tc::mbar_wait(&dzempty[0], (uint32_t)(it - 1) & 1);
@@ -542,6 +574,15 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&bfull[buf]);
       if (gw == 0) TMT(it, 13);
+      if (early) {  // the next stage's run rows (their first loads were in flight during the pass above)
+        tc::named_bar(9 + grp, 256);  // every warp is done with this stage's run rows
+#pragma unroll
+        for (int e = 0; e < 2; ++e) store_run(buf, nr2, gw * RPIT + e * 8 * RPIT + sub, eg[e], ey[e], ex[e]);
+        runs_from(buf, nr2, gw * RPIT + 2 * 8 * RPIT);
+        tc::named_bar(9 + grp, 256);
+      } else if (nxt) {
+        prep(it + 2);
+      }
     }
     // epilogue: TMEM accumulators -> part[c]; the four warps of a lane quarter split the columns
     tc::mbar_wait(acc_full, 0);
