@@ -1,3 +1,4 @@
 mkdir -p gpurun_out/c4
-timeout 900 python -m pytest tests/test_gpu_bwd_tm.py tests/test_gpu_parity.py tests/test_gpu_compact.py tests/test_gpu_fullsize.py -x -q > gpurun_out/c4/pytest.log 2>&1; echo "rc $?" >> gpurun_out/c4/pytest.log
-for c in mag am wikikg2; do timeout 300 python bench.py --config $c --steps 30 --warmup 5 --no-e2e --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(\"$c\", round(d[\"ms_per_step\"],3), d[\"phases_ms_per_step\"])" >> gpurun_out/c4/variants.txt; done
+mv variants/trace.so /tmp/trace.so
+cp paper_2301_06284_b200/librgnn.so /tmp/base.so; cp /tmp/trace.so paper_2301_06284_b200/librgnn.so
+bash tools/gpu_call3.sh; cp /tmp/base.so paper_2301_06284_b200/librgnn.so
