@@ -59,9 +59,6 @@ struct TmCfg {
 #define RGNN_TM_EARLY 0  // 1: build the group's next run table and request its first run rows before this stage's
                         // per-position pass (measured r02: 2.49 -> 3.05 ms on ogbn-mag)
 #endif
-#ifndef RGNN_TM_L1PF
-#define RGNN_TM_L1PF 0  // 1: the next stage's run rows prefetched into L1 by the producers (measured r02: 2.44 -> 2.47 ms)
-#endif
 #ifndef RGNN_TM_XPF
 #define RGNN_TM_XPF 2  // X rows of stage it + STAGES + XPF - 1 prefetched to L2 when stage it is issued (0: off)
 #endif
@@ -69,7 +66,11 @@ struct TmCfg {
   static constexpr int ST_FIT = (227 * 1024 - FIXED) / (A_BYTES + SC_BYTES);
   static constexpr int STAGES = ST_FIT > RGNN_TM_SMAX ? RGNN_TM_SMAX : ST_FIT;
   static constexpr int SMEM = FIXED + STAGES * (A_BYTES + SC_BYTES);
-  static constexpr int PW = 4, CW = 16;          // producers, two compute groups of 8 warps
+#ifndef RGNN_TM_PW
+#define RGNN_TM_PW 4  // producer warps (the first four stage the per-position scalars; 8 measured slower: 2.50 -> 2.69 ms,
+                      // the compute warps lose registers at 800 threads)
+#endif
+  static constexpr int PW = RGNN_TM_PW, CW = 16;  // producers, two compute groups of 8 warps
   static constexpr int THREADS = 32 * (1 + PW + CW);
   static constexpr int ZOFF = N + 32;            // TMEM: [0,N) dW, [N,N+16) Db, Z buffers at ZOFF, ZOFF+N
   static constexpr int NCOLS = ZOFF + 2 * N <= 256 ? 256 : 512;
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
     for (int i = 0; i < C::STAGES; ++i) {
       tc::mbar_init(&a_full[i], C::PW * 32);
       tc::mbar_init(&empty[i], 1);
-      tc::mbar_init(&idx_full[i], C::PW * 32);
+      tc::mbar_init(&idx_full[i], 4 * 32);  // producer warps 0..3 stage the destinations
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&zfull[i], 1);
@@ -230,28 +231,44 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
 
   if (warp >= 1 && warp <= C::PW) {
     // ------------------------------------------------------------ producers
+    // warps 0..3 of the producers stage the per-position scalars (one position per thread); all PW warps
+    // copy X rows, MT / PW rows each (more warps issue a stage's copies sooner)
+    constexpr int RWX = MT / C::PW;  // X rows per producer warp
     const int pw = warp - 1, lp = pw * 32 + lane;
-    auto load_idx = [&](int it, int& src, int& v, int& p, int& zr) {
+    const bool spos = pw < 4;        // this warp stages scalars
+    auto load_idx = [&](int it, int& v, int& p, int& zr) {
       p = row0 + it * MT + lp;
-      const int pc = min(p, row1 - 1);  // padding rows re-read a valid X row; their dZ is zero
-      src = __ldg(pr.src_s + pc);
+      const int pc = min(p, row1 - 1);
       v = __ldg(pr.dst_s + pc);
       zr = pr.zmap ? __ldg(pr.zmap + pc) : pc;
     };
+    auto load_src = [&](int it) {  // lanes < RWX: source row of X row pw * RWX + lane of stage it
+      const int q = min(row0 + it * MT + pw * RWX + (lane % RWX), row1 - 1);  // padding rows re-read a valid row
+      return __ldg(pr.src_s + q);
+    };
     int src = 0, v = 0, p = 0, zr = 0;
-    if (nsub > 0) load_idx(0, src, v, p, zr);
+    if (nsub > 0) {
+      src = load_src(0);
+      if (spos) load_idx(0, v, p, zr);
+    }
     // the indices the prefetches need are loaded one iteration before they are used (a prefetch that
     // waits for its own index load costs the producer a memory latency per stage)
     constexpr int XA = C::STAGES + RGNN_TM_XPF - 1;  // X rows prefetched XA stages ahead
-    auto pf_src = [&](int it) { const int q = row0 + it * MT + lp; return q < row1 ? __ldg(pr.src_s + q) : -1; };
-    auto pf_dst = [&](int it) { const int q = row0 + it * MT + lp; return q < row1 ? __ldg(pr.dst_s + q) : -1; };
+    auto pf_src = [&](int it) {
+      const int q = row0 + it * MT + pw * RWX + (lane % RWX);
+      return (lane < RWX && q < row1) ? __ldg(pr.src_s + q) : -1;
+    };
+    auto pf_dst = [&](int it) { const int q = row0 + it * MT + lp; return (spos && q < row1) ? __ldg(pr.dst_s + q) : -1; };
     int xs = RGNN_TM_XPF > 0 ? pf_src(XA) : -1;
     int rv = RGNN_TM_RPF > 0 ? pf_dst(RGNN_TM_RPF) : -1;
     for (int it = 0; it < nsub; ++it) {
       const int st = it % C::STAGES;
       const uint32_t use = (uint32_t)(it / C::STAGES);
       int nsrc = 0, nv = 0, np = 0, nzr = 0;
-      if (it + 1 < nsub) load_idx(it + 1, nsrc, nv, np, nzr);
+      if (it + 1 < nsub) {
+        nsrc = load_src(it + 1);
+        if (spos) load_idx(it + 1, nv, np, nzr);
+      }
       const int xs_n = RGNN_TM_XPF > 0 ? pf_src(it + 1 + XA) : -1;
       const int rv_n = RGNN_TM_RPF > 0 ? pf_dst(it + 1 + RGNN_TM_RPF) : -1;
       if (RGNN_TM_XPF > 0 && xs >= 0) {  // L2 prefetch of a later stage's X rows (the ring is only STAGES deep)
@@ -262,27 +279,29 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
       if (pw == 0) TMT(it, 0);
       if (use > 0) tc::mbar_wait(&empty[st], (use - 1) & 1);
       if (pw == 0) TMT(it, 1);
-      // the stage's destinations go out first (plain stores + idx_full): the compute group finds the
-      // stage's runs and reads their rows while the X rows are still in flight
-      sDst(st)[lp] = p < row1 ? v : -1;
-      tc::mbar_arrive(&idx_full[st]);
-      if (p < row1) {
-        cp_async4(sSs(st) + lp, pr.s_src + zr);
-        cp_async4(sLse(st) + lp, pr.lse + v);
+      if (spos) {
+        // the stage's destinations go out first (plain stores + idx_full): the compute group finds the
+        // stage's runs and reads their rows while the X rows are still in flight
+        sDst(st)[lp] = p < row1 ? v : -1;
+        tc::mbar_arrive(&idx_full[st]);
+        if (p < row1) {
+          cp_async4(sSs(st) + lp, pr.s_src + zr);
+          cp_async4(sLse(st) + lp, pr.lse + v);
+        }
       }
       uint8_t* a = sA(st);
 #pragma unroll
-      for (int i = 0; i < 32 / C::RPI; ++i) {  // all row indices first, then the copies back to back
+      for (int i = 0; i < RWX / C::RPI; ++i) {  // all row indices first, then the copies back to back
         const int rr = i * C::RPI + lane / C::CPR;
         const int c = lane % C::CPR;
         const int xr = __shfl_sync(0xffffffffu, src, rr);
-        tc::cp_async16(a + swz(c, pw * 32 + rr, MT), pr.X + (size_t)xr * K + c * 8);
+        tc::cp_async16(a + swz(c, pw * RWX + rr, MT), pr.X + (size_t)xr * K + c * 8);
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&a_full[st])) : "memory");
       if (pw == 0) TMT(it, 2);
       // L2 prefetch of the per-destination rows (dY, Y, x of each run head) of stage it + RGNN_TM_RPF, so
       // that they have arrived when a compute group reads them (it does so as soon as a stage is issued)
-      if (RGNN_TM_RPF > 0) {
+      if (RGNN_TM_RPF > 0 && spos) {
         const int vf = rv;
         const int vfp = __shfl_up_sync(0xffffffffu, vf, 1);
         if (vf >= 0 && (lane == 0 || vfp != vf)) {
@@ -296,21 +315,6 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
           }
 #pragma unroll
           for (int o = 0; o < K * 2; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(xp + o));
-        }
-      }
-      if (RGNN_TM_L1PF && it + 1 < nsub) {  // the next stage's run rows into this SM's L1 (its run pass reads them)
-        const int vp1 = __shfl_up_sync(0xffffffffu, nv, 1);
-        if (np < row1 && (lane == 0 || vp1 != nv)) {
-          const char* gp = reinterpret_cast<const char*>(pr.dY + (size_t)nv * N);
-          const char* yp = reinterpret_cast<const char*>(pr.Y + (size_t)nv * N);
-          const char* xp = reinterpret_cast<const char*>(pr.X + (pr.v0 + nv) * (int64_t)K);
-#pragma unroll
-          for (int o = 0; o < N * 4; o += 128) {
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(gp + o));
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(yp + o));
-          }
-#pragma unroll
-          for (int o = 0; o < K * 2; o += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(xp + o));
         }
       }
       src = nsrc; v = nv; p = np; zr = nzr;
