@@ -70,11 +70,17 @@ struct TmCfg {
 #define RGNN_TM_PW 4  // producer warps (the first four stage the per-position scalars; 8 measured slower: 2.50 -> 2.69 ms,
                       // the compute warps lose registers at 800 threads)
 #endif
-  static constexpr int PW = RGNN_TM_PW, CW = 16;  // producers, two compute groups of 8 warps
+#ifndef RGNN_TM_CW
+#define RGNN_TM_CW 16  // compute warps: two groups of CW / 2 (16: two warps per lane quarter splitting the columns;
+                       // 8, one warp per quarter over all columns, measured 2.48 -> 2.99 ms)
+#endif
+  static constexpr int PW = RGNN_TM_PW, CW = RGNN_TM_CW;  // producers, two compute groups of CW / 2 warps
+  static constexpr int WPG = CW / 2;             // warps per compute group
+  static constexpr int HPQ = WPG / 4;            // warps per TMEM lane quarter in a group (column parts)
   static constexpr int THREADS = 32 * (1 + PW + CW);
   static constexpr int ZOFF = N + 32;            // TMEM: [0,N) dW, [N,N+16) Db, Z buffers at ZOFF, ZOFF+N
   static constexpr int NCOLS = ZOFF + 2 * N <= 256 ? 256 : 512;
-  static constexpr int NH = N / 2;               // columns per compute half
+  static constexpr int NH = N / HPQ;             // columns per compute warp
   static constexpr int CPR = K * 2 / 16;         // 16-byte chunks per X row
   static constexpr int RPI = 32 / CPR;           // X rows per warp-wide cp.async
   static constexpr int LPR = N / 4;              // per-run pass: lanes per G row (4 floats each)
@@ -377,10 +383,10 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
   } else {
     // ------------------------------------------------------------ compute warps
     const int cw = warp - 1 - C::PW;   // 0..15
-    const int grp = cw >> 3;           // compute group: stages it with it % 2 == grp (TMEM / dZ / run buffer grp)
-    const int gw = cw & 7;             // warp within the group
+    const int grp = cw / C::WPG;       // compute group: stages it with it % 2 == grp (TMEM / dZ / run buffer grp)
+    const int gw = cw % C::WPG;        // warp within the group
     const int q = warp & 3;            // TMEM lane quarter this warp may access
-    const int h = (cw >> 2) & 1;       // column half
+    const int h = gw >> 2;             // column part (HPQ warps per lane quarter)
     const int lp = q * 32 + lane;      // stage row (TMEM lane) = position of this thread
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     constexpr int LPR = C::LPR, RPIT = C::RUNS_PI, BATCH = 4, KPL = K / LPR;
@@ -453,21 +459,21 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
       }
     };
     auto runs_from = [&](int buf, int nruns, int j0) {  // runs j0, j0 + 8 RPIT, ... of this warp, BATCH at a time
-      for (; j0 < nruns; j0 += 8 * RPIT * BATCH) {
+      for (; j0 < nruns; j0 += C::WPG * RPIT * BATCH) {
         float4 g[BATCH], y[BATCH];
         float xv[BATCH][KPL];
 #pragma unroll
-        for (int b = 0; b < BATCH; ++b) load_run(buf, nruns, j0 + b * 8 * RPIT + sub, g[b], y[b], xv[b]);
+        for (int b = 0; b < BATCH; ++b) load_run(buf, nruns, j0 + b * C::WPG * RPIT + sub, g[b], y[b], xv[b]);
 #pragma unroll
-        for (int b = 0; b < BATCH; ++b) store_run(buf, nruns, j0 + b * 8 * RPIT + sub, g[b], y[b], xv[b]);
+        for (int b = 0; b < BATCH; ++b) store_run(buf, nruns, j0 + b * C::WPG * RPIT + sub, g[b], y[b], xv[b]);
       }
     };
     auto prep = [&](int it) {  // blocking: the group's previous stage is finished by all its warps first
-      tc::named_bar(9 + grp, 256);
+      tc::named_bar(9 + grp, C::WPG * 32);
       const int nr = build_table(it);
-      tc::named_bar(9 + grp, 256);
+      tc::named_bar(9 + grp, C::WPG * 32);
       runs_from(it & 1, nr, gw * RPIT);
-      tc::named_bar(9 + grp, 256);  // run rows and scalars visible to the group
+      tc::named_bar(9 + grp, C::WPG * 32);  // run rows and scalars visible to the group
     };
     if (grp < nsub) prep(grp);
     for (int it = grp; it < nsub; it += 2) {
@@ -497,13 +503,13 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
       if (RGNN_TM_EARLY && nxt) {
         if (gw == 0 && lane == 0)
           sFlag[grp] = tc::mbar_try(&idx_full[(it + 2) % C::STAGES], (uint32_t)((it + 2) / C::STAGES) & 1) ? 1 : 0;
-        tc::named_bar(9 + grp, 256);  // every warp has read this stage's run entries; the flag is visible
+        tc::named_bar(9 + grp, C::WPG * 32);  // every warp has read this stage's run entries; the flag is visible
         early = sFlag[grp] != 0;
         if (early) {
           nr2 = build_table(it + 2);
-          tc::named_bar(9 + grp, 256);
+          tc::named_bar(9 + grp, C::WPG * 32);
 #pragma unroll
-          for (int e = 0; e < 2; ++e) load_run(buf, nr2, gw * RPIT + e * 8 * RPIT + sub, eg[e], ey[e], ex[e]);
+          for (int e = 0; e < 2; ++e) load_run(buf, nr2, gw * RPIT + e * C::WPG * RPIT + sub, eg[e], ey[e], ex[e]);
         }
       }
       if (gw == 0) TMT(it, 10);
@@ -560,10 +566,12 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
       if (lane == 0) tc::mbar_arrive(&zempty[buf]);
       if (gw == 0) TMT(it, 11);
       // the two halves' partial dots, summed in a fixed order
-      sT[(buf * 2 + h) * MT + lp] = t;
-      tc::named_bar(1 + grp * 4 + q, 64);
+      if (C::HPQ == 2) {
+        sT[(buf * 2 + h) * MT + lp] = t;
+        tc::named_bar(1 + grp * 4 + q, 64);
+      }
       if (gw == 0) TMT(it, 12);
-      const float dot = sT[(buf * 2 + 0) * MT + lp] + sT[(buf * 2 + 1) * MT + lp];
+      const float dot = C::HPQ == 2 ? sT[(buf * 2 + 0) * MT + lp] + sT[(buf * 2 + 1) * MT + lp] : t;
       const float dp = valid ? alpha * (dot - S) * (pre > 0.f ? 1.f : pr.slope) : 0.f;
       if (h == 0) {
         // dpre as hi + lo bf16 (columns 0, 1 of the side operand): Db = X_src^T dpre to ~2^-16
@@ -579,11 +587,11 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
       if (lane == 0) tc::mbar_arrive(&bfull[buf]);
       if (gw == 0) TMT(it, 13);
       if (early) {  // the next stage's run rows (their first loads were in flight during the pass above)
-        tc::named_bar(9 + grp, 256);  // every warp is done with this stage's run rows
+        tc::named_bar(9 + grp, C::WPG * 32);  // every warp is done with this stage's run rows
 #pragma unroll
-        for (int e = 0; e < 2; ++e) store_run(buf, nr2, gw * RPIT + e * 8 * RPIT + sub, eg[e], ey[e], ex[e]);
-        runs_from(buf, nr2, gw * RPIT + 2 * 8 * RPIT);
-        tc::named_bar(9 + grp, 256);
+        for (int e = 0; e < 2; ++e) store_run(buf, nr2, gw * RPIT + e * C::WPG * RPIT + sub, eg[e], ey[e], ex[e]);
+        runs_from(buf, nr2, gw * RPIT + 2 * C::WPG * RPIT);
+        tc::named_bar(9 + grp, C::WPG * 32);
       } else if (nxt) {
         prep(it + 2);
       }
@@ -594,7 +602,7 @@ __global__ void __launch_bounds__(TmCfg<K, N>::THREADS, 1) k_bwd_rgat_tm(BwdTmPa
     const int row = K == 128 ? q * 32 + lane : q * 16 + lane;  // M = 64: lanes 0..15 of each quarter
     const bool rvalid = K == 128 || lane < 16;
     float* out = pr.part + (size_t)blockIdx.x * (K * N + K);
-    for (int c0 = ((cw >> 2) & 3) * 16; c0 < N; c0 += 64) {
+    for (int c0 = (cw >> 2) * 16; c0 < N; c0 += (C::CW / 4) * 16) {  // the CW / 4 warps of a lane quarter
       uint32_t vv[16];
       tc::tmem_ld16(tl + c0, vv);
       tc::tmem_ld_wait();
