@@ -443,7 +443,10 @@ __device__ __forceinline__ void narrow_rows(const AggArgs& a, int64_t warp0, int
 #define RGNN_WALK_USMEM 1  // measured r02: AM walk 0.618 -> 0.595 ms, ogbn-mag 1.815 -> 1.792 ms
 #endif
 template <typename T, int K, int N, bool RGAT, bool USM = false>
-__global__ void __launch_bounds__(256, RGAT ? RGNN_NARROW_MINB_RGAT : 3) k_aggregate_narrow(AggArgs a) {
+#ifndef RGNN_NARROW_MINB_RGCN
+#define RGNN_NARROW_MINB_RGCN 4  // measured r02 end, wikikg2 walk: 3 / 4 / 5 / 6 blocks 0.861 / 0.783 / 0.829 / 0.832 ms
+#endif
+__global__ void __launch_bounds__(256, RGAT ? RGNN_NARROW_MINB_RGAT : RGNN_NARROW_MINB_RGCN) k_aggregate_narrow(AggArgs a) {
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   extern __shared__ float4 su4[];
   const float* Uw = a.U;
