@@ -466,6 +466,10 @@ __global__ void __launch_bounds__(256, RGAT ? RGNN_NARROW_MINB_RGAT : RGNN_NARRO
 #ifndef RGNN_AGG_MINB
 #define RGNN_AGG_MINB 4
 #endif
+#ifndef RGNN_AGG_MINB128
+#define RGNN_AGG_MINB128 3  // d_out = 128 (measured r02 end: ogbn-mag wide walk 1.808 -> 1.768 ms with 3; at d_out = 64
+                            // AM 0.594 -> 0.628 ms, so 4 stays there)
+#endif
 #ifndef RGNN_AGG_PREFETCH
 #define RGNN_AGG_PREFETCH 1
 #endif
@@ -473,7 +477,7 @@ __global__ void __launch_bounds__(256, RGAT ? RGNN_NARROW_MINB_RGAT : RGNN_NARRO
 #define RGNN_RING 4  // cp.async ring depth of the RGCN walk (steps of Z rows in flight + 1)
 #endif
 template <typename T, int K, int N, bool RGAT, bool CACHE>
-__global__ void __launch_bounds__(256, RGNN_AGG_MINB) k_aggregate(AggArgs a) {
+__global__ void __launch_bounds__(256, N >= 128 ? RGNN_AGG_MINB128 : RGNN_AGG_MINB) k_aggregate(AggArgs a) {
   using S = WalkShape<T, K, N>;
   constexpr int EPL = S::EPL, L = S::L, G = S::G, UNR = S::UNR, B = S::B, KPL = S::KPL;
   const T* Z = static_cast<const T*>(a.Z);
@@ -639,7 +643,10 @@ __global__ void __launch_bounds__(256, RGNN_AGG_MINB) k_aggregate(AggArgs a) {
 // mbarrier (expect_tx = the step's row bytes), instead of L 16-byte cp.async per row: one instruction per
 // row (tools/bulk_gather_bench.cu: random 256-byte rows at 6.9 TB/s, as many as register-held loads).
 template <typename T, int K, int N, bool RGAT, int RING, bool CACHE, bool BULK = false>
-__global__ void __launch_bounds__(256) k_aggregate_ring(AggArgs a) {
+#ifndef RGNN_RING_MINB
+#define RGNN_RING_MINB 4  // measured r02 end, wikikg2: minimum 1 / 4 / 5 blocks 0.845 / 0.782 / 0.784 ms
+#endif
+__global__ void __launch_bounds__(256, RGNN_RING_MINB) k_aggregate_ring(AggArgs a) {
   using S = WalkShape<T, K, N>;
   constexpr int EPL = S::EPL, L = S::L, G = S::G, UNR = S::UNR, B = S::B, KPL = S::KPL;
   constexpr int ROWB = N * (int)sizeof(T);
